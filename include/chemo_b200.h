@@ -1,0 +1,240 @@
+/*
+ * chemo_b200.h -- C ABI of the B200-native chemotaxis hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and POD parameter
+ * structs (no torch or CUDA types in the signatures; streams are passed as
+ * void*).  The caller owns every state and output buffer; the library owns
+ * only scratch (cell tables, sort buffers, FFT plans, status words) inside a
+ * context.  A context is bound to one device and one stream and is not
+ * thread-safe.
+ *
+ * Each function replaces one seam of the reference package (paths relative
+ * to /root/reference/pkg/src/chemosim), see INTEGRATION.md for the binding:
+ *
+ *   cs_soft_forces       motion.py:248-265  soft_forces -> _soft_forces_fused (:165-245)
+ *   cs_soft_force_pairs  (pair-set export of the same loop)
+ *   cs_em_step           motion.py:268-282  em_step
+ *   cs_apply_boundaries  motion.py:405-430  apply_boundaries -> _boundaries_kernel (:355-402)
+ *   cs_deposit           coupling.py:141-187 deposit / deposit_both (_cic_scatter :113-138,
+ *                                            _gauss_scatter_pair :77-110)
+ *   cs_bilinear          coupling.py:216-262 _bilinear (interpolate / field_at / refresh)
+ *   cs_gradient          field.py:242-245   gradient (d1x/d1y CSR matvecs, :128-137)
+ *   cs_field_ops_*       field.py:173-201   build_operators + Operators.solve (:162-170)
+ *   cs_field_step        field.py:209-239   step_field
+ *   cs_sim_*             engine.py:369-387  Realisation._step_inner (fused, K steps)
+ *
+ * Status codes mirror the reference kernel's (motion.py:357-358); the
+ * Python layer raises the reference's exception types and messages.
+ */
+#ifndef CHEMO_B200_H
+#define CHEMO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+enum cs_code {
+    CS_OK = 0,
+    CS_NONFINITE = 1,        /* non-finite coordinate (motion.py:361-362) */
+    CS_OVERSHOOT = 2,        /* overshoot beyond one width (motion.py:388-389) */
+    CS_UNSETTLED = 3,        /* reflection failed to settle (motion.py:399-400) */
+    CS_FIELD_NONFINITE = 4,  /* step_field non-finite (field.py:229-231) */
+    CS_ERR_CUDA = -1,
+    CS_ERR_PARAM = -2,
+    CS_ERR_NOMEM = -3,
+    CS_ERR_CUFFT = -4
+};
+
+enum cs_prec { CS_F64 = 0, CS_F32 = 1 };
+enum cs_deposit_kind { CS_GAUSSIAN = 0, CS_CIC = 1 };
+
+typedef struct cs_ctx cs_ctx;
+typedef struct cs_field_ops cs_field_ops;
+typedef struct cs_sim cs_sim;
+
+/* Box [lo, hi] per axis (spatial_index.py:20-62). */
+typedef struct {
+    double lo[2];
+    double hi[2];
+    int32_t periodic[2];
+} cs_domain;
+
+/* Pair table indexed t_i * 2 + t_j (t = 0 when the type array is NULL).
+ * Homogeneous reference: all eps = epsilon, all cutoff = cutoff.
+ * cell_cutoff sets the binning: n_ax = max(1, (int)(size_ax / cell_cutoff))
+ * (motion.py:171-172); it must be >= every cutoff entry. */
+typedef struct {
+    double eps[4];
+    double cutoff[4];
+    double cell_cutoff;
+} cs_pair_params;
+
+/* Node-centred grid (field.py:33-80): flat l = j * n_c + i, x fastest. */
+typedef struct {
+    int32_t n_c;
+    int32_t periodic;   /* 0 neumann, 1 periodic */
+    double lo[2];
+    double spacing[2];
+} cs_grid;
+
+int cs_abi_version(void);
+const char *cs_last_error(void);
+
+int cs_ctx_create(int device, void *stream, cs_ctx **out);
+int cs_ctx_set_stream(cs_ctx *ctx, void *stream);
+int cs_ctx_sync(cs_ctx *ctx);
+int cs_ctx_destroy(cs_ctx *ctx);
+
+/* out (n, 2) f64 = soft pair forces.  pos is (n, 2) f64 or f32 per prec. */
+int cs_soft_forces(cs_ctx *ctx, int32_t prec, const void *pos,
+                   const uint8_t *type, int64_t n, const cs_domain *dom,
+                   const cs_pair_params *pp, double *out);
+
+/* pairs (cap, 2) int64 (i, j) in the reference accumulation order (i
+ * ascending, then ring cell, then j ascending); *count = total pairs (may
+ * exceed cap, in which case nothing is written).  out may be NULL. */
+int cs_soft_force_pairs(cs_ctx *ctx, int32_t prec, const void *pos,
+                        const uint8_t *type, int64_t n, const cs_domain *dom,
+                        const cs_pair_params *pp, int64_t *pairs, int64_t cap,
+                        int64_t *count);
+
+/* out = ((pos + sqrt((2 D) dt) xi) + drift dt) + force dt; pos/xi/out in
+ * prec, diffusion (n) f64, drift/force (n, 2) f64 (NULL = zero). */
+int cs_em_step(cs_ctx *ctx, int32_t prec, const void *pos,
+               const double *diffusion, const double *drift,
+               const double *force, const void *xi, double dt, int64_t n,
+               void *out);
+
+/* Resolves x (the proposal buffer) against the box in place, shifts anchor
+ * on periodic wraps and, on success, copies x into positions (may be NULL).
+ * Returns CS_OK or the reference status with the first offending particle
+ * (non-finite: lowest index; otherwise lowest (axis, index)). */
+int cs_apply_boundaries(cs_ctx *ctx, int32_t prec, void *x, void *anchor,
+                        void *positions, int64_t n, const cs_domain *dom,
+                        int64_t *bad_i, int32_t *bad_ax);
+
+/* rho_a / rho_b (n_c^2, prec) are overwritten.  route[p]: 0 -> rho_a,
+ * 1 -> rho_b, other -> skipped (NULL: every particle -> rho_a).  For CS_CIC
+ * h and cutoff are ignored.  Returns CS_ERR_PARAM for a periodic gaussian
+ * stamp wider than the grid (coupling.py:156-157). */
+int cs_deposit(cs_ctx *ctx, int32_t prec, const void *pos,
+               const uint8_t *route, int64_t n, const cs_grid *grid,
+               int32_t kind, double h, double cutoff, void *rho_a,
+               void *rho_b);
+
+/* out (np, m) = bilinear samples of values (n_c^2, m); *clamped = number of
+ * clamped coordinates (neumann only). */
+int cs_bilinear(cs_ctx *ctx, int32_t prec, const void *points, int64_t np,
+                const void *values, int32_t m, const cs_grid *grid, void *out,
+                int64_t *clamped);
+
+/* grad (n_c^2, 2) = (d1x c, d1y c). */
+int cs_gradient(cs_ctx *ctx, int32_t prec, const void *c, const cs_grid *grid,
+                void *grad);
+
+/* Prepared implicit solver for (I - dt d_c L) x = rhs. */
+int cs_field_ops_create(cs_ctx *ctx, int32_t prec, const cs_grid *grid,
+                        double d_c, double dt, cs_field_ops **out);
+int cs_field_ops_destroy(cs_field_ops *ops);
+int cs_field_solve(cs_field_ops *ops, const void *rhs, void *out);
+
+/* One semi-implicit step of c in place.  *nonfinite = 1 when the new field
+ * has a non-finite value (c is then left unchanged); *neg_mass = weighted
+ * mass of the negative entries (0 if none). */
+int cs_field_step(cs_field_ops *ops, void *c, const void *rho_a,
+                  const void *rho_b, double k_alpha, double k_beta,
+                  double gamma, int32_t *nonfinite, double *neg_mass);
+
+/* y = exp(x) on the device with the glibc-exact restatement (test seam). */
+int cs_exp_batch(cs_ctx *ctx, const double *x, double *y, int64_t n);
+
+/* ---------------------------------------------------------------------- */
+/* Fused K-step pipeline (Realisation._step_inner, engine.py:369-387).      */
+/* ---------------------------------------------------------------------- */
+typedef struct {
+    int64_t n;
+    int32_t prec;            /* storage of pos/next/anchor/xi and grid arrays */
+    int32_t n_types;         /* 1 (type may be NULL) or 2 */
+    cs_domain domain;
+    int32_t interaction;     /* 0 none, 1 soft */
+    cs_pair_params pairs;
+    double amp[2];           /* per-type sqrt((2 D) dt) */
+    double dt;
+    int32_t field_active;    /* deposit + step_field + gradient each step */
+    int32_t refresh_active;  /* bilinear refresh of drift each step */
+    cs_grid grid;
+    double d_c, k_alpha, k_beta, gamma;
+    int32_t deposit_kind;
+    double kernel_h, kernel_cutoff;
+    int32_t secretes[2];     /* type t deposits into rho_a */
+    int32_t consumes[2];     /* type t deposits into rho_b */
+    double chi[2];
+    int32_t chi_pinned[2];   /* drift of type t is pinned to zero */
+    int32_t store_samples;   /* write drift / local_c every step */
+    int32_t store_next;      /* write next_pos every step */
+} cs_sim_params;
+
+typedef struct {
+    void *pos;               /* (n, 2) prec, in/out */
+    void *next_pos;          /* (n, 2) prec, optional */
+    void *anchor;            /* (n, 2) prec, in/out */
+    const uint8_t *type;     /* (n,) or NULL */
+    double *drift;           /* (n, 2) f64; read when refresh is off */
+    double *local_c;         /* (n,) f64, optional */
+    void *c;                 /* (n_c^2) prec */
+    void *grad;              /* (n_c^2, 2) prec */
+    void *rho_a, *rho_b;     /* (n_c^2) prec */
+} cs_sim_state;
+
+typedef struct {
+    int32_t code;            /* enum cs_code */
+    int32_t step;            /* failing step (relative to the first call since
+                                the last reset), -1 if none */
+    int64_t particle;
+    int32_t axis;
+    int64_t clamped;         /* clamped interpolation coordinates */
+    int64_t neg_mass_steps;  /* steps with negative weighted mass < -1e-12 */
+    double first_neg_mass;
+    int64_t steps_done;
+} cs_status;
+
+int cs_sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out);
+int cs_sim_destroy(cs_sim *sim);
+/* Enqueue k steps on the context stream (asynchronous).  xi points at the
+ * Brownian increments of the first step, (n, 2) prec per step, successive
+ * steps xi_stride elements apart. */
+int cs_sim_step(cs_sim *sim, const cs_sim_state *st, const void *xi,
+                int64_t xi_stride, int32_t k_steps);
+/* Synchronise and read the status accumulated since the last reset. */
+int cs_sim_status(cs_sim *sim, cs_status *out);
+int cs_sim_reset_status(cs_sim *sim);
+/* Launch count of the most recent cs_sim_step call (kernels of this
+ * library; cuFFT's internal kernels are not counted). */
+int64_t cs_sim_launches(cs_sim *sim);
+
+/* Per-stage device time (CUDA events around each stage on the context
+ * stream).  Enabling resets the accumulators. */
+enum cs_stage {
+    CS_STAGE_DEPOSIT = 0,   /* zero rho + deposit */
+    CS_STAGE_SOLVE = 1,     /* rhs + implicit solve */
+    CS_STAGE_GRADIENT = 2,  /* gradient + field checks */
+    CS_STAGE_BIN = 3,       /* cell list */
+    CS_STAGE_FORCE = 4,     /* pair forces */
+    CS_STAGE_UPDATE = 5,    /* refresh + EM + boundaries */
+    CS_N_STAGES = 6
+};
+int cs_sim_set_profiling(cs_sim *sim, int32_t on);
+/* Device address and size of the simulation's status word, so a caller can
+ * read it back asynchronously (e.g. into pinned memory) after every step. */
+void *cs_sim_status_device(cs_sim *sim);
+int64_t cs_sim_status_bytes(void);
+int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,373 @@
+// capi.cu -- the extern "C" boundary (include/chemo_b200.h).
+#include <math.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace cs {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int Buf::ensure(size_t need) {
+    if (need <= bytes && p) return CS_OK;
+    if (p) {
+        cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    if (need == 0) need = 16;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e != cudaSuccess) {
+        set_error("cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
+        p = nullptr;
+        return CS_ERR_NOMEM;
+    }
+    bytes = need;
+    return CS_OK;
+}
+
+void Buf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+BinGeom make_geom(const cs_domain &d, double cell_cutoff) {
+    BinGeom g;
+    g.lo0 = d.lo[0];
+    g.lo1 = d.lo[1];
+    g.size0 = d.hi[0] - d.lo[0];
+    g.size1 = d.hi[1] - d.lo[1];
+    // motion.py:171-174: n = max(1, int(size / cutoff)); eff = size / n
+    long long n0 = (long long)(g.size0 / cell_cutoff);
+    long long n1 = (long long)(g.size1 / cell_cutoff);
+    g.n0 = (int)(n0 < 1 ? 1 : n0);
+    g.n1 = (int)(n1 < 1 ? 1 : n1);
+    g.eff0 = g.size0 / g.n0;
+    g.eff1 = g.size1 / g.n1;
+    g.per0 = d.periodic[0] != 0;
+    g.per1 = d.periodic[1] != 0;
+    return g;
+}
+
+PairTab make_pairtab(const cs_pair_params &pp) {
+    PairTab t;
+    for (int k = 0; k < 4; k++) {
+        t.eps[k] = pp.eps[k];
+        t.cut2[k] = pp.cutoff[k] * pp.cutoff[k];
+    }
+    return t;
+}
+
+GridGeom make_grid_geom(const cs_grid &g) {
+    GridGeom gg;
+    gg.n = g.n_c;
+    gg.per = g.periodic != 0;
+    gg.lo0 = g.lo[0];
+    gg.lo1 = g.lo[1];
+    gg.d0 = g.spacing[0];
+    gg.d1 = g.spacing[1];
+    return gg;
+}
+
+int launch_em_step(cs_ctx *ctx, int prec, const void *pos, const double *D, const double *drift,
+                   const double *force, const void *xi, double dt, long long n, void *out);
+int launch_boundaries(cs_ctx *ctx, int prec, void *x, void *anchor, long long n,
+                      const cs_domain &d, DevStatus *st);
+int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
+                   const GridGeom &gg, int kind, double h, double cutoff,
+                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
+                   bool zero_first);
+bool gauss_too_wide(const GridGeom &gg, double cutoff);
+int launch_bilinear(cs_ctx *ctx, int prec, const void *pts, long long np, const void *vals, int m,
+                    const GridGeom &gg, void *out, unsigned long long *clamped);
+int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
+                    DevStatus *st, int step);
+int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
+                     cs_field_ops **out);
+void field_ops_destroy(cs_field_ops *ops);
+int field_solve_rhs(cs_field_ops *ops, void *out);
+int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
+              double kb, double gamma, const DevStatus *st);
+int field_load_rhs(cs_field_ops *ops, const void *rhs);
+int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out);
+void sim_destroy(cs_sim *sim);
+int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k);
+int sim_status(cs_sim *sim, cs_status *out);
+int sim_reset_status(cs_sim *sim);
+
+__global__ void k_exp(const double *x, double *y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = cs_exp(x[i]);
+}
+
+static int check_prec(int prec) {
+    if (prec != CS_F64 && prec != CS_F32) {
+        set_error("unknown precision %d", prec);
+        return CS_ERR_PARAM;
+    }
+    return CS_OK;
+}
+
+static int check_pairs(const cs_pair_params *pp) {
+    for (int k = 0; k < 4; k++) {
+        if (!(pp->eps[k] > 0) || !(pp->cutoff[k] > 0)) {
+            set_error("pair table entries must be positive");
+            return CS_ERR_PARAM;
+        }
+        if (pp->cutoff[k] > pp->cell_cutoff) {
+            set_error("cell_cutoff must cover every pair cutoff");
+            return CS_ERR_PARAM;
+        }
+    }
+    return CS_OK;
+}
+
+// status word for the standalone seams
+static int local_status(cs_ctx *ctx, DevStatus **out) {
+    CS_TRY(ctx->status.ensure(sizeof(DevStatus)));
+    DevStatus init{};
+    init.key = ~0ULL;
+    init.step = -1;
+    CS_CUDA(cudaMemcpyAsync(ctx->status.p, &init, sizeof(init), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    *out = ctx->dstat();
+    return CS_OK;
+}
+
+}  // namespace cs
+
+using namespace cs;
+
+extern "C" {
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+const char *cs_last_error(void) { return g_err; }
+
+int cs_ctx_create(int device, void *stream, cs_ctx **out) {
+    CS_CUDA(cudaSetDevice(device));
+    auto *ctx = new cs_ctx();
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)stream;
+    *out = ctx;
+    return CS_OK;
+}
+
+int cs_ctx_set_stream(cs_ctx *ctx, void *stream) {
+    ctx->stream = (cudaStream_t)stream;
+    return CS_OK;
+}
+
+int cs_ctx_sync(cs_ctx *ctx) {
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CS_OK;
+}
+
+int cs_ctx_destroy(cs_ctx *ctx) {
+    if (!ctx) return CS_OK;
+    cudaStreamSynchronize(ctx->stream);
+    for (Buf *b : {&ctx->keys, &ctx->skeys, &ctx->counts, &ctx->starts, &ctx->order,
+                   &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->status, &ctx->pair_counts,
+                   &ctx->pair_offsets, &ctx->host_scratch})
+        b->release();
+    delete ctx;
+    return CS_OK;
+}
+
+int cs_soft_forces(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *type, int64_t n,
+                   const cs_domain *dom, const cs_pair_params *pp, double *out) {
+    CS_TRY(check_prec(prec));
+    CS_TRY(check_pairs(pp));
+    const BinGeom g = make_geom(*dom, pp->cell_cutoff);
+    CS_TRY(bin_particles(ctx, prec, pos, n, g));
+    CS_TRY(launch_soft_forces(ctx, prec, pos, type, n, g, make_pairtab(*pp), out, nullptr));
+    return CS_OK;
+}
+
+int cs_soft_force_pairs(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *type,
+                        int64_t n, const cs_domain *dom, const cs_pair_params *pp,
+                        int64_t *pairs, int64_t cap, int64_t *count) {
+    CS_TRY(check_prec(prec));
+    CS_TRY(check_pairs(pp));
+    const BinGeom g = make_geom(*dom, pp->cell_cutoff);
+    CS_TRY(bin_particles(ctx, prec, pos, n, g));
+    CS_TRY(run_soft_force_pairs(ctx, prec, pos, type, n, g, make_pairtab(*pp), pairs, cap, count));
+    return CS_OK;
+}
+
+int cs_em_step(cs_ctx *ctx, int32_t prec, const void *pos, const double *diffusion,
+               const double *drift, const double *force, const void *xi, double dt, int64_t n,
+               void *out) {
+    CS_TRY(check_prec(prec));
+    return launch_em_step(ctx, prec, pos, diffusion, drift, force, xi, dt, n, out);
+}
+
+int cs_apply_boundaries(cs_ctx *ctx, int32_t prec, void *x, void *anchor, void *positions,
+                        int64_t n, const cs_domain *dom, int64_t *bad_i, int32_t *bad_ax) {
+    CS_TRY(check_prec(prec));
+    DevStatus *st;
+    CS_TRY(local_status(ctx, &st));
+    CS_TRY(launch_boundaries(ctx, prec, x, anchor, n, *dom, st));
+    DevStatus d;
+    CS_CUDA(cudaMemcpyAsync(&d, st, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *bad_i = -1;
+    *bad_ax = -1;
+    if (d.key != ~0ULL) {
+        const int rank = (int)(d.key >> 60);
+        *bad_i = (int64_t)((d.key >> 3) & ((1ULL << 57) - 1));
+        *bad_ax = rank >= 1 ? rank - 1 : 0;
+        return (int)(d.key & 7ULL);
+    }
+    if (positions && positions != x && n > 0) {
+        const size_t es = prec == CS_F64 ? 8 : 4;
+        CS_CUDA(cudaMemcpyAsync(positions, x, (size_t)n * 2 * es, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    }
+    return CS_OK;
+}
+
+int cs_deposit(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *route, int64_t n,
+               const cs_grid *grid, int32_t kind, double h, double cutoff, void *rho_a,
+               void *rho_b) {
+    CS_TRY(check_prec(prec));
+    const GridGeom gg = make_grid_geom(*grid);
+    if (kind == CS_GAUSSIAN) {
+        if (!(h > 0) || !(cutoff > 0)) {
+            set_error("kernel bandwidth and cutoff must be positive");
+            return CS_ERR_PARAM;
+        }
+        if (gauss_too_wide(gg, cutoff)) {
+            set_error("gaussian cutoff spans more than the periodic grid");
+            return CS_ERR_PARAM;
+        }
+    }
+    const unsigned char bits[3] = {1, 2, 0};
+    void *rb = rho_b;
+    Buf *tmp = nullptr;
+    if (!rb) {  // single-output call: route everything to rho_a
+        tmp = &ctx->tmp;
+        CS_TRY(tmp->ensure((size_t)grid->n_c * grid->n_c * (prec == CS_F64 ? 8 : 4)));
+        rb = tmp->p;
+    }
+    return launch_deposit(ctx, prec, pos, route, n, gg, kind, h, cutoff, bits, rho_a, rb, nullptr,
+                          true);
+}
+
+int cs_bilinear(cs_ctx *ctx, int32_t prec, const void *points, int64_t np, const void *values,
+                int32_t m, const cs_grid *grid, void *out, int64_t *clamped) {
+    CS_TRY(check_prec(prec));
+    CS_TRY(ctx->tmp.ensure(sizeof(unsigned long long)));
+    unsigned long long *cl = ctx->tmp.as<unsigned long long>();
+    CS_CUDA(cudaMemsetAsync(cl, 0, sizeof(unsigned long long), ctx->stream));
+    CS_TRY(launch_bilinear(ctx, prec, points, np, values, m, make_grid_geom(*grid), out, cl));
+    unsigned long long h = 0;
+    CS_CUDA(cudaMemcpyAsync(&h, cl, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *clamped = (int64_t)h;
+    return CS_OK;
+}
+
+int cs_gradient(cs_ctx *ctx, int32_t prec, const void *c, const cs_grid *grid, void *grad) {
+    CS_TRY(check_prec(prec));
+    return launch_gradient(ctx, prec, c, make_grid_geom(*grid), grad, nullptr, -1);
+}
+
+int cs_field_ops_create(cs_ctx *ctx, int32_t prec, const cs_grid *grid, double d_c, double dt,
+                        cs_field_ops **out) {
+    CS_TRY(check_prec(prec));
+    *out = nullptr;
+    cs_field_ops *ops = nullptr;
+    const int rc = field_ops_create(ctx, prec, grid, d_c, dt, &ops);
+    if (rc != CS_OK) {
+        field_ops_destroy(ops);
+        return rc;
+    }
+    *out = ops;
+    return CS_OK;
+}
+
+int cs_field_ops_destroy(cs_field_ops *ops) {
+    field_ops_destroy(ops);
+    return CS_OK;
+}
+
+int cs_field_solve(cs_field_ops *ops, const void *rhs, void *out) {
+    CS_TRY(field_load_rhs(ops, rhs));
+    return field_solve_rhs(ops, out);
+}
+
+int cs_field_step(cs_field_ops *ops, void *c, const void *rho_a, const void *rho_b,
+                  double k_alpha, double k_beta, double gamma, int32_t *nonfinite,
+                  double *neg_mass) {
+    cs_ctx *ctx = ops->ctx;
+    const size_t m = (size_t)ops->gg.n * ops->gg.n;
+    const size_t es = ops->prec == CS_F64 ? 8 : 4;
+    CS_TRY(field_rhs(ops, c, rho_a, rho_b, k_alpha, k_beta, gamma, nullptr));
+    // solve into scratch so a non-finite result leaves c untouched
+    CS_TRY(ctx->tmp.ensure(m * es * 3 + 64));
+    void *cn = ctx->tmp.p;
+    void *grad = (char *)ctx->tmp.p + m * es;
+    CS_TRY(field_solve_rhs(ops, cn));
+    DevStatus *st;
+    CS_TRY(local_status(ctx, &st));
+    CS_TRY(launch_gradient(ctx, ops->prec, cn, ops->gg, grad, st, -1));
+    DevStatus d;
+    CS_CUDA(cudaMemcpyAsync(&d, st, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *nonfinite = d.field_bad;
+    *neg_mass = d.neg_flag ? d.neg_mass : 0.0;
+    if (!d.field_bad)
+        CS_CUDA(cudaMemcpyAsync(c, cn, m * es, cudaMemcpyDeviceToDevice, ctx->stream));
+    return CS_OK;
+}
+
+int cs_exp_batch(cs_ctx *ctx, const double *x, double *y, int64_t n) {
+    if (n == 0) return CS_OK;
+    k_exp<<<grid_for(n, 256), 256, 0, ctx->stream>>>(x, y, n);
+    CS_LAUNCH_CHECK();
+    return CS_OK;
+}
+
+int cs_sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
+    CS_TRY(check_prec(p->prec));
+    if (p->interaction == 1) CS_TRY(check_pairs(&p->pairs));
+    if (p->field_active && p->deposit_kind == CS_GAUSSIAN &&
+        gauss_too_wide(make_grid_geom(p->grid), p->kernel_cutoff)) {
+        set_error("gaussian cutoff spans more than the periodic grid");
+        return CS_ERR_PARAM;
+    }
+    *out = nullptr;
+    cs_sim *sim = nullptr;
+    const int rc = sim_create(ctx, p, &sim);
+    if (rc != CS_OK) {
+        sim_destroy(sim);
+        return rc;
+    }
+    *out = sim;
+    return CS_OK;
+}
+
+int cs_sim_destroy(cs_sim *sim) {
+    sim_destroy(sim);
+    return CS_OK;
+}
+
+int cs_sim_step(cs_sim *sim, const cs_sim_state *st, const void *xi, int64_t xi_stride,
+                int32_t k_steps) {
+    return sim_step(sim, st, xi, xi_stride, k_steps);
+}
+
+int cs_sim_status(cs_sim *sim, cs_status *out) { return sim_status(sim, out); }
+int cs_sim_reset_status(cs_sim *sim) { return sim_reset_status(sim); }
+
+}  // extern "C"

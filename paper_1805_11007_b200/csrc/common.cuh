@@ -1,0 +1,282 @@
+// common.cuh -- shared device helpers, context and scratch management.
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/chemo_b200.h"
+#include "glibc_exp.h"
+
+namespace cs {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+
+#define CS_CUDA(call)                                                        \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess) {                                             \
+            ::cs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,       \
+                            cudaGetErrorString(e_));                         \
+            return CS_ERR_CUDA;                                              \
+        }                                                                    \
+    } while (0)
+
+#define CS_LAUNCH_CHECK()                                                    \
+    do {                                                                     \
+        cudaError_t e_ = cudaGetLastError();                                 \
+        if (e_ != cudaSuccess) {                                             \
+            ::cs::set_error("%s:%d launch: %s", __FILE__, __LINE__,          \
+                            cudaGetErrorString(e_));                         \
+            return CS_ERR_CUDA;                                              \
+        }                                                                    \
+    } while (0)
+
+#define CS_TRY(expr)                                                         \
+    do {                                                                     \
+        int rc_ = (expr);                                                    \
+        if (rc_ != CS_OK) return rc_;                                        \
+    } while (0)
+
+// ---------------------------------------------------------------- scratch
+struct Buf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t need);  // grow-only, contents not preserved
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// Device status word shared by every kernel of a fused step: kernels return
+// immediately once `abort` is set (a later step must not run on a state the
+// reference would have refused).
+struct DevStatus {
+    unsigned long long key;   // min over (rank, particle, code), ~0 = ok
+    int abort;
+    int step;
+    int field_bad;
+    int pad;
+    long long clamped;
+    long long neg_steps;
+    double first_neg;
+    double neg_mass;          // scratch: this step's negative weighted mass
+    int neg_flag;             // scratch: this step saw a negative node
+    int pad2;
+};
+
+// error key: rank 0 = non-finite (lowest index wins), rank 1 + ax = axis
+// error; within a rank the lowest particle index wins.
+__host__ __device__ inline unsigned long long err_key(int rank, long long i, int code) {
+    return ((unsigned long long)rank << 60) | ((unsigned long long)i << 3) |
+           (unsigned long long)code;
+}
+
+}  // namespace cs
+
+struct cs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status,
+        pair_counts, pair_offsets, host_scratch;
+    cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
+    int64_t launches = 0;
+};
+
+namespace cs {
+
+// ---------------------------------------------------------------- math
+// Explicitly rounded binary64 arithmetic: the reference (numba/numpy) never
+// contracts a*b+c, so neither may the parity-critical kernels.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+__host__ __device__ __forceinline__ long long pymod(long long a, long long n) {
+    long long r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+template <class P> struct Vec2;
+template <> struct Vec2<double> { using T = double2; };
+template <> struct Vec2<float> { using T = float2; };
+
+template <class P>
+__device__ __forceinline__ void load2(const P *__restrict__ a, long long i, double &x, double &y) {
+    auto v = reinterpret_cast<const typename Vec2<P>::T *>(a)[i];
+    x = (double)v.x;
+    y = (double)v.y;
+}
+template <class P>
+__device__ __forceinline__ void store2(P *__restrict__ a, long long i, double x, double y) {
+    typename Vec2<P>::T v;
+    v.x = (P)x;
+    v.y = (P)y;
+    reinterpret_cast<typename Vec2<P>::T *>(a)[i] = v;
+}
+
+// Cell geometry of the reference binning (motion.py:171-174).
+struct BinGeom {
+    int n0, n1;
+    double lo0, lo1, size0, size1, eff0, eff1;
+    int per0, per1;
+};
+
+BinGeom make_geom(const cs_domain &d, double cell_cutoff);
+
+__device__ __forceinline__ int cell_axis(double v, double lo, double eff, int n) {
+    double f = floor(ddiv(dsub(v, lo), eff));
+    if (!(f >= 0.0)) return 0;  // also NaN -> 0
+    if (f >= (double)n) return n - 1;
+    return (int)f;
+}
+
+struct PairTab {
+    double eps[4];
+    double cut2[4];
+};
+PairTab make_pairtab(const cs_pair_params &pp);
+
+// Grid geometry (field.py:33-66) for coupling kernels.
+struct GridGeom {
+    int n;
+    int per;
+    double lo0, lo1, d0, d1;
+};
+GridGeom make_grid_geom(const cs_grid &g);
+
+// Bilinear stencil of coupling.py:216-258 (_bilinear): corner node indices
+// and weights in the reference arithmetic; returns the number of clamped
+// coordinates (neumann hull clamp).
+struct Bilin {
+    long long r00, r10, r01, r11;
+    double w00, w10, w01, w11;
+};
+__device__ __forceinline__ int bilinear_stencil(double px, double py, const GridGeom &gg,
+                                                Bilin &b) {
+    int clamped = 0;
+    double u0 = ddiv(dsub(px, gg.lo0), gg.d0);
+    double u1 = ddiv(dsub(py, gg.lo1), gg.d1);
+    long long b0, b1, c0, c1;
+    double f0, f1;
+    const int n = gg.n;
+    if (gg.per) {
+        const double f0f = floor(u0), f1f = floor(u1);
+        b0 = pymod((long long)f0f, n);
+        b1 = pymod((long long)f1f, n);
+        f0 = dsub(u0, f0f);
+        f1 = dsub(u1, f1f);
+        c0 = (b0 + 1) % n;
+        c1 = (b1 + 1) % n;
+    } else {
+        const double nm1 = (double)(n - 1);
+        if (u0 < 0.0) { u0 = 0.0; clamped++; }
+        else if (u0 > nm1) { u0 = nm1; clamped++; }
+        if (u1 < 0.0) { u1 = 0.0; clamped++; }
+        else if (u1 > nm1) { u1 = nm1; clamped++; }
+        b0 = (long long)floor(u0);
+        if (b0 > n - 2) b0 = n - 2;
+        b1 = (long long)floor(u1);
+        if (b1 > n - 2) b1 = n - 2;
+        f0 = dsub(u0, (double)b0);
+        f1 = dsub(u1, (double)b1);
+        c0 = b0 + 1;
+        c1 = b1 + 1;
+    }
+    b.w00 = dmul(dsub(1.0, f0), dsub(1.0, f1));
+    b.w10 = dmul(f0, dsub(1.0, f1));
+    b.w01 = dmul(dsub(1.0, f0), f1);
+    b.w11 = dmul(f0, f1);
+    b.r00 = b1 * n + b0;
+    b.r10 = b1 * n + c0;
+    b.r01 = c1 * n + b0;
+    b.r11 = c1 * n + c0;
+    return clamped;
+}
+
+// sum in the reference order: ((w00 v00 + w10 v10) + w01 v01) + w11 v11
+template <class G>
+__device__ __forceinline__ double bilinear_apply(const Bilin &b, const G *__restrict__ v, int m,
+                                                 int k) {
+    const double a = dmul(b.w00, (double)v[b.r00 * m + k]);
+    const double c = dmul(b.w10, (double)v[b.r10 * m + k]);
+    const double d = dmul(b.w01, (double)v[b.r01 * m + k]);
+    const double e = dmul(b.w11, (double)v[b.r11 * m + k]);
+    return dadd(dadd(dadd(a, c), d), e);
+}
+
+// One axis of _boundaries_kernel (motion.py:363-401).  Returns 0, 2 or 3.
+__device__ __forceinline__ int boundary_axis(double &v, double &a, double lo, double hi,
+                                             int per) {
+    const double size = dsub(hi, lo);
+    if (per) {
+        const double k = floor(ddiv(dsub(v, lo), size));
+        if (k != 0.0) {
+            const double shift = dmul(k, size);
+            v = dsub(v, shift);
+            a = dsub(a, shift);
+        }
+        for (int it = 0; it < 2; it++) {
+            if (v >= hi) {
+                v = dsub(v, size);
+                a = dsub(a, size);
+            } else if (v < lo) {
+                v = dadd(v, size);
+                a = dadd(a, size);
+            } else {
+                break;
+            }
+        }
+        return 0;
+    }
+    if (v > dadd(hi, size) || v < dsub(lo, size)) return 2;
+    for (int it = 0; it < 4; it++) {
+        if (v > hi) v = dsub(dmul(2.0, hi), v);
+        else if (v < lo) v = dsub(dmul(2.0, lo), v);
+        else return 0;
+    }
+    return 3;
+}
+
+inline int grid_for(long long n, int block, int max_blocks = 148 * 64) {
+    long long g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------- launchers
+// bins.cu
+int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g);
+int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n);
+// forces.cu
+int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,
+                       long long n, const BinGeom &g, const PairTab &pt, double *out,
+                       const DevStatus *st);
+// motion.cu / field.cu / sim.cu
+int record_error(cs_ctx *ctx);
+int run_soft_force_pairs(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,
+                         long long n, const BinGeom &g, const PairTab &pt,
+                         int64_t *pairs, int64_t cap, int64_t *count);
+
+}  // namespace cs
+
+// ------------------------------------------------------------------ ops
+struct cs_field_ops {
+    cs_ctx *ctx = nullptr;
+    int prec = CS_F64;
+    cs::GridGeom gg{};
+    int kind = 0;  // 0 identity, 1 dct, 2 fft
+    double dt = 0, d_c = 0;
+    double *F = nullptr, *Inv = nullptr, *E = nullptr, *T1 = nullptr, *T2 = nullptr;
+    double *lx = nullptr, *ly = nullptr;
+    void *rhs = nullptr;   // G (fft / identity) or double (dct)
+    void *spec = nullptr;  // complex n x (n/2+1)
+    cufftHandle pf = 0, pi = 0;
+    bool have_plans = false;
+};
+

@@ -1,0 +1,674 @@
+// field.cu -- grid side of the hot path: deposits, the semi-implicit field
+// step, the gradient stencil and bilinear sampling.
+//
+// References (chemosim/):
+//   deposits       coupling.py:45-187  (_gauss_scatter_pair, _cic_scatter)
+//   rhs            field.py:220-227    c(1 - dt g) + (dt ka) ra - (rb c)(dt kb)
+//   solve          field.py:162-201    (I - dt d_c L) c' = rhs
+//                  neumann: DCT-I modal solve, 4 dense GEMMs through the
+//                  cosine basis (here: fp64 tiled GEMM kernels, same basis);
+//                  periodic: the reference factors the sparse system with
+//                  SuperLU; the same circulant system is diagonalised here by
+//                  a 2-D real FFT (cuFFT D2Z/Z2D or R2C/C2R), which is exact
+//                  up to rounding and the only feasible route at 4096^2+.
+//   checks         field.py:229-238    non-finite -> FloatingPointError,
+//                  negative weighted mass < -1e-12 -> warning
+//   gradient       field.py:128-137, 242-245  CSR rows in column order
+//   bilinear       coupling.py:216-262
+// Deposits accumulate with native f64 (or f32) atomics in L2; the stamp
+// arithmetic is the reference's, only the summation order of concurrent
+// contributions differs (T1 tolerance 1e-12).
+#include <cufft.h>
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace cs {
+
+// ------------------------------------------------------------------ deposit
+struct Route {
+    unsigned char bits[3];  // indexed by min(type, 2): bit0 -> rho_a, bit1 -> rho_b
+};
+
+__device__ __forceinline__ unsigned route_bits(const uint8_t *type, long long p, const Route &r) {
+    const unsigned t = type ? (unsigned)type[p] : 0u;
+    return r.bits[t < 2u ? t : 2u];
+}
+
+template <class G>
+__device__ __forceinline__ void atomic_add_g(G *a, double v);
+template <>
+__device__ __forceinline__ void atomic_add_g<double>(double *a, double v) {
+    atomicAdd(a, v);
+}
+template <>
+__device__ __forceinline__ void atomic_add_g<float>(float *a, double v) {
+    atomicAdd(a, (float)v);
+}
+
+template <class P, class G>
+__global__ void k_deposit_cic(const P *__restrict__ pos, const uint8_t *__restrict__ type,
+                              long long n, GridGeom gg, Route route, G *__restrict__ ra,
+                              G *__restrict__ rb, const DevStatus *st) {
+    if (st && st->abort) return;
+    const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
+    const int nc = gg.n;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const unsigned bits = route_bits(type, p, route);
+        if (!bits) continue;
+        double x, y;
+        load2(pos, p, x, y);
+        const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
+        const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+        long long b0, b1, c0, c1;
+        double f0, f1;
+        if (gg.per) {
+            const double base0 = floor(u0), base1 = floor(u1);
+            f0 = dsub(u0, base0);
+            f1 = dsub(u1, base1);
+            b0 = pymod((long long)base0, nc);
+            b1 = pymod((long long)base1, nc);
+            c0 = (b0 + 1) % nc;
+            c1 = (b1 + 1) % nc;
+        } else {
+            b0 = (long long)floor(u0);
+            b1 = (long long)floor(u1);
+            b0 = b0 < 0 ? 0 : (b0 > nc - 2 ? nc - 2 : b0);
+            b1 = b1 < 0 ? 0 : (b1 > nc - 2 ? nc - 2 : b1);
+            f0 = dsub(u0, (double)b0);
+            f1 = dsub(u1, (double)b1);
+            c0 = b0 + 1;
+            c1 = b1 + 1;
+        }
+        const double w00 = dmul(dmul(dsub(1.0, f0), dsub(1.0, f1)), unit);
+        const double w10 = dmul(dmul(f0, dsub(1.0, f1)), unit);
+        const double w01 = dmul(dmul(dsub(1.0, f0), f1), unit);
+        const double w11 = dmul(dmul(f0, f1), unit);
+        for (int which = 0; which < 2; which++) {
+            if (!(bits & (1u << which))) continue;
+            G *out = which == 0 ? ra : rb;
+            atomic_add_g(&out[b1 * nc + b0], w00);
+            atomic_add_g(&out[b1 * nc + c0], w10);
+            atomic_add_g(&out[c1 * nc + b0], w01);
+            atomic_add_g(&out[c1 * nc + c0], w11);
+        }
+    }
+}
+
+struct GaussParams {
+    double inv_norm, two_h2, cut2;
+    int w0, w1;
+};
+
+template <class P, class G>
+__global__ void k_deposit_gauss(const P *__restrict__ pos, const uint8_t *__restrict__ type,
+                                long long n, GridGeom gg, Route route, GaussParams gp,
+                                G *__restrict__ ra, G *__restrict__ rb, const DevStatus *st) {
+    if (st && st->abort) return;
+    const int nc = gg.n;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        const unsigned bits = route_bits(type, p, route);
+        if (!bits) continue;
+        double x, y;
+        load2(pos, p, x, y);
+        const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
+        const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+        const long long b0 = (long long)floor(dadd(u0, 0.5));
+        const long long b1 = (long long)floor(dadd(u1, 0.5));
+        for (int o1 = -gp.w1; o1 <= gp.w1; o1++) {
+            long long j = b1 + o1;
+            if (gg.per) j = pymod(j, nc);
+            else if (j < 0 || j >= nc) continue;
+            const double dy = dmul(dsub(u1, (double)(b1 + o1)), gg.d1);
+            const double dy2 = dmul(dy, dy);
+            for (int o0 = -gp.w0; o0 <= gp.w0; o0++) {
+                long long i = b0 + o0;
+                if (gg.per) i = pymod(i, nc);
+                else if (i < 0 || i >= nc) continue;
+                const double dxp = dmul(dsub(u0, (double)(b0 + o0)), gg.d0);
+                const double r2 = dadd(dmul(dxp, dxp), dy2);
+                if (r2 <= gp.cut2) {
+                    const double v = dmul(gp.inv_norm, cs_exp(-ddiv(r2, gp.two_h2)));
+                    if (bits & 1u) atomic_add_g(&ra[j * nc + i], v);
+                    if (bits & 2u) atomic_add_g(&rb[j * nc + i], v);
+                }
+            }
+        }
+    }
+}
+
+GaussParams make_gauss(const GridGeom &gg, double h, double cutoff) {
+    GaussParams gp;
+    gp.inv_norm = 1.0 / (2.0 * M_PI * h * h);
+    gp.two_h2 = 2.0 * h * h;
+    gp.cut2 = cutoff * cutoff;
+    gp.w0 = (int)floor(cutoff / gg.d0 + 0.5);
+    gp.w1 = (int)floor(cutoff / gg.d1 + 0.5);
+    return gp;
+}
+
+int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
+                   const GridGeom &gg, int kind, double h, double cutoff,
+                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
+                   bool zero_first) {
+    const size_t m = (size_t)gg.n * gg.n;
+    const size_t es = prec == CS_F64 ? 8 : 4;
+    if (zero_first) {
+        CS_CUDA(cudaMemsetAsync(ra, 0, m * es, ctx->stream));
+        CS_CUDA(cudaMemsetAsync(rb, 0, m * es, ctx->stream));
+    }
+    if (n == 0) return CS_OK;
+    Route r;
+    r.bits[0] = bits[0];
+    r.bits[1] = bits[1];
+    r.bits[2] = bits[2];
+    const int B = 256;
+    const int G = grid_for(n, B);
+    if (kind == CS_CIC) {
+        if (prec == CS_F64)
+            k_deposit_cic<double, double><<<G, B, 0, ctx->stream>>>(
+                (const double *)pos, type, n, gg, r, (double *)ra, (double *)rb, st);
+        else
+            k_deposit_cic<float, float><<<G, B, 0, ctx->stream>>>(
+                (const float *)pos, type, n, gg, r, (float *)ra, (float *)rb, st);
+    } else {
+        const GaussParams gp = make_gauss(gg, h, cutoff);
+        if (prec == CS_F64)
+            k_deposit_gauss<double, double><<<G, B, 0, ctx->stream>>>(
+                (const double *)pos, type, n, gg, r, gp, (double *)ra, (double *)rb, st);
+        else
+            k_deposit_gauss<float, float><<<G, B, 0, ctx->stream>>>(
+                (const float *)pos, type, n, gg, r, gp, (float *)ra, (float *)rb, st);
+    }
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+bool gauss_too_wide(const GridGeom &gg, double cutoff) {
+    const double dmin = gg.d0 < gg.d1 ? gg.d0 : gg.d1;
+    return gg.per && ((int)floor(cutoff / dmin + 0.5)) * 2 + 1 > gg.n;
+}
+
+// ------------------------------------------------------------------ bilinear
+template <class P, class G>
+__global__ void k_bilinear(const P *__restrict__ pts, long long np, const G *__restrict__ vals,
+                           int m, GridGeom gg, G *__restrict__ out,
+                           unsigned long long *__restrict__ clamped) {
+    int local = 0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
+         p += (long long)gridDim.x * blockDim.x) {
+        double x, y;
+        load2(pts, p, x, y);
+        Bilin b;
+        local += bilinear_stencil(x, y, gg, b);
+        for (int k = 0; k < m; k++) out[p * m + k] = (G)bilinear_apply(b, vals, m, k);
+    }
+    if (local) atomicAdd(clamped, (unsigned long long)local);
+}
+
+int launch_bilinear(cs_ctx *ctx, int prec, const void *pts, long long np, const void *vals, int m,
+                    const GridGeom &gg, void *out, unsigned long long *clamped) {
+    if (np == 0) return CS_OK;
+    const int B = 256;
+    if (prec == CS_F64)
+        k_bilinear<double, double><<<grid_for(np, B), B, 0, ctx->stream>>>(
+            (const double *)pts, np, (const double *)vals, m, gg, (double *)out, clamped);
+    else
+        k_bilinear<float, float><<<grid_for(np, B), B, 0, ctx->stream>>>(
+            (const float *)pts, np, (const float *)vals, m, gg, (float *)out, clamped);
+    CS_LAUNCH_CHECK();
+    return CS_OK;
+}
+
+// ------------------------------------------------------------------ gradient
+// d1 coefficients (field.py:128-137), each entry value / (2 h) as the
+// reference's lil / scalar division produces them.
+struct D1Coef {
+    double m1, p1;        // interior / periodic: -1/(2h), +1/(2h)
+    double l0, l1, l2;    // neumann row 0: -3, 4, -1 over 2h
+    double r0, r1, r2;    // neumann row n-1 (cols n-3, n-2, n-1): 1, -4, 3 over 2h
+};
+D1Coef make_d1(double h) {
+    const double two_h = 2.0 * h;
+    D1Coef c;
+    c.m1 = -1.0 / two_h;
+    c.p1 = 1.0 / two_h;
+    c.l0 = -3.0 / two_h;
+    c.l1 = 4.0 / two_h;
+    c.l2 = -1.0 / two_h;
+    c.r0 = 1.0 / two_h;
+    c.r1 = -4.0 / two_h;
+    c.r2 = 3.0 / two_h;
+    return c;
+}
+
+template <class G>
+__device__ __forceinline__ double d1_at(const G *__restrict__ c, long long base, long long stride,
+                                        int i, int n, int per, const D1Coef &k) {
+    if (per) {
+        const int im = i == 0 ? n - 1 : i - 1, ip = i == n - 1 ? 0 : i + 1;
+        const double am = dmul(k.m1, (double)c[base + im * stride]);
+        const double ap = dmul(k.p1, (double)c[base + ip * stride]);
+        return im < ip ? dadd(dadd(0.0, am), ap) : dadd(dadd(0.0, ap), am);
+    }
+    if (i == 0)
+        return dadd(dadd(dadd(0.0, dmul(k.l0, (double)c[base])),
+                         dmul(k.l1, (double)c[base + stride])),
+                    dmul(k.l2, (double)c[base + 2 * stride]));
+    if (i == n - 1)
+        return dadd(dadd(dadd(0.0, dmul(k.r0, (double)c[base + (long long)(n - 3) * stride])),
+                         dmul(k.r1, (double)c[base + (long long)(n - 2) * stride])),
+                    dmul(k.r2, (double)c[base + (long long)(n - 1) * stride]));
+    return dadd(dadd(0.0, dmul(k.m1, (double)c[base + (long long)(i - 1) * stride])),
+                dmul(k.p1, (double)c[base + (long long)(i + 1) * stride]));
+}
+
+// grad = (d1x c, d1y c); when st != NULL also the step_field post-checks on
+// c: any non-finite node and the weighted mass of the negative nodes.
+template <class G>
+__global__ void __launch_bounds__(256)
+k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double wcell,
+           G *__restrict__ grad, DevStatus *st) {
+    if (st && st->abort) return;
+    const long long m = (long long)n * n;
+    double neg = 0.0;
+    int bad = 0, anyneg = 0;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+         l += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(l / n), i = (int)(l - (long long)j * n);
+        const double gx = d1_at(c, (long long)j * n, 1, i, n, per, kx);
+        const double gy = d1_at(c, (long long)i, n, j, n, per, ky);
+        store2(grad, l, gx, gy);
+        if (st) {
+            const double v = (double)c[l];
+            if (!isfinite(v)) bad = 1;
+            if (v < 0.0) {
+                double w = wcell;
+                if (!per) {
+                    const double wi = (i == 0 || i == n - 1) ? 0.5 : 1.0;
+                    const double wj = (j == 0 || j == n - 1) ? 0.5 : 1.0;
+                    w = (wj * wi) * wcell;
+                }
+                neg += w * v;
+                anyneg = 1;
+            }
+        }
+    }
+    if (!st) return;
+    // block reduction of the negative mass, one atomic per block
+    __shared__ double s_neg[8];
+    __shared__ int s_flags[8];
+    for (int o = 16; o > 0; o >>= 1) {
+        neg += __shfl_xor_sync(0xffffffffu, neg, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        anyneg |= __shfl_xor_sync(0xffffffffu, anyneg, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_neg[warp] = neg;
+        s_flags[warp] = bad | (anyneg << 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        int f = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            t += s_neg[w];
+            f |= s_flags[w];
+        }
+        if (f & 1) atomicExch(&st->field_bad, 1);
+        if (f & 2) {
+            atomicAdd(&st->neg_mass, t);
+            atomicExch(&st->neg_flag, 1);
+        }
+    }
+}
+
+// Serial epilogue of the field checks of one step.
+__global__ void k_field_finish(DevStatus *st, int step) {
+    if (st->abort) return;
+    if (st->field_bad) {
+        st->key = err_key(0, 0, CS_FIELD_NONFINITE);
+        st->abort = 1;
+        st->step = step;
+    }
+    if (st->neg_flag && st->neg_mass < -1e-12) {
+        if (st->neg_steps == 0) st->first_neg = st->neg_mass;
+        st->neg_steps += 1;
+    }
+    st->neg_flag = 0;
+    st->neg_mass = 0.0;
+}
+
+int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
+                    DevStatus *st, int step) {
+    const long long m = (long long)gg.n * gg.n;
+    const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
+    const double wcell = gg.d0 * gg.d1;
+    const int B = 256;
+    if (prec == CS_F64)
+        k_gradient<double><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
+            (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st);
+    else
+        k_gradient<float><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
+            (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    if (st && step >= 0) {
+        k_field_finish<<<1, 1, 0, ctx->stream>>>(st, step);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    return CS_OK;
+}
+
+// ------------------------------------------------------------------ rhs
+struct RhsCoef {
+    double one_m_dtg, dka, dkb;
+    int has_g, has_a, has_b;
+};
+
+template <class G, class R>
+__global__ void k_rhs(const G *__restrict__ c, const G *__restrict__ ra, const G *__restrict__ rb,
+                      long long m, RhsCoef k, R *__restrict__ rhs, const DevStatus *st) {
+    if (st && st->abort) return;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+         l += (long long)gridDim.x * blockDim.x) {
+        const double cv = (double)c[l];
+        double r = k.has_g ? dmul(cv, k.one_m_dtg) : cv;
+        if (k.has_a) r = dadd(r, dmul(k.dka, (double)ra[l]));
+        if (k.has_b) r = dsub(r, dmul(dmul((double)rb[l], cv), k.dkb));
+        rhs[l] = (R)r;
+    }
+}
+
+// ------------------------------------------------------------------ GEMM
+// C = A * op(B) (row-major n x n fp64), op = transpose when TB; optional
+// element-wise scale by E; output to O.  64x64 tiles, 256 threads, 4x4 per
+// thread, K-step 16 staged through shared memory.
+template <bool TB, class O>
+__global__ void __launch_bounds__(256)
+k_gemm(const double *__restrict__ A, const double *__restrict__ B, const double *__restrict__ E,
+       O *__restrict__ C, int n) {
+    __shared__ double As[16][64 + 1];
+    __shared__ double Bs[16][64 + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < n; k0 += 16) {
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+            const int kk = e & 15, r = e >> 4;
+            const int gr = row0 + r, gk = k0 + kk;
+            As[kk][r] = (gr < n && gk < n) ? A[(long long)gr * n + gk] : 0.0;
+            const int gc = col0 + r;
+            double bv = 0.0;
+            if (gc < n && gk < n) bv = TB ? B[(long long)gc * n + gk] : B[(long long)gk * n + gc];
+            Bs[kk][r] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; kk++) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                a[u] = As[kk][ty + 16 * u];
+                b[u] = Bs[kk][tx + 16 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const int r = row0 + ty + 16 * u, cc = col0 + tx + 16 * v;
+            if (r < n && cc < n) {
+                double val = acc[u][v];
+                if (E) val *= E[(long long)r * n + cc];
+                C[(long long)r * n + cc] = (O)val;
+            }
+        }
+}
+
+template <class O>
+int gemm(cs_ctx *ctx, const double *A, const double *B, bool tb, const double *E, O *C, int n) {
+    dim3 grid((n + 63) / 64, (n + 63) / 64);
+    if (tb) k_gemm<true, O><<<grid, 256, 0, ctx->stream>>>(A, B, E, C, n);
+    else k_gemm<false, O><<<grid, 256, 0, ctx->stream>>>(A, B, E, C, n);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+// ------------------------------------------------------------------ FFT
+template <class CT>
+__global__ void k_mode_scale(CT *__restrict__ spec, int n, const double *__restrict__ lx,
+                             const double *__restrict__ ly, double dtdc, double inv_nn) {
+    const int nh = n / 2 + 1;
+    const long long m = (long long)n * nh;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+         l += (long long)gridDim.x * blockDim.x) {
+        const int ky = (int)(l / nh), kx = (int)(l - (long long)ky * nh);
+        const double s = inv_nn / (1.0 - dtdc * (ly[ky] + lx[kx]));
+        CT v = spec[l];
+        v.x = v.x * s;
+        v.y = v.y * s;
+        spec[l] = v;
+    }
+}
+
+}  // namespace cs
+
+namespace cs {
+
+static int cufft_check(cufftResult r, const char *what) {
+    if (r != CUFFT_SUCCESS) {
+        set_error("cuFFT %s failed (%d)", what, (int)r);
+        return CS_ERR_CUFFT;
+    }
+    return CS_OK;
+}
+
+int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
+                     cs_field_ops **out) {
+    if (!(dt > 0)) {
+        set_error("dt must be positive");
+        return CS_ERR_PARAM;
+    }
+    if (g->n_c < 3) {
+        set_error("n_c must be at least 3");
+        return CS_ERR_PARAM;
+    }
+    auto *ops = new cs_field_ops();
+    ops->ctx = ctx;
+    ops->prec = prec;
+    ops->gg = make_grid_geom(*g);
+    ops->dt = dt;
+    ops->d_c = d_c;
+    const int n = g->n_c;
+    const size_t m = (size_t)n * n;
+    const size_t es = prec == CS_F64 ? 8 : 4;
+    *out = ops;
+    if (d_c * dt == 0.0) {
+        ops->kind = 0;
+        CS_CUDA(cudaMalloc(&ops->rhs, m * es));
+        return CS_OK;
+    }
+    if (!g->periodic) {
+        // DCT-I basis (field.py:190-196): F[k][j] = w_j cos(pi k j / (n-1)),
+        // w = 1 at the ends and 2 inside (scipy dct type 1 of the identity);
+        // its inverse is F / (2 (n-1)).
+        ops->kind = 1;
+        std::vector<double> F(m), Inv(m), E(m), lam_x(n), lam_y(n);
+        const long long period = 2LL * (n - 1);
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++) {
+                const long long kj = ((long long)k * j) % period;
+                const double c = cos(M_PI * (double)kj / (double)(n - 1));
+                const double w = (j == 0 || j == n - 1) ? 1.0 : 2.0;
+                F[(size_t)k * n + j] = w * c;
+                Inv[(size_t)k * n + j] = w * c / (double)period;
+            }
+        for (int k = 0; k < n; k++) {
+            lam_x[k] = (2.0 * cos(M_PI * k / (n - 1)) - 2.0) / (ops->gg.d0 * ops->gg.d0);
+            lam_y[k] = (2.0 * cos(M_PI * k / (n - 1)) - 2.0) / (ops->gg.d1 * ops->gg.d1);
+        }
+        for (int ky = 0; ky < n; ky++)
+            for (int kx = 0; kx < n; kx++)
+                E[(size_t)ky * n + kx] = 1.0 / (1.0 - dt * d_c * (lam_y[ky] + lam_x[kx]));
+        CS_CUDA(cudaMalloc(&ops->F, m * 8));
+        CS_CUDA(cudaMalloc(&ops->Inv, m * 8));
+        CS_CUDA(cudaMalloc(&ops->E, m * 8));
+        CS_CUDA(cudaMalloc(&ops->T1, m * 8));
+        CS_CUDA(cudaMalloc(&ops->T2, m * 8));
+        CS_CUDA(cudaMalloc(&ops->rhs, m * 8));
+        CS_CUDA(cudaMemcpy(ops->F, F.data(), m * 8, cudaMemcpyHostToDevice));
+        CS_CUDA(cudaMemcpy(ops->Inv, Inv.data(), m * 8, cudaMemcpyHostToDevice));
+        CS_CUDA(cudaMemcpy(ops->E, E.data(), m * 8, cudaMemcpyHostToDevice));
+        return CS_OK;
+    }
+    // periodic: eigenvalues (2 cos(2 pi k / n) - 2) / h^2 of the circulant
+    // 1-D Laplacians of field.py:114-125.
+    ops->kind = 2;
+    std::vector<double> lx(n), ly(n);
+    for (int k = 0; k < n; k++) {
+        lx[k] = (2.0 * cos(2.0 * M_PI * k / n) - 2.0) / (ops->gg.d0 * ops->gg.d0);
+        ly[k] = (2.0 * cos(2.0 * M_PI * k / n) - 2.0) / (ops->gg.d1 * ops->gg.d1);
+    }
+    CS_CUDA(cudaMalloc(&ops->lx, n * 8));
+    CS_CUDA(cudaMalloc(&ops->ly, n * 8));
+    CS_CUDA(cudaMemcpy(ops->lx, lx.data(), n * 8, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(ops->ly, ly.data(), n * 8, cudaMemcpyHostToDevice));
+    const size_t nh = (size_t)n / 2 + 1;
+    CS_CUDA(cudaMalloc(&ops->rhs, m * es));
+    CS_CUDA(cudaMalloc(&ops->spec, (size_t)n * nh * 2 * es));
+    CS_TRY(cufft_check(cufftPlan2d(&ops->pf, n, n, prec == CS_F64 ? CUFFT_D2Z : CUFFT_R2C),
+                       "plan fwd"));
+    CS_TRY(cufft_check(cufftPlan2d(&ops->pi, n, n, prec == CS_F64 ? CUFFT_Z2D : CUFFT_C2R),
+                       "plan inv"));
+    ops->have_plans = true;
+    return CS_OK;
+}
+
+void field_ops_destroy(cs_field_ops *ops) {
+    if (!ops) return;
+    if (ops->have_plans) {
+        cufftDestroy(ops->pf);
+        cufftDestroy(ops->pi);
+    }
+    for (void *p : {(void *)ops->F, (void *)ops->Inv, (void *)ops->E, (void *)ops->T1,
+                    (void *)ops->T2, (void *)ops->lx, (void *)ops->ly, ops->rhs, ops->spec})
+        if (p) cudaFree(p);
+    delete ops;
+}
+
+// out = solve(ops->rhs) for the prepared system.  out has the grid dtype.
+int field_solve_rhs(cs_field_ops *ops, void *out) {
+    cs_ctx *ctx = ops->ctx;
+    const int n = ops->gg.n;
+    const size_t m = (size_t)n * n;
+    const size_t es = ops->prec == CS_F64 ? 8 : 4;
+    if (ops->kind == 0) {
+        if (out != ops->rhs)
+            CS_CUDA(cudaMemcpyAsync(out, ops->rhs, m * es, cudaMemcpyDeviceToDevice, ctx->stream));
+        return CS_OK;
+    }
+    if (ops->kind == 1) {
+        // modal = E * (F X F^T); out = Inv modal Inv^T (field.py:166-167)
+        const double *X = (const double *)ops->rhs;
+        CS_TRY(gemm<double>(ctx, ops->F, X, false, nullptr, ops->T1, n));
+        CS_TRY(gemm<double>(ctx, ops->T1, ops->F, true, ops->E, ops->T2, n));
+        CS_TRY(gemm<double>(ctx, ops->Inv, ops->T2, false, nullptr, ops->T1, n));
+        if (ops->prec == CS_F64)
+            CS_TRY(gemm<double>(ctx, ops->T1, ops->Inv, true, nullptr, (double *)out, n));
+        else
+            CS_TRY(gemm<float>(ctx, ops->T1, ops->Inv, true, nullptr, (float *)out, n));
+        return CS_OK;
+    }
+    CS_TRY(cufft_check(cufftSetStream(ops->pf, ctx->stream), "stream"));
+    CS_TRY(cufft_check(cufftSetStream(ops->pi, ctx->stream), "stream"));
+    const double dtdc = ops->dt * ops->d_c;
+    const double inv_nn = 1.0 / ((double)n * (double)n);
+    const int B = 256;
+    const long long ms = (long long)n * (n / 2 + 1);
+    if (ops->prec == CS_F64) {
+        CS_TRY(cufft_check(cufftExecD2Z(ops->pf, (cufftDoubleReal *)ops->rhs,
+                                        (cufftDoubleComplex *)ops->spec),
+                           "D2Z"));
+        k_mode_scale<double2><<<grid_for(ms, B, 148 * 16), B, 0, ctx->stream>>>(
+            (double2 *)ops->spec, n, ops->lx, ops->ly, dtdc, inv_nn);
+        CS_LAUNCH_CHECK();
+        CS_TRY(cufft_check(cufftExecZ2D(ops->pi, (cufftDoubleComplex *)ops->spec,
+                                        (cufftDoubleReal *)out),
+                           "Z2D"));
+    } else {
+        CS_TRY(cufft_check(cufftExecR2C(ops->pf, (cufftReal *)ops->rhs, (cufftComplex *)ops->spec),
+                           "R2C"));
+        k_mode_scale<float2><<<grid_for(ms, B, 148 * 16), B, 0, ctx->stream>>>(
+            (float2 *)ops->spec, n, ops->lx, ops->ly, dtdc, inv_nn);
+        CS_LAUNCH_CHECK();
+        CS_TRY(cufft_check(cufftExecC2R(ops->pi, (cufftComplex *)ops->spec, (cufftReal *)out),
+                           "C2R"));
+    }
+    ctx->launches += 1;  // k_mode_scale (cuFFT's own kernels not counted)
+    return CS_OK;
+}
+
+int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
+              double kb, double gamma, const DevStatus *st) {
+    cs_ctx *ctx = ops->ctx;
+    const double dt = ops->dt;
+    RhsCoef k;
+    k.has_g = gamma != 0.0;
+    k.has_a = ka != 0.0;
+    k.has_b = kb != 0.0;
+    k.one_m_dtg = 1.0 - dt * gamma;
+    k.dka = dt * ka;
+    k.dkb = dt * kb;
+    const long long m = (long long)ops->gg.n * ops->gg.n;
+    const int B = 256;
+    const int G = grid_for(m, B, 148 * 16);
+    if (ops->prec == CS_F64) {
+        k_rhs<double, double><<<G, B, 0, ctx->stream>>>((const double *)c, (const double *)ra,
+                                                        (const double *)rb, m, k,
+                                                        (double *)ops->rhs, st);
+    } else if (ops->kind == 1) {
+        k_rhs<float, double><<<G, B, 0, ctx->stream>>>((const float *)c, (const float *)ra,
+                                                       (const float *)rb, m, k,
+                                                       (double *)ops->rhs, st);
+    } else {
+        k_rhs<float, float><<<G, B, 0, ctx->stream>>>((const float *)c, (const float *)ra,
+                                                      (const float *)rb, m, k,
+                                                      (float *)ops->rhs, st);
+    }
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+// copy an external rhs (grid dtype) into the ops' rhs slot (solve seam)
+int field_load_rhs(cs_field_ops *ops, const void *rhs) {
+    cs_ctx *ctx = ops->ctx;
+    const long long m = (long long)ops->gg.n * ops->gg.n;
+    if (ops->kind == 1 && ops->prec == CS_F32) {
+        RhsCoef k{};  // identity: rhs = c
+        k_rhs<float, double><<<grid_for(m, 256, 148 * 16), 256, 0, ctx->stream>>>(
+            (const float *)rhs, nullptr, nullptr, m, k, (double *)ops->rhs, nullptr);
+        CS_LAUNCH_CHECK();
+        return CS_OK;
+    }
+    const size_t es = ops->prec == CS_F64 ? 8 : 4;
+    CS_CUDA(cudaMemcpyAsync(ops->rhs, rhs, (size_t)m * es, cudaMemcpyDeviceToDevice, ctx->stream));
+    return CS_OK;
+}
+
+}  // namespace cs

@@ -23,8 +23,10 @@
 #include <string.h>
 
 #ifdef __CUDACC__
-#define CS_HD __host__ __device__ __forceinline__
-#define CS_EXP_TABLE_ATTR __device__ __constant__
+#define CS_HD __device__ __forceinline__
+/* plain global memory (L1-resident, 2 KB): lanes index it divergently, which
+ * the constant cache would serialise */
+#define CS_EXP_TABLE_ATTR __device__ static
 #else
 #define CS_HD static inline
 #define CS_EXP_TABLE_ATTR static
@@ -50,8 +52,8 @@ static inline double cs_as_f64_(uint64_t u) { double x; memcpy(&x, &u, 8); retur
 #define CS_SUB(a, b) ((a) - (b))
 #endif
 
-#ifdef __CUDA_ARCH__
-#define CS_EXP_TAB(i) cs_exp_tab[i]
+#ifdef __CUDACC__
+#define CS_EXP_TAB(i) __ldg(&cs_exp_tab[i])
 #else
 #define CS_EXP_TAB(i) cs_exp_tab[i]
 #endif

@@ -1,0 +1,364 @@
+// sim.cu -- the fused per-step pipeline (Realisation._step_inner,
+// engine.py:369-387) run for K steps on the device without host syncs.
+//
+// Per step, in the reference stage order:
+//   field (if active):  zero rho -> deposit -> rhs -> implicit solve -> gradient
+//                       (+ non-finite / negative-mass checks, field.py:229-238)
+//   forces (if soft):   bin (count, scan, scatter, in-cell sort) -> pair sum
+//   update:             bilinear refresh of drift/local_c at the start-of-step
+//                       positions (coupling.py:302-325), EM proposal with
+//                       xi[k] (motion.py:268-282), boundaries with anchor
+//                       bookkeeping and status (motion.py:355-402), commit.
+// The refresh is fused into the update kernel: both read only the particle's
+// own start-of-step position and the freshly updated field, exactly the
+// values the reference's separate refresh stage reads.
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cs {
+
+int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
+                   const GridGeom &gg, int kind, double h, double cutoff,
+                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
+                   bool zero_first);
+int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
+                    DevStatus *st, int step);
+int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
+                     cs_field_ops **out);
+void field_ops_destroy(cs_field_ops *ops);
+int field_solve_rhs(cs_field_ops *ops, void *out);
+int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
+              double kb, double gamma, const DevStatus *st);
+
+struct UpdateArgs {
+    const void *xi;
+    void *pos, *anchor, *next;
+    const uint8_t *type;
+    const double *force;  // (n, 2) or NULL
+    double *drift;        // read when !refresh; written when refresh && store
+    double *local_c;
+    const void *c, *grad;
+    long long n;
+    double amp[2], dt, chi[2];
+    int chi_pinned[2];
+    int refresh, store_samples, store_next;
+    cs_domain dom;
+    GridGeom gg;
+};
+
+template <class P>
+__global__ void __launch_bounds__(256) k_update(UpdateArgs a, DevStatus *st, int step) {
+    if (st->abort) return;
+    const P *xi = (const P *)a.xi;
+    P *pos = (P *)a.pos;
+    P *anchor = (P *)a.anchor;
+    int clamped = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int t = a.type ? (a.type[i] ? 1 : 0) : 0;
+        double x, y;
+        load2(pos, i, x, y);
+        double dr0 = 0.0, dr1 = 0.0;
+        if (a.refresh) {
+            Bilin b;
+            clamped += 2 * bilinear_stencil(x, y, a.gg, b);
+            const P *g = (const P *)a.grad;
+            dr0 = bilinear_apply(b, g, 2, 0);
+            dr1 = bilinear_apply(b, g, 2, 1);
+            if (a.chi_pinned[t]) {
+                dr0 = 0.0;
+                dr1 = 0.0;
+            } else if (a.chi[t] != 1.0) {
+                dr0 = dmul(dr0, a.chi[t]);
+                dr1 = dmul(dr1, a.chi[t]);
+            }
+            if (a.store_samples) {
+                a.local_c[i] = bilinear_apply(b, (const P *)a.c, 1, 0);
+                reinterpret_cast<double2 *>(a.drift)[i] = make_double2(dr0, dr1);
+            }
+        } else if (a.drift) {
+            const double2 d = reinterpret_cast<const double2 *>(a.drift)[i];
+            dr0 = d.x;
+            dr1 = d.y;
+        }
+        double f0 = 0.0, f1 = 0.0;
+        if (a.force) {
+            const double2 f = reinterpret_cast<const double2 *>(a.force)[i];
+            f0 = f.x;
+            f1 = f.y;
+        }
+        double x0, x1;
+        load2(xi, i, x0, x1);
+        const double amp = a.amp[t];
+        double v[2];
+        v[0] = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(dr0, a.dt)), dmul(f0, a.dt));
+        v[1] = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(dr1, a.dt)), dmul(f1, a.dt));
+        if (!(isfinite(v[0]) && isfinite(v[1]))) {
+            atomicMin(&st->key, err_key(0, i, CS_NONFINITE));
+            st->abort = 1;
+            st->step = step;
+            if (a.next) store2((P *)a.next, i, v[0], v[1]);
+            continue;
+        }
+        double an[2];
+        load2(anchor, i, an[0], an[1]);
+        bool ok = true;
+        for (int ax = 0; ax < 2; ax++) {
+            const double raw = v[ax];
+            const int code = boundary_axis(v[ax], an[ax], a.dom.lo[ax], a.dom.hi[ax],
+                                           a.dom.periodic[ax]);
+            if (code) {
+                atomicMin(&st->key, err_key(1 + ax, i, code));
+                st->abort = 1;
+                st->step = step;
+                v[ax] = raw;
+                ok = false;
+                break;
+            }
+        }
+        if (a.store_next) store2((P *)a.next, i, v[0], v[1]);
+        if (!ok) continue;
+        store2(pos, i, v[0], v[1]);
+        store2(anchor, i, an[0], an[1]);
+    }
+    if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
+}
+
+}  // namespace cs
+
+struct cs_sim {
+    cs_ctx *ctx = nullptr;
+    cs_sim_params p{};
+    cs::BinGeom geom{};
+    cs::PairTab pt{};
+    cs::GridGeom gg{};
+    cs_field_ops *ops = nullptr;
+    int steps_done = 0;
+    int64_t last_launches = 0;
+    unsigned char bits[3] = {0, 0, 0};
+    cs::Buf status;  // this simulation's DevStatus
+    cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
+    // optional per-stage device timing (CUDA events on the step stream)
+    int profiling = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    size_t ev_next = 0;
+    double stage_ms[CS_N_STAGES] = {};
+    cudaEvent_t next_event() {
+        if (ev_next == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_next++];
+    }
+};
+
+namespace cs {
+
+int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
+    if (p->n < 0 || p->n >= (1LL << 31) - 1) {
+        set_error("particle count out of range");
+        return CS_ERR_PARAM;
+    }
+    auto *sim = new cs_sim();
+    sim->ctx = ctx;
+    sim->p = *p;
+    *out = sim;
+    if (p->interaction == 1) {
+        sim->geom = make_geom(p->domain, p->pairs.cell_cutoff);
+        sim->pt = make_pairtab(p->pairs);
+        CS_TRY(ctx->force.ensure(sizeof(double) * 2 * (size_t)(p->n > 0 ? p->n : 1)));
+    }
+    if (p->field_active || p->refresh_active) sim->gg = make_grid_geom(p->grid);
+    for (int t = 0; t < 2; t++)
+        sim->bits[t] = (unsigned char)((p->secretes[t] ? 1 : 0) | (p->consumes[t] ? 2 : 0));
+    sim->bits[2] = 0;
+    if (p->field_active) CS_TRY(field_ops_create(ctx, p->prec, &p->grid, p->d_c, p->dt, &sim->ops));
+    CS_TRY(sim->status.ensure(sizeof(DevStatus)));
+    DevStatus init{};
+    init.key = ~0ULL;
+    init.step = -1;
+    CS_CUDA(cudaMemcpy(sim->status.p, &init, sizeof(init), cudaMemcpyHostToDevice));
+    return CS_OK;
+}
+
+void sim_destroy(cs_sim *sim) {
+    if (!sim) return;
+    field_ops_destroy(sim->ops);
+    sim->status.release();
+    delete sim;
+}
+
+int sim_reset_status(cs_sim *sim) {
+    DevStatus init{};
+    init.key = ~0ULL;
+    init.step = -1;
+    CS_CUDA(cudaMemcpyAsync(sim->status.p, &init, sizeof(init), cudaMemcpyHostToDevice,
+                            sim->ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(sim->ctx->stream));
+    sim->steps_done = 0;
+    return CS_OK;
+}
+
+// Stage timing: a begin event before the stage's first launch and an end
+// event after its last; durations are summed when the caller asks.
+struct StageMark {
+    cs_sim *sim;
+    int stage;
+    cudaEvent_t b = nullptr;
+    StageMark(cs_sim *s, int st) : sim(s), stage(st) {
+        if (sim->profiling) {
+            b = sim->next_event();
+            cudaEventRecord(b, sim->ctx->stream);
+        }
+    }
+    ~StageMark() {
+        if (sim->profiling) {
+            cudaEvent_t e = sim->next_event();
+            cudaEventRecord(e, sim->ctx->stream);
+            sim->marks.push_back({stage, {b, e}});
+        }
+    }
+};
+
+int sim_collect_stage_times(cs_sim *sim) {
+    if (sim->marks.empty()) return CS_OK;
+    CS_CUDA(cudaStreamSynchronize(sim->ctx->stream));
+    for (auto &m : sim->marks) {
+        float ms = 0.f;
+        CS_CUDA(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
+        sim->stage_ms[m.first] += ms;
+    }
+    sim->marks.clear();
+    sim->ev_next = 0;
+    return CS_OK;
+}
+
+int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k) {
+    cs_ctx *ctx = sim->ctx;
+    const cs_sim_params &p = sim->p;
+    DevStatus *st = sim->dstat();
+    const size_t es = p.prec == CS_F64 ? 8 : 4;
+    const long long n = p.n;
+    const int64_t l0 = ctx->launches;
+    for (int kk = 0; kk < k; kk++) {
+        const int step = sim->steps_done + kk;
+        const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
+        if (p.field_active) {
+            {
+                StageMark m(sim, CS_STAGE_DEPOSIT);
+                CS_TRY(launch_deposit(ctx, p.prec, s->pos, s->type, n, sim->gg, p.deposit_kind,
+                                      p.kernel_h, p.kernel_cutoff, sim->bits, s->rho_a, s->rho_b,
+                                      st, true));
+            }
+            {
+                StageMark m(sim, CS_STAGE_SOLVE);
+                CS_TRY(field_rhs(sim->ops, s->c, s->rho_a, s->rho_b, p.k_alpha, p.k_beta,
+                                 p.gamma, st));
+                CS_TRY(field_solve_rhs(sim->ops, s->c));
+            }
+            {
+                StageMark m(sim, CS_STAGE_GRADIENT);
+                CS_TRY(launch_gradient(ctx, p.prec, s->c, sim->gg, s->grad, st, step));
+            }
+        }
+        const double *force = nullptr;
+        if (p.interaction == 1) {
+            {
+                StageMark m(sim, CS_STAGE_BIN);
+                CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom));
+            }
+            StageMark m(sim, CS_STAGE_FORCE);
+            CS_TRY(launch_soft_forces(ctx, p.prec, s->pos, s->type, n, sim->geom, sim->pt,
+                                      ctx->force.as<double>(), st));
+            force = ctx->force.as<double>();
+        }
+        UpdateArgs a;
+        a.xi = xik;
+        a.pos = s->pos;
+        a.anchor = s->anchor;
+        a.next = s->next_pos;
+        a.type = s->type;
+        a.force = force;
+        a.drift = s->drift;
+        a.local_c = s->local_c;
+        a.c = s->c;
+        a.grad = s->grad;
+        a.n = n;
+        a.amp[0] = p.amp[0];
+        a.amp[1] = p.amp[1];
+        a.dt = p.dt;
+        a.chi[0] = p.chi[0];
+        a.chi[1] = p.chi[1];
+        a.chi_pinned[0] = p.chi_pinned[0];
+        a.chi_pinned[1] = p.chi_pinned[1];
+        a.refresh = p.refresh_active;
+        a.store_samples = p.store_samples && s->drift && s->local_c;
+        a.store_next = p.store_next && s->next_pos;
+        a.dom = p.domain;
+        a.gg = sim->gg;
+        if (n > 0) {
+            StageMark m(sim, CS_STAGE_UPDATE);
+            const int B = 256;
+            if (p.prec == CS_F64)
+                k_update<double><<<grid_for(n, B), B, 0, ctx->stream>>>(a, st, step);
+            else
+                k_update<float><<<grid_for(n, B), B, 0, ctx->stream>>>(a, st, step);
+            CS_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+    }
+    sim->steps_done += k;
+    sim->last_launches = ctx->launches - l0;
+    return CS_OK;
+}
+
+int sim_status(cs_sim *sim, cs_status *out) {
+    cs_ctx *ctx = sim->ctx;
+    DevStatus d;
+    CS_CUDA(cudaMemcpyAsync(&d, sim->status.p, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    out->code = CS_OK;
+    out->step = -1;
+    out->particle = -1;
+    out->axis = -1;
+    if (d.key != ~0ULL) {
+        const int rank = (int)(d.key >> 60);
+        out->code = (int)(d.key & 7ULL);
+        out->particle = (long long)((d.key >> 3) & ((1ULL << 57) - 1));
+        out->axis = rank >= 1 ? rank - 1 : 0;
+        out->step = d.step;
+        if (out->code == CS_FIELD_NONFINITE) {
+            out->particle = -1;
+            out->axis = -1;
+        }
+    }
+    out->clamped = d.clamped;
+    out->neg_mass_steps = d.neg_steps;
+    out->first_neg_mass = d.first_neg;
+    out->steps_done = sim->steps_done;
+    return CS_OK;
+}
+
+}  // namespace cs
+
+extern "C" int64_t cs_sim_launches(cs_sim *sim) { return sim ? sim->last_launches : 0; }
+
+extern "C" void *cs_sim_status_device(cs_sim *sim) { return sim ? sim->status.p : nullptr; }
+extern "C" int64_t cs_sim_status_bytes(void) { return (int64_t)sizeof(cs::DevStatus); }
+
+extern "C" int cs_sim_set_profiling(cs_sim *sim, int32_t on) {
+    CS_TRY(cs::sim_collect_stage_times(sim));
+    sim->profiling = on ? 1 : 0;
+    for (double &v : sim->stage_ms) v = 0.0;
+    return CS_OK;
+}
+
+extern "C" int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n) {
+    CS_TRY(cs::sim_collect_stage_times(sim));
+    for (int i = 0; i < n && i < CS_N_STAGES; i++) ms[i] = sim->stage_ms[i];
+    return CS_OK;
+}

@@ -1,0 +1,113 @@
+"""CPU-only checks of the host side: the C-ABI library loads and exports
+every symbol include/chemo_b200.h declares, parameter objects validate like
+the reference's, and the pair-table / status plumbing is right.  No compute
+call is made (there is no GPU here)."""
+
+import ctypes
+import math
+import re
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1805_11007_b200 as cs
+from paper_1805_11007_b200 import _native as N
+
+from conftest import ROOT
+
+
+def _declared():
+    src = open(f"{ROOT}/include/chemo_b200.h").read()
+    return set(re.findall(r"^\s*(?:int|int64_t|void \*|const char \*)\s*\**\s*(cs_\w+)\(",
+                          src, re.M))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load_library()
+    decl = _declared()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert {n for n, _, _ in N.SIGNATURES} == decl
+    assert lib.cs_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    # offsets that the C side relies on (x86-64 SysV)
+    assert ctypes.sizeof(N.Domain_t) == 40
+    assert ctypes.sizeof(N.PairParams_t) == 72
+    assert ctypes.sizeof(N.Grid_t) == 40
+    assert N.SimParams_t.store_next.offset + 4 <= ctypes.sizeof(N.SimParams_t)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", N.SO_PATH], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_compute_calls_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    pop = cs.Population(ids=np.arange(2), positions=np.zeros((2, 2)),
+                        next_positions=np.zeros((2, 2)), species=np.zeros(2, np.uint8),
+                        drift=np.zeros((2, 2)), local_concentration=np.zeros(2),
+                        start_anchor=np.zeros((2, 2)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        cs.soft_forces(pop, cs.Domain.square(1.0), cs.MotionParams(dt=1e-7))
+
+
+def test_pair_table_reduces_to_homogeneous_bitwise():
+    eps = 0.005
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        homo = cs.MotionParams(epsilon=eps, cutoff=2.0 * eps, dt=1e-9)
+        het = cs.MotionParams(epsilon=eps, cutoff=2.0 * eps, dt=1e-9, radius_alpha=eps,
+                              radius_beta=eps)
+    assert homo.pair_table() == het.pair_table()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        het = cs.MotionParams(epsilon=eps, dt=1e-9, radius_alpha=0.005, radius_beta=0.01)
+    e, c, cell = het.pair_table()
+    assert e == [0.005, 0.0075, 0.0075, 0.01]
+    assert c == [0.01, 0.015, 0.015, 0.02] and cell == 0.02
+
+
+def test_simconfig_matches_reference_defaults_and_validation():
+    c = cs.SimConfig.preset("fig1")
+    assert c.dt == pytest.approx((0.23 * 0.02) ** 2 / 4.0, rel=1e-15)
+    assert c.n_steps == 9452
+    assert c.motion_params().cutoff == 0.1
+    with pytest.raises(ValueError, match="unknown experiment"):
+        cs.SimConfig(experiment="warp")
+    with pytest.raises(ValueError, match="at least one particle"):
+        cs.SimConfig(n_alpha_0=0, n_beta_0=0)
+    with pytest.raises(ValueError, match="precision"):
+        cs.SimConfig(precision="fp16", r_alpha=0.0)
+    with pytest.warns(UserWarning, match="destabilise"):
+        cs.SimConfig(n_alpha_0=5, n_beta_0=5, gamma=200.0, dt=0.01, r_alpha=0.0,
+                     interaction="none", n_c=11)
+
+
+def test_sim_params_struct_amplitudes_match_numpy():
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        mp = cs.MotionParams(d_alpha=1.0, d_beta=0.5, epsilon=0.005, cutoff=0.01, dt=1e-5)
+    p = cs.sim_params_struct(n=10, prec=N.CS_F64, domain=cs.Domain.square(1.0), motion=mp,
+                             dt=1e-5, field_active=False, refresh_active=False, grid=None,
+                             fparams=None, kernel=None, secretes=(1, 0), consumes=(0, 1),
+                             chi=(0.0, 1.0), chi_pinned=(1, 0), store_samples=0, store_next=0)
+    amp = np.sqrt(2.0 * np.array([1.0, 0.5]) * 1e-5)
+    assert p.amp[0] == amp[0] and p.amp[1] == amp[1]
+    assert p.pairs.cell_cutoff == 0.01
+
+
+def test_clustered_positions_wrap_into_box():
+    dom = cs.Domain.square(1.0, periodic=True)
+    pos = cs.clustered_positions(100000, dom, np.random.default_rng(0))
+    assert np.all(pos >= -0.5) and np.all(pos < 0.5)

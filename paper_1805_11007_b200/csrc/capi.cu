@@ -314,9 +314,10 @@ int cs_field_step(cs_field_ops *ops, void *c, const void *rho_a, const void *rho
     const size_t es = ops->prec == CS_F64 ? 8 : 4;
     CS_TRY(field_rhs(ops, c, rho_a, rho_b, k_alpha, k_beta, gamma, nullptr));
     // solve into scratch so a non-finite result leaves c untouched
-    CS_TRY(ctx->tmp.ensure(m * es * 3 + 64));
+    const size_t off = (m * es + 255) & ~(size_t)255;  // 256-B aligned sub-buffers
+    CS_TRY(ctx->tmp.ensure(off + 2 * m * es + 256));
     void *cn = ctx->tmp.p;
-    void *grad = (char *)ctx->tmp.p + m * es;
+    void *grad = (char *)ctx->tmp.p + off;
     CS_TRY(field_solve_rhs(ops, cn));
     DevStatus *st;
     CS_TRY(local_status(ctx, &st));

@@ -359,6 +359,8 @@ def main():
         for k in range(K):
             sim.step(xi[(W + k) % blocks], 1)
             launches += sim.launches()
+        sim.export_state()  # the job's result back in the caller's (id-ordered) arrays
+        launches += 1 if sim.engine == "sorted" else 0
         end.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -425,6 +427,7 @@ def main():
             "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s",
                               "frac": step_gbs / peak, "algorithmic_bytes_per_step": ab["total"]},
             "stage_ms": {k: round(v, 4) for k, v in stages.items()},
+            "engine": sim.engine,
             "clocks": clocks.summary(),
             "gpu_launches": launches,
             "e2e": e2e,

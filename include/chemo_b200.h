@@ -176,7 +176,17 @@ typedef struct {
     int32_t chi_pinned[2];   /* drift of type t is pinned to zero */
     int32_t store_samples;   /* write drift / local_c every step */
     int32_t store_next;      /* write next_pos every step */
+    int32_t engine;          /* CS_ENGINE_AUTO / _DIRECT / _SORTED */
 } cs_sim_params;
+
+/* Engines.  DIRECT keeps the reference layout (rows in id order) and
+ * supports every option.  SORTED (fp32 storage only) keeps cell-sorted
+ * particle records inside the library: the caller's pos/anchor/rho arrays
+ * are read on the first step (or cs_sim_import) and written back only by
+ * cs_sim_export; drift/local_c/next_pos are not stored per step.  AUTO picks
+ * SORTED for fp32 runs that need none of the per-step stores and whose cell
+ * occupancy is low (<= 4 per cell), DIRECT otherwise. */
+enum cs_engine { CS_ENGINE_AUTO = 0, CS_ENGINE_DIRECT = 1, CS_ENGINE_SORTED = 2 };
 
 typedef struct {
     void *pos;               /* (n, 2) prec, in/out */
@@ -212,6 +222,13 @@ int cs_sim_step(cs_sim *sim, const cs_sim_state *st, const void *xi,
 /* Synchronise and read the status accumulated since the last reset. */
 int cs_sim_status(cs_sim *sim, cs_status *out);
 int cs_sim_reset_status(cs_sim *sim);
+/* Engine in use (CS_ENGINE_DIRECT or CS_ENGINE_SORTED). */
+int cs_sim_engine(cs_sim *sim);
+/* SORTED engine: (re)load the internal state from the caller's arrays /
+ * write it back (positions, anchors, deposited densities).  No-ops for
+ * DIRECT.  Both are enqueued on the context stream. */
+int cs_sim_import(cs_sim *sim, const cs_sim_state *st);
+int cs_sim_export(cs_sim *sim, const cs_sim_state *st);
 /* Launch count of the most recent cs_sim_step call (kernels of this
  * library; cuFFT's internal kernels are not counted). */
 int64_t cs_sim_launches(cs_sim *sim);

@@ -36,8 +36,13 @@ class OracleSim:
     def __init__(self, pos, types, *, lo, hi, periodic, dt, diffusion,
                  interaction="soft", eps_tab=None, cut_tab=None,
                  cell_cutoff=None, chi=(0.0, 1.0), chi_pinned=(True, False),
-                 field=None, refresh_active=None, fp32=False, nthreads=1):
+                 field=None, refresh_active=None, fp32=False, nthreads=1,
+                 anchor_mode="round"):
         self.fp32 = bool(fp32)
+        # fp32 anchors: "round" = rounded to binary32 after every step (the
+        # direct engine's storage); "wraps" = start - k L kept exactly and
+        # rounded only when read (the sorted engine's wrap counters)
+        self.anchor_mode = anchor_mode
         self.pos = np.array(pos, dtype=np.float64).reshape(-1, 2)
         if self.fp32:
             self.pos = self.pos.astype(np.float32).astype(np.float64)
@@ -168,7 +173,8 @@ class OracleSim:
                                   f"particle {i} axis {ax}")
         if self.fp32:
             nxt = nxt.astype(np.float32).astype(np.float64)
-            self.anchor = self.anchor.astype(np.float32).astype(np.float64)
+            if self.anchor_mode == "round":
+                self.anchor = self.anchor.astype(np.float32).astype(np.float64)
         self.pos = nxt
         self._tick("boundaries", t0)
         self.force = force

@@ -20,6 +20,7 @@ SO_PATH = os.path.join(HERE, "_build", "libchemo_b200.so")
 CS_OK, CS_NONFINITE, CS_OVERSHOOT, CS_UNSETTLED, CS_FIELD_NONFINITE = 0, 1, 2, 3, 4
 CS_F64, CS_F32 = 0, 1
 CS_GAUSSIAN, CS_CIC = 0, 1
+CS_ENGINE_AUTO, CS_ENGINE_DIRECT, CS_ENGINE_SORTED = 0, 1, 2
 
 C_i32, C_i64, C_f64, C_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -44,7 +45,7 @@ class SimParams_t(ctypes.Structure):
                 ("gamma", C_f64), ("deposit_kind", C_i32), ("kernel_h", C_f64),
                 ("kernel_cutoff", C_f64), ("secretes", C_i32 * 2), ("consumes", C_i32 * 2),
                 ("chi", C_f64 * 2), ("chi_pinned", C_i32 * 2), ("store_samples", C_i32),
-                ("store_next", C_i32)]
+                ("store_next", C_i32), ("engine", C_i32)]
 
 
 class SimState_t(ctypes.Structure):
@@ -95,6 +96,9 @@ SIGNATURES = [
     ("cs_sim_launches", C_i64, [C_p]),
     ("cs_sim_set_profiling", C_i32, [C_p, C_i32]),
     ("cs_sim_stage_times", C_i32, [C_p, C_p, C_i32]),
+    ("cs_sim_engine", C_i32, [C_p]),
+    ("cs_sim_import", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
+    ("cs_sim_export", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
     ("cs_sim_status_device", C_p, [C_p]),
     ("cs_sim_status_bytes", C_i64, []),
 ]

@@ -15,6 +15,7 @@
 //                  handful of particles, insertion sort is exact and cheap)
 // The result is bit-identical to the reference's `order`/`starts`.
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace cs {
 
@@ -66,96 +67,6 @@ __global__ void k_seg_sort(int *__restrict__ order, const int *__restrict__ skey
 }
 
 // ------------------------------------------------------------------ scan
-// Single-pass exclusive scan with decoupled look-back.  Tile = BLOCK*ITEMS
-// consecutive counts; each tile publishes (status, value) packed in one
-// 64-bit word: status 1 = local aggregate, 2 = inclusive prefix.
-constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_ITEMS = 8;
-constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(SCAN_BLOCK)
-k_scan(const int *__restrict__ in, int *__restrict__ out, long long n,
-       unsigned long long *__restrict__ flags, unsigned int *__restrict__ tile_counter) {
-    __shared__ unsigned int s_tile;
-    __shared__ int s_warp[SCAN_BLOCK / 32];
-    __shared__ int s_prefix;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const long long tile = s_tile;
-    const long long base = tile * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
-    int v[SCAN_ITEMS];
-    int tsum = 0;
-    if (base + SCAN_ITEMS <= n) {
-        const int4 a = *reinterpret_cast<const int4 *>(in + base);
-        const int4 b = *reinterpret_cast<const int4 *>(in + base + 4);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
-#pragma unroll
-        for (int k = 0; k < SCAN_ITEMS; k++) v[k] = (base + k < n) ? in[base + k] : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; k++) tsum += v[k];
-    // block exclusive scan of thread sums
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        int w = lane < SCAN_BLOCK / 32 ? s_warp[lane] : 0;
-        int wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += y;
-        }
-        if (lane < SCAN_BLOCK / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
-        if (lane == SCAN_BLOCK / 32 - 1) {
-            const int total = wi;
-            // publish and look back (single thread)
-            int prefix = 0;
-            if (tile == 0) {
-                st_release(&flags[0], (2ULL << 32) | (unsigned)total);
-            } else {
-                st_release(&flags[tile], (1ULL << 32) | (unsigned)total);
-                long long j = tile - 1;
-                while (true) {
-                    const unsigned long long f = ld_acquire(&flags[j]);
-                    const unsigned s = (unsigned)(f >> 32);
-                    if (s == 0) continue;
-                    prefix += (int)(unsigned)(f & 0xffffffffu);
-                    if (s == 2) break;
-                    j--;
-                }
-                st_release(&flags[tile], (2ULL << 32) | (unsigned)(prefix + total));
-            }
-            s_prefix = prefix;
-        }
-    }
-    __syncthreads();
-    int run = s_prefix + s_warp[warp] + (incl - tsum);
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; k++) {
-        if (base + k < n) out[base + k] = run;
-        run += v[k];
-    }
-    if (base < n && base + SCAN_ITEMS >= n) out[n] = run;  // starts[nflat] = total
-}
-
 int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n) {
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     CS_TRY(ctx->tile_flags.ensure(sizeof(unsigned long long) * (tiles + 2)));

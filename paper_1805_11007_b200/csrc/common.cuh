@@ -76,6 +76,8 @@ __host__ __device__ inline unsigned long long err_key(int rank, long long i, int
 
 }  // namespace cs
 
+struct cs_fast;
+
 struct cs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;

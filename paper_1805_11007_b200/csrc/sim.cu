@@ -32,6 +32,27 @@ int field_solve_rhs(cs_field_ops *ops, void *out);
 int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
               double kb, double gamma, const DevStatus *st);
 
+struct FastStepCfg {
+    const cs_sim_params *p;
+    BinGeom g;
+    PairTab pt;
+    GridGeom gg;
+    cs_field_ops *ops;
+    unsigned char bits[3];
+};
+int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg);
+void fast_destroy(cs_fast *f);
+int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
+                const BinGeom &g, const GridGeom &gg, const unsigned char bits[3]);
+int fast_export(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
+                const GridGeom &gg);
+int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
+               DevStatus *st, int step);
+int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
+                   const void *xi, DevStatus *st, int step);
+int fast_resort(cs_ctx *ctx, cs_fast *f, long long n);
+bool fast_imported(const cs_fast *f);
+
 struct UpdateArgs {
     const void *xi;
     void *pos, *anchor, *next;
@@ -138,6 +159,8 @@ struct cs_sim {
     int steps_done = 0;
     int64_t last_launches = 0;
     unsigned char bits[3] = {0, 0, 0};
+    int engine = CS_ENGINE_DIRECT;
+    cs_fast *fast = nullptr;
     cs::Buf status;  // this simulation's DevStatus
     cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
     // optional per-stage device timing (CUDA events on the step stream)
@@ -177,6 +200,25 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
         sim->bits[t] = (unsigned char)((p->secretes[t] ? 1 : 0) | (p->consumes[t] ? 2 : 0));
     sim->bits[2] = 0;
     if (p->field_active) CS_TRY(field_ops_create(ctx, p->prec, &p->grid, p->d_c, p->dt, &sim->ops));
+    // engine selection
+    {
+        const BinGeom g = make_geom(p->domain, p->interaction == 1 ? p->pairs.cell_cutoff : 1e300);
+        const double per_cell = (double)p->n / ((double)g.n0 * (double)g.n1);
+        bool want_sorted = p->engine == CS_ENGINE_SORTED ||
+                           (p->engine == CS_ENGINE_AUTO && p->prec == CS_F32 &&
+                            !p->store_samples && !p->store_next && per_cell <= 4.0);
+        if (want_sorted && p->prec != CS_F32) {
+            set_error("the sorted engine stores binary32 records (prec must be CS_F32)");
+            return CS_ERR_PARAM;
+        }
+        if (want_sorted) {
+            sim->engine = CS_ENGINE_SORTED;
+            sim->geom = g;
+            sim->pt = make_pairtab(p->pairs);
+            const GridGeom gg = make_grid_geom(p->grid);
+            CS_TRY(fast_create(&sim->fast, p->n, g, p->field_active ? &gg : nullptr));
+        }
+    }
     CS_TRY(sim->status.ensure(sizeof(DevStatus)));
     DevStatus init{};
     init.key = ~0ULL;
@@ -188,6 +230,7 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
 void sim_destroy(cs_sim *sim) {
     if (!sim) return;
     field_ops_destroy(sim->ops);
+    fast_destroy(sim->fast);
     sim->status.release();
     delete sim;
 }
@@ -244,6 +287,42 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
     const size_t es = p.prec == CS_F64 ? 8 : 4;
     const long long n = p.n;
     const int64_t l0 = ctx->launches;
+    if (sim->engine == CS_ENGINE_SORTED) {
+        FastStepCfg c;
+        c.p = &p;
+        c.g = sim->geom;
+        c.pt = sim->pt;
+        c.gg = sim->gg;
+        c.ops = sim->ops;
+        c.bits[0] = sim->bits[0];
+        c.bits[1] = sim->bits[1];
+        c.bits[2] = 0;
+        if (!fast_imported(sim->fast)) {
+            StageMark m(sim, CS_STAGE_BIN);
+            CS_TRY(fast_import(ctx, sim->fast, p, s, sim->geom, sim->gg, sim->bits));
+        }
+        for (int kk = 0; kk < k; kk++) {
+            const int step = sim->steps_done + kk;
+            const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
+            if (p.field_active) {
+                {
+                    StageMark m(sim, CS_STAGE_SOLVE);
+                    CS_TRY(fast_field(ctx, sim->fast, c, s, st, step));
+                }
+                StageMark m(sim, CS_STAGE_GRADIENT);
+                CS_TRY(launch_gradient(ctx, p.prec, s->c, sim->gg, s->grad, st, step));
+            }
+            {
+                StageMark m(sim, CS_STAGE_FORCE);
+                CS_TRY(fast_particles(ctx, sim->fast, c, s, xik, st, step));
+            }
+            StageMark m(sim, CS_STAGE_BIN);
+            CS_TRY(fast_resort(ctx, sim->fast, n));
+        }
+        sim->steps_done += k;
+        sim->last_launches = ctx->launches - l0;
+        return CS_OK;
+    }
     for (int kk = 0; kk < k; kk++) {
         const int step = sim->steps_done + kk;
         const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
@@ -346,6 +425,18 @@ int sim_status(cs_sim *sim, cs_status *out) {
 }  // namespace cs
 
 extern "C" int64_t cs_sim_launches(cs_sim *sim) { return sim ? sim->last_launches : 0; }
+
+extern "C" int cs_sim_engine(cs_sim *sim) { return sim->engine; }
+
+extern "C" int cs_sim_import(cs_sim *sim, const cs_sim_state *st) {
+    if (sim->engine != CS_ENGINE_SORTED) return CS_OK;
+    return cs::fast_import(sim->ctx, sim->fast, sim->p, st, sim->geom, sim->gg, sim->bits);
+}
+
+extern "C" int cs_sim_export(cs_sim *sim, const cs_sim_state *st) {
+    if (sim->engine != CS_ENGINE_SORTED) return CS_OK;
+    return cs::fast_export(sim->ctx, sim->fast, sim->p, st, sim->gg);
+}
 
 extern "C" void *cs_sim_status_device(cs_sim *sim) { return sim ? sim->status.p : nullptr; }
 extern "C" int64_t cs_sim_status_bytes(void) { return (int64_t)sizeof(cs::DevStatus); }

@@ -112,6 +112,7 @@ class SimConfig:
     initial_positions: str = "default"
     n_clusters: int = 64
     cluster_sigma: float = 0.02
+    engine: str = "auto"            # auto | direct | sorted (fp32 only)
 
     def __post_init__(self):
         if self.experiment not in EXPERIMENTS:
@@ -158,6 +159,10 @@ class SimConfig:
             raise ValueError(f"unknown alpha_init {self.alpha_init!r}")
         if self.initial_positions not in ("default", "clusters"):
             raise ValueError(f"unknown initial_positions {self.initial_positions!r}")
+        if self.engine not in ("auto", "direct", "sorted"):
+            raise ValueError(f"unknown engine {self.engine!r}")
+        if self.engine == "sorted" and self.precision != "fp32":
+            raise ValueError("the sorted engine needs precision='fp32'")
         self.motion_params()
         self.field_params()
         self.kernel()
@@ -253,7 +258,7 @@ class Observables:
 def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, field_active,
                       refresh_active, grid: Grid | None, fparams: FieldParams | None,
                       kernel: Kernel | None, secretes, consumes, chi, chi_pinned,
-                      store_samples, store_next) -> N.SimParams_t:
+                      store_samples, store_next, engine: str = "auto") -> N.SimParams_t:
     p = N.SimParams_t()
     p.n = int(n)
     p.prec = prec
@@ -285,6 +290,8 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
         p.chi_pinned[t] = int(bool(chi_pinned[t]))
     p.store_samples = int(bool(store_samples))
     p.store_next = int(bool(store_next))
+    p.engine = {"auto": N.CS_ENGINE_AUTO, "direct": N.CS_ENGINE_DIRECT,
+                "sorted": N.CS_ENGINE_SORTED}[engine]
     return p
 
 
@@ -326,6 +333,20 @@ class DeviceSim:
         st = N.Status_t()
         N.check(N.load_library().cs_sim_status(self._h, ctypes.byref(st)), "cs_sim_status")
         return st
+
+    @property
+    def engine(self) -> str:
+        e = int(N.load_library().cs_sim_engine(self._h))
+        return "sorted" if e == N.CS_ENGINE_SORTED else "direct"
+
+    def import_state(self) -> None:
+        """Reload the engine's internal state from the state tensors."""
+        N.check(N.load_library().cs_sim_import(self._h, ctypes.byref(self._st)), "cs_sim_import")
+
+    def export_state(self) -> None:
+        """Write the engine's internal state back into the state tensors
+        (sorted engine; a no-op for the direct engine)."""
+        N.check(N.load_library().cs_sim_export(self._h, ctypes.byref(self._st)), "cs_sim_export")
 
     def launches(self) -> int:
         return int(N.load_library().cs_sim_launches(self._h))
@@ -423,13 +444,17 @@ class Realisation:
         self._chi_pinned = (chi_alpha is None, False)
         if self.refresh_active:
             self._initial_refresh()
+        # fp64 keeps the reference's per-step drift / local_c / next_positions
+        # stores; fp32 runs drop them so the sorted engine can be used
+        self._stores = config.precision == "fp64" or config.engine == "direct"
         params = sim_params_struct(
             n=len(host), prec=N.prec_code(dt_), domain=self.domain, motion=self.motion,
             dt=self.dt, field_active=self.field_active, refresh_active=self.refresh_active,
             grid=self.grid, fparams=fp, kernel=self.kernel,
             secretes=(config.secrete_alpha, config.secrete_beta),
             consumes=(config.consume_alpha, config.consume_beta), chi=self._chi,
-            chi_pinned=self._chi_pinned, store_samples=True, store_next=True)
+            chi_pinned=self._chi_pinned, store_samples=self._stores,
+            store_next=self._stores, engine=config.engine)
         self._sim = DeviceSim(params, self._state)
         self._warned_clamp = 0
         self._warned_neg = 0
@@ -536,6 +561,7 @@ class Realisation:
         k = xi_host.shape[0]
         xi = torch.as_tensor(xi_host, device="cuda").to(self.dtype).contiguous()
         self._sim.step(xi, k)
+        self._sim.export_state()
         st = self._sim.status()
         self._report_warnings(st)
         if st.code != N.CS_OK:
@@ -544,8 +570,9 @@ class Realisation:
             try:
                 if st.code == N.CS_FIELD_NONFINITE:
                     raise FloatingPointError("field update produced non-finite values")
+                src = "next_pos" if self._sim.engine == "direct" else "pos"
                 raise_boundary_status(st.code, int(st.particle), int(st.axis),
-                                      self._state["next_pos"].double().cpu().numpy())
+                                      self._state[src].double().cpu().numpy())
             except (SimulationError, FloatingPointError, ValueError) as exc:
                 raise SimulationError(f"step {st.step}: {exc}") from exc
         self.step_index += k

@@ -187,6 +187,8 @@ def make_state(cfg: dict, rank: int):
                                  cutoff=2.0 * cfg["eps"], dt=DT)
     fp = cs.FieldParams(d_c=cfg.get("d_c", 0.0), k_alpha=cfg.get("k_alpha", 0.0),
                         k_beta=cfg.get("k_beta", 0.0), gamma=cfg.get("gamma", 0.0))
+    if os.environ.get("CS_BENCH_NO_INTERACTION"):  # diagnostics only
+        mp.interaction = "none"
     params = cs.sim_params_struct(
         n=n, prec=0 if cfg["prec"] == "fp64" else 1, domain=dom, motion=mp, dt=DT,
         field_active=cfg["field"], refresh_active=cfg["field"] or cfg.get("c0") == "linear_x",

@@ -67,7 +67,7 @@ __global__ void k_seg_sort(int *__restrict__ order, const int *__restrict__ skey
 }
 
 // ------------------------------------------------------------------ scan
-int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n) {
+int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n, int *zero_in) {
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     CS_TRY(ctx->tile_flags.ensure(sizeof(unsigned long long) * (tiles + 2)));
     unsigned long long *flags = ctx->tile_flags.as<unsigned long long>();
@@ -77,7 +77,7 @@ int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n) {
         CS_CUDA(cudaMemsetAsync(out, 0, sizeof(int), ctx->stream));
         return CS_OK;
     }
-    k_scan<<<(unsigned)tiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, n, flags, counter);
+    k_scan<<<(unsigned)tiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, n, flags, counter, zero_in);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;

@@ -58,6 +58,15 @@ BinGeom make_geom(const cs_domain &d, double cell_cutoff) {
     return g;
 }
 
+ExactDiv make_exact_div(double b) {
+    ExactDiv d;
+    d.b = b;
+    d.inv = 1.0 / b;
+    int e = 0;
+    d.pow2 = (b > 0.0 && frexp(b, &e) == 0.5) ? 1 : 0;
+    return d;
+}
+
 PairTab make_pairtab(const cs_pair_params &pp) {
     PairTab t;
     for (int k = 0; k < 4; k++) {
@@ -90,7 +99,7 @@ bool gauss_too_wide(const GridGeom &gg, double cutoff);
 int launch_bilinear(cs_ctx *ctx, int prec, const void *pts, long long np, const void *vals, int m,
                     const GridGeom &gg, void *out, unsigned long long *clamped);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
-                    DevStatus *st, int step);
+                    DevStatus *st, int step, int *zero_q = nullptr);
 int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
                      cs_field_ops **out);
 void field_ops_destroy(cs_field_ops *ops);

@@ -137,6 +137,36 @@ __device__ __forceinline__ int cell_axis(double v, double lo, double eff, int n)
     return (int)f;
 }
 
+// fl(a / b) and floor(fl(a / b)) without a division in the common case.
+// When b is a power of two a * (1/b) is exact.  Otherwise q = a * fl(1/b)
+// is within 3 ulp of fl(a/b), so floor(q) == floor(fl(a/b)) unless q lies
+// within a (generous) 2^-49 relative band of an integer, where the exact
+// quotient is recomputed.
+struct ExactDiv {
+    double b, inv;
+    int pow2;
+};
+ExactDiv make_exact_div(double b);
+__device__ __forceinline__ double ediv(double a, const ExactDiv &d) {
+    return d.pow2 ? dmul(a, d.inv) : ddiv(a, d.b);
+}
+static __device__ __noinline__ double floor_ddiv(double a, double b) { return floor(ddiv(a, b)); }
+__device__ __forceinline__ double floor_div(double a, const ExactDiv &d) {
+    const double q = dmul(a, d.inv);
+    double f = floor(q);
+    if (!d.pow2) {
+        const double tol = fabs(q) * 0x1p-49 + 0x1p-1022;
+        if (dsub(q, f) < tol || dsub(dadd(f, 1.0), q) < tol) f = floor_ddiv(a, d.b);
+    }
+    return f;
+}
+__device__ __forceinline__ int cell_axis_fast(double v, double lo, const ExactDiv &eff, int n) {
+    const double f = floor_div(dsub(v, lo), eff);
+    if (!(f >= 0.0)) return 0;
+    if (f >= (double)n) return n - 1;
+    return (int)f;
+}
+
 struct PairTab {
     double eps[4];
     double cut2[4];
@@ -254,7 +284,8 @@ inline int grid_for(long long n, int block, int max_blocks = 148 * 64) {
 // ---------------------------------------------------------------- launchers
 // bins.cu
 int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g);
-int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n);
+int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n,
+                       int *zero_in = nullptr);
 // forces.cu
 int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,
                        long long n, const BinGeom &g, const PairTab &pt, double *out,

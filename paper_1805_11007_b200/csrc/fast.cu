@@ -51,7 +51,7 @@ struct FastArgs {
     const Rec *rec;
     const int *starts;
     Rec *tmp;
-    int *keys;
+    int2 *keyrank;      // (new cell key, rank inside the cell) per old slot
     int *counts;
     const float *xi;    // this step's (N, 2) increments, indexed by id
     const float *grad;  // (n_c^2, 2)
@@ -60,46 +60,118 @@ struct FastArgs {
     BinGeom g;
     PairTab pt;
     GridGeom gg;
+    ExactDiv eff0, eff1, gd0, gd1, sz0, sz1;
     double amp[2], dt, chi[2];
     int chi_pinned[2];
     int refresh, deposit, interact;
     unsigned bits[2];
     double half0, half1;
+    float halff0, halff1, sizef0, sizef1;
+    float cutf2[4];     // binary32 prefilter: cut2 * (1 + 1e-5)
     cs_domain dom;
 };
 
-// minimum image with the |dx| <= L/2 shortcut: round(dx/L) is then +-0 and
-// dx - L*(+-0) == dx exactly (dx is never -0.0: x - x = +0 under RN)
-__device__ __forceinline__ double min_image(double dx, double size, double half) {
-    if (fabs(dx) <= half) return dx;
-    return dsub(dx, dmul(size, rint(ddiv(dx, size))));
+// Random gather of the step's increments: keep the 80 MB slice in L2
+// (evict_last) while the streamed arrays pass through (evict_first).
+__device__ __forceinline__ float2 ld_evict_last(const float2 *p) {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+                 : "=f"(v.x), "=f"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
 }
 
-__device__ __forceinline__ bool pair_term(const Rec &r, double xi, double yi, int ti,
-                                          const FastArgs &a, double &tx, double &ty,
-                                          bool want_term) {
-    double dx0 = dsub((double)r.x, xi);
-    double dx1 = dsub((double)r.y, yi);
-    if (a.g.per0) dx0 = min_image(dx0, a.g.size0, a.half0);
-    if (a.g.per1) dx1 = min_image(dx1, a.g.size1, a.half1);
+// Launch parameters of k_fast_step live in constant memory: every thread
+// reads the same words, and nothing has to be copied into registers or
+// marshalled through the out-of-line helpers.
+__constant__ FastArgs cA;
+
+// minimum image with the |dx| <= L/2 shortcut: round(dx/L) is then +-0 and
+// dx - L*(+-0) == dx exactly (dx is never -0.0: x - x = +0 under RN)
+__device__ __noinline__ double min_image_slow(double dx, double size) {
+    return dsub(dx, dmul(size, rint(ddiv(dx, size))));
+}
+__device__ __forceinline__ double min_image(double dx, double size, double half) {
+    if (fabs(dx) <= half) return dx;
+    return min_image_slow(dx, size);
+}
+
+// The pair term of an accepted pair (motion.py:240-243), out of line: it is
+// reached ~1.1 times per particle and carries the exp and two divisions.
+__device__ __noinline__ double2 pair_term(double dx0, double dx1, double r2, double eps) {
+    const double rr = dsqrt(r2);
+    const double s = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
+    return make_double2(dmul(s, dx0), dmul(s, dx1));
+}
+
+struct PairRow {  // table row of this particle's type: index = partner type
+    double cut2_0, cut2_1, eps_0, eps_1;
+    float cf_0, cf_1;
+    __device__ __forceinline__ double cut2(int tj) const { return tj ? cut2_1 : cut2_0; }
+    __device__ __forceinline__ double eps(int tj) const { return tj ? eps_1 : eps_0; }
+    __device__ __forceinline__ float cf(int tj) const { return tj ? cf_1 : cf_0; }
+};
+
+// Exact reference pair test (motion.py:231-239).  Returns r2 > 0 when
+// accepted (displacement in dx0/dx1), 0 otherwise.  A binary32 prefilter
+// runs first: it never rejects an accepted pair (every binary32 op has
+// relative error <= 2^-24, far inside the 1e-5 margin of cf).
+__device__ __forceinline__ double pair_test(float xjf, float yjf, float xf, float yf, double x,
+                                            double y, float cf, double cut2, double &dx0,
+                                            double &dx1) {
+    float fx = xjf - xf, fy = yjf - yf;
+    if (cA.g.per0 && fabsf(fx) > cA.halff0) fx -= copysignf(cA.sizef0, fx);
+    if (cA.g.per1 && fabsf(fy) > cA.halff1) fy -= copysignf(cA.sizef1, fy);
+    if (fmaf(fx, fx, fy * fy) > cf) return 0.0;
+    dx0 = dsub((double)xjf, x);
+    dx1 = dsub((double)yjf, y);
+    if (cA.g.per0) dx0 = min_image(dx0, cA.g.size0, cA.half0);
+    if (cA.g.per1) dx1 = min_image(dx1, cA.g.size1, cA.half1);
     const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
-    const int t = ti * 2 + (int)(r.meta >> 31);
-    if (r2 > a.pt.cut2[t] || r2 == 0.0) return false;
-    if (want_term) {
-        const double eps = a.pt.eps[t];
-        const double rr = dsqrt(r2);
-        const double s = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
-        tx = dmul(s, dx0);
-        ty = dmul(s, dx1);
+    if (r2 > cut2 || r2 == 0.0) return 0.0;
+    return r2;
+}
+
+// Several accepted pairs in one cell: add them in ascending partner id.
+__device__ __noinline__ double2 cell_ordered(const float4 *__restrict__ rec, long long t, int kb,
+                                             int ke, int nacc, float xf, float yf, double x,
+                                             double y, PairRow pr, double fx, double fy) {
+    long long last = -1;
+    for (int r = 0; r < nacc; r++) {
+        unsigned best = 0xffffffffu;
+        int bk = -1;
+        for (int k = kb; k < ke; k++) {
+            if (k == t) continue;
+            const float4 q = __ldg(rec + k);
+            const unsigned meta = __float_as_uint(q.z);
+            const unsigned idk = meta & ID_MASK;
+            if ((long long)idk <= last || idk >= best) continue;
+            const int tj = (int)(meta >> 31);
+            double d0, d1;
+            if (pair_test(q.x, q.y, xf, yf, x, y, pr.cf(tj), pr.cut2(tj), d0, d1) > 0.0) {
+                best = idk;
+                bk = k;
+            }
+        }
+        const float4 q = __ldg(rec + bk);
+        const int tj = (int)(__float_as_uint(q.z) >> 31);
+        double d0, d1;
+        const double r2 = pair_test(q.x, q.y, xf, yf, x, y, pr.cf(tj), pr.cut2(tj), d0, d1);
+        const double2 tt = pair_term(d0, d1, r2, pr.eps(tj));
+        fx = dadd(fx, tt.x);
+        fy = dadd(fy, tt.y);
+        last = best;
     }
-    return true;
+    return make_double2(fx, fy);
 }
 
 __device__ __forceinline__ int boundary_axis_wraps(double &v, int &w, double lo, double hi,
-                                                   int per) {
-    const double size = dsub(hi, lo);
+                                                   const ExactDiv &sz, int per) {
+    const double size = sz.b;
     if (per) {
-        const double k = floor(ddiv(dsub(v, lo), size));
+        const double k = floor_div(dsub(v, lo), sz);
         if (k != 0.0) {
             v = dsub(v, dmul(k, size));
             w += (int)k;
@@ -126,202 +198,436 @@ __device__ __forceinline__ int boundary_axis_wraps(double &v, int &w, double lo,
     return 3;
 }
 
-__device__ __forceinline__ void cic_deposit_q(double x, double y, const GridGeom &gg,
-                                              int *__restrict__ out) {
+__device__ __forceinline__ int wrap_index(double base, int n) {
+    const int ib = (int)base;  // positions lie in [lo, hi]: base in [-1, n]
+    if (ib >= 0 && ib < n) return ib;
+    if (ib >= n && ib < 2 * n) return ib - n;
+    if (ib < 0 && ib >= -n) return ib + n;
+    return (int)pymod((long long)base, n);
+}
+
+// CIC corner nodes and weights in the reference arithmetic
+// (coupling.py:119-135; for in-hull points identical to the bilinear
+// stencil of coupling.py:221-258), u = (x - lo) / d with an exact division
+struct Cic {
+    int i00, i10, i01, i11;
+    double w00, w10, w01, w11;
+    double f0, f1;  // fractional offsets the weights derive from
+};
+__device__ __noinline__ Cic cic_stencil(double x, double y, GridGeom gg, ExactDiv d0,
+                                        ExactDiv d1) {
+    Cic c;
     const int nc = gg.n;
-    const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
-    const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
-    long long b0, b1, c0, c1;
+    const double u0 = ediv(dsub(x, gg.lo0), d0);
+    const double u1 = ediv(dsub(y, gg.lo1), d1);
+    int b0, b1, c0, c1;
     double f0, f1;
     if (gg.per) {
         const double base0 = floor(u0), base1 = floor(u1);
         f0 = dsub(u0, base0);
         f1 = dsub(u1, base1);
-        b0 = pymod((long long)base0, nc);
-        b1 = pymod((long long)base1, nc);
-        c0 = (b0 + 1) % nc;
-        c1 = (b1 + 1) % nc;
+        b0 = wrap_index(base0, nc);
+        b1 = wrap_index(base1, nc);
+        c0 = b0 + 1 == nc ? 0 : b0 + 1;
+        c1 = b1 + 1 == nc ? 0 : b1 + 1;
     } else {
-        b0 = (long long)floor(u0);
-        b1 = (long long)floor(u1);
-        b0 = b0 < 0 ? 0 : (b0 > nc - 2 ? nc - 2 : b0);
-        b1 = b1 < 0 ? 0 : (b1 > nc - 2 ? nc - 2 : b1);
+        const double fl0 = floor(u0), fl1 = floor(u1);
+        b0 = fl0 < 0.0 ? 0 : (fl0 > nc - 2 ? nc - 2 : (int)fl0);
+        b1 = fl1 < 0.0 ? 0 : (fl1 > nc - 2 ? nc - 2 : (int)fl1);
         f0 = dsub(u0, (double)b0);
         f1 = dsub(u1, (double)b1);
         c0 = b0 + 1;
         c1 = b1 + 1;
     }
     const double g0 = dsub(1.0, f0), g1 = dsub(1.0, f1);
-    atomicAdd(&out[b1 * nc + b0], __double2int_rn(dmul(dmul(g0, g1), Q_SCALE)));
-    atomicAdd(&out[b1 * nc + c0], __double2int_rn(dmul(dmul(f0, g1), Q_SCALE)));
-    atomicAdd(&out[c1 * nc + b0], __double2int_rn(dmul(dmul(g0, f1), Q_SCALE)));
-    atomicAdd(&out[c1 * nc + c0], __double2int_rn(dmul(dmul(f0, f1), Q_SCALE)));
+    c.f0 = f0;
+    c.f1 = f1;
+    c.w00 = dmul(g0, g1);
+    c.w10 = dmul(f0, g1);
+    c.w01 = dmul(g0, f1);
+    c.w11 = dmul(f0, f1);
+    c.i00 = b1 * nc + b0;
+    c.i10 = b1 * nc + c0;
+    c.i01 = c1 * nc + b0;
+    c.i11 = c1 * nc + c0;
+    return c;
 }
 
-__global__ void __launch_bounds__(256)
-k_fast_step(FastArgs a, DevStatus *st, int step) {
+__device__ __forceinline__ void cic_deposit_q(const Cic &c, int *__restrict__ out) {
+    atomicAdd(&out[c.i00], __double2int_rn(dmul(c.w00, Q_SCALE)));
+    atomicAdd(&out[c.i10], __double2int_rn(dmul(c.w10, Q_SCALE)));
+    atomicAdd(&out[c.i01], __double2int_rn(dmul(c.w01, Q_SCALE)));
+    atomicAdd(&out[c.i11], __double2int_rn(dmul(c.w11, Q_SCALE)));
+}
+
+// Generic ring walk for the rare particles the fast path does not cover
+// (cells on a periodic seam or wall, axes with < 3 cells, > ACC_MAX accepted
+// pairs): per-cell loop in ring order, ascending id inside a cell.
+__device__ __noinline__ double2 ring_forces_generic(const float4 *__restrict__ rec,
+                                                    const int *__restrict__ starts, long long t,
+                                                    float xf, float yf, double x, double y,
+                                                    int cx, int cy, int n0, int n1,
+                                                    PairRow pr) {
+    double fx = 0.0, fy = 0.0;
+    for (int c9 = 0; c9 < 9; c9++) {
+        const int o1 = c9 / 3 - 1, o0 = c9 % 3 - 1;
+        int g1 = cy + o1, g0 = cx + o0;
+        if (cA.g.per1) {
+            if ((n1 == 1 && o1 != 0) || (n1 == 2 && o1 == 1)) continue;
+            g1 = g1 < 0 ? g1 + n1 : (g1 >= n1 ? g1 - n1 : g1);
+        } else if (g1 < 0 || g1 >= n1) {
+            continue;
+        }
+        if (cA.g.per0) {
+            if ((n0 == 1 && o0 != 0) || (n0 == 2 && o0 == 1)) continue;
+            g0 = g0 < 0 ? g0 + n0 : (g0 >= n0 ? g0 - n0 : g0);
+        } else if (g0 < 0 || g0 >= n0) {
+            continue;
+        }
+        const int f = g1 * n0 + g0;
+        const int kb = starts[f], ke = starts[f + 1];
+        int nacc = 0;
+        for (int k = kb; k < ke; k++) {
+            if (k == t) continue;
+            const float4 r = __ldg(rec + k);
+            const int tj = (int)(__float_as_uint(r.z) >> 31);
+            double d0, d1;
+            if (pair_test(r.x, r.y, xf, yf, x, y, pr.cf(tj), pr.cut2(tj), d0, d1) > 0.0)
+                nacc++;
+        }
+        if (nacc > 0) {
+            const double2 ff = cell_ordered(rec, t, kb, ke, nacc, xf, yf, x, y, pr, fx, fy);
+            fx = ff.x;
+            fy = ff.y;
+        }
+    }
+    return make_double2(fx, fy);
+}
+
+constexpr int ACC_MAX = 8;          // accepted pairs buffered per particle
+constexpr int WARPS_PER_BLOCK = 8;  // k_fast_step block = 256 threads
+constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
+
+struct WarpQueue {
+    // per-lane regions [lane * ACC_MAX, +ACC_MAX): the (ring cell, id) sort
+    // keys, then -- once every lane has sorted -- the x terms in their place
+    union {
+        unsigned long long key[QCAP];
+        double tx[QCAP];
+    };
+    int k[QCAP];                   // partner slot of each accepted pair
+    double ty[QCAP];
+    int incl[32];                  // inclusive prefix of the per-lane counts
+    float ox[32], oy[32];          // owner coordinates
+    int oti[32];
+};
+
+__global__ void __launch_bounds__(256, 2)
+k_fast_step(DevStatus *st, int step) {
+    const FastArgs &a = cA;
+    __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
+    WarpQueue &wq = wq_all[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
     const bool dead = st->abort != 0;
     const int m = a.gg.n * a.gg.n;
-    int clamped = 0;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const Rec me = a.rec[t];
-        const double x = (double)me.x, y = (double)me.y;
-        const int ti = (int)(me.meta >> 31);
-        const unsigned id = me.meta & ID_MASK;
-        // ---- pair forces over the reference ring, canonical order
+    const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
+    const int n0 = a.g.n0, n1 = a.g.n1;
+    const long long wstride = (long long)gridDim.x * blockDim.x;
+    long long pend_t = -1;  // the previous iteration's (slot, key, rank): the
+    int pend_key = 0, pend_rank = 0;  // atomic's return is awaited a whole iteration later
+    // warp-uniform loop: every lane runs the same number of iterations so the
+    // whole warp can take part in the cooperative pair-term phase
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+         base < a.n; base += wstride) {
+        const long long t = base + lane;
+        const bool live = t < a.n;
+        float4 mer = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live) mer = __ldcs(rec + t);  // read once: stream past L2
+        const float xf = mer.x, yf = mer.y;
+        const unsigned meta = __float_as_uint(mer.z);
+        const unsigned wbits = __float_as_uint(mer.w);
+        const double x = (double)xf, y = (double)yf;
+        const int ti = (int)(meta >> 31);
+        const unsigned id = meta & ID_MASK;
+        // issue the two random-access reads of this particle first so they
+        // overlap the force sweep: xi[id] and the gradient at its cell corners
+        float2 z = make_float2(0.f, 0.f);
+        if (live) z = ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
+        const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
+        const bool do_drift = live && a.refresh && !dead && !pinned;
+        float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
+        double bf0 = 0.0, bf1 = 0.0;
+        if (do_drift) {
+            const Cic bst = cic_stencil(x, y, a.gg, a.gd0, a.gd1);
+            bf0 = bst.f0;
+            bf1 = bst.f1;
+            const float2 *g2 = reinterpret_cast<const float2 *>(a.grad);
+            v00 = __ldg(g2 + bst.i00);
+            v10 = __ldg(g2 + bst.i10);
+            v01 = __ldg(g2 + bst.i01);
+            v11 = __ldg(g2 + bst.i11);
+        }
+        // ---- pair forces over the reference ring (motion.py:206-243)
         double fx = 0.0, fy = 0.0;
-        if (!dead && a.interact) {
-            const int cx = cell_axis(x, a.g.lo0, a.g.eff0, a.g.n0);
-            const int cy = cell_axis(y, a.g.lo1, a.g.eff1, a.g.n1);
-            for (int o1 = -1; o1 <= 1; o1++) {
-                int g1 = cy + o1;
-                if (a.g.per1) {
-                    if (a.g.n1 == 1 && o1 != 0) continue;
-                    if (a.g.n1 == 2 && o1 == 1) continue;
-                    g1 = g1 < 0 ? g1 + a.g.n1 : (g1 >= a.g.n1 ? g1 - a.g.n1 : g1);
-                } else if (g1 < 0 || g1 >= a.g.n1) {
-                    continue;
+        int nacc = 0;
+        unsigned long long *akey = wq.key + lane * ACC_MAX;  // this lane's region
+        int *ak = wq.k + lane * ACC_MAX;
+        PairRow pr;
+        pr.cut2_0 = ti ? a.pt.cut2[2] : a.pt.cut2[0];
+        pr.cut2_1 = ti ? a.pt.cut2[3] : a.pt.cut2[1];
+        pr.eps_0 = ti ? a.pt.eps[2] : a.pt.eps[0];
+        pr.eps_1 = ti ? a.pt.eps[3] : a.pt.eps[1];
+        pr.cf_0 = ti ? a.cutf2[2] : a.cutf2[0];
+        pr.cf_1 = ti ? a.cutf2[3] : a.cutf2[1];
+        if (live && !dead && a.interact) {
+            const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
+            const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
+            bool generic = cx < 1 || cx + 1 >= n0 || n1 < 3;
+            if (!generic) {
+                // the three cells of each ring row are consecutive in the
+                // cell table: one contiguous slot segment per row, cell
+                // boundaries inside it give the ring position o0
+                int sa[3], s1[3], s2[3], len[3];
+#pragma unroll
+                for (int r = 0; r < 3; r++) {
+                    int g1 = cy + r - 1;
+                    bool in = true;
+                    if (a.g.per1) g1 = g1 < 0 ? g1 + n1 : (g1 >= n1 ? g1 - n1 : g1);
+                    else in = g1 >= 0 && g1 < n1;
+                    if (in) {
+                        const int f = g1 * n0 + cx - 1;
+                        sa[r] = __ldg(a.starts + f);
+                        s1[r] = __ldg(a.starts + f + 1);
+                        s2[r] = __ldg(a.starts + f + 2);
+                        len[r] = __ldg(a.starts + f + 3) - sa[r];
+                    } else {
+                        sa[r] = s1[r] = s2[r] = 0;
+                        len[r] = 0;
+                    }
                 }
-                for (int o0 = -1; o0 <= 1; o0++) {
-                    int g0 = cx + o0;
-                    if (a.g.per0) {
-                        if (a.g.n0 == 1 && o0 != 0) continue;
-                        if (a.g.n0 == 2 && o0 == 1) continue;
-                        g0 = g0 < 0 ? g0 + a.g.n0 : (g0 >= a.g.n0 ? g0 - a.g.n0 : g0);
-                    } else if (g0 < 0 || g0 >= a.g.n0) {
-                        continue;
+                const int total = len[0] + len[1] + len[2];
+                auto slot_of = [&](int it, int &r) {
+                    if (it < len[0]) {
+                        r = 0;
+                        return sa[0] + it;
                     }
-                    const int f = g1 * a.g.n0 + g0;
-                    const int kb = a.starts[f], ke = a.starts[f + 1];
-                    int nacc = 0;
-                    double tx1 = 0.0, ty1 = 0.0;
-                    for (int k = kb; k < ke; k++) {
-                        if (k == t) continue;
-                        double tx, ty;
-                        if (pair_term(a.rec[k], x, y, ti, a, tx, ty, nacc == 0)) {
-                            if (nacc == 0) {
-                                tx1 = tx;
-                                ty1 = ty;
-                            }
-                            nacc++;
-                        }
+                    if (it < len[0] + len[1]) {
+                        r = 1;
+                        return sa[1] + it - len[0];
                     }
-                    if (nacc == 1) {
-                        fx = dadd(fx, tx1);
-                        fy = dadd(fy, ty1);
-                    } else if (nacc > 1) {
-                        // ascending id among the accepted members
-                        long long last = -1;
-                        for (int r = 0; r < nacc; r++) {
-                            unsigned best = 0xffffffffu;
-                            int bk = -1;
-                            for (int k = kb; k < ke; k++) {
-                                if (k == t) continue;
-                                const Rec rk = a.rec[k];
-                                const unsigned idk = rk.meta & ID_MASK;
-                                if ((long long)idk <= last || idk >= best) continue;
-                                double tx, ty;
-                                if (pair_term(rk, x, y, ti, a, tx, ty, false)) {
-                                    best = idk;
-                                    bk = k;
-                                }
-                            }
-                            double tx, ty;
-                            pair_term(a.rec[bk], x, y, ti, a, tx, ty, true);
-                            fx = dadd(fx, tx);
-                            fy = dadd(fy, ty);
-                            last = best;
-                        }
+                    r = 2;
+                    return sa[2] + it - len[0] - len[1];
+                };
+                int rn = 0;
+                int kn = total > 0 ? slot_of(0, rn) : 0;
+                float4 qn = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (total > 0) qn = __ldg(rec + kn);
+                for (int it = 0; it < total; it++) {
+                    // candidate it is in qn; prefetch candidate it + 1
+                    const int r = rn, k = kn;
+                    const float4 q = qn;
+                    if (it + 1 < total) {
+                        kn = slot_of(it + 1, rn);
+                        qn = __ldg(rec + kn);
                     }
+                    if (k == t) continue;
+                    const unsigned qm = __float_as_uint(q.z);
+                    const int tj = (int)(qm >> 31);
+                    // binary32 prefilter only; the exact reference test runs
+                    // in the warp-cooperative phase below
+                    float ddx = q.x - xf, ddy = q.y - yf;
+                    if (a.g.per0 && fabsf(ddx) > a.halff0) ddx -= copysignf(a.sizef0, ddx);
+                    if (a.g.per1 && fabsf(ddy) > a.halff1) ddy -= copysignf(a.sizef1, ddy);
+                    if (fmaf(ddx, ddx, ddy * ddy) > pr.cf(tj)) continue;
+                    const int sr1 = r == 0 ? s1[0] : (r == 1 ? s1[1] : s1[2]);
+                    const int sr2 = r == 0 ? s2[0] : (r == 1 ? s2[1] : s2[2]);
+                    const unsigned c9 = (unsigned)(r * 3 + (k >= sr1) + (k >= sr2));
+                    if (nacc < ACC_MAX) {
+                        akey[nacc] = ((unsigned long long)c9 << 32) | (qm & ID_MASK);
+                        ak[nacc] = k;
+                    }
+                    nacc++;
+                }
+                if (nacc > ACC_MAX) generic = true;
+            }
+            if (generic) {
+                const double2 ff = ring_forces_generic(rec, a.starts, t, xf, yf, x, y, cx, cy,
+                                                       n0, n1, pr);
+                fx = ff.x;
+                fy = ff.y;
+                nacc = 0;
+            } else {
+                // canonical order: ring cell, then ascending id (arrivals are
+                // already grouped by ring cell; sort the few entries fully)
+                for (int i = 1; i < nacc; i++) {
+                    const unsigned long long kk = akey[i];
+                    const int kv = ak[i];
+                    int j = i - 1;
+                    while (j >= 0 && akey[j] > kk) {
+                        akey[j + 1] = akey[j];
+                        ak[j + 1] = ak[j];
+                        j--;
+                    }
+                    akey[j + 1] = kk;
+                    ak[j + 1] = kv;
                 }
             }
         }
-        // ---- drift refresh at the start-of-step position
+        // ---- cooperative pair terms: the warp's accepted pairs (in the
+        // lanes' shared-memory regions) are evaluated ~1/32 per lane, then
+        // each owner adds its own terms in canonical order
+        {
+            int incl = nacc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int T = __shfl_sync(0xffffffffu, incl, 31);
+            if (T > 0) {
+                wq.incl[lane] = incl;
+                wq.ox[lane] = xf;
+                wq.oy[lane] = yf;
+                wq.oti[lane] = ti;
+                __syncwarp();
+                for (int e = lane; e < T; e += 32) {
+                    // owner = first lane whose inclusive count exceeds e
+                    int ow = 0;
+#pragma unroll
+                    for (int step2 = 16; step2 > 0; step2 >>= 1)
+                        if (wq.incl[ow + step2 - 1] <= e) ow += step2;
+                    const int j = e - (ow ? wq.incl[ow - 1] : 0);
+                    const int slot = ow * ACC_MAX + j;
+                    const float oxf = wq.ox[ow], oyf = wq.oy[ow];
+                    const int oti = wq.oti[ow];
+                    const float4 q = __ldg(rec + wq.k[slot]);
+                    const int tj = (int)(__float_as_uint(q.z) >> 31);
+                    const int tt = oti * 2 + tj;
+                    const double c2 = tt == 0 ? a.pt.cut2[0]
+                                              : (tt == 1 ? a.pt.cut2[1]
+                                                         : (tt == 2 ? a.pt.cut2[2] : a.pt.cut2[3]));
+                    const double ep = tt == 0 ? a.pt.eps[0]
+                                              : (tt == 1 ? a.pt.eps[1]
+                                                         : (tt == 2 ? a.pt.eps[2] : a.pt.eps[3]));
+                    double d0, d1;
+                    const double r2 = pair_test(q.x, q.y, oxf, oyf, (double)oxf, (double)oyf,
+                                                3.0e38f, c2, d0, d1);
+                    if (r2 > 0.0) {  // accepted by the exact reference test
+                        const double2 term = pair_term(d0, d1, r2, ep);
+                        wq.tx[slot] = term.x;
+                        wq.ty[slot] = term.y;
+                    } else {
+                        wq.k[slot] = -1;  // prefilter false positive: no contribution
+                    }
+                }
+                __syncwarp();
+                for (int j = 0; j < nacc; j++) {
+                    if (wq.k[lane * ACC_MAX + j] < 0) continue;
+                    fx = dadd(fx, wq.tx[lane * ACC_MAX + j]);
+                    fy = dadd(fy, wq.ty[lane * ACC_MAX + j]);
+                }
+            }
+            __syncwarp();
+        }
+        if (!live) continue;
+        // ---- drift refresh at the start-of-step position (coupling.py:302-325)
+        const double chi = ti ? a.chi[1] : a.chi[0];
         double dr0 = 0.0, dr1 = 0.0;
-        if (a.refresh && !dead) {
-            Bilin b;
-            clamped += 2 * bilinear_stencil(x, y, a.gg, b);
-            dr0 = bilinear_apply(b, a.grad, 2, 0);
-            dr1 = bilinear_apply(b, a.grad, 2, 1);
-            if (a.chi_pinned[ti]) {
-                dr0 = 0.0;
-                dr1 = 0.0;
-            } else if (a.chi[ti] != 1.0) {
-                dr0 = dmul(dr0, a.chi[ti]);
-                dr1 = dmul(dr1, a.chi[ti]);
+        if (do_drift) {
+            Cic b;  // bilinear weights (coupling.py:251-254) from the kept offsets
+            const double g0 = dsub(1.0, bf0), g1 = dsub(1.0, bf1);
+            b.w00 = dmul(g0, g1);
+            b.w10 = dmul(bf0, g1);
+            b.w01 = dmul(g0, bf1);
+            b.w11 = dmul(bf0, bf1);
+            dr0 = dadd(dadd(dadd(dmul(b.w00, (double)v00.x), dmul(b.w10, (double)v10.x)),
+                            dmul(b.w01, (double)v01.x)),
+                       dmul(b.w11, (double)v11.x));
+            dr1 = dadd(dadd(dadd(dmul(b.w00, (double)v00.y), dmul(b.w10, (double)v10.y)),
+                            dmul(b.w01, (double)v01.y)),
+                       dmul(b.w11, (double)v11.y));
+            if (chi != 1.0) {
+                dr0 = dmul(dr0, chi);
+                dr1 = dmul(dr1, chi);
             }
         }
         // ---- EM proposal (motion.py:281-282)
-        const float2 z = __ldg(reinterpret_cast<const float2 *>(a.xi) + id);
-        const double amp = a.amp[ti];
-        double v[2];
-        v[0] = dadd(dadd(dadd(x, dmul(amp, (double)z.x)), dmul(dr0, a.dt)), dmul(fx, a.dt));
-        v[1] = dadd(dadd(dadd(y, dmul(amp, (double)z.y)), dmul(dr1, a.dt)), dmul(fy, a.dt));
-        int w[2] = {me.wx, me.wy};
+        const double amp = ti ? a.amp[1] : a.amp[0];
+        double v0 = dadd(dadd(dadd(x, dmul(amp, (double)z.x)), dmul(dr0, a.dt)), dmul(fx, a.dt));
+        double v1 = dadd(dadd(dadd(y, dmul(amp, (double)z.y)), dmul(dr1, a.dt)), dmul(fy, a.dt));
+        int w0 = (short)(wbits & 0xffffu), w1 = (short)(wbits >> 16);
         bool ok = !dead;
-        if (ok && !(isfinite(v[0]) && isfinite(v[1]))) {
+        if (ok && !(isfinite(v0) && isfinite(v1))) {
             atomicMin(&st->key, err_key(0, id, CS_NONFINITE));
             st->abort = 1;
             st->step = step;
             ok = false;
         }
         if (ok) {
-            for (int ax = 0; ax < 2; ax++) {
-                const double raw = v[ax];
-                const int code = boundary_axis_wraps(v[ax], w[ax], a.dom.lo[ax], a.dom.hi[ax],
-                                                     a.dom.periodic[ax]);
-                if (code) {
-                    atomicMin(&st->key, err_key(1 + ax, id, code));
-                    st->abort = 1;
-                    st->step = step;
-                    v[ax] = raw;  // the raw proposal stays visible for the message
-                    ok = false;
-                    break;
-                }
+            const double r0 = v0, r1 = v1;
+            int code = boundary_axis_wraps(v0, w0, a.dom.lo[0], a.dom.hi[0], a.sz0,
+                                           a.dom.periodic[0]);
+            int ax = 0;
+            if (!code) {
+                code = boundary_axis_wraps(v1, w1, a.dom.lo[1], a.dom.hi[1], a.sz1,
+                                           a.dom.periodic[1]);
+                ax = 1;
+            }
+            if (code) {
+                atomicMin(&st->key, err_key(1 + ax, id, code));
+                st->abort = 1;
+                st->step = step;
+                if (ax == 0) v0 = r0;  // the raw proposal stays visible for the message
+                else v1 = r1;
+                ok = false;
             }
         }
-        Rec out;
+        float4 out;
         if (dead) {
-            out = me;
+            out = mer;
         } else {
-            out.x = (float)v[0];
-            out.y = (float)v[1];
-            out.meta = me.meta;
-            out.wx = (short)w[0];
-            out.wy = (short)w[1];
+            out.x = (float)v0;
+            out.y = (float)v1;
+            out.z = mer.z;
+            out.w = __uint_as_float(((unsigned)(w1 & 0xffff) << 16) | (unsigned)(w0 & 0xffff));
         }
-        // ---- bin the stored (binary32) coordinate for the next step
+        // ---- bin the stored (binary32) coordinate for the next step; the
+        // histogram atomic's return value is the record's rank in its cell
         const double nx = (double)out.x, ny = (double)out.y;
-        const int key = cell_axis(ny, a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
-                        cell_axis(nx, a.g.lo0, a.g.eff0, a.g.n0);
-        a.tmp[t] = out;
-        a.keys[t] = key;
-        atomicAdd(&a.counts[key], 1);
+        const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
+                        cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
+        __stcs(reinterpret_cast<float4 *>(a.tmp) + t, out);
+        if (pend_t >= 0) __stcs(a.keyrank + pend_t, make_int2(pend_key, pend_rank));
+        pend_rank = atomicAdd(&a.counts[key], 1);
+        pend_key = key;
+        pend_t = t;
         if (a.deposit && ok) {
-            const unsigned bits = a.bits[ti];
-            if (bits & 1u) cic_deposit_q(nx, ny, a.gg, a.rho_q);
-            if (bits & 2u) cic_deposit_q(nx, ny, a.gg, a.rho_q + m);
+            const unsigned bits = ti ? a.bits[1] : a.bits[0];
+            if (bits) {
+                const Cic c = cic_stencil(nx, ny, a.gg, a.gd0, a.gd1);
+                if (bits & 1u) cic_deposit_q(c, a.rho_q);
+                if (bits & 2u) cic_deposit_q(c, a.rho_q + m);
+            }
         }
     }
-    if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
+    if (pend_t >= 0) a.keyrank[pend_t] = make_int2(pend_key, pend_rank);
 }
 
 __global__ void __launch_bounds__(256)
-k_fast_scatter(const Rec *__restrict__ tmp, const int *__restrict__ keys, long long n,
-               const int *__restrict__ starts, int *__restrict__ counts, Rec *__restrict__ out) {
+k_fast_scatter(const Rec *__restrict__ tmp, const int2 *__restrict__ keyrank, long long n,
+               const int *__restrict__ starts, Rec *__restrict__ out) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
-        const int key = keys[t];
-        const int slot = starts[key] + atomicSub(&counts[key], 1) - 1;
-        out[slot] = tmp[t];
+        const int2 kr = keyrank[t];
+        const float4 r = __ldcs(reinterpret_cast<const float4 *>(tmp) + t);
+        reinterpret_cast<float4 *>(out)[starts[kr.x] + kr.y] = r;
     }
 }
 
-// caller arrays (id order) -> records (id order) + keys + histogram
+// caller arrays (id order) -> records (id order) + keys/ranks + histogram
 __global__ void k_fast_import(const float *__restrict__ pos, const float *__restrict__ anchor,
                               const uint8_t *__restrict__ type, long long n, BinGeom g,
-                              Rec *__restrict__ tmp, int *__restrict__ keys,
+                              Rec *__restrict__ tmp, int2 *__restrict__ keyrank,
                               int *__restrict__ counts, float *__restrict__ anchor0) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -336,20 +642,22 @@ __global__ void k_fast_import(const float *__restrict__ pos, const float *__rest
         reinterpret_cast<float2 *>(anchor0)[i] = reinterpret_cast<const float2 *>(anchor)[i];
         const int key = cell_axis((double)p.y, g.lo1, g.eff1, g.n1) * g.n0 +
                         cell_axis((double)p.x, g.lo0, g.eff0, g.n0);
-        keys[i] = key;
-        atomicAdd(&counts[key], 1);
+        keyrank[i] = make_int2(key, atomicAdd(&counts[key], 1));
     }
 }
 
 __global__ void k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeom gg,
-                               unsigned bits0, unsigned bits1, int *__restrict__ rho_q) {
+                               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
+                               int *__restrict__ rho_q) {
     const int m = gg.n * gg.n;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
         const Rec r = rec[t];
         const unsigned bits = (r.meta >> 31) ? bits1 : bits0;
-        if (bits & 1u) cic_deposit_q((double)r.x, (double)r.y, gg, rho_q);
-        if (bits & 2u) cic_deposit_q((double)r.x, (double)r.y, gg, rho_q + m);
+        if (!bits) continue;
+        const Cic c = cic_stencil((double)r.x, (double)r.y, gg, d0, d1);
+        if (bits & 1u) cic_deposit_q(c, rho_q);
+        if (bits & 2u) cic_deposit_q(c, rho_q + m);
     }
 }
 
@@ -384,16 +692,14 @@ __global__ void k_fast_rho_export(const int *__restrict__ q, long long m2, doubl
 // deposits of the coming update
 template <class R>
 __global__ void __launch_bounds__(256)
-k_fast_rhs(const float *__restrict__ c, int *__restrict__ q, long long m, double one_m_dtg,
+k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, double one_m_dtg,
            double dka, double dkb, int has_g, int has_a, int has_b, double scale,
            R *__restrict__ rhs, const DevStatus *st) {
     if (st->abort) return;
     for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
          l += (long long)gridDim.x * blockDim.x) {
         const double cv = (double)c[l];
-        const int qa = q[l], qb = q[l + m];
-        q[l] = 0;
-        q[l + m] = 0;
+        const int qa = q[l], qb = q[l + m];  // zeroed later by the gradient kernel
         double r = has_g ? dmul(cv, one_m_dtg) : cv;
         if (has_a) r = dadd(r, dmul(dka, dmul((double)qa, scale)));
         if (has_b) r = dsub(r, dmul(dmul(dmul((double)qb, scale), cv), dkb));
@@ -415,7 +721,7 @@ namespace cs {
 
 int field_solve_rhs(cs_field_ops *ops, void *out);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
-                    DevStatus *st, int step);
+                    DevStatus *st, int step, int *zero_q = nullptr);
 
 int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg) {
     auto *f = new cs_fast();
@@ -425,7 +731,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
     CS_TRY(f->tmp.ensure(nr));
-    CS_TRY(f->keys.ensure(sizeof(int) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(f->keys.ensure(sizeof(int2) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->counts.ensure(sizeof(int) * (size_t)f->nflat));
     CS_CUDA(cudaMemset(f->counts.p, 0, f->counts.bytes));
     CS_TRY(f->starts[0].ensure(sizeof(int) * (size_t)(f->nflat + 1)));
@@ -447,11 +753,13 @@ void fast_destroy(cs_fast *f) {
 }
 
 static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
-    CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), f->starts[nxt].as<int>(), f->nflat));
+    // scan the histogram into the next cell table and reset it in the same pass
+    CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), f->starts[nxt].as<int>(), f->nflat,
+                              f->counts.as<int>()));
     if (n > 0) {
         k_fast_scatter<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-            f->tmp.as<Rec>(), f->keys.as<int>(), n, f->starts[nxt].as<int>(),
-            f->counts.as<int>(), f->rec[nxt].as<Rec>());
+            f->tmp.as<Rec>(), f->keys.as<int2>(), n, f->starts[nxt].as<int>(),
+            f->rec[nxt].as<Rec>());
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -465,7 +773,7 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     if (n > 0) {
         k_fast_import<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
             (const float *)s->pos, (const float *)s->anchor, s->type, n, g, f->tmp.as<Rec>(),
-            f->keys.as<int>(), f->counts.as<int>(), f->anchor0.as<float>());
+            f->keys.as<int2>(), f->counts.as<int>(), f->anchor0.as<float>());
         CS_LAUNCH_CHECK();
     }
     CS_TRY(fast_sort(ctx, f, n, 0));
@@ -473,7 +781,8 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
         CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
         if (n > 0) {
             k_fast_deposit<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-                f->rec[0].as<Rec>(), n, gg, bits[0], bits[1], f->rho_q.as<int>());
+                f->rec[0].as<Rec>(), n, gg, make_exact_div(gg.d0), make_exact_div(gg.d1),
+                bits[0], bits[1], f->rho_q.as<int>());
             CS_LAUNCH_CHECK();
         }
     }
@@ -540,7 +849,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.rec = f->rec[f->cur].as<Rec>();
     a.starts = f->starts[f->cur].as<int>();
     a.tmp = f->tmp.as<Rec>();
-    a.keys = f->keys.as<int>();
+    a.keyrank = f->keys.as<int2>();
     a.counts = f->counts.as<int>();
     a.xi = (const float *)xi;
     a.grad = (const float *)s->grad;
@@ -561,9 +870,31 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.deposit = p.field_active;
     a.half0 = 0.5 * c.g.size0;
     a.half1 = 0.5 * c.g.size1;
+    a.halff0 = (float)a.half0;
+    a.halff1 = (float)a.half1;
+    a.sizef0 = (float)c.g.size0;
+    a.sizef1 = (float)c.g.size1;
+    for (int k = 0; k < 4; k++) a.cutf2[k] = (float)(a.pt.cut2[k] * (1.0 + 1e-5));
+    a.eff0 = make_exact_div(c.g.eff0);
+    a.eff1 = make_exact_div(c.g.eff1);
+    a.gd0 = make_exact_div(c.gg.d0 > 0 ? c.gg.d0 : 1.0);
+    a.gd1 = make_exact_div(c.gg.d1 > 0 ? c.gg.d1 : 1.0);
+    a.sz0 = make_exact_div(p.domain.hi[0] - p.domain.lo[0]);
+    a.sz1 = make_exact_div(p.domain.hi[1] - p.domain.lo[1]);
     a.dom = p.domain;
     if (n > 0) {
-        k_fast_step<<<grid_for(n, 256), 256, 0, ctx->stream>>>(a, st, step);
+        static int resident = 0;  // blocks of k_fast_step resident per SM
+        if (!resident) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_step, 256, 0);
+            if (resident < 1) resident = 1;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long want = (n + 255) / 256;
+        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
+        CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0, cudaMemcpyHostToDevice,
+                                        ctx->stream));
+        k_fast_step<<<grid, 256, 0, ctx->stream>>>(st, step);
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -571,6 +902,8 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
 }
 
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n) { return fast_sort(ctx, f, n, 1 - f->cur); }
+
+int *fast_rho_q(cs_fast *f) { return f->rho_q.p ? f->rho_q.as<int>() : nullptr; }
 
 bool fast_imported(const cs_fast *f) { return f && f->imported; }
 

@@ -273,7 +273,7 @@ __device__ __forceinline__ double d1_at(const G *__restrict__ c, long long base,
 template <class G>
 __global__ void __launch_bounds__(256)
 k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double wcell,
-           G *__restrict__ grad, DevStatus *st) {
+           G *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q) {
     if (st && st->abort) return;
     const long long m = (long long)n * n;
     double neg = 0.0;
@@ -284,6 +284,10 @@ k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double
         const double gx = d1_at(c, (long long)j * n, 1, i, n, per, kx);
         const double gy = d1_at(c, (long long)i, n, j, n, per, ky);
         store2(grad, l, gx, gy);
+        if (zero_q) {  // sorted engine: clear the deposit grids (no load of them here)
+            zero_q[l] = 0;
+            zero_q[l + m] = 0;
+        }
         if (st) {
             const double v = (double)c[l];
             if (!isfinite(v)) bad = 1;
@@ -346,17 +350,17 @@ __global__ void k_field_finish(DevStatus *st, int step) {
 }
 
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
-                    DevStatus *st, int step) {
+                    DevStatus *st, int step, int *zero_q) {
     const long long m = (long long)gg.n * gg.n;
     const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
     const double wcell = gg.d0 * gg.d1;
     const int B = 256;
     if (prec == CS_F64)
         k_gradient<double><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
-            (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st);
+            (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st, zero_q);
     else
         k_gradient<float><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
-            (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st);
+            (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st, zero_q);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     if (st && step >= 0) {

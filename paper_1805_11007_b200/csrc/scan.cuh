@@ -25,7 +25,8 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
 
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan(const int *__restrict__ in, int *__restrict__ out, long long n,
-       unsigned long long *__restrict__ flags, unsigned int *__restrict__ tile_counter) {
+       unsigned long long *__restrict__ flags, unsigned int *__restrict__ tile_counter,
+       int *__restrict__ zero_in = nullptr) {
     __shared__ unsigned int s_tile;
     __shared__ int s_part[SCAN_VEC][SCAN_BLOCK / 32];
     __shared__ int s_prefix;
@@ -127,6 +128,16 @@ k_scan(const int *__restrict__ in, int *__restrict__ out, long long n,
             if (e + 3 < n) out[e + 3] = o.w;
         }
         if (e < n && e + 4 >= n) out[n] = run;
+        // reset the histogram for the next step; the loaded values have been
+        // consumed above, so these stores do not race their own loads
+        if (zero_in) {
+            if (e + 4 <= n) {
+                *reinterpret_cast<int4 *>(zero_in + e) = make_int4(0, 0, 0, 0);
+            } else {
+                for (int q = 0; q < 4; q++)
+                    if (e + q < n) zero_in[e + q] = 0;
+            }
+        }
     }
 }
 

@@ -24,7 +24,7 @@ int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, 
                    const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
                    bool zero_first);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
-                    DevStatus *st, int step);
+                    DevStatus *st, int step, int *zero_q = nullptr);
 int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
                      cs_field_ops **out);
 void field_ops_destroy(cs_field_ops *ops);
@@ -52,6 +52,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
                    const void *xi, DevStatus *st, int step);
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n);
 bool fast_imported(const cs_fast *f);
+int *fast_rho_q(cs_fast *f);
 
 struct UpdateArgs {
     const void *xi;
@@ -310,7 +311,8 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                     CS_TRY(fast_field(ctx, sim->fast, c, s, st, step));
                 }
                 StageMark m(sim, CS_STAGE_GRADIENT);
-                CS_TRY(launch_gradient(ctx, p.prec, s->c, sim->gg, s->grad, st, step));
+                CS_TRY(launch_gradient(ctx, p.prec, s->c, sim->gg, s->grad, st, step,
+                                       fast_rho_q(sim->fast)));
             }
             {
                 StageMark m(sim, CS_STAGE_FORCE);

@@ -95,7 +95,7 @@ _REASONS = {
 
 
 class ClockSampler:
-    def __init__(self, device_index: int, period: float = 0.1):
+    def __init__(self, device_index: int, period: float = 0.01):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -305,7 +305,7 @@ def reference_arm(args, cfg, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -18,7 +18,9 @@ def summary(path):
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         k = d["Kernel Name"].split("(")[0][:60]
-        agg.setdefault(k, []).append(float(d["Metric Value"]) * (1e-3 if d["Metric Unit"] == "nsecond" else 1.0))
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                 "ms": 1e3}.get(d["Metric Unit"], 1.0)
+        agg.setdefault(k, []).append(float(d["Metric Value"].replace(",", "")) * scale)
     return agg
 
 

@@ -11,13 +11,18 @@
 // per-particle traffic is coalesced and neighbour cells are contiguous.
 //
 // Per step (after the field step of sim.cu):
-//   k_fast_step    one thread per sorted slot: pair forces over the 3x3
-//                  reference ring, bilinear drift, EM proposal with
-//                  xi[id], boundaries with wrap counting, new cell key +
-//                  histogram atomic, CIC deposit of the new position for
-//                  the next step's field (integer atomics, deterministic)
-//   k_scan         exclusive scan of the histogram -> next cell table
+//   k_fast_forces  pair forces over the 3x3 reference ring per sorted slot
+//                  (binary32 prefilter in the candidate loop, exact test and
+//                  pair terms evaluated warp-cooperatively, canonical order)
+//   k_fast_update  bilinear drift, EM proposal with xi[id], boundaries with
+//                  wrap counting, new cell key + histogram atomic (its
+//                  return value is the record's rank in the new cell)
+//   k_scan         exclusive scan of the histogram -> next cell table (and
+//                  histogram reset)
 //   k_fast_scatter counting-sort scatter of the new records
+//   k_fast_deposit CIC deposit of the new positions for the next step's
+//                  field, over the freshly sorted records (L2-local integer
+//                  reductions, deterministic)
 //
 // Force summation order.  Inside a cell the records are in arbitrary
 // (atomic-arrival) order, so the kernel does not rely on storage order:
@@ -31,6 +36,8 @@
 // Deposits accumulate w * 2^22 (w = CIC corner weight) in int32 per node:
 // integer addition is associative, so the field is run-to-run
 // deterministic; resolution 2.4e-7 of a particle mass per contribution.
+#include <stdlib.h>
+
 #include <utility>
 
 #include "common.cuh"
@@ -52,6 +59,11 @@ struct FastArgs {
     const int *starts;
     Rec *tmp;
     int2 *keyrank;      // (new cell key, rank inside the cell) per old slot
+    double2 *force;     // pair force per sorted slot (binary64)
+    int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
+                        // 2 skip deposits, 4 skip histogram atomics,
+                        // 8 deposit inside k_fast_update (old order) instead of
+                        // after the sort
     int *counts;
     const float *xi;    // this step's (N, 2) increments, indexed by id
     const float *grad;  // (n_c^2, 2)
@@ -83,7 +95,7 @@ __device__ __forceinline__ float2 ld_evict_last(const float2 *p) {
     return v;
 }
 
-// Launch parameters of k_fast_step live in constant memory: every thread
+// Launch parameters of the sorted-engine kernels live in constant memory: every thread
 // reads the same words, and nothing has to be copied into registers or
 // marshalled through the out-of-line helpers.
 __constant__ FastArgs cA;
@@ -305,7 +317,7 @@ __device__ __noinline__ double2 ring_forces_generic(const float4 *__restrict__ r
 }
 
 constexpr int ACC_MAX = 8;          // accepted pairs buffered per particle
-constexpr int WARPS_PER_BLOCK = 8;  // k_fast_step block = 256 threads
+constexpr int WARPS_PER_BLOCK = 8;  // k_fast_forces block = 256 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
 
 struct WarpQueue {
@@ -322,19 +334,19 @@ struct WarpQueue {
     int oti[32];
 };
 
+// Pair forces of every sorted slot -> force[t] (binary64).  Warp-uniform
+// loop so that the whole warp can take part in the cooperative pair-term
+// phase.
 __global__ void __launch_bounds__(256, 2)
-k_fast_step(DevStatus *st, int step) {
+k_fast_forces(const DevStatus *st) {
     const FastArgs &a = cA;
     __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
     WarpQueue &wq = wq_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const bool dead = st->abort != 0;
-    const int m = a.gg.n * a.gg.n;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
     const int n0 = a.g.n0, n1 = a.g.n1;
     const long long wstride = (long long)gridDim.x * blockDim.x;
-    long long pend_t = -1;  // the previous iteration's (slot, key, rank): the
-    int pend_key = 0, pend_rank = 0;  // atomic's return is awaited a whole iteration later
     // warp-uniform loop: every lane runs the same number of iterations so the
     // whole warp can take part in the cooperative pair-term phase
     for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
@@ -342,31 +354,11 @@ k_fast_step(DevStatus *st, int step) {
         const long long t = base + lane;
         const bool live = t < a.n;
         float4 mer = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (live) mer = __ldcs(rec + t);  // read once: stream past L2
+        if (live) mer = __ldg(rec + t);
         const float xf = mer.x, yf = mer.y;
         const unsigned meta = __float_as_uint(mer.z);
-        const unsigned wbits = __float_as_uint(mer.w);
         const double x = (double)xf, y = (double)yf;
         const int ti = (int)(meta >> 31);
-        const unsigned id = meta & ID_MASK;
-        // issue the two random-access reads of this particle first so they
-        // overlap the force sweep: xi[id] and the gradient at its cell corners
-        float2 z = make_float2(0.f, 0.f);
-        if (live) z = ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
-        const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
-        const bool do_drift = live && a.refresh && !dead && !pinned;
-        float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
-        double bf0 = 0.0, bf1 = 0.0;
-        if (do_drift) {
-            const Cic bst = cic_stencil(x, y, a.gg, a.gd0, a.gd1);
-            bf0 = bst.f0;
-            bf1 = bst.f1;
-            const float2 *g2 = reinterpret_cast<const float2 *>(a.grad);
-            v00 = __ldg(g2 + bst.i00);
-            v10 = __ldg(g2 + bst.i10);
-            v01 = __ldg(g2 + bst.i01);
-            v11 = __ldg(g2 + bst.i11);
-        }
         // ---- pair forces over the reference ring (motion.py:206-243)
         double fx = 0.0, fy = 0.0;
         int nacc = 0;
@@ -382,71 +374,61 @@ k_fast_step(DevStatus *st, int step) {
         if (live && !dead && a.interact) {
             const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
             const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
-            bool generic = cx < 1 || cx + 1 >= n0 || n1 < 3;
+            // fast path: interior cells only (no periodic wrap of the ring and,
+            // with >= 5 cells per axis, |dx| <= 2 cells < L/2 so the minimum
+            // image is the identity); seam/wall cells take the generic walk
+            bool generic = cx < 1 || cx + 2 > n0 || cy < 1 || cy + 2 > n1 || n0 < 5 || n1 < 5;
             if (!generic) {
                 // the three cells of each ring row are consecutive in the
                 // cell table: one contiguous slot segment per row, cell
                 // boundaries inside it give the ring position o0
-                int sa[3], s1[3], s2[3], len[3];
+                int sa[3], s1[3], s2[3], se[3], len[3];
 #pragma unroll
-                for (int r = 0; r < 3; r++) {
-                    int g1 = cy + r - 1;
-                    bool in = true;
-                    if (a.g.per1) g1 = g1 < 0 ? g1 + n1 : (g1 >= n1 ? g1 - n1 : g1);
-                    else in = g1 >= 0 && g1 < n1;
-                    if (in) {
-                        const int f = g1 * n0 + cx - 1;
-                        sa[r] = __ldg(a.starts + f);
-                        s1[r] = __ldg(a.starts + f + 1);
-                        s2[r] = __ldg(a.starts + f + 2);
-                        len[r] = __ldg(a.starts + f + 3) - sa[r];
-                    } else {
-                        sa[r] = s1[r] = s2[r] = 0;
-                        len[r] = 0;
+                for (int r = 0; r < 3; r++) {  // all 12 table loads issued together
+                    const int f = (cy + r - 1) * n0 + cx - 1;
+                    sa[r] = __ldg(a.starts + f);
+                    s1[r] = __ldg(a.starts + f + 1);
+                    s2[r] = __ldg(a.starts + f + 2);
+                    se[r] = __ldg(a.starts + f + 3);
+                }
+#pragma unroll
+                for (int r = 0; r < 3; r++) len[r] = se[r] - sa[r];
+                // The three row segments are walked in lock step: iteration i
+                // issues the i-th candidate of every row at once (three
+                // independent loads in flight).  Only the binary32 prefilter
+                // runs here -- the exact reference test is done in the warp's
+                // cooperative phase.  Enqueue order = ring order: rows are
+                // re-sorted by (ring cell, id) before the terms are summed.
+                const int t32 = (int)t;
+                const int lmax = max(len[0], max(len[1], len[2]));
+                for (int i = 0; i < lmax; i++) {
+                    float4 q[3];
+#pragma unroll
+                    for (int r = 0; r < 3; r++)
+                        if (i < len[r]) q[r] = __ldg(rec + sa[r] + i);
+#pragma unroll
+                    for (int r = 0; r < 3; r++) {
+                        if (i >= len[r]) continue;
+                        const int k = sa[r] + i;
+                        const float ddx = q[r].x - xf, ddy = q[r].y - yf;
+                        const float cf = (__float_as_uint(q[r].z) >> 31) ? pr.cf_1 : pr.cf_0;
+                        if (fmaf(ddx, ddx, ddy * ddy) > cf || k == t32) continue;
+                        if (nacc < ACC_MAX) ak[nacc] = k | (r << 30);  // row in the top bits
+                        nacc++;
                     }
                 }
-                const int total = len[0] + len[1] + len[2];
-                auto slot_of = [&](int it, int &r) {
-                    if (it < len[0]) {
-                        r = 0;
-                        return sa[0] + it;
+                if (nacc <= ACC_MAX) {
+                    // sort keys (ring cell, id) of the enqueued candidates
+                    for (int j = 0; j < nacc; j++) {
+                        const int kr = ak[j];
+                        const int r = kr >> 30, k = kr & 0x3fffffff;
+                        const int sr1 = r == 0 ? s1[0] : (r == 1 ? s1[1] : s1[2]);
+                        const int sr2 = r == 0 ? s2[0] : (r == 1 ? s2[1] : s2[2]);
+                        const unsigned c9 = (unsigned)(r * 3 + (k >= sr1) + (k >= sr2));
+                        const unsigned idk = __float_as_uint(__ldg(&rec[k].z)) & ID_MASK;
+                        akey[j] = ((unsigned long long)c9 << 32) | idk;
+                        ak[j] = k;
                     }
-                    if (it < len[0] + len[1]) {
-                        r = 1;
-                        return sa[1] + it - len[0];
-                    }
-                    r = 2;
-                    return sa[2] + it - len[0] - len[1];
-                };
-                int rn = 0;
-                int kn = total > 0 ? slot_of(0, rn) : 0;
-                float4 qn = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (total > 0) qn = __ldg(rec + kn);
-                for (int it = 0; it < total; it++) {
-                    // candidate it is in qn; prefetch candidate it + 1
-                    const int r = rn, k = kn;
-                    const float4 q = qn;
-                    if (it + 1 < total) {
-                        kn = slot_of(it + 1, rn);
-                        qn = __ldg(rec + kn);
-                    }
-                    if (k == t) continue;
-                    const unsigned qm = __float_as_uint(q.z);
-                    const int tj = (int)(qm >> 31);
-                    // binary32 prefilter only; the exact reference test runs
-                    // in the warp-cooperative phase below
-                    float ddx = q.x - xf, ddy = q.y - yf;
-                    if (a.g.per0 && fabsf(ddx) > a.halff0) ddx -= copysignf(a.sizef0, ddx);
-                    if (a.g.per1 && fabsf(ddy) > a.halff1) ddy -= copysignf(a.sizef1, ddy);
-                    if (fmaf(ddx, ddx, ddy * ddy) > pr.cf(tj)) continue;
-                    const int sr1 = r == 0 ? s1[0] : (r == 1 ? s1[1] : s1[2]);
-                    const int sr2 = r == 0 ? s2[0] : (r == 1 ? s2[1] : s2[2]);
-                    const unsigned c9 = (unsigned)(r * 3 + (k >= sr1) + (k >= sr2));
-                    if (nacc < ACC_MAX) {
-                        akey[nacc] = ((unsigned long long)c9 << 32) | (qm & ID_MASK);
-                        ak[nacc] = k;
-                    }
-                    nacc++;
                 }
                 if (nacc > ACC_MAX) generic = true;
             }
@@ -529,7 +511,50 @@ k_fast_step(DevStatus *st, int step) {
             }
             __syncwarp();
         }
-        if (!live) continue;
+        if (live) a.force[t] = make_double2(fx, fy);
+    }
+}
+
+// Per sorted slot: drift refresh, EM proposal, boundaries, new cell key and
+// rank, deposit of the new position for the next step's field.
+__global__ void __launch_bounds__(256)
+k_fast_update(DevStatus *st, int step) {
+    const FastArgs &a = cA;
+    const bool dead = st->abort != 0;
+    const int m = a.gg.n * a.gg.n;
+    const int n0 = a.g.n0, n1 = a.g.n1;
+    const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const float4 mer = __ldcs(rec + t);
+        const float xf = mer.x, yf = mer.y;
+        const unsigned meta = __float_as_uint(mer.z);
+        const unsigned wbits = __float_as_uint(mer.w);
+        const double x = (double)xf, y = (double)yf;
+        const int ti = (int)(meta >> 31);
+        const unsigned id = meta & ID_MASK;
+        const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + id)
+                                       : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
+        double fx = 0.0, fy = 0.0;
+        if (a.interact) {
+            const double2 f = __ldcs(a.force + t);
+            fx = f.x;
+            fy = f.y;
+        }
+        const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
+        const bool do_drift = a.refresh && !dead && !pinned;
+        float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
+        double bf0 = 0.0, bf1 = 0.0;
+        if (do_drift) {
+            const Cic bst = cic_stencil(x, y, a.gg, a.gd0, a.gd1);
+            bf0 = bst.f0;
+            bf1 = bst.f1;
+            const float2 *g2 = reinterpret_cast<const float2 *>(a.grad);
+            v00 = __ldg(g2 + bst.i00);
+            v10 = __ldg(g2 + bst.i10);
+            v01 = __ldg(g2 + bst.i01);
+            v11 = __ldg(g2 + bst.i11);
+        }
         // ---- drift refresh at the start-of-step position (coupling.py:302-325)
         const double chi = ti ? a.chi[1] : a.chi[0];
         double dr0 = 0.0, dr1 = 0.0;
@@ -596,12 +621,10 @@ k_fast_step(DevStatus *st, int step) {
         const double nx = (double)out.x, ny = (double)out.y;
         const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
                         cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
+        const int rank = (a.debug & 4) ? 0 : atomicAdd(&a.counts[key], 1);
         __stcs(reinterpret_cast<float4 *>(a.tmp) + t, out);
-        if (pend_t >= 0) __stcs(a.keyrank + pend_t, make_int2(pend_key, pend_rank));
-        pend_rank = atomicAdd(&a.counts[key], 1);
-        pend_key = key;
-        pend_t = t;
-        if (a.deposit && ok) {
+        __stcs(a.keyrank + t, make_int2(key, rank));
+        if (a.deposit && ok && (a.debug & 8) && !(a.debug & 2)) {
             const unsigned bits = ti ? a.bits[1] : a.bits[0];
             if (bits) {
                 const Cic c = cic_stencil(nx, ny, a.gg, a.gd0, a.gd1);
@@ -610,7 +633,6 @@ k_fast_step(DevStatus *st, int step) {
             }
         }
     }
-    if (pend_t >= 0) a.keyrank[pend_t] = make_int2(pend_key, pend_rank);
 }
 
 __global__ void __launch_bounds__(256)
@@ -652,7 +674,11 @@ __global__ void k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeo
     const int m = gg.n * gg.n;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
-        const Rec r = rec[t];
+        const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rec) + t);
+        Rec r;
+        r.x = rv.x;
+        r.y = rv.y;
+        r.meta = __float_as_uint(rv.z);
         const unsigned bits = (r.meta >> 31) ? bits1 : bits0;
         if (!bits) continue;
         const Cic c = cic_stencil((double)r.x, (double)r.y, gg, d0, d1);
@@ -711,7 +737,7 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 
 // ---------------------------------------------------------------------------
 struct cs_fast {
-    cs::Buf rec[2], tmp, keys, counts, starts[2], anchor0, rho_q;
+    cs::Buf rec[2], tmp, keys, counts, starts[2], anchor0, rho_q, force;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
@@ -732,6 +758,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->rec[1].ensure(nr));
     CS_TRY(f->tmp.ensure(nr));
     CS_TRY(f->keys.ensure(sizeof(int2) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->counts.ensure(sizeof(int) * (size_t)f->nflat));
     CS_CUDA(cudaMemset(f->counts.p, 0, f->counts.bytes));
     CS_TRY(f->starts[0].ensure(sizeof(int) * (size_t)(f->nflat + 1)));
@@ -747,7 +774,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->tmp, &f->keys, &f->counts, &f->starts[0],
-                   &f->starts[1], &f->anchor0, &f->rho_q})
+                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force})
         b->release();
     delete f;
 }
@@ -850,6 +877,11 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.starts = f->starts[f->cur].as<int>();
     a.tmp = f->tmp.as<Rec>();
     a.keyrank = f->keys.as<int2>();
+    a.force = f->force.as<double2>();
+    {
+        const char *dbg = getenv("CS_FAST_DEBUG");
+        a.debug = dbg ? atoi(dbg) : 0;
+    }
     a.counts = f->counts.as<int>();
     a.xi = (const float *)xi;
     a.grad = (const float *)s->grad;
@@ -883,9 +915,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.sz1 = make_exact_div(p.domain.hi[1] - p.domain.lo[1]);
     a.dom = p.domain;
     if (n > 0) {
-        static int resident = 0;  // blocks of k_fast_step resident per SM
+        static int resident = 0;  // blocks of k_fast_forces resident per SM
         if (!resident) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_step, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_forces, 256, 0);
             if (resident < 1) resident = 1;
         }
         int sms = 148;
@@ -894,14 +926,53 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
         CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0, cudaMemcpyHostToDevice,
                                         ctx->stream));
-        k_fast_step<<<grid, 256, 0, ctx->stream>>>(st, step);
+        if (a.interact) {
+            k_fast_forces<<<grid, 256, 0, ctx->stream>>>(st);
+            CS_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        // persistent grid: one contiguous processing front, so the atomics'
+        // working set (cell histogram + deposit rows near the front) stays in L2
+        static int resident_u = 0;
+        if (!resident_u) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident_u, k_fast_update, 256, 0);
+            if (resident_u < 1) resident_u = 1;
+        }
+        const int grid_u =
+            (int)(want < (long long)sms * resident_u ? want : (long long)sms * resident_u);
+        k_fast_update<<<grid_u, 256, 0, ctx->stream>>>(st, step);
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
     }
     return CS_OK;
 }
 
-int fast_resort(cs_ctx *ctx, cs_fast *f, long long n) { return fast_sort(ctx, f, n, 1 - f->cur); }
+// Next step's deposit over the freshly sorted records: consecutive threads
+// hit adjacent grid lines, so the reductions stay in L2 (deposited from the
+// old order they scattered over +-50 cell rows and missed L2 almost always).
+int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
+                const unsigned char bits[3]) {
+    CS_TRY(fast_sort(ctx, f, n, 1 - f->cur));
+    const char *dbg = getenv("CS_FAST_DEBUG");
+    const int debug = dbg ? atoi(dbg) : 0;
+    if (p.field_active && n > 0 && !(debug & (8 | 2))) {
+        static int resident = 0;
+        if (!resident) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_deposit, 256, 0);
+            if (resident < 1) resident = 1;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long want = (n + 255) / 256;
+        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
+        k_fast_deposit<<<grid, 256, 0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), n, gg,
+                                                      make_exact_div(gg.d0), make_exact_div(gg.d1),
+                                                      bits[0], bits[1], f->rho_q.as<int>());
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    return CS_OK;
+}
 
 int *fast_rho_q(cs_fast *f) { return f->rho_q.p ? f->rho_q.as<int>() : nullptr; }
 

@@ -50,7 +50,8 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
                DevStatus *st, int step);
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
                    const void *xi, DevStatus *st, int step);
-int fast_resort(cs_ctx *ctx, cs_fast *f, long long n);
+int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
+                const unsigned char bits[3]);
 bool fast_imported(const cs_fast *f);
 int *fast_rho_q(cs_fast *f);
 
@@ -319,7 +320,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 CS_TRY(fast_particles(ctx, sim->fast, c, s, xik, st, step));
             }
             StageMark m(sim, CS_STAGE_BIN);
-            CS_TRY(fast_resort(ctx, sim->fast, n));
+            CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits));
         }
         sim->steps_done += k;
         sim->last_launches = ctx->launches - l0;

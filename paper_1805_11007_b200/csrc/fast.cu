@@ -784,7 +784,19 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
     CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), f->starts[nxt].as<int>(), f->nflat,
                               f->counts.as<int>()));
     if (n > 0) {
-        k_fast_scatter<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        // persistent grid: a single processing front, so the destinations of
+        // the 16-byte scattered records (within ~+-50 cell rows of the front)
+        // complete their sectors in L2 before write-back
+        static int resident = 0;
+        if (!resident) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_scatter, 256, 0);
+            if (resident < 1) resident = 1;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long want = (n + 255) / 256;
+        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
+        k_fast_scatter<<<grid, 256, 0, ctx->stream>>>(
             f->tmp.as<Rec>(), f->keys.as<int2>(), n, f->starts[nxt].as<int>(),
             f->rec[nxt].as<Rec>());
         CS_LAUNCH_CHECK();

@@ -393,41 +393,80 @@ k_fast_forces(const DevStatus *st) {
                 }
 #pragma unroll
                 for (int r = 0; r < 3; r++) len[r] = se[r] - sa[r];
-                // The three row segments are walked in lock step: iteration i
-                // issues the i-th candidate of every row at once (three
-                // independent loads in flight).  Only the binary32 prefilter
-                // runs here -- the exact reference test is done in the warp's
-                // cooperative phase.  Enqueue order = ring order: rows are
-                // re-sorted by (ring cell, id) before the terms are summed.
-                const int t32 = (int)t;
-                const int lmax = max(len[0], max(len[1], len[2]));
-                for (int i = 0; i < lmax; i++) {
-                    float4 q[3];
-#pragma unroll
-                    for (int r = 0; r < 3; r++)
-                        if (i < len[r]) q[r] = __ldg(rec + sa[r] + i);
-#pragma unroll
-                    for (int r = 0; r < 3; r++) {
-                        if (i >= len[r]) continue;
-                        const int k = sa[r] + i;
-                        const float ddx = q[r].x - xf, ddy = q[r].y - yf;
-                        const float cf = (__float_as_uint(q[r].z) >> 31) ? pr.cf_1 : pr.cf_0;
-                        if (fmaf(ddx, ddx, ddy * ddy) > cf || k == t32) continue;
-                        if (nacc < ACC_MAX) ak[nacc] = k | (r << 30);  // row in the top bits
-                        nacc++;
+                // Candidate walk: the binary32 prefilter only, hits recorded
+                // as bits of per-row masks (row segments hold <= 32 records
+                // in the fast path).  The three rows are walked in lock step
+                // so three independent loads are in flight.
+                if (len[0] > 32 || len[1] > 32 || len[2] > 32) {
+                    generic = true;
+                } else {
+                    unsigned m0 = 0u, m1 = 0u, m2 = 0u;
+                    const int lmax = max(len[0], max(len[1], len[2]));
+                    // branch-free body: every row loads a valid record each
+                    // iteration (its last candidate, or the particle itself
+                    // for an empty row) and the mask bit is predicated
+                    const int t32 = (int)t;
+                    const int b0 = len[0] ? sa[0] : t32, e0 = len[0] ? len[0] - 1 : 0;
+                    const int b1 = len[1] ? sa[1] : t32, e1 = len[1] ? len[1] - 1 : 0;
+                    const int b2 = len[2] ? sa[2] : t32, e2 = len[2] ? len[2] - 1 : 0;
+                    for (int i = 0; i < lmax; i++) {
+                        const float4 q0 = __ldg(rec + b0 + min(i, e0));
+                        const float4 q1 = __ldg(rec + b1 + min(i, e1));
+                        const float4 q2 = __ldg(rec + b2 + min(i, e2));
+                        const float d0x = q0.x - xf, d0y = q0.y - yf;
+                        const float d1x = q1.x - xf, d1y = q1.y - yf;
+                        const float d2x = q2.x - xf, d2y = q2.y - yf;
+                        const float c0 = (__float_as_uint(q0.z) >> 31) ? pr.cf_1 : pr.cf_0;
+                        const float c1 = (__float_as_uint(q1.z) >> 31) ? pr.cf_1 : pr.cf_0;
+                        const float c2 = (__float_as_uint(q2.z) >> 31) ? pr.cf_1 : pr.cf_0;
+                        const unsigned bit = 1u << i;
+                        m0 |= (i < len[0] && fmaf(d0x, d0x, d0y * d0y) <= c0) ? bit : 0u;
+                        m1 |= (i < len[1] && fmaf(d1x, d1x, d1y * d1y) <= c1) ? bit : 0u;
+                        m2 |= (i < len[2] && fmaf(d2x, d2x, d2y * d2y) <= c2) ? bit : 0u;
                     }
-                }
-                if (nacc <= ACC_MAX) {
-                    // sort keys (ring cell, id) of the enqueued candidates
-                    for (int j = 0; j < nacc; j++) {
-                        const int kr = ak[j];
-                        const int r = kr >> 30, k = kr & 0x3fffffff;
-                        const int sr1 = r == 0 ? s1[0] : (r == 1 ? s1[1] : s1[2]);
-                        const int sr2 = r == 0 ? s2[0] : (r == 1 ? s2[1] : s2[2]);
-                        const unsigned c9 = (unsigned)(r * 3 + (k >= sr1) + (k >= sr2));
-                        const unsigned idk = __float_as_uint(__ldg(&rec[k].z)) & ID_MASK;
-                        akey[j] = ((unsigned long long)c9 << 32) | idk;
-                        ak[j] = k;
+                    m1 &= ~(1u << (t32 - sa[1]));  // the particle itself (middle row)
+                    nacc = __popc(m0) + __popc(m1) + __popc(m2);
+                    if (nacc <= ACC_MAX && nacc > 0) {
+                        // expand in ring order: rows, then slots (= cells in
+                        // o0 order); only hits sharing a cell may need the
+                        // ascending-id fix-up
+                        int j = 0;
+                        unsigned long long prev = 0;
+                        bool sorted = true;
+#pragma unroll
+                        for (int r = 0; r < 3; r++) {
+                            unsigned mm = r == 0 ? m0 : (r == 1 ? m1 : m2);
+                            while (mm) {
+                                const int i = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                const int k = sa[r] + i;
+                                const unsigned c9 =
+                                    (unsigned)(r * 3 + (k >= s1[r]) + (k >= s2[r]));
+                                const unsigned idk =
+                                    __float_as_uint(__ldg(&rec[k].z)) & ID_MASK;
+                                const unsigned long long kk =
+                                    ((unsigned long long)c9 << 32) | idk;
+                                sorted &= kk > prev || j == 0;
+                                prev = kk;
+                                akey[j] = kk;
+                                ak[j] = k;
+                                j++;
+                            }
+                        }
+                        if (!sorted) {
+                            for (int u = 1; u < nacc; u++) {
+                                const unsigned long long kk = akey[u];
+                                const int kv = ak[u];
+                                int v = u - 1;
+                                while (v >= 0 && akey[v] > kk) {
+                                    akey[v + 1] = akey[v];
+                                    ak[v + 1] = ak[v];
+                                    v--;
+                                }
+                                akey[v + 1] = kk;
+                                ak[v + 1] = kv;
+                            }
+                        }
                     }
                 }
                 if (nacc > ACC_MAX) generic = true;
@@ -438,21 +477,6 @@ k_fast_forces(const DevStatus *st) {
                 fx = ff.x;
                 fy = ff.y;
                 nacc = 0;
-            } else {
-                // canonical order: ring cell, then ascending id (arrivals are
-                // already grouped by ring cell; sort the few entries fully)
-                for (int i = 1; i < nacc; i++) {
-                    const unsigned long long kk = akey[i];
-                    const int kv = ak[i];
-                    int j = i - 1;
-                    while (j >= 0 && akey[j] > kk) {
-                        akey[j + 1] = akey[j];
-                        ak[j + 1] = ak[j];
-                        j--;
-                    }
-                    akey[j + 1] = kk;
-                    ak[j + 1] = kv;
-                }
             }
         }
         // ---- cooperative pair terms: the warp's accepted pairs (in the

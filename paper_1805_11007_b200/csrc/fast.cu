@@ -317,7 +317,7 @@ __device__ __noinline__ double2 ring_forces_generic(const float4 *__restrict__ r
 }
 
 constexpr int ACC_MAX = 8;          // accepted pairs buffered per particle
-constexpr int WARPS_PER_BLOCK = 8;  // k_fast_forces block = 256 threads
+constexpr int WARPS_PER_BLOCK = 4;  // k_fast_forces block = 128 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
 
 struct WarpQueue {
@@ -337,7 +337,7 @@ struct WarpQueue {
 // Pair forces of every sorted slot -> force[t] (binary64).  Warp-uniform
 // loop so that the whole warp can take part in the cooperative pair-term
 // phase.
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(128, 6)
 k_fast_forces(const DevStatus *st) {
     const FastArgs &a = cA;
     __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
@@ -953,17 +953,19 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     if (n > 0) {
         static int resident = 0;  // blocks of k_fast_forces resident per SM
         if (!resident) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_forces, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_forces, 128, 0);
             if (resident < 1) resident = 1;
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long want_f = (n + 127) / 128;
+        const int grid =
+            (int)(want_f < (long long)sms * resident ? want_f : (long long)sms * resident);
         const long long want = (n + 255) / 256;
-        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
         CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0, cudaMemcpyHostToDevice,
                                         ctx->stream));
         if (a.interact) {
-            k_fast_forces<<<grid, 256, 0, ctx->stream>>>(st);
+            k_fast_forces<<<grid, 128, 0, ctx->stream>>>(st);
             CS_LAUNCH_CHECK();
             ctx->launches += 1;
         }

@@ -278,9 +278,10 @@ k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double
     const long long m = (long long)n * n;
     double neg = 0.0;
     int bad = 0, anyneg = 0;
-    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
-         l += (long long)gridDim.x * blockDim.x) {
-        const int j = (int)(l / n), i = (int)(l - (long long)j * n);
+    // rows j = blockIdx.x + k gridDim.x; threads stride along the row
+    for (int j = blockIdx.x; j < n; j += gridDim.x)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const long long l = (long long)j * n + i;
         const double gx = d1_at(c, (long long)j * n, 1, i, n, per, kx);
         const double gy = d1_at(c, (long long)i, n, j, n, per, ky);
         store2(grad, l, gx, gy);
@@ -355,11 +356,12 @@ int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, vo
     const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
     const double wcell = gg.d0 * gg.d1;
     const int B = 256;
+    const int g2 = gg.n < 148 * 8 ? gg.n : 148 * 8;
     if (prec == CS_F64)
-        k_gradient<double><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
+        k_gradient<double><<<g2, B, 0, ctx->stream>>>(
             (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st, zero_q);
     else
-        k_gradient<float><<<grid_for(m, B, 148 * 16), B, 0, ctx->stream>>>(
+        k_gradient<float><<<g2, B, 0, ctx->stream>>>(
             (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st, zero_q);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
@@ -454,19 +456,35 @@ int gemm(cs_ctx *ctx, const double *A, const double *B, bool tb, const double *E
 }
 
 // ------------------------------------------------------------------ FFT
+// spectrum row ky (blockIdx.y), modes kx along x: multiply by
+// 1 / (n^2 (1 - dt d_c (lambda_y + lambda_x)))
 template <class CT>
-__global__ void k_mode_scale(CT *__restrict__ spec, int n, const double *__restrict__ lx,
-                             const double *__restrict__ ly, double dtdc, double inv_nn) {
+__global__ void __launch_bounds__(256)
+k_mode_scale(CT *__restrict__ spec, int n, const double *__restrict__ lx,
+             const double *__restrict__ ly, double dtdc, double inv_nn) {
     const int nh = n / 2 + 1;
-    const long long m = (long long)n * nh;
-    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
-         l += (long long)gridDim.x * blockDim.x) {
-        const int ky = (int)(l / nh), kx = (int)(l - (long long)ky * nh);
-        const double s = inv_nn / (1.0 - dtdc * (ly[ky] + lx[kx]));
-        CT v = spec[l];
-        v.x = v.x * s;
-        v.y = v.y * s;
-        spec[l] = v;
+    constexpr int U = 8;  // loads in flight per thread
+    for (int ky = blockIdx.x; ky < n; ky += gridDim.x) {
+        const double lyv = __ldg(ly + ky);
+        CT *row = spec + (long long)ky * nh;
+        for (int k0 = threadIdx.x; k0 < nh; k0 += U * blockDim.x) {
+            CT v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int kx = k0 + u * blockDim.x;
+                if (kx < nh) v[u] = row[kx];
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int kx = k0 + u * blockDim.x;
+                if (kx < nh) {
+                    const double s = inv_nn / (1.0 - dtdc * (lyv + __ldg(lx + kx)));
+                    v[u].x = v[u].x * s;
+                    v[u].y = v[u].y * s;
+                    row[kx] = v[u];
+                }
+            }
+        }
     }
 }
 
@@ -608,7 +626,7 @@ int field_solve_rhs(cs_field_ops *ops, void *out) {
         CS_TRY(cufft_check(cufftExecD2Z(ops->pf, (cufftDoubleReal *)ops->rhs,
                                         (cufftDoubleComplex *)ops->spec),
                            "D2Z"));
-        k_mode_scale<double2><<<grid_for(ms, B, 148 * 16), B, 0, ctx->stream>>>(
+        k_mode_scale<double2><<<(n < 148 * 8 ? n : 148 * 8), B, 0, ctx->stream>>>(
             (double2 *)ops->spec, n, ops->lx, ops->ly, dtdc, inv_nn);
         CS_LAUNCH_CHECK();
         CS_TRY(cufft_check(cufftExecZ2D(ops->pi, (cufftDoubleComplex *)ops->spec,
@@ -617,7 +635,7 @@ int field_solve_rhs(cs_field_ops *ops, void *out) {
     } else {
         CS_TRY(cufft_check(cufftExecR2C(ops->pf, (cufftReal *)ops->rhs, (cufftComplex *)ops->spec),
                            "R2C"));
-        k_mode_scale<float2><<<grid_for(ms, B, 148 * 16), B, 0, ctx->stream>>>(
+        k_mode_scale<float2><<<(n < 148 * 8 ? n : 148 * 8), B, 0, ctx->stream>>>(
             (float2 *)ops->spec, n, ops->lx, ops->ly, dtdc, inv_nn);
         CS_LAUNCH_CHECK();
         CS_TRY(cufft_check(cufftExecC2R(ops->pi, (cufftComplex *)ops->spec, (cufftReal *)out),

@@ -61,9 +61,7 @@ struct FastArgs {
     int2 *keyrank;      // (new cell key, rank inside the cell) per old slot
     double2 *force;     // pair force per sorted slot (binary64)
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
-                        // 2 skip deposits, 4 skip histogram atomics,
-                        // 8 deposit inside k_fast_update (old order) instead of
-                        // after the sort
+                        // 2 skip deposits, 4 skip histogram atomics
     int *counts;
     const float *xi;    // this step's (N, 2) increments, indexed by id
     const float *grad;  // (n_c^2, 2)
@@ -321,15 +319,11 @@ constexpr int WARPS_PER_BLOCK = 4;  // k_fast_forces block = 128 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
 
 struct WarpQueue {
-    // per-lane regions [lane * ACC_MAX, +ACC_MAX): the (ring cell, id) sort
-    // keys, then -- once every lane has sorted -- the x terms in their place
-    union {
-        unsigned long long key[QCAP];
-        double tx[QCAP];
-    };
-    int k[QCAP];                   // partner slot of each accepted pair
-    double ty[QCAP];
-    int incl[32];                  // inclusive prefix of the per-lane counts
+    int ak[QCAP];                  // per-lane regions [lane * ACC_MAX, +ACC_MAX): the
+                                   // lane's prefilter hits (slots) in canonical order
+    int ck[QCAP];                  // compact pair index e -> partner slot
+    double tx[QCAP], ty[QCAP];     // compact pair index e -> pair term
+    unsigned char own[QCAP];       // compact pair index e -> owner lane
     float ox[32], oy[32];          // owner coordinates
     int oti[32];
 };
@@ -362,8 +356,7 @@ k_fast_forces(const DevStatus *st) {
         // ---- pair forces over the reference ring (motion.py:206-243)
         double fx = 0.0, fy = 0.0;
         int nacc = 0;
-        unsigned long long *akey = wq.key + lane * ACC_MAX;  // this lane's region
-        int *ak = wq.k + lane * ACC_MAX;
+        int *ak = wq.ak + lane * ACC_MAX;  // this lane's region
         PairRow pr;
         pr.cut2_0 = ti ? a.pt.cut2[2] : a.pt.cut2[0];
         pr.cut2_1 = ti ? a.pt.cut2[3] : a.pt.cut2[1];
@@ -379,94 +372,43 @@ k_fast_forces(const DevStatus *st) {
             // image is the identity); seam/wall cells take the generic walk
             bool generic = cx < 1 || cx + 2 > n0 || cy < 1 || cy + 2 > n1 || n0 < 5 || n1 < 5;
             if (!generic) {
-                // the three cells of each ring row are consecutive in the
-                // cell table: one contiguous slot segment per row, cell
-                // boundaries inside it give the ring position o0
-                int sa[3], s1[3], s2[3], se[3], len[3];
+                // The three cells of each ring row are consecutive in the cell
+                // table, and inside a cell the records are in ascending id
+                // (k_fast_cellsort): slot order along the rows r = o1 + 1 is
+                // exactly the reference's ring order (o1, o0, id).  The walk
+                // runs over the concatenated row segments, tests the binary32
+                // prefilter and appends hits in that order.
+                int sa[3], se[3];
 #pragma unroll
-                for (int r = 0; r < 3; r++) {  // all 12 table loads issued together
+                for (int r = 0; r < 3; r++) {  // all 6 table loads issued together
                     const int f = (cy + r - 1) * n0 + cx - 1;
                     sa[r] = __ldg(a.starts + f);
-                    s1[r] = __ldg(a.starts + f + 1);
-                    s2[r] = __ldg(a.starts + f + 2);
                     se[r] = __ldg(a.starts + f + 3);
                 }
-#pragma unroll
-                for (int r = 0; r < 3; r++) len[r] = se[r] - sa[r];
-                // Candidate walk: the binary32 prefilter only, hits recorded
-                // as bits of per-row masks (row segments hold <= 32 records
-                // in the fast path).  The three rows are walked in lock step
-                // so three independent loads are in flight.
-                if (len[0] > 32 || len[1] > 32 || len[2] > 32) {
-                    generic = true;
-                } else {
-                    unsigned m0 = 0u, m1 = 0u, m2 = 0u;
-                    const int lmax = max(len[0], max(len[1], len[2]));
-                    // branch-free body: every row loads a valid record each
-                    // iteration (its last candidate, or the particle itself
-                    // for an empty row) and the mask bit is predicated
-                    const int t32 = (int)t;
-                    const int b0 = len[0] ? sa[0] : t32, e0 = len[0] ? len[0] - 1 : 0;
-                    const int b1 = len[1] ? sa[1] : t32, e1 = len[1] ? len[1] - 1 : 0;
-                    const int b2 = len[2] ? sa[2] : t32, e2 = len[2] ? len[2] - 1 : 0;
-                    for (int i = 0; i < lmax; i++) {
-                        const float4 q0 = __ldg(rec + b0 + min(i, e0));
-                        const float4 q1 = __ldg(rec + b1 + min(i, e1));
-                        const float4 q2 = __ldg(rec + b2 + min(i, e2));
-                        const float d0x = q0.x - xf, d0y = q0.y - yf;
-                        const float d1x = q1.x - xf, d1y = q1.y - yf;
-                        const float d2x = q2.x - xf, d2y = q2.y - yf;
-                        const float c0 = (__float_as_uint(q0.z) >> 31) ? pr.cf_1 : pr.cf_0;
-                        const float c1 = (__float_as_uint(q1.z) >> 31) ? pr.cf_1 : pr.cf_0;
-                        const float c2 = (__float_as_uint(q2.z) >> 31) ? pr.cf_1 : pr.cf_0;
-                        const unsigned bit = 1u << i;
-                        m0 |= (i < len[0] && fmaf(d0x, d0x, d0y * d0y) <= c0) ? bit : 0u;
-                        m1 |= (i < len[1] && fmaf(d1x, d1x, d1y * d1y) <= c1) ? bit : 0u;
-                        m2 |= (i < len[2] && fmaf(d2x, d2x, d2y * d2y) <= c2) ? bit : 0u;
+                const int e0 = se[0] - sa[0];
+                const int e01 = e0 + se[1] - sa[1];
+                const int tot = e01 + se[2] - sa[2];
+                const int d1 = sa[1] - e0, d2 = sa[2] - e01;
+                const int t32 = (int)t;
+                for (int j = 0; j < tot; j += 2) {  // two loads in flight per lane
+                    const int jb = min(j + 1, tot - 1);
+                    const int ka = j + (j < e0 ? sa[0] : (j < e01 ? d1 : d2));
+                    const int kb = jb + (jb < e0 ? sa[0] : (jb < e01 ? d1 : d2));
+                    const float4 qa = __ldg(rec + ka);
+                    const float4 qb = __ldg(rec + kb);
+                    const float dax = qa.x - xf, day = qa.y - yf;
+                    const float dbx = qb.x - xf, dby = qb.y - yf;
+                    const float ca = (__float_as_uint(qa.z) >> 31) ? pr.cf_1 : pr.cf_0;
+                    const float cb = (__float_as_uint(qb.z) >> 31) ? pr.cf_1 : pr.cf_0;
+                    const bool ha = ka != t32 && fmaf(dax, dax, day * day) <= ca;
+                    const bool hb = j + 1 < tot && kb != t32 && fmaf(dbx, dbx, dby * dby) <= cb;
+                    if (ha) {
+                        if (nacc < ACC_MAX) ak[nacc] = ka;
+                        nacc++;
                     }
-                    m1 &= ~(1u << (t32 - sa[1]));  // the particle itself (middle row)
-                    nacc = __popc(m0) + __popc(m1) + __popc(m2);
-                    if (nacc <= ACC_MAX && nacc > 0) {
-                        // expand in ring order: rows, then slots (= cells in
-                        // o0 order); only hits sharing a cell may need the
-                        // ascending-id fix-up
-                        int j = 0;
-                        unsigned long long prev = 0;
-                        bool sorted = true;
-#pragma unroll
-                        for (int r = 0; r < 3; r++) {
-                            unsigned mm = r == 0 ? m0 : (r == 1 ? m1 : m2);
-                            while (mm) {
-                                const int i = __ffs(mm) - 1;
-                                mm &= mm - 1;
-                                const int k = sa[r] + i;
-                                const unsigned c9 =
-                                    (unsigned)(r * 3 + (k >= s1[r]) + (k >= s2[r]));
-                                const unsigned idk =
-                                    __float_as_uint(__ldg(&rec[k].z)) & ID_MASK;
-                                const unsigned long long kk =
-                                    ((unsigned long long)c9 << 32) | idk;
-                                sorted &= kk > prev || j == 0;
-                                prev = kk;
-                                akey[j] = kk;
-                                ak[j] = k;
-                                j++;
-                            }
-                        }
-                        if (!sorted) {
-                            for (int u = 1; u < nacc; u++) {
-                                const unsigned long long kk = akey[u];
-                                const int kv = ak[u];
-                                int v = u - 1;
-                                while (v >= 0 && akey[v] > kk) {
-                                    akey[v + 1] = akey[v];
-                                    ak[v + 1] = ak[v];
-                                    v--;
-                                }
-                                akey[v + 1] = kk;
-                                ak[v + 1] = kv;
-                            }
-                        }
+                    if (hb) {
+                        if (nacc < ACC_MAX) ak[nacc] = kb;
+                        nacc++;
                     }
                 }
                 if (nacc > ACC_MAX) generic = true;
@@ -491,46 +433,34 @@ k_fast_forces(const DevStatus *st) {
             }
             const int T = __shfl_sync(0xffffffffu, incl, 31);
             if (T > 0) {
-                wq.incl[lane] = incl;
+                const int excl = incl - nacc;
+                for (int j = 0; j < nacc; j++) {
+                    wq.own[excl + j] = lane;
+                    wq.ck[excl + j] = ak[j];
+                }
                 wq.ox[lane] = xf;
                 wq.oy[lane] = yf;
                 wq.oti[lane] = ti;
                 __syncwarp();
                 for (int e = lane; e < T; e += 32) {
-                    // owner = first lane whose inclusive count exceeds e
-                    int ow = 0;
-#pragma unroll
-                    for (int step2 = 16; step2 > 0; step2 >>= 1)
-                        if (wq.incl[ow + step2 - 1] <= e) ow += step2;
-                    const int j = e - (ow ? wq.incl[ow - 1] : 0);
-                    const int slot = ow * ACC_MAX + j;
+                    const int ow = wq.own[e];
                     const float oxf = wq.ox[ow], oyf = wq.oy[ow];
-                    const int oti = wq.oti[ow];
-                    const float4 q = __ldg(rec + wq.k[slot]);
-                    const int tj = (int)(__float_as_uint(q.z) >> 31);
-                    const int tt = oti * 2 + tj;
-                    const double c2 = tt == 0 ? a.pt.cut2[0]
-                                              : (tt == 1 ? a.pt.cut2[1]
-                                                         : (tt == 2 ? a.pt.cut2[2] : a.pt.cut2[3]));
-                    const double ep = tt == 0 ? a.pt.eps[0]
-                                              : (tt == 1 ? a.pt.eps[1]
-                                                         : (tt == 2 ? a.pt.eps[2] : a.pt.eps[3]));
+                    const float4 q = __ldg(rec + wq.ck[e]);
+                    const int tt = wq.oti[ow] * 2 + (int)(__float_as_uint(q.z) >> 31);
                     double d0, d1;
                     const double r2 = pair_test(q.x, q.y, oxf, oyf, (double)oxf, (double)oyf,
-                                                3.0e38f, c2, d0, d1);
-                    if (r2 > 0.0) {  // accepted by the exact reference test
-                        const double2 term = pair_term(d0, d1, r2, ep);
-                        wq.tx[slot] = term.x;
-                        wq.ty[slot] = term.y;
-                    } else {
-                        wq.k[slot] = -1;  // prefilter false positive: no contribution
-                    }
+                                                3.0e38f, a.pt.cut2[tt], d0, d1);
+                    // a prefilter false positive contributes +0.0: the running
+                    // sums start at +0.0 and so are never -0.0, and x + 0.0 == x
+                    double2 term = make_double2(0.0, 0.0);
+                    if (r2 > 0.0) term = pair_term(d0, d1, r2, a.pt.eps[tt]);
+                    wq.tx[e] = term.x;
+                    wq.ty[e] = term.y;
                 }
                 __syncwarp();
                 for (int j = 0; j < nacc; j++) {
-                    if (wq.k[lane * ACC_MAX + j] < 0) continue;
-                    fx = dadd(fx, wq.tx[lane * ACC_MAX + j]);
-                    fy = dadd(fy, wq.ty[lane * ACC_MAX + j]);
+                    fx = dadd(fx, wq.tx[excl + j]);
+                    fy = dadd(fy, wq.ty[excl + j]);
                 }
             }
             __syncwarp();
@@ -648,25 +578,37 @@ k_fast_update(DevStatus *st, int step) {
         const int rank = (a.debug & 4) ? 0 : atomicAdd(&a.counts[key], 1);
         __stcs(reinterpret_cast<float4 *>(a.tmp) + t, out);
         __stcs(a.keyrank + t, make_int2(key, rank));
-        if (a.deposit && ok && (a.debug & 8) && !(a.debug & 2)) {
-            const unsigned bits = ti ? a.bits[1] : a.bits[0];
-            if (bits) {
-                const Cic c = cic_stencil(nx, ny, a.gg, a.gd0, a.gd1);
-                if (bits & 1u) cic_deposit_q(c, a.rho_q);
-                if (bits & 2u) cic_deposit_q(c, a.rho_q + m);
-            }
-        }
     }
 }
+
+// Counting-sort scatter: record t -> starts[key] + rank.  SCATTER_U records
+// per thread per iteration so that their key/rank, record and cell-table
+// loads are all in flight together (one record per iteration is bound by two
+// dependent load latencies); a block covers SCATTER_U * 256 consecutive slots.
+constexpr int SCATTER_U = 4;
 
 __global__ void __launch_bounds__(256)
 k_fast_scatter(const Rec *__restrict__ tmp, const int2 *__restrict__ keyrank, long long n,
                const int *__restrict__ starts, Rec *__restrict__ out) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int2 kr = keyrank[t];
-        const float4 r = __ldcs(reinterpret_cast<const float4 *>(tmp) + t);
-        reinterpret_cast<float4 *>(out)[starts[kr.x] + kr.y] = r;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x * SCATTER_U + threadIdx.x; t0 < n;
+         t0 += (long long)gridDim.x * blockDim.x * SCATTER_U) {
+        int2 kr[SCATTER_U];
+        float4 r[SCATTER_U];
+#pragma unroll
+        for (int u = 0; u < SCATTER_U; u++) {
+            const long long t = t0 + (long long)u * blockDim.x;
+            if (t < n) {
+                kr[u] = __ldcs(keyrank + t);
+                r[u] = __ldcs(reinterpret_cast<const float4 *>(tmp) + t);
+            }
+        }
+        int dst[SCATTER_U];
+#pragma unroll
+        for (int u = 0; u < SCATTER_U; u++)
+            if (t0 + (long long)u * blockDim.x < n) dst[u] = __ldg(starts + kr[u].x) + kr[u].y;
+#pragma unroll
+        for (int u = 0; u < SCATTER_U; u++)
+            if (t0 + (long long)u * blockDim.x < n) reinterpret_cast<float4 *>(out)[dst[u]] = r[u];
     }
 }
 
@@ -692,20 +634,106 @@ __global__ void k_fast_import(const float *__restrict__ pos, const float *__rest
     }
 }
 
-__global__ void k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeom gg,
-                               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
-                               int *__restrict__ rho_q) {
+// After the counting-sort scatter: put every cell's records in ascending id
+// (the scatter ranks are atomic-arrival order), which makes slot order the
+// reference's in-cell order for k_fast_forces, and CIC-deposit them for the
+// next step's field.  A warp owns groups of 32 consecutive cells: one
+// coalesced load of a group's records (~19 at the benchmark density, one per
+// lane); the cell heads form a 32-bit mask (one warp OR), from which each
+// record reads its cell's extent; it ranks itself by id among the cell's
+// records with shuffles and is written back only if it moves.  Warps own
+// disjoint slot ranges and __syncwarp orders every lane's read before any
+// write, so the permutation is in place.  Consecutive lanes deposit onto
+// neighbouring grid nodes (L2-local integer reductions, deterministic).
+__device__ __noinline__ void cell_insertion_sort(float4 *r4, int kb, int ke) {
+    for (int i = kb + 1; i < ke; i++) {
+        const float4 r = r4[i];
+        const unsigned id = __float_as_uint(r.z) & ID_MASK;
+        int j = i - 1;
+        while (j >= kb) {
+            const float4 q = r4[j];
+            if ((__float_as_uint(q.z) & ID_MASK) <= id) break;
+            r4[j + 1] = q;
+            j--;
+        }
+        if (j != i - 1) r4[j + 1] = r;
+    }
+}
+
+__device__ __noinline__ void deposit_record(float4 rv, const GridGeom &gg, const ExactDiv &d0,
+                                            const ExactDiv &d1, unsigned bits, int *rho_q,
+                                            int m) {
+    const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
+    if (bits & 1u) cic_deposit_q(c, rho_q);
+    if (bits & 2u) cic_deposit_q(c, rho_q + m);
+}
+
+__global__ void __launch_bounds__(256)
+k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGeom gg,
+               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q) {
+    float4 *r4 = reinterpret_cast<float4 *>(rec);
+    const int m = gg.n * gg.n;
+    const int lane = threadIdx.x & 31;
+    const unsigned below = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;  // bits 0..lane
+    for (long long c0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell;
+         c0 += (long long)gridDim.x * blockDim.x) {
+        const long long c = c0 + lane < ncell ? c0 + lane : ncell;
+        const int st = starts[c];
+        const int en = c < ncell ? starts[c + 1] : st;
+        const int base = __shfl_sync(0xffffffffu, st, 0);
+        const int cnt = __shfl_sync(0xffffffffu, en, 31) - base;
+        if (cnt > 32) {  // dense group (rare): serial per cell
+            if (en - st >= 2) cell_insertion_sort(r4, st, en);
+            for (int k = st; k < en; k++) {
+                const float4 rv = r4[k];
+                const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
+                if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
+            }
+            continue;
+        }
+        const bool valid = lane < cnt;
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) r = r4[base + lane];
+        const unsigned id = __float_as_uint(r.z) & ID_MASK;
+        const unsigned heads = __reduce_or_sync(0xffffffffu, en > st ? 1u << (st - base) : 0u);
+        const int s0 = 31 - __clz(heads & below);  // first slot of my cell (lane units)
+        const unsigned above = heads & ~below;
+        const int e1 = above ? __ffs(above) - 1 : cnt;
+        const int len = valid ? e1 - s0 : 0;
+        const int lmax = __reduce_max_sync(0xffffffffu, (unsigned)len);
+        int dst = -1;
+        if (lmax >= 2) {
+            int rank = 0;
+            for (int k = 0; k < lmax; k++) {
+                const unsigned idk = __shfl_sync(0xffffffffu, id, min(s0 + k, 31));
+                rank += (k < len && idk < id) ? 1 : 0;
+            }
+            if (len >= 2 && s0 + rank != lane) dst = base + s0 + rank;
+            // every lane's record must be read before any lane overwrites a
+            // slot: the shuffles order only registers, __syncwarp also memory
+            __syncwarp();
+            if (dst >= 0) r4[dst] = r;
+        }
+        if (valid) {
+            const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
+            if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, m);
+        }
+    }
+}
+
+// CIC deposit of the sorted records for the next step's field: consecutive
+// threads hit adjacent grid nodes, so the integer reductions stay L2-local
+// (deterministic: integer addition is associative).
+__global__ void __launch_bounds__(256)
+k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeom gg, ExactDiv d0, ExactDiv d1,
+               unsigned bits0, unsigned bits1, int *__restrict__ rho_q) {
     const int m = gg.n * gg.n;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
         const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rec) + t);
-        Rec r;
-        r.x = rv.x;
-        r.y = rv.y;
-        r.meta = __float_as_uint(rv.z);
-        const unsigned bits = (r.meta >> 31) ? bits1 : bits0;
+        const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
         if (!bits) continue;
-        const Cic c = cic_stencil((double)r.x, (double)r.y, gg, d0, d1);
+        const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
         if (bits & 1u) cic_deposit_q(c, rho_q);
         if (bits & 2u) cic_deposit_q(c, rho_q + m);
     }
@@ -818,7 +846,7 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        const long long want = (n + 255) / 256;
+        const long long want = (n + 256 * SCATTER_U - 1) / (256 * SCATTER_U);
         const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
         k_fast_scatter<<<grid, 256, 0, ctx->stream>>>(
             f->tmp.as<Rec>(), f->keys.as<int2>(), n, f->starts[nxt].as<int>(),
@@ -827,6 +855,37 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
         ctx->launches += 1;
     }
     f->cur = nxt;
+    return CS_OK;
+}
+
+static int persistent_grid(cs_ctx *ctx, const void *kern, int block, long long work,
+                           int *resident) {
+    if (!*resident) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(resident, kern, block, 0);
+        if (*resident < 1) *resident = 1;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const long long want = (work + block - 1) / block;
+    return (int)(want < (long long)sms * *resident ? want : (long long)sms * *resident);
+}
+
+// in-cell id order + the next step's deposit over the freshly sorted records
+static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
+                        const unsigned char bits[3]) {
+    if (p.n <= 0) return CS_OK;
+    const char *dbg = getenv("CS_FAST_DEBUG");
+    const int debug = dbg ? atoi(dbg) : 0;
+    const bool dep = p.field_active && !(debug & 2);
+    static int res = 0;
+    const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
+    k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, f->nflat, &res), 256,
+                     0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), f->starts[f->cur].as<int>(),
+                                       f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
+                                       dep ? bits[0] : 0u, dep ? bits[1] : 0u,
+                                       f->rho_q.as<int>());
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
     return CS_OK;
 }
 
@@ -840,15 +899,8 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
         CS_LAUNCH_CHECK();
     }
     CS_TRY(fast_sort(ctx, f, n, 0));
-    if (p.field_active) {
-        CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
-        if (n > 0) {
-            k_fast_deposit<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-                f->rec[0].as<Rec>(), n, gg, make_exact_div(gg.d0), make_exact_div(gg.d1),
-                bits[0], bits[1], f->rho_q.as<int>());
-            CS_LAUNCH_CHECK();
-        }
-    }
+    if (p.field_active) CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
+    CS_TRY(fast_cellfix(ctx, f, p, gg, bits));
     f->imported = true;
     return CS_OK;
 }
@@ -904,8 +956,9 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
     return CS_OK;
 }
 
+// part: 1 = pair forces, 2 = update (drift, EM, boundaries, binning)
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
-                   const void *xi, DevStatus *st, int step) {
+                   const void *xi, DevStatus *st, int step, int part) {
     const cs_sim_params &p = *c.p;
     const long long n = p.n;
     FastArgs a;
@@ -962,13 +1015,15 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         const int grid =
             (int)(want_f < (long long)sms * resident ? want_f : (long long)sms * resident);
         const long long want = (n + 255) / 256;
-        CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0, cudaMemcpyHostToDevice,
-                                        ctx->stream));
-        if (a.interact) {
+        if (part & 1)  // the update reuses the forces' constant block
+            CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0,
+                                            cudaMemcpyHostToDevice, ctx->stream));
+        if (a.interact && (part & 1)) {
             k_fast_forces<<<grid, 128, 0, ctx->stream>>>(st);
             CS_LAUNCH_CHECK();
             ctx->launches += 1;
         }
+        if (!(part & 2)) return CS_OK;
         // persistent grid: one contiguous processing front, so the atomics'
         // working set (cell histogram + deposit rows near the front) stays in L2
         static int resident_u = 0;
@@ -989,26 +1044,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
 // hit adjacent grid lines, so the reductions stay in L2 (deposited from the
 // old order they scattered over +-50 cell rows and missed L2 almost always).
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3]) {
-    CS_TRY(fast_sort(ctx, f, n, 1 - f->cur));
-    const char *dbg = getenv("CS_FAST_DEBUG");
-    const int debug = dbg ? atoi(dbg) : 0;
-    if (p.field_active && n > 0 && !(debug & (8 | 2))) {
-        static int resident = 0;
-        if (!resident) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_deposit, 256, 0);
-            if (resident < 1) resident = 1;
-        }
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        const long long want = (n + 255) / 256;
-        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
-        k_fast_deposit<<<grid, 256, 0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), n, gg,
-                                                      make_exact_div(gg.d0), make_exact_div(gg.d1),
-                                                      bits[0], bits[1], f->rho_q.as<int>());
-        CS_LAUNCH_CHECK();
-        ctx->launches += 1;
-    }
+                const unsigned char bits[3], int part) {
+    if (part & 1) CS_TRY(fast_sort(ctx, f, n, 1 - f->cur));
+    if (part & 2) CS_TRY(fast_cellfix(ctx, f, p, gg, bits));
     return CS_OK;
 }
 

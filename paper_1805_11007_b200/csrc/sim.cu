@@ -49,9 +49,9 @@ int fast_export(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
 int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
                DevStatus *st, int step);
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
-                   const void *xi, DevStatus *st, int step);
+                   const void *xi, DevStatus *st, int step, int part);
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3]);
+                const unsigned char bits[3], int part);
 bool fast_imported(const cs_fast *f);
 int *fast_rho_q(cs_fast *f);
 
@@ -317,10 +317,19 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
             }
             {
                 StageMark m(sim, CS_STAGE_FORCE);
-                CS_TRY(fast_particles(ctx, sim->fast, c, s, xik, st, step));
+                CS_TRY(fast_particles(ctx, sim->fast, c, s, xik, st, step, 1));
             }
-            StageMark m(sim, CS_STAGE_BIN);
-            CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits));
+            {
+                StageMark m(sim, CS_STAGE_UPDATE);
+                CS_TRY(fast_particles(ctx, sim->fast, c, s, xik, st, step, 2));
+            }
+            {
+                StageMark m(sim, CS_STAGE_BIN);
+                CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 1));
+            }
+            // in-cell id order + deposit for the next step's field
+            StageMark m(sim, CS_STAGE_DEPOSIT);
+            CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 2));
         }
         sim->steps_done += k;
         sim->last_launches = ctx->launches - l0;

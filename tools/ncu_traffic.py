@@ -7,7 +7,8 @@ import sys
 
 TIME = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
         "s": 1.0, "second": 1.0}
-KERNELS = {"k_fast_step": "force_update", "k_scan": "scan", "k_fast_scatter": "scatter"}
+KERNELS = {"k_fast_forces": "forces", "k_fast_update": "update", "k_scan": "scan",
+           "k_fast_scatter": "scatter"}
 
 
 def main(rep, out, config):

@@ -270,6 +270,17 @@ __device__ __forceinline__ void cic_deposit_q(const Cic &c, int *__restrict__ ou
     atomicAdd(&out[c.i11], __double2int_rn(dmul(c.w11, Q_SCALE)));
 }
 
+__device__ __forceinline__ PairRow make_pair_row(int ti) {
+    PairRow pr;
+    pr.cut2_0 = ti ? cA.pt.cut2[2] : cA.pt.cut2[0];
+    pr.cut2_1 = ti ? cA.pt.cut2[3] : cA.pt.cut2[1];
+    pr.eps_0 = ti ? cA.pt.eps[2] : cA.pt.eps[0];
+    pr.eps_1 = ti ? cA.pt.eps[3] : cA.pt.eps[1];
+    pr.cf_0 = ti ? cA.cutf2[2] : cA.cutf2[0];
+    pr.cf_1 = ti ? cA.cutf2[3] : cA.cutf2[1];
+    return pr;
+}
+
 // Generic ring walk for the rare particles the fast path does not cover
 // (cells on a periodic seam or wall, axes with < 3 cells, > ACC_MAX accepted
 // pairs): per-cell loop in ring order, ascending id inside a cell.
@@ -319,65 +330,65 @@ constexpr int WARPS_PER_BLOCK = 4;  // k_fast_forces block = 128 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
 
 struct WarpQueue {
-    int ak[QCAP];                  // per-lane regions [lane * ACC_MAX, +ACC_MAX): the
-                                   // lane's prefilter hits (slots) in canonical order
-    int ck[QCAP];                  // compact pair index e -> partner slot
-    double tx[QCAP], ty[QCAP];     // compact pair index e -> pair term
-    unsigned char own[QCAP];       // compact pair index e -> owner lane
+    int ck[QCAP];                  // queue entry -> partner slot
+    unsigned short oj[QCAP];       // queue entry -> owner term index lane * ACC_MAX + j
+    double tx[QCAP], ty[QCAP];     // owner term index -> pair term (lane regions)
     float ox[32], oy[32];          // owner coordinates
     int oti[32];
 };
 
-// Pair forces of every sorted slot -> force[t] (binary64).  Warp-uniform
-// loop so that the whole warp can take part in the cooperative pair-term
-// phase.
+// Pair forces of every sorted slot -> force[t] (binary64).
+//
+// Per warp iteration (32 consecutive slots, one per lane):
+//  1. candidate walk, warp-uniform: each lane runs over its ring's three row
+//     segments (the three cells of a ring row are consecutive in the cell
+//     table, and inside a cell the records are in ascending id
+//     (k_fast_cellfix), so slot order along the rows is exactly the
+//     reference's ring order (o1, o0, id)); binary32 prefilter hits are
+//     enqueued into the warp's queue at ballot/popc positions, tagged with
+//     the owner's term index lane * ACC_MAX + j (j = the owner's j-th hit);
+//  2. the queue is evaluated ~1/32 per lane: exact reference test (binary64)
+//     and pair term, written to the owner's term index (+0.0 for prefilter
+//     false positives: the owners' sums start at +0.0 and so are never -0.0,
+//     and x + 0.0 == x);
+//  3. each owner adds its terms in j order = canonical order.
+// Ring cells on a periodic seam or a wall, axes with < 5 cells, and lanes
+// with > ACC_MAX hits take the generic walk (ring_forces_generic) instead.
 __global__ void __launch_bounds__(128, 6)
 k_fast_forces(const DevStatus *st) {
     const FastArgs &a = cA;
     __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
     WarpQueue &wq = wq_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;  // lanes below this one
     const bool dead = st->abort != 0;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
     const int n0 = a.g.n0, n1 = a.g.n1;
     const long long wstride = (long long)gridDim.x * blockDim.x;
-    // warp-uniform loop: every lane runs the same number of iterations so the
-    // whole warp can take part in the cooperative pair-term phase
     for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
          base < a.n; base += wstride) {
         const long long t = base + lane;
+        const int t32 = (int)t;
         const bool live = t < a.n;
         float4 mer = make_float4(0.f, 0.f, 0.f, 0.f);
         if (live) mer = __ldg(rec + t);
         const float xf = mer.x, yf = mer.y;
-        const unsigned meta = __float_as_uint(mer.z);
         const double x = (double)xf, y = (double)yf;
-        const int ti = (int)(meta >> 31);
-        // ---- pair forces over the reference ring (motion.py:206-243)
+        const int ti = (int)(__float_as_uint(mer.z) >> 31);
+        const float cf0 = ti ? a.cutf2[2] : a.cutf2[0];
+        const float cf1 = ti ? a.cutf2[3] : a.cutf2[1];
         double fx = 0.0, fy = 0.0;
-        int nacc = 0;
-        int *ak = wq.ak + lane * ACC_MAX;  // this lane's region
-        PairRow pr;
-        pr.cut2_0 = ti ? a.pt.cut2[2] : a.pt.cut2[0];
-        pr.cut2_1 = ti ? a.pt.cut2[3] : a.pt.cut2[1];
-        pr.eps_0 = ti ? a.pt.eps[2] : a.pt.eps[0];
-        pr.eps_1 = ti ? a.pt.eps[3] : a.pt.eps[1];
-        pr.cf_0 = ti ? a.cutf2[2] : a.cutf2[0];
-        pr.cf_1 = ti ? a.cutf2[3] : a.cutf2[1];
+        int nacc = 0, tot = 0;
+        bool generic = false;
+        // ring row segments, compacted to the non-empty ones: the walk visits
+        // [k, kend), then [nb1, ne1), then [nb2, ne2)
+        int k = t32, kend = t32, nb1 = t32, ne1 = t32, nb2 = t32, ne2 = t32;
+        int cx = 0, cy = 0;
         if (live && !dead && a.interact) {
-            const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
-            const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
-            // fast path: interior cells only (no periodic wrap of the ring and,
-            // with >= 5 cells per axis, |dx| <= 2 cells < L/2 so the minimum
-            // image is the identity); seam/wall cells take the generic walk
-            bool generic = cx < 1 || cx + 2 > n0 || cy < 1 || cy + 2 > n1 || n0 < 5 || n1 < 5;
+            cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
+            cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
+            generic = cx < 1 || cx + 2 > n0 || cy < 1 || cy + 2 > n1 || n0 < 5 || n1 < 5;
             if (!generic) {
-                // The three cells of each ring row are consecutive in the cell
-                // table, and inside a cell the records are in ascending id
-                // (k_fast_cellsort): slot order along the rows r = o1 + 1 is
-                // exactly the reference's ring order (o1, o0, id).  The walk
-                // runs over the concatenated row segments, tests the binary32
-                // prefilter and appends hits in that order.
                 int sa[3], se[3];
 #pragma unroll
                 for (int r = 0; r < 3; r++) {  // all 6 table loads issued together
@@ -385,83 +396,97 @@ k_fast_forces(const DevStatus *st) {
                     sa[r] = __ldg(a.starts + f);
                     se[r] = __ldg(a.starts + f + 3);
                 }
-                const int e0 = se[0] - sa[0];
-                const int e01 = e0 + se[1] - sa[1];
-                const int tot = e01 + se[2] - sa[2];
-                const int d1 = sa[1] - e0, d2 = sa[2] - e01;
-                const int t32 = (int)t;
-                for (int j = 0; j < tot; j += 2) {  // two loads in flight per lane
-                    const int jb = min(j + 1, tot - 1);
-                    const int ka = j + (j < e0 ? sa[0] : (j < e01 ? d1 : d2));
-                    const int kb = jb + (jb < e0 ? sa[0] : (jb < e01 ? d1 : d2));
-                    const float4 qa = __ldg(rec + ka);
-                    const float4 qb = __ldg(rec + kb);
-                    const float dax = qa.x - xf, day = qa.y - yf;
-                    const float dbx = qb.x - xf, dby = qb.y - yf;
-                    const float ca = (__float_as_uint(qa.z) >> 31) ? pr.cf_1 : pr.cf_0;
-                    const float cb = (__float_as_uint(qb.z) >> 31) ? pr.cf_1 : pr.cf_0;
-                    const bool ha = ka != t32 && fmaf(dax, dax, day * day) <= ca;
-                    const bool hb = j + 1 < tot && kb != t32 && fmaf(dbx, dbx, dby * dby) <= cb;
-                    if (ha) {
-                        if (nacc < ACC_MAX) ak[nacc] = ka;
-                        nacc++;
-                    }
-                    if (hb) {
-                        if (nacc < ACC_MAX) ak[nacc] = kb;
-                        nacc++;
+                tot = (se[0] - sa[0]) + (se[1] - sa[1]) + (se[2] - sa[2]);
+#pragma unroll
+                for (int r = 2; r >= 0; r--) {  // push front, skipping empty rows
+                    if (se[r] > sa[r]) {
+                        nb2 = nb1;
+                        ne2 = ne1;
+                        nb1 = k;
+                        ne1 = kend;
+                        k = sa[r];
+                        kend = se[r];
                     }
                 }
-                if (nacc > ACC_MAX) generic = true;
-            }
-            if (generic) {
-                const double2 ff = ring_forces_generic(rec, a.starts, t, xf, yf, x, y, cx, cy,
-                                                       n0, n1, pr);
-                fx = ff.x;
-                fy = ff.y;
-                nacc = 0;
             }
         }
-        // ---- cooperative pair terms: the warp's accepted pairs (in the
-        // lanes' shared-memory regions) are evaluated ~1/32 per lane, then
-        // each owner adds its own terms in canonical order
-        {
-            int incl = nacc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+        // ---- 1. candidate walk (warp-uniform trip count)
+        const int totmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
+        int qn = 0;  // queue length (warp-uniform)
+        for (int j = 0; j < totmax; j += 2) {
+            const int ka = k;
+            if (++k == kend) {
+                k = nb1;
+                kend = ne1;
+                nb1 = nb2;
+                ne1 = ne2;
             }
-            const int T = __shfl_sync(0xffffffffu, incl, 31);
-            if (T > 0) {
-                const int excl = incl - nacc;
-                for (int j = 0; j < nacc; j++) {
-                    wq.own[excl + j] = lane;
-                    wq.ck[excl + j] = ak[j];
-                }
-                wq.ox[lane] = xf;
-                wq.oy[lane] = yf;
-                wq.oti[lane] = ti;
-                __syncwarp();
-                for (int e = lane; e < T; e += 32) {
-                    const int ow = wq.own[e];
-                    const float oxf = wq.ox[ow], oyf = wq.oy[ow];
-                    const float4 q = __ldg(rec + wq.ck[e]);
-                    const int tt = wq.oti[ow] * 2 + (int)(__float_as_uint(q.z) >> 31);
-                    double d0, d1;
-                    const double r2 = pair_test(q.x, q.y, oxf, oyf, (double)oxf, (double)oyf,
-                                                3.0e38f, a.pt.cut2[tt], d0, d1);
-                    // a prefilter false positive contributes +0.0: the running
-                    // sums start at +0.0 and so are never -0.0, and x + 0.0 == x
-                    double2 term = make_double2(0.0, 0.0);
-                    if (r2 > 0.0) term = pair_term(d0, d1, r2, a.pt.eps[tt]);
-                    wq.tx[e] = term.x;
-                    wq.ty[e] = term.y;
-                }
-                __syncwarp();
-                for (int j = 0; j < nacc; j++) {
-                    fx = dadd(fx, wq.tx[excl + j]);
-                    fy = dadd(fy, wq.ty[excl + j]);
-                }
+            const int kb = k;
+            if (++k == kend) {
+                k = nb1;
+                kend = ne1;
+                nb1 = nb2;
+                ne1 = ne2;
+            }
+            const float4 qa = __ldg(rec + (j < tot ? ka : t32));
+            const float4 qb = __ldg(rec + (j + 1 < tot ? kb : t32));
+            const float dax = qa.x - xf, day = qa.y - yf;
+            const float dbx = qb.x - xf, dby = qb.y - yf;
+            const float ca = (__float_as_uint(qa.z) >> 31) ? cf1 : cf0;
+            const float cb = (__float_as_uint(qb.z) >> 31) ? cf1 : cf0;
+            const bool ha = j < tot && ka != t32 && fmaf(dax, dax, day * day) <= ca;
+            const bool hb = j + 1 < tot && kb != t32 && fmaf(dbx, dbx, dby * dby) <= cb;
+            const unsigned ma = __ballot_sync(0xffffffffu, ha && nacc < ACC_MAX);
+            if (ha && nacc < ACC_MAX) {
+                const int e = qn + __popc(ma & lt);
+                wq.ck[e] = ka;
+                wq.oj[e] = (unsigned short)(lane * ACC_MAX + nacc);
+            }
+            nacc += ha;
+            qn += __popc(ma);
+            const unsigned mb = __ballot_sync(0xffffffffu, hb && nacc < ACC_MAX);
+            if (hb && nacc < ACC_MAX) {
+                const int e = qn + __popc(mb & lt);
+                wq.ck[e] = kb;
+                wq.oj[e] = (unsigned short)(lane * ACC_MAX + nacc);
+            }
+            nacc += hb;
+            qn += __popc(mb);
+        }
+        if (nacc > ACC_MAX) generic = true;  // its queued terms are computed, not used
+        if (generic) {
+            const double2 ff = ring_forces_generic(rec, a.starts, t, xf, yf, x, y, cx, cy, n0,
+                                                   n1, make_pair_row(ti));
+            fx = ff.x;
+            fy = ff.y;
+            nacc = 0;
+        }
+        // ---- 2. queue evaluation
+        if (qn > 0) {
+            wq.ox[lane] = xf;
+            wq.oy[lane] = yf;
+            wq.oti[lane] = ti;
+            __syncwarp();
+            for (int e = lane; e < qn; e += 32) {
+                const int o = wq.oj[e];
+                const int ow = o / ACC_MAX;
+                const float4 q = __ldg(rec + wq.ck[e]);
+                const int tt = wq.oti[ow] * 2 + (int)(__float_as_uint(q.z) >> 31);
+                // interior ring (fast path): |dx| <= 2 cells < L/2, so the
+                // minimum image is the identity (motion.py:231-236)
+                const double d0 = dsub((double)q.x, (double)wq.ox[ow]);
+                const double d1 = dsub((double)q.y, (double)wq.oy[ow]);
+                const double r2 = dadd(dmul(d0, d0), dmul(d1, d1));
+                double2 term = make_double2(0.0, 0.0);
+                if (!(r2 > a.pt.cut2[tt] || r2 == 0.0)) term = pair_term(d0, d1, r2, a.pt.eps[tt]);
+                wq.tx[o] = term.x;
+                wq.ty[o] = term.y;
+            }
+            __syncwarp();
+            // ---- 3. owners add their terms in canonical order
+            for (int j = 0; j < nacc; j++) {
+                fx = dadd(fx, wq.tx[lane * ACC_MAX + j]);
+                fy = dadd(fy, wq.ty[lane * ACC_MAX + j]);
             }
             __syncwarp();
         }

@@ -58,10 +58,11 @@ struct FastArgs {
     const Rec *rec;
     const int *starts;
     Rec *tmp;
-    int2 *keyrank;      // (new cell key, rank inside the cell) per old slot
+    int *keys;          // new cell key per old slot
     double2 *force;     // pair force per sorted slot (binary64)
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
-                        // 2 skip deposits, 4 skip histogram atomics
+                        // 2 skip deposits, 4 skip histogram atomics,
+                        // 32 xi read at the slot index (timing only: wrong results)
     int *counts;
     const float *xi;    // this step's (N, 2) increments, indexed by id
     const float *grad;  // (n_c^2, 2)
@@ -364,6 +365,8 @@ k_fast_forces(const DevStatus *st) {
     const bool dead = st->abort != 0;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
     const int n0 = a.g.n0, n1 = a.g.n1;
+    // persistent grid, warps sweep the slots together (a narrow processing
+    // front: ring rows are shared by concurrently running warps)
     const long long wstride = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
          base < a.n; base += wstride) {
@@ -512,8 +515,9 @@ k_fast_update(DevStatus *st, int step) {
         const double x = (double)xf, y = (double)yf;
         const int ti = (int)(meta >> 31);
         const unsigned id = meta & ID_MASK;
-        const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + id)
-                                       : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
+        const unsigned zi = (a.debug & 32) ? (unsigned)t : id;  // 32: diagnostic only
+        const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + zi)
+                                       : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + zi);
         double fx = 0.0, fy = 0.0;
         if (a.interact) {
             const double2 f = __ldcs(a.force + t);
@@ -595,42 +599,45 @@ k_fast_update(DevStatus *st, int step) {
             out.z = mer.z;
             out.w = __uint_as_float(((unsigned)(w1 & 0xffff) << 16) | (unsigned)(w0 & 0xffff));
         }
-        // ---- bin the stored (binary32) coordinate for the next step; the
-        // histogram atomic's return value is the record's rank in its cell
+        // ---- bin the stored (binary32) coordinate for the next step (cell
+        // histogram: a reduction, no value returned)
         const double nx = (double)out.x, ny = (double)out.y;
         const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
                         cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
-        const int rank = (a.debug & 4) ? 0 : atomicAdd(&a.counts[key], 1);
+        if (!(a.debug & 4)) atomicAdd(&a.counts[key], 1);
         __stcs(reinterpret_cast<float4 *>(a.tmp) + t, out);
-        __stcs(a.keyrank + t, make_int2(key, rank));
+        __stcs(a.keys + t, key);
     }
 }
 
-// Counting-sort scatter: record t -> starts[key] + rank.  SCATTER_U records
-// per thread per iteration so that their key/rank, record and cell-table
-// loads are all in flight together (one record per iteration is bound by two
-// dependent load latencies); a block covers SCATTER_U * 256 consecutive slots.
+// Counting-sort scatter.  The scan left cell c's first slot in cur[c + 1]
+// (cur[0] == 0); each record claims cur[key + 1]++ , so afterwards
+// cur[c] == starts[c] for every c: the array is the next cell table.  The
+// arrival order inside a cell is arbitrary; k_fast_cellfix restores id order.
+// SCATTER_U records per thread per iteration keep their key, record and
+// claim round trips in flight together; a block covers SCATTER_U * 256
+// consecutive slots.
 constexpr int SCATTER_U = 4;
 
 __global__ void __launch_bounds__(256)
-k_fast_scatter(const Rec *__restrict__ tmp, const int2 *__restrict__ keyrank, long long n,
-               const int *__restrict__ starts, Rec *__restrict__ out) {
+k_fast_scatter(const Rec *__restrict__ tmp, const int *__restrict__ keys, long long n,
+               int *__restrict__ cur, Rec *__restrict__ out) {
     for (long long t0 = (long long)blockIdx.x * blockDim.x * SCATTER_U + threadIdx.x; t0 < n;
          t0 += (long long)gridDim.x * blockDim.x * SCATTER_U) {
-        int2 kr[SCATTER_U];
+        int key[SCATTER_U];
         float4 r[SCATTER_U];
 #pragma unroll
         for (int u = 0; u < SCATTER_U; u++) {
             const long long t = t0 + (long long)u * blockDim.x;
             if (t < n) {
-                kr[u] = __ldcs(keyrank + t);
+                key[u] = __ldcs(keys + t);
                 r[u] = __ldcs(reinterpret_cast<const float4 *>(tmp) + t);
             }
         }
         int dst[SCATTER_U];
 #pragma unroll
         for (int u = 0; u < SCATTER_U; u++)
-            if (t0 + (long long)u * blockDim.x < n) dst[u] = __ldg(starts + kr[u].x) + kr[u].y;
+            if (t0 + (long long)u * blockDim.x < n) dst[u] = atomicAdd(cur + key[u] + 1, 1);
 #pragma unroll
         for (int u = 0; u < SCATTER_U; u++)
             if (t0 + (long long)u * blockDim.x < n) reinterpret_cast<float4 *>(out)[dst[u]] = r[u];
@@ -640,7 +647,7 @@ k_fast_scatter(const Rec *__restrict__ tmp, const int2 *__restrict__ keyrank, lo
 // caller arrays (id order) -> records (id order) + keys/ranks + histogram
 __global__ void k_fast_import(const float *__restrict__ pos, const float *__restrict__ anchor,
                               const uint8_t *__restrict__ type, long long n, BinGeom g,
-                              Rec *__restrict__ tmp, int2 *__restrict__ keyrank,
+                              Rec *__restrict__ tmp, int *__restrict__ keys,
                               int *__restrict__ counts, float *__restrict__ anchor0) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -655,7 +662,8 @@ __global__ void k_fast_import(const float *__restrict__ pos, const float *__rest
         reinterpret_cast<float2 *>(anchor0)[i] = reinterpret_cast<const float2 *>(anchor)[i];
         const int key = cell_axis((double)p.y, g.lo1, g.eff1, g.n1) * g.n0 +
                         cell_axis((double)p.x, g.lo0, g.eff0, g.n0);
-        keyrank[i] = make_int2(key, atomicAdd(&counts[key], 1));
+        keys[i] = key;
+        atomicAdd(&counts[key], 1);
     }
 }
 
@@ -813,6 +821,8 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 }  // namespace cs
 
 // ---------------------------------------------------------------------------
+constexpr int STARTS_OFF = 3;
+
 struct cs_fast {
     cs::Buf rec[2], tmp, keys, counts, starts[2], anchor0, rho_q, force;
     int cur = 0;
@@ -826,6 +836,8 @@ int field_solve_rhs(cs_field_ops *ops, void *out);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
                     DevStatus *st, int step, int *zero_q = nullptr);
 
+static int *cell_table(cs_fast *f, int b) { return f->starts[b].as<int>() + STARTS_OFF; }
+
 int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg) {
     auto *f = new cs_fast();
     *out = f;
@@ -834,12 +846,18 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
     CS_TRY(f->tmp.ensure(nr));
-    CS_TRY(f->keys.ensure(sizeof(int2) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(f->keys.ensure(sizeof(int) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->counts.ensure(sizeof(int) * (size_t)f->nflat));
     CS_CUDA(cudaMemset(f->counts.p, 0, f->counts.bytes));
-    CS_TRY(f->starts[0].ensure(sizeof(int) * (size_t)(f->nflat + 1)));
-    CS_TRY(f->starts[1].ensure(sizeof(int) * (size_t)(f->nflat + 1)));
+    // cell tables: nflat + 1 starts plus one slot for the scan's shifted
+    // output (k_fast_scatter); the table begins STARTS_OFF ints into its
+    // buffer so that the scan's vector stores (at table + 1) stay 16-B
+    // aligned; entry 0 stays 0
+    for (int b = 0; b < 2; b++) {
+        CS_TRY(f->starts[b].ensure(sizeof(int) * (size_t)(f->nflat + 2 + STARTS_OFF)));
+        CS_CUDA(cudaMemset(f->starts[b].p, 0, f->starts[b].bytes));
+    }
     CS_TRY(f->anchor0.ensure(sizeof(float) * 2 * (size_t)(n > 0 ? n : 1)));
     if (gg) {
         CS_TRY(f->rho_q.ensure(sizeof(int) * 2 * (size_t)gg->n * gg->n));
@@ -858,7 +876,7 @@ void fast_destroy(cs_fast *f) {
 
 static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
     // scan the histogram into the next cell table and reset it in the same pass
-    CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), f->starts[nxt].as<int>(), f->nflat,
+    CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), cell_table(f, nxt) + 1, f->nflat,
                               f->counts.as<int>()));
     if (n > 0) {
         // persistent grid: a single processing front, so the destinations of
@@ -874,7 +892,7 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
         const long long want = (n + 256 * SCATTER_U - 1) / (256 * SCATTER_U);
         const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
         k_fast_scatter<<<grid, 256, 0, ctx->stream>>>(
-            f->tmp.as<Rec>(), f->keys.as<int2>(), n, f->starts[nxt].as<int>(),
+            f->tmp.as<Rec>(), f->keys.as<int>(), n, cell_table(f, nxt),
             f->rec[nxt].as<Rec>());
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
@@ -905,7 +923,7 @@ static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const G
     static int res = 0;
     const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
     k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, f->nflat, &res), 256,
-                     0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), f->starts[f->cur].as<int>(),
+                     0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), cell_table(f, f->cur),
                                        f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
                                        dep ? bits[0] : 0u, dep ? bits[1] : 0u,
                                        f->rho_q.as<int>());
@@ -920,7 +938,7 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     if (n > 0) {
         k_fast_import<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
             (const float *)s->pos, (const float *)s->anchor, s->type, n, g, f->tmp.as<Rec>(),
-            f->keys.as<int2>(), f->counts.as<int>(), f->anchor0.as<float>());
+            f->keys.as<int>(), f->counts.as<int>(), f->anchor0.as<float>());
         CS_LAUNCH_CHECK();
     }
     CS_TRY(fast_sort(ctx, f, n, 0));
@@ -957,6 +975,7 @@ struct FastStepCfg {
     GridGeom gg;
     cs_field_ops *ops;
     unsigned char bits[3];
+    int overlap = 0;  // the field solve runs concurrently on a side stream
 };
 
 int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
@@ -988,9 +1007,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     const long long n = p.n;
     FastArgs a;
     a.rec = f->rec[f->cur].as<Rec>();
-    a.starts = f->starts[f->cur].as<int>();
+    a.starts = cell_table(f, f->cur);
     a.tmp = f->tmp.as<Rec>();
-    a.keyrank = f->keys.as<int2>();
+    a.keys = f->keys.as<int>();
     a.force = f->force.as<double2>();
     {
         const char *dbg = getenv("CS_FAST_DEBUG");
@@ -1036,9 +1055,12 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        // with the field solve running concurrently (side stream), leave one
+        // block's worth of registers per SM to its kernels
+        const int per_sm = (c.overlap && resident > 1) ? resident - 1 : resident;
         const long long want_f = (n + 127) / 128;
         const int grid =
-            (int)(want_f < (long long)sms * resident ? want_f : (long long)sms * resident);
+            (int)(want_f < (long long)sms * per_sm ? want_f : (long long)sms * per_sm);
         const long long want = (n + 255) / 256;
         if (part & 1)  // the update reuses the forces' constant block
             CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0,

@@ -16,6 +16,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "_build", "libchemo_b200.so")
+if os.environ.get("CS_LIB"):  # tuning experiments: an alternative build of the same sources
+    SO_PATH = os.path.abspath(os.environ["CS_LIB"])
 
 CS_OK, CS_NONFINITE, CS_OVERSHOOT, CS_UNSETTLED, CS_FIELD_NONFINITE = 0, 1, 2, 3, 4
 CS_F64, CS_F32 = 0, 1

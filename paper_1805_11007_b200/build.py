@@ -46,17 +46,24 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          extra: list[str] | None = None) -> str:
+    """``out``/``extra``: an alternative output path and extra nvcc flags
+    (tuning experiments, e.g. ``-DCS_SCATTER_U=8``; load one with CS_LIB)."""
+    so = out or SO
+    if not force and out is None and up_to_date():
         return SO
     os.makedirs(OUT_DIR, exist_ok=True)
+    obj_dir = OUT_DIR if out is None else so + ".objs"
+    os.makedirs(obj_dir, exist_ok=True)
     objs = []
     nv = nvcc()
     cuda_lib = os.path.join(os.path.dirname(os.path.dirname(nv)), "lib64")
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-              *ARCH, "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
+              *ARCH, "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include"),
+              *(extra or [])]
     for src in sources():
-        obj = os.path.join(OUT_DIR, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         cmd = [nv, "-c", src, "-o", obj, *common]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -65,16 +72,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     cmd = [nv, "-shared", *ARCH, "-o", tmp, *objs, "-L", cuda_lib, "-lcufft",
            "-Xlinker", f"-rpath={cuda_lib}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, extra=extra))

@@ -499,7 +499,10 @@ k_fast_forces(const DevStatus *st) {
 
 // Per sorted slot: drift refresh, EM proposal, boundaries, new cell key and
 // rank, deposit of the new position for the next step's field.
-__global__ void __launch_bounds__(256)
+#ifndef CS_UPDATE_MINB
+#define CS_UPDATE_MINB 5  // measured: (256) 245 us, (256,5) 220, (256,6) 272
+#endif
+__global__ void __launch_bounds__(256, CS_UPDATE_MINB)
 k_fast_update(DevStatus *st, int step) {
     const FastArgs &a = cA;
     const bool dead = st->abort != 0;
@@ -617,7 +620,10 @@ k_fast_update(DevStatus *st, int step) {
 // SCATTER_U records per thread per iteration keep their key, record and
 // claim round trips in flight together; a block covers SCATTER_U * 256
 // consecutive slots.
-constexpr int SCATTER_U = 4;
+#ifndef CS_SCATTER_U
+#define CS_SCATTER_U 8
+#endif
+constexpr int SCATTER_U = CS_SCATTER_U;
 
 __global__ void __launch_bounds__(256)
 k_fast_scatter(const Rec *__restrict__ tmp, const int *__restrict__ keys, long long n,

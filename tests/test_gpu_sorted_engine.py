@@ -143,3 +143,40 @@ def test_sorted_engine_reports_nonfinite_with_reference_message():
     real._sim.import_state()
     with pytest.raises(cs.SimulationError, match=r"step 1: non-finite coordinate for particle 17"):
         real.step()
+
+
+def test_fused_spectral_solve_4096_vs_oracle_and_cufft(monkeypatch):
+    """The fused three-pass periodic solve (csrc/spectral.cu, used for a
+    binary32 4096^2 grid): one step against the fp64 oracle (the tolerance of
+    the 256^2 test above) and against the same engine's cuFFT path, from a
+    non-zero field so that decay, secretion and consumption all enter."""
+    n, n_c = 200_000, 4096
+    pos, sp, xi = _inputs(n, 5)
+    rng = np.random.default_rng(9)
+    c0 = (0.5 + 0.1 * rng.standard_normal(n_c * n_c)).astype(np.float32).astype(np.float64)
+    x = torch.as_tensor(xi, device="cuda")
+    res = {}
+    for mode in ("fused", "cufft"):
+        if mode == "cufft":
+            monkeypatch.setenv("CS_CUFFT", "1")
+        else:
+            monkeypatch.delenv("CS_CUFFT", raising=False)
+        a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c, c0=c0)
+        a.step(x[0], 1)
+        a.export_state()
+        assert a.status().code == 0
+        res[mode] = {k: sa[k].double().cpu().numpy() for k in ("pos", "c", "grad")}
+    monkeypatch.delenv("CS_CUFFT", raising=False)
+    cmax = np.abs(res["cufft"]["c"]).max()
+    assert np.max(np.abs(res["fused"]["c"] - res["cufft"]["c"])) <= 1e-6 * cmax
+    e, c, cell = oracle.pair_table(radii=(0.002, 0.004))
+    field = dict(n_c=n_c, boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=0.03, gamma=0.1,
+                 kernel="cic", secretes=(True, False), consumes=(False, True),
+                 c0=c0, splu_max=0)
+    o = OracleSim(pos.astype(np.float64), sp, lo=[-0.5] * 2, hi=[0.5] * 2,
+                  periodic=(True, True), dt=1e-5, diffusion=(1.0, 0.5), eps_tab=e, cut_tab=c,
+                  cell_cutoff=cell, chi=(1.0, -0.5), chi_pinned=(False, False), field=field,
+                  fp32=True, anchor_mode="wraps", nthreads=os.cpu_count())
+    o.step(xi[0].astype(np.float64))
+    assert np.max(np.abs(res["fused"]["c"] - o.c)) <= 1e-5 * max(1.0, np.abs(o.c).max())
+    assert np.max(np.abs(res["fused"]["pos"] - o.pos)) <= 4 * 2.0 ** -24

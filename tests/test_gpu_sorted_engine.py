@@ -180,3 +180,27 @@ def test_fused_spectral_solve_4096_vs_oracle_and_cufft(monkeypatch):
     o.step(xi[0].astype(np.float64))
     assert np.max(np.abs(res["fused"]["c"] - o.c)) <= 1e-5 * max(1.0, np.abs(o.c).max())
     assert np.max(np.abs(res["fused"]["pos"] - o.pos)) <= 4 * 2.0 ** -24
+
+
+def test_vectorized_periodic_gradient_bitwise_equals_generic(monkeypatch):
+    """k_gradient_per4 (16-byte accesses, periodic binary32 grids) against the
+    generic k_gradient: identical bits over several coupled steps."""
+    n, n_c = 60_000, 512
+    pos, sp, xi = _inputs(n, 11)
+    rng = np.random.default_rng(2)
+    c0 = (0.2 + 0.05 * rng.standard_normal(n_c * n_c)).astype(np.float32).astype(np.float64)
+    x = torch.as_tensor(xi, device="cuda")
+    out = {}
+    for mode in ("vec", "generic"):
+        if mode == "generic":
+            monkeypatch.setenv("CS_GRAD_GENERIC", "1")
+        else:
+            monkeypatch.delenv("CS_GRAD_GENERIC", raising=False)
+        a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c, c0=c0)
+        a.step(x, 5)
+        a.export_state()
+        assert a.status().code == 0
+        out[mode] = {k: sa[k].clone() for k in ("pos", "c", "grad")}
+    monkeypatch.delenv("CS_GRAD_GENERIC", raising=False)
+    for k in ("pos", "c", "grad"):
+        assert torch.equal(out["vec"][k], out["generic"][k]), k

@@ -43,6 +43,9 @@ enum cs_code {
     CS_OVERSHOOT = 2,        /* overshoot beyond one width (motion.py:388-389) */
     CS_UNSETTLED = 3,        /* reflection failed to settle (motion.py:399-400) */
     CS_FIELD_NONFINITE = 4,  /* step_field non-finite (field.py:229-231) */
+    CS_DEPOSIT_OVERFLOW = 5, /* sorted engine only: a cell holds more particles than its
+                                int32 fixed-point deposit can sum exactly (no reference
+                                counterpart; the direct engine has no such limit) */
     CS_ERR_CUDA = -1,
     CS_ERR_PARAM = -2,
     CS_ERR_NOMEM = -3,

@@ -709,21 +709,30 @@ __device__ __noinline__ void deposit_record(float4 rv, const GridGeom &gg, const
 
 __global__ void __launch_bounds__(256)
 k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGeom gg,
-               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q) {
+               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q,
+               int cell_max, DevStatus *st, int step) {
     float4 *r4 = reinterpret_cast<float4 *>(rec);
+    DevStatus *dst_ = st;
     const int m = gg.n * gg.n;
     const int lane = threadIdx.x & 31;
     const unsigned below = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;  // bits 0..lane
     for (long long c0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell;
          c0 += (long long)gridDim.x * blockDim.x) {
         const long long c = c0 + lane < ncell ? c0 + lane : ncell;
-        const int st = starts[c];
-        const int en = c < ncell ? starts[c + 1] : st;
-        const int base = __shfl_sync(0xffffffffu, st, 0);
+        const int st0 = starts[c];
+        const int en = c < ncell ? starts[c + 1] : st0;
+        const int base = __shfl_sync(0xffffffffu, st0, 0);
         const int cnt = __shfl_sync(0xffffffffu, en, 31) - base;
+        if ((bits0 | bits1) && en - st0 > cell_max) {
+            // a grid node could collect > 511 particle masses of 2^22: its
+            // int32 fixed-point sum would overflow
+            atomicMin(&dst_->key, err_key(3, c, CS_DEPOSIT_OVERFLOW));
+            dst_->abort = 1;
+            dst_->step = step;
+        }
         if (cnt > 32) {  // dense group (rare): serial per cell
-            if (en - st >= 2) cell_insertion_sort(r4, st, en);
-            for (int k = st; k < en; k++) {
+            if (en - st0 >= 2) cell_insertion_sort(r4, st0, en);
+            for (int k = st0; k < en; k++) {
                 const float4 rv = r4[k];
                 const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
                 if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
@@ -734,7 +743,7 @@ k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGe
         float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) r = r4[base + lane];
         const unsigned id = __float_as_uint(r.z) & ID_MASK;
-        const unsigned heads = __reduce_or_sync(0xffffffffu, en > st ? 1u << (st - base) : 0u);
+        const unsigned heads = __reduce_or_sync(0xffffffffu, en > st0 ? 1u << (st0 - base) : 0u);
         const int s0 = 31 - __clz(heads & below);  // first slot of my cell (lane units)
         const unsigned above = heads & ~below;
         const int e1 = above ? __ffs(above) - 1 : cnt;
@@ -834,6 +843,7 @@ struct cs_fast {
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
+    double eff0 = 1.0, eff1 = 1.0;  // cell sides
 };
 
 namespace cs {
@@ -853,6 +863,8 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     auto *f = new cs_fast();
     *out = f;
     f->nflat = (long long)g.n0 * g.n1;
+    f->eff0 = g.eff0;
+    f->eff1 = g.eff1;
     const size_t nr = sizeof(Rec) * (size_t)(n > 0 ? n : 1);
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
@@ -924,9 +936,19 @@ static int persistent_grid(cs_ctx *ctx, const void *kern, int block, long long w
     return (int)(want < (long long)sms * *resident ? want : (long long)sms * *resident);
 }
 
+// Largest cell population for which the int32 fixed-point deposit is exact:
+// a node's CIC support (two grid spacings per axis) overlaps at most
+// floor(2 d / eff) + 2 cells per axis, and a node overflows only past 511
+// contributions of 2^22.
+static int deposit_cell_max(const GridGeom &gg, const cs_fast *f) {
+    const double k0 = floor(2.0 * gg.d0 / f->eff0) + 2.0, k1 = floor(2.0 * gg.d1 / f->eff1) + 2.0;
+    const double m = floor(511.0 / (k0 * k1));
+    return m < 1.0 ? 1 : (int)m;
+}
+
 // in-cell id order + the next step's deposit over the freshly sorted records
 static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
-                        const unsigned char bits[3]) {
+                        const unsigned char bits[3], DevStatus *st, int step) {
     if (p.n <= 0) return CS_OK;
     const char *dbg = getenv("CS_FAST_DEBUG");
     const int debug = dbg ? atoi(dbg) : 0;
@@ -937,14 +959,15 @@ static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const G
                      0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), cell_table(f, f->cur),
                                        f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
                                        dep ? bits[0] : 0u, dep ? bits[1] : 0u,
-                                       f->rho_q.as<int>());
+                                       f->rho_q.as<int>(), deposit_cell_max(gg, f), st, step);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;
 }
 
 int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
-                const BinGeom &g, const GridGeom &gg, const unsigned char bits[3]) {
+                const BinGeom &g, const GridGeom &gg, const unsigned char bits[3], DevStatus *st,
+                int step) {
     const long long n = p.n;
     if (n > 0) {
         k_fast_import<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
@@ -954,7 +977,7 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     }
     CS_TRY(fast_sort(ctx, f, n, 0));
     if (p.field_active) CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
-    CS_TRY(fast_cellfix(ctx, f, p, gg, bits));
+    CS_TRY(fast_cellfix(ctx, f, p, gg, bits, st, step));
     f->imported = true;
     return CS_OK;
 }
@@ -1114,9 +1137,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
 // hit adjacent grid lines, so the reductions stay in L2 (deposited from the
 // old order they scattered over +-50 cell rows and missed L2 almost always).
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3], int part) {
+                const unsigned char bits[3], int part, DevStatus *st, int step) {
     if (part & 1) CS_TRY(fast_sort(ctx, f, n, 1 - f->cur));
-    if (part & 2) CS_TRY(fast_cellfix(ctx, f, p, gg, bits));
+    if (part & 2) CS_TRY(fast_cellfix(ctx, f, p, gg, bits, st, step));
     return CS_OK;
 }
 

@@ -45,7 +45,8 @@ struct FastStepCfg {
 int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg);
 void fast_destroy(cs_fast *f);
 int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
-                const BinGeom &g, const GridGeom &gg, const unsigned char bits[3]);
+                const BinGeom &g, const GridGeom &gg, const unsigned char bits[3], DevStatus *st,
+                int step);
 int fast_export(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
                 const GridGeom &gg);
 int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
@@ -53,7 +54,7 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
                    const void *xi, DevStatus *st, int step, int part);
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3], int part);
+                const unsigned char bits[3], int part, DevStatus *st, int step);
 bool fast_imported(const cs_fast *f);
 int *fast_rho_q(cs_fast *f);
 
@@ -328,7 +329,8 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         c.bits[2] = 0;
         if (!fast_imported(sim->fast)) {
             StageMark m(sim, CS_STAGE_BIN);
-            CS_TRY(fast_import(ctx, sim->fast, p, s, sim->geom, sim->gg, sim->bits));
+            CS_TRY(fast_import(ctx, sim->fast, p, s, sim->geom, sim->gg, sim->bits, st,
+                               sim->steps_done));
         }
         // fork/join of the field solve (skipped while profiling, so that the
         // stage times stay additive)
@@ -372,11 +374,11 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
             }
             {
                 StageMark m(sim, CS_STAGE_BIN);
-                CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 1));
+                CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 1, st, step));
             }
             // in-cell id order + deposit for the next step's field
             StageMark m(sim, CS_STAGE_DEPOSIT);
-            CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 2));
+            CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 2, st, step));
         }
         sim->steps_done += k;
         sim->last_launches = ctx->launches - l0;
@@ -469,7 +471,7 @@ int sim_status(cs_sim *sim, cs_status *out) {
         out->particle = (long long)((d.key >> 3) & ((1ULL << 57) - 1));
         out->axis = rank >= 1 ? rank - 1 : 0;
         out->step = d.step;
-        if (out->code == CS_FIELD_NONFINITE) {
+        if (out->code == CS_FIELD_NONFINITE || out->code == CS_DEPOSIT_OVERFLOW) {
             out->particle = -1;
             out->axis = -1;
         }
@@ -489,7 +491,8 @@ extern "C" int cs_sim_engine(cs_sim *sim) { return sim->engine; }
 
 extern "C" int cs_sim_import(cs_sim *sim, const cs_sim_state *st) {
     if (sim->engine != CS_ENGINE_SORTED) return CS_OK;
-    return cs::fast_import(sim->ctx, sim->fast, sim->p, st, sim->geom, sim->gg, sim->bits);
+    return cs::fast_import(sim->ctx, sim->fast, sim->p, st, sim->geom, sim->gg, sim->bits,
+                           sim->dstat(), sim->steps_done);
 }
 
 extern "C" int cs_sim_export(cs_sim *sim, const cs_sim_state *st) {

@@ -570,6 +570,10 @@ class Realisation:
             try:
                 if st.code == N.CS_FIELD_NONFINITE:
                     raise FloatingPointError("field update produced non-finite values")
+                if st.code == N.CS_DEPOSIT_OVERFLOW:
+                    raise SimulationError(
+                        "too many particles in one cell for the sorted engine's int32 "
+                        "fixed-point deposit; use engine='direct'")
                 src = "next_pos" if self._sim.engine == "direct" else "pos"
                 raise_boundary_status(st.code, int(st.particle), int(st.axis),
                                       self._state[src].double().cpu().numpy())

@@ -204,3 +204,21 @@ def test_vectorized_periodic_gradient_bitwise_equals_generic(monkeypatch):
     monkeypatch.delenv("CS_GRAD_GENERIC", raising=False)
     for k in ("pos", "c", "grad"):
         assert torch.equal(out["vec"][k], out["generic"][k]), k
+
+
+def test_sorted_engine_reports_fixed_point_deposit_overflow():
+    """A cell holding more particles than the int32 fixed-point deposit can
+    sum exactly (511 masses of 2^22 per grid node) stops the sorted engine with
+    CS_DEPOSIT_OVERFLOW instead of wrapping silently."""
+    n, n_c = 20_000, 256
+    pos, sp, xi = _inputs(n, 4)
+    # 200 particles in one cell; here a node's CIC support spans 2 x 2 cells
+    # (grid spacing 1/256 < cell side 0.008), so the limit is 511 / 4 = 127
+    pos[:200] = np.float32(0.1)
+    a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c)
+    a.step(torch.as_tensor(xi[0], device="cuda"), 1)
+    st = a.status()
+    assert st.code == cs._native.CS_DEPOSIT_OVERFLOW
+    b, sb = _sim(pos[200:], sp[200:], engine="sorted", field=True, n_c=n_c)
+    b.step(torch.as_tensor(xi[0, 200:], device="cuda"), 1)
+    assert b.status().code == 0

@@ -710,7 +710,7 @@ __device__ __noinline__ void deposit_record(float4 rv, const GridGeom &gg, const
 __global__ void __launch_bounds__(256)
 k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGeom gg,
                ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q,
-               int cell_max, DevStatus *st, int step) {
+               int cell_max, DevStatus *st, int step, int deposit) {
     float4 *r4 = reinterpret_cast<float4 *>(rec);
     DevStatus *dst_ = st;
     const int m = gg.n * gg.n;
@@ -732,7 +732,7 @@ k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGe
         }
         if (cnt > 32) {  // dense group (rare): serial per cell
             if (en - st0 >= 2) cell_insertion_sort(r4, st0, en);
-            for (int k = st0; k < en; k++) {
+            for (int k = st0; deposit && k < en; k++) {
                 const float4 rv = r4[k];
                 const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
                 if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
@@ -762,7 +762,7 @@ k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGe
             __syncwarp();
             if (dst >= 0) r4[dst] = r;
         }
-        if (valid) {
+        if (valid && deposit) {
             const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
             if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, m);
         }
@@ -784,6 +784,91 @@ k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeom gg, ExactDiv d
         const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
         if (bits & 1u) cic_deposit_q(c, rho_q);
         if (bits & 2u) cic_deposit_q(c, rho_q + m);
+    }
+}
+
+// Deposit by rows (periodic grids): one block per grid row j gathers the CIC
+// weights of every particle whose stencil touches row j -- base row j - 1 or
+// j (coupling.py:119-135) -- from the contiguous slot ranges of the cell rows
+// that can hold such particles (one row of margin each side), accumulates
+// them in shared memory as int32 fixed point and writes row j of both grids
+// in full: no global atomics, no grid reset, and the sums equal the atomic
+// deposit's bit for bit (integer addition is associative).
+#ifndef CS_DEP_ROWS
+#define CS_DEP_ROWS 2
+#endif
+constexpr int DEP_ROWS = CS_DEP_ROWS;  // grid rows per block of k_fast_deposit_rows
+
+__global__ void __launch_bounds__(512)
+k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts, BinGeom g,
+                    GridGeom gg, ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
+                    int *__restrict__ rho_q) {
+    extern __shared__ int acc[];  // [DEP_ROWS][2][n]
+    const int n = gg.n, j0 = blockIdx.x * DEP_ROWS;
+    const long long m = (long long)n * n;
+    for (int i = threadIdx.x; i < DEP_ROWS * 2 * n; i += blockDim.x) acc[i] = 0;
+    __syncthreads();
+    // cell rows that can hold a particle with y in [lo + (j0-1) d, lo + (j0+R) d):
+    // the cell index is monotone in y, so the rows of the (slightly widened)
+    // window ends bound it
+    const double ylo = dsub(dadd(gg.lo1, dmul((double)(j0 - 1), gg.d1)), 1e-9);
+    const double yhi = dadd(dadd(gg.lo1, dmul((double)(j0 + DEP_ROWS), gg.d1)), 1e-9);
+    const int cy0 = (int)floor(ddiv(dsub(ylo, g.lo1), g.eff1));
+    const int cy1 = (int)floor(ddiv(dsub(yhi, g.lo1), g.eff1));
+    const float4 *r4 = reinterpret_cast<const float4 *>(rec);
+    for (int cyw = cy0; cyw <= cy1; cyw++) {
+        int cy = cyw % g.n1;
+        if (cy < 0) cy += g.n1;
+        if (cyw - cy0 >= g.n1) break;  // fewer cell rows than the window
+        const int kb = starts[(long long)cy * g.n0], ke = starts[(long long)(cy + 1) * g.n0];
+        for (int k = kb + threadIdx.x; k < ke; k += blockDim.x) {
+            const float4 rv = __ldg(r4 + k);
+            const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
+            if (!bits) continue;
+            // the periodic branch of cic_stencil, y first (the row filter)
+            const double u1 = ediv(dsub((double)rv.y, gg.lo1), d1);
+            const double base1 = floor(u1);
+            const int b1 = wrap_index(base1, n);
+            const int c1 = b1 + 1 == n ? 0 : b1 + 1;
+            int rb = b1 - j0, rc = c1 - j0;  // rows of this block's window, if any
+            if (rb < 0) rb += n;
+            if (rc < 0) rc += n;
+            const bool hb = rb < DEP_ROWS, hc = rc < DEP_ROWS;
+            if (!hb && !hc) continue;
+            const double f1 = dsub(u1, base1);
+            const double u0 = ediv(dsub((double)rv.x, gg.lo0), d0);
+            const double base0 = floor(u0);
+            const double f0 = dsub(u0, base0);
+            const int b0 = wrap_index(base0, n);
+            const int c0 = b0 + 1 == n ? 0 : b0 + 1;
+            const double g0 = dsub(1.0, f0);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (!(h ? hc : hb)) continue;
+                const double wy = h ? f1 : dsub(1.0, f1);  // row b1: g1, row c1: f1
+                const int qa = __double2int_rn(dmul(dmul(g0, wy), Q_SCALE));
+                const int qb = __double2int_rn(dmul(dmul(f0, wy), Q_SCALE));
+                int *row = acc + (h ? rc : rb) * 2 * n;
+                if (bits & 1u) {
+                    atomicAdd(&row[b0], qa);
+                    atomicAdd(&row[c0], qb);
+                }
+                if (bits & 2u) {
+                    atomicAdd(&row[n + b0], qa);
+                    atomicAdd(&row[n + c0], qb);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int r = 0; r < DEP_ROWS; r++) {
+        const int j = j0 + r;
+        if (j >= n) break;
+        int *ra = rho_q + (long long)j * n, *rbp = rho_q + m + (long long)j * n;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            ra[i] = acc[r * 2 * n + i];
+            rbp[i] = acc[r * 2 * n + n + i];
+        }
     }
 }
 
@@ -844,6 +929,8 @@ struct cs_fast {
     bool imported = false;
     long long nflat = 0;
     double eff0 = 1.0, eff1 = 1.0;  // cell sides
+    cs::BinGeom g{};
+    bool gather = false;            // deposit by grid rows (k_fast_deposit_rows)
 };
 
 namespace cs {
@@ -865,6 +952,11 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     f->nflat = (long long)g.n0 * g.n1;
     f->eff0 = g.eff0;
     f->eff1 = g.eff1;
+    f->g = g;
+    // periodic domain and grid, accumulators of a grid row fit in shared memory
+    f->gather = gg && gg->per && g.per0 && g.per1 && gg->n >= 2 &&
+                (size_t)gg->n * DEP_ROWS * 8 <= 200 * 1024 &&
+                !getenv("CS_ATOMIC_DEPOSIT");
     const size_t nr = sizeof(Rec) * (size_t)(n > 0 ? n : 1);
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
@@ -955,13 +1047,29 @@ static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const G
     const bool dep = p.field_active && !(debug & 2);
     static int res = 0;
     const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
+    const bool rows = dep && f->gather;
     k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, f->nflat, &res), 256,
                      0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), cell_table(f, f->cur),
                                        f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
                                        dep ? bits[0] : 0u, dep ? bits[1] : 0u,
-                                       f->rho_q.as<int>(), deposit_cell_max(gg, f), st, step);
+                                       f->rho_q.as<int>(), deposit_cell_max(gg, f), st, step,
+                                       dep && !rows);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
+    if (rows) {
+        const int smem = (int)(DEP_ROWS * 2 * sizeof(int) * (size_t)gg.n);
+        static int smem_set = 0;
+        if (smem > 48 * 1024 && smem > smem_set) {
+            CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            smem_set = smem;
+        }
+        k_fast_deposit_rows<<<(gg.n + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
+            f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
+            make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>());
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
     return CS_OK;
 }
 
@@ -1143,7 +1251,9 @@ int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, co
     return CS_OK;
 }
 
-int *fast_rho_q(cs_fast *f) { return f->rho_q.p ? f->rho_q.as<int>() : nullptr; }
+// deposit grids the gradient kernel must clear (none when they are written
+// in full by k_fast_deposit_rows)
+int *fast_rho_q(cs_fast *f) { return f->rho_q.p && !f->gather ? f->rho_q.as<int>() : nullptr; }
 
 bool fast_imported(const cs_fast *f) { return f && f->imported; }
 

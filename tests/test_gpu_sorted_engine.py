@@ -222,3 +222,26 @@ def test_sorted_engine_reports_fixed_point_deposit_overflow():
     b, sb = _sim(pos[200:], sp[200:], engine="sorted", field=True, n_c=n_c)
     b.step(torch.as_tensor(xi[0, 200:], device="cuda"), 1)
     assert b.status().code == 0
+
+
+def test_row_gather_deposit_bitwise_equals_atomic_deposit(monkeypatch):
+    """k_fast_deposit_rows (periodic grids: deposit gathered per grid row, no
+    atomics to HBM) against the atomic deposit: identical fixed-point grids,
+    hence identical fields and positions, over several steps."""
+    n, n_c = 60_000, 512
+    pos, sp, xi = _inputs(n, 13)
+    x = torch.as_tensor(xi, device="cuda")
+    out = {}
+    for mode in ("rows", "atomic"):
+        if mode == "atomic":
+            monkeypatch.setenv("CS_ATOMIC_DEPOSIT", "1")
+        else:
+            monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
+        a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c)
+        a.step(x, 6)
+        a.export_state()
+        assert a.status().code == 0
+        out[mode] = {k: sa[k].clone() for k in ("pos", "c", "grad", "rho_a", "rho_b")}
+    monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
+    for k in out["rows"]:
+        assert torch.equal(out["rows"][k], out["atomic"][k]), k

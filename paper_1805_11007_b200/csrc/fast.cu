@@ -716,55 +716,71 @@ k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGe
     const int m = gg.n * gg.n;
     const int lane = threadIdx.x & 31;
     const unsigned below = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;  // bits 0..lane
-    for (long long c0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell;
-         c0 += (long long)gridDim.x * blockDim.x) {
-        const long long c = c0 + lane < ncell ? c0 + lane : ncell;
-        const int st0 = starts[c];
-        const int en = c < ncell ? starts[c + 1] : st0;
-        const int base = __shfl_sync(0xffffffffu, st0, 0);
-        const int cnt = __shfl_sync(0xffffffffu, en, 31) - base;
-        if ((bits0 | bits1) && en - st0 > cell_max) {
-            // a grid node could collect > 511 particle masses of 2^22: its
-            // int32 fixed-point sum would overflow
-            atomicMin(&dst_->key, err_key(3, c, CS_DEPOSIT_OVERFLOW));
-            dst_->abort = 1;
-            dst_->step = step;
+    constexpr int G = 2;  // 32-cell groups per warp iteration: their loads overlap
+    const long long gstride = (long long)gridDim.x * blockDim.x * G;
+    for (long long cg = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * G;
+         cg < ncell; cg += gstride) {
+        int st0[G], en[G], base[G], cnt[G];
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+            const long long c = cg + 32 * q + lane < ncell ? cg + 32 * q + lane : ncell;
+            st0[q] = starts[c];
+            en[q] = c < ncell ? starts[c + 1] : st0[q];
         }
-        if (cnt > 32) {  // dense group (rare): serial per cell
-            if (en - st0 >= 2) cell_insertion_sort(r4, st0, en);
-            for (int k = st0; deposit && k < en; k++) {
-                const float4 rv = r4[k];
-                const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
-                if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
+        float4 r[G];
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+            base[q] = __shfl_sync(0xffffffffu, st0[q], 0);
+            cnt[q] = __shfl_sync(0xffffffffu, en[q], 31) - base[q];
+            r[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (lane < cnt[q] && cnt[q] <= 32) r[q] = r4[base[q] + lane];
+        }
+        int dst[G];
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+            dst[q] = -1;
+            if ((bits0 | bits1) && en[q] - st0[q] > cell_max) {
+                // a grid node could collect > 511 particle masses of 2^22: its
+                // int32 fixed-point sum would overflow
+                atomicMin(&dst_->key, err_key(3, cg + 32 * q + lane, CS_DEPOSIT_OVERFLOW));
+                dst_->abort = 1;
+                dst_->step = step;
             }
-            continue;
-        }
-        const bool valid = lane < cnt;
-        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) r = r4[base + lane];
-        const unsigned id = __float_as_uint(r.z) & ID_MASK;
-        const unsigned heads = __reduce_or_sync(0xffffffffu, en > st0 ? 1u << (st0 - base) : 0u);
-        const int s0 = 31 - __clz(heads & below);  // first slot of my cell (lane units)
-        const unsigned above = heads & ~below;
-        const int e1 = above ? __ffs(above) - 1 : cnt;
-        const int len = valid ? e1 - s0 : 0;
-        const int lmax = __reduce_max_sync(0xffffffffu, (unsigned)len);
-        int dst = -1;
-        if (lmax >= 2) {
+            if (cnt[q] > 32) continue;  // dense group (rare): serial, below
+            const bool valid = lane < cnt[q];
+            const unsigned id = __float_as_uint(r[q].z) & ID_MASK;
+            const unsigned heads = __reduce_or_sync(
+                0xffffffffu, en[q] > st0[q] ? 1u << (st0[q] - base[q]) : 0u);
+            const int s0 = 31 - __clz(heads & below);  // first slot of my cell (lane units)
+            const unsigned above = heads & ~below;
+            const int e1 = above ? __ffs(above) - 1 : cnt[q];
+            const int len = valid ? e1 - s0 : 0;
+            const int lmax = __reduce_max_sync(0xffffffffu, (unsigned)len);
+            if (lmax < 2) continue;
             int rank = 0;
             for (int k = 0; k < lmax; k++) {
                 const unsigned idk = __shfl_sync(0xffffffffu, id, min(s0 + k, 31));
                 rank += (k < len && idk < id) ? 1 : 0;
             }
-            if (len >= 2 && s0 + rank != lane) dst = base + s0 + rank;
-            // every lane's record must be read before any lane overwrites a
-            // slot: the shuffles order only registers, __syncwarp also memory
-            __syncwarp();
-            if (dst >= 0) r4[dst] = r;
+            if (len >= 2 && s0 + rank != lane) dst[q] = base[q] + s0 + rank;
         }
-        if (valid && deposit) {
-            const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
-            if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, m);
+        // every lane's records must be read before any lane overwrites a slot:
+        // the shuffles order only registers, __syncwarp also memory
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+            if (dst[q] >= 0) r4[dst[q]] = r[q];
+            if (cnt[q] > 32) {
+                if (en[q] - st0[q] >= 2) cell_insertion_sort(r4, st0[q], en[q]);
+                for (int k = st0[q]; deposit && k < en[q]; k++) {
+                    const float4 rv = r4[k];
+                    const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
+                    if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
+                }
+            } else if (deposit && lane < cnt[q]) {
+                const unsigned bits = (__float_as_uint(r[q].z) >> 31) ? bits1 : bits0;
+                if (bits) deposit_record(r[q], gg, d0, d1, bits, rho_q, m);
+            }
         }
     }
 }
@@ -1048,7 +1064,8 @@ static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const G
     static int res = 0;
     const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
     const bool rows = dep && f->gather;
-    k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, f->nflat, &res), 256,
+    k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, (f->nflat + 1) / 2,
+                                     &res), 256,
                      0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), cell_table(f, f->cur),
                                        f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
                                        dep ? bits[0] : 0u, dep ? bits[1] : 0u,

@@ -46,6 +46,9 @@ enum cs_code {
     CS_DEPOSIT_OVERFLOW = 5, /* sorted engine only: a cell holds more particles than its
                                 int32 fixed-point deposit can sum exactly (no reference
                                 counterpart; the direct engine has no such limit) */
+    CS_SORT_OVERFLOW = 6,    /* sorted engine only: a bucket of 256 consecutive cells received
+                                more records than its region holds (a local density far
+                                above the run's initial one; no reference counterpart) */
     CS_ERR_CUDA = -1,
     CS_ERR_PARAM = -2,
     CS_ERR_NOMEM = -3,

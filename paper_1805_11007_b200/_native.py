@@ -21,6 +21,7 @@ if os.environ.get("CS_LIB"):  # tuning experiments: an alternative build of the 
 
 CS_OK, CS_NONFINITE, CS_OVERSHOOT, CS_UNSETTLED, CS_FIELD_NONFINITE = 0, 1, 2, 3, 4
 CS_DEPOSIT_OVERFLOW = 5
+CS_SORT_OVERFLOW = 6
 CS_F64, CS_F32 = 0, 1
 CS_GAUSSIAN, CS_CIC = 0, 1
 CS_ENGINE_AUTO, CS_ENGINE_DIRECT, CS_ENGINE_SORTED = 0, 1, 2

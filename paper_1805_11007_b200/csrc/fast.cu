@@ -53,17 +53,33 @@ struct __align__(16) Rec {
 
 constexpr double Q_SCALE = 4194304.0;  // 2^22
 constexpr unsigned ID_MASK = 0x7fffffffu;
+// bucket sort: buckets of BUCKET_CELLS consecutive cells (flat index)
+constexpr int BUCKET_SHIFT = 10;
+constexpr int BSORT_THREADS = 256;
+constexpr int CELLS_PER_THREAD = (1 << BUCKET_SHIFT) / BSORT_THREADS;
+static_assert(CELLS_PER_THREAD == 4, "k_bucket_sort owns 4 cells (one int4) per thread");
+// every bucket has SUBB claim counters and region parts (a record picks one
+// by its lane): the claims of a bucket spread over SUBB addresses, so the
+// same-address atomic chains at the L2 are SUBB times shorter
+#ifndef CS_SUBB
+#define CS_SUBB 8
+#endif
+constexpr int SUBB = CS_SUBB;
+static_assert(SUBB >= 1 && SUBB <= 32 && (SUBB & (SUBB - 1)) == 0, "SUBB: power of two <= 32");
+constexpr int BUCKET_CELLS = 1 << BUCKET_SHIFT;
 
 struct FastArgs {
     const Rec *rec;
     const int *starts;
-    Rec *tmp;
-    int *keys;          // new cell key per old slot
+    Rec *region;        // sub-bucket q = b * SUBB + s owns slots [q * cap, (q + 1) * cap)
+    int *fill;          // records claimed per sub-bucket (zeroed by the bucket scan)
+    long long cap;      // slots per sub-bucket region
     double2 *force;     // pair force per sorted slot (binary64)
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
-                        // 2 skip deposits, 4 skip histogram atomics,
+                        // 2 skip deposits, 4 store records at the slot index
+                        // without claims, 8 the same plus a fire-and-forget
+                        // claim (4/8/32: timing only, wrong results)
                         // 32 xi read at the slot index (timing only: wrong results)
-    int *counts;
     const float *xi;    // this step's (N, 2) increments, indexed by id
     const float *grad;  // (n_c^2, 2)
     int *rho_q;         // 2 * m fixed-point deposits (a | b)
@@ -502,6 +518,18 @@ k_fast_forces(const DevStatus *st) {
 #ifndef CS_UPDATE_MINB
 #define CS_UPDATE_MINB 5  // measured: (256) 245 us, (256,5) 220, (256,6) 272
 #endif
+// store a record at its claimed bucket slot (or flag the overflow)
+__device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, int step, int b,
+                                            int slot, float4 out) {
+    if (slot < a.cap) {
+        reinterpret_cast<float4 *>(a.region)[(long long)b * a.cap + slot] = out;
+    } else {
+        atomicMin(&st->key, err_key(3, b / SUBB, CS_SORT_OVERFLOW));
+        st->abort = 1;
+        st->step = step;
+    }
+}
+
 __global__ void __launch_bounds__(256, CS_UPDATE_MINB)
 k_fast_update(DevStatus *st, int step) {
     const FastArgs &a = cA;
@@ -509,9 +537,28 @@ k_fast_update(DevStatus *st, int step) {
     const int m = a.gg.n * a.gg.n;
     const int n0 = a.g.n0, n1 = a.g.n1;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const float4 mer = __ldcs(rec + t);
+    // the bucket claim of one iteration is consumed (record stored at its
+    // slot) in the next, after that iteration's loads are in flight: the
+    // atomic's round trip overlaps them instead of stalling the warp
+    float4 p_out = make_float4(0.f, 0.f, 0.f, 0.f);
+    int p_b = -1, p_slot = 0;
+    // the record and pair force of the next iteration are loaded one
+    // iteration ahead (their latency overlaps this iteration's work)
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    float4 n_mer = make_float4(0.f, 0.f, 0.f, 0.f);
+    double2 n_f = make_double2(0.0, 0.0);
+    if (t < a.n) {
+        n_mer = __ldcs(rec + t);
+        if (a.interact) n_f = __ldcs(a.force + t);
+    }
+    for (; t < a.n; t += stride) {
+        const float4 mer = n_mer;
+        const double2 f = n_f;
+        if (t + stride < a.n) {
+            n_mer = __ldcs(rec + t + stride);
+            if (a.interact) n_f = __ldcs(a.force + t + stride);
+        }
         const float xf = mer.x, yf = mer.y;
         const unsigned meta = __float_as_uint(mer.z);
         const unsigned wbits = __float_as_uint(mer.w);
@@ -521,12 +568,8 @@ k_fast_update(DevStatus *st, int step) {
         const unsigned zi = (a.debug & 32) ? (unsigned)t : id;  // 32: diagnostic only
         const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + zi)
                                        : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + zi);
-        double fx = 0.0, fy = 0.0;
-        if (a.interact) {
-            const double2 f = __ldcs(a.force + t);
-            fx = f.x;
-            fy = f.y;
-        }
+        const double fx = f.x, fy = f.y;  // zero without interactions
+        if (p_b >= 0) claim_store(a, st, step, p_b, p_slot, p_out);
         const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
         const bool do_drift = a.refresh && !dead && !pinned;
         float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
@@ -607,54 +650,25 @@ k_fast_update(DevStatus *st, int step) {
         const double nx = (double)out.x, ny = (double)out.y;
         const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
                         cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
-        if (!(a.debug & 4)) atomicAdd(&a.counts[key], 1);
-        __stcs(reinterpret_cast<float4 *>(a.tmp) + t, out);
-        __stcs(a.keys + t, key);
-    }
-}
-
-// Counting-sort scatter.  The scan left cell c's first slot in cur[c + 1]
-// (cur[0] == 0); each record claims cur[key + 1]++ , so afterwards
-// cur[c] == starts[c] for every c: the array is the next cell table.  The
-// arrival order inside a cell is arbitrary; k_fast_cellfix restores id order.
-// SCATTER_U records per thread per iteration keep their key, record and
-// claim round trips in flight together; a block covers SCATTER_U * 256
-// consecutive slots.
-#ifndef CS_SCATTER_U
-#define CS_SCATTER_U 8
-#endif
-constexpr int SCATTER_U = CS_SCATTER_U;
-
-__global__ void __launch_bounds__(256)
-k_fast_scatter(const Rec *__restrict__ tmp, const int *__restrict__ keys, long long n,
-               int *__restrict__ cur, Rec *__restrict__ out) {
-    for (long long t0 = (long long)blockIdx.x * blockDim.x * SCATTER_U + threadIdx.x; t0 < n;
-         t0 += (long long)gridDim.x * blockDim.x * SCATTER_U) {
-        int key[SCATTER_U];
-        float4 r[SCATTER_U];
-#pragma unroll
-        for (int u = 0; u < SCATTER_U; u++) {
-            const long long t = t0 + (long long)u * blockDim.x;
-            if (t < n) {
-                key[u] = __ldcs(keys + t);
-                r[u] = __ldcs(reinterpret_cast<const float4 *>(tmp) + t);
-            }
+        p_b = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
+        if (a.debug & 12) {  // timing diagnostics only (wrong results)
+            if (a.debug & 8) atomicAdd(&a.fill[p_b], 1);
+            reinterpret_cast<float4 *>(a.region)[t] = out;
+            p_b = -1;
+            continue;
         }
-        int dst[SCATTER_U];
-#pragma unroll
-        for (int u = 0; u < SCATTER_U; u++)
-            if (t0 + (long long)u * blockDim.x < n) dst[u] = atomicAdd(cur + key[u] + 1, 1);
-#pragma unroll
-        for (int u = 0; u < SCATTER_U; u++)
-            if (t0 + (long long)u * blockDim.x < n) reinterpret_cast<float4 *>(out)[dst[u]] = r[u];
+        p_slot = atomicAdd(&a.fill[p_b], 1);
+        p_out = out;
     }
+    if (p_b >= 0) claim_store(a, st, step, p_b, p_slot, p_out);
 }
 
-// caller arrays (id order) -> records (id order) + keys/ranks + histogram
+// caller arrays (id order) -> records claimed into their bucket regions
+// (the same claim as k_fast_update's), anchors kept as the wrap origin
 __global__ void k_fast_import(const float *__restrict__ pos, const float *__restrict__ anchor,
                               const uint8_t *__restrict__ type, long long n, BinGeom g,
-                              Rec *__restrict__ tmp, int *__restrict__ keys,
-                              int *__restrict__ counts, float *__restrict__ anchor0) {
+                              Rec *__restrict__ region, int *__restrict__ fill, long long cap,
+                              float *__restrict__ anchor0, DevStatus *st) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const float2 p = reinterpret_cast<const float2 *>(pos)[i];
@@ -664,142 +678,181 @@ __global__ void k_fast_import(const float *__restrict__ pos, const float *__rest
         r.meta = (unsigned)i | ((type && type[i]) ? 0x80000000u : 0u);
         r.wx = 0;
         r.wy = 0;
-        tmp[i] = r;
         reinterpret_cast<float2 *>(anchor0)[i] = reinterpret_cast<const float2 *>(anchor)[i];
         const int key = cell_axis((double)p.y, g.lo1, g.eff1, g.n1) * g.n0 +
                         cell_axis((double)p.x, g.lo0, g.eff0, g.n0);
-        keys[i] = key;
-        atomicAdd(&counts[key], 1);
-    }
-}
-
-// After the counting-sort scatter: put every cell's records in ascending id
-// (the scatter ranks are atomic-arrival order), which makes slot order the
-// reference's in-cell order for k_fast_forces, and CIC-deposit them for the
-// next step's field.  A warp owns groups of 32 consecutive cells: one
-// coalesced load of a group's records (~19 at the benchmark density, one per
-// lane); the cell heads form a 32-bit mask (one warp OR), from which each
-// record reads its cell's extent; it ranks itself by id among the cell's
-// records with shuffles and is written back only if it moves.  Warps own
-// disjoint slot ranges and __syncwarp orders every lane's read before any
-// write, so the permutation is in place.  Consecutive lanes deposit onto
-// neighbouring grid nodes (L2-local integer reductions, deterministic).
-__device__ __noinline__ void cell_insertion_sort(float4 *r4, int kb, int ke) {
-    for (int i = kb + 1; i < ke; i++) {
-        const float4 r = r4[i];
-        const unsigned id = __float_as_uint(r.z) & ID_MASK;
-        int j = i - 1;
-        while (j >= kb) {
-            const float4 q = r4[j];
-            if ((__float_as_uint(q.z) & ID_MASK) <= id) break;
-            r4[j + 1] = q;
-            j--;
+        const int q = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
+        const int slot = atomicAdd(&fill[q], 1);
+        if (slot < cap) {
+            region[(long long)q * cap + slot] = r;
+        } else {
+            atomicMin(&st->key, err_key(3, q / SUBB, CS_SORT_OVERFLOW));
+            st->abort = 1;
         }
-        if (j != i - 1) r4[j + 1] = r;
     }
 }
 
-__device__ __noinline__ void deposit_record(float4 rv, const GridGeom &gg, const ExactDiv &d0,
-                                            const ExactDiv &d1, unsigned bits, int *rho_q,
-                                            int m) {
+__device__ __noinline__ void deposit_record(float4 rv, GridGeom gg, ExactDiv d0, ExactDiv d1,
+                                            unsigned bits, int *rho_q, int m) {
     const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
     if (bits & 1u) cic_deposit_q(c, rho_q);
     if (bits & 2u) cic_deposit_q(c, rho_q + m);
 }
 
-__global__ void __launch_bounds__(256)
-k_fast_cellfix(Rec *rec, const int *__restrict__ starts, long long ncell, GridGeom gg,
-               ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q,
-               int cell_max, DevStatus *st, int step, int deposit) {
-    float4 *r4 = reinterpret_cast<float4 *>(rec);
-    DevStatus *dst_ = st;
-    const int m = gg.n * gg.n;
-    const int lane = threadIdx.x & 31;
-    const unsigned below = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;  // bits 0..lane
-    constexpr int G = 2;  // 32-cell groups per warp iteration: their loads overlap
-    const long long gstride = (long long)gridDim.x * blockDim.x * G;
-    for (long long cg = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * G;
-         cg < ncell; cg += gstride) {
-        int st0[G], en[G], base[G], cnt[G];
-#pragma unroll
-        for (int q = 0; q < G; q++) {
-            const long long c = cg + 32 * q + lane < ncell ? cg + 32 * q + lane : ncell;
-            st0[q] = starts[c];
-            en[q] = c < ncell ? starts[c + 1] : st0[q];
+// Bucket sort: one block per bucket of BUCKET_CELLS consecutive cells (flat,
+// y-major index).  k_fast_update / k_fast_import claimed a slot for every
+// record in its bucket's region (arrival order); k_scan turned the claim
+// counts into the bucket offsets boff[].  The block
+//   1. loads the bucket's records (coalesced) and recomputes each record's
+//      cell exactly as the claim did (cell_axis_fast on the stored binary32
+//      coordinates), counting the cells in shared memory;
+//   2. scans the cell counts -> the bucket's slice of the next cell table;
+//   3. ranks every record inside its cell by particle id (the reference's
+//      in-cell order, motion.py:195-199: a stable counting sort of ids), and
+//      writes it to boff[b] + cell start + rank: the output is cell-sorted,
+//      id-sorted inside a cell, and contiguous;
+//   4. (atomic deposit mode) CIC-deposits the bucket's records: neighbouring
+//      cells, so the integer reductions stay L2-local and deterministic.
+// A cell more populated than the int32 fixed-point deposit can sum exactly
+// stops the run with CS_DEPOSIT_OVERFLOW.
+__global__ void __launch_bounds__(BSORT_THREADS)
+k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long long cap,
+              long long nbucket, BinGeom g, ExactDiv eff0, ExactDiv eff1, long long nflat,
+              Rec *__restrict__ out, int *__restrict__ starts, GridGeom gg, ExactDiv d0,
+              ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q, int deposit,
+              int cell_max, DevStatus *st, int step) {
+    // [SUBB cap] codes (cell | arrival << 10 | part << 25), [SUBB cap] ids by slot
+    extern __shared__ int s_dyn[];
+    __shared__ int s_pre[SUBB + 1];
+    __shared__ __align__(16) int s_cnt[BUCKET_CELLS];
+    __shared__ __align__(16) int s_beg[BUCKET_CELLS + 4];
+    __shared__ int s_wsum[BSORT_THREADS / 32];
+    int *s_code = s_dyn;
+    unsigned *s_id = reinterpret_cast<unsigned *>(s_dyn + SUBB * cap);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long b = blockIdx.x;
+    // the bucket's records: its SUBB region parts, concatenated (part q
+    // holds local indices s_pre[q] .. s_pre[q + 1])
+    const int off = boff[b * SUBB];
+    if (warp == 0) {
+        int c = 0;
+        if (lane < SUBB) {
+            c = boff[b * SUBB + lane + 1] - boff[b * SUBB + lane];
+            if (c > cap) c = (int)cap;  // overflowed part: the run is already stopped
         }
-        float4 r[G];
+        int v = c;
 #pragma unroll
-        for (int q = 0; q < G; q++) {
-            base[q] = __shfl_sync(0xffffffffu, st0[q], 0);
-            cnt[q] = __shfl_sync(0xffffffffu, en[q], 31) - base[q];
-            r[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (lane < cnt[q] && cnt[q] <= 32) r[q] = r4[base[q] + lane];
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += u;
         }
-        int dst[G];
+        if (lane < SUBB) s_pre[lane + 1] = v;
+        if (lane == 0) s_pre[0] = 0;
+    }
+    const float4 *r4 = reinterpret_cast<const float4 *>(region) + b * SUBB * cap;
+    const long long cell0 = b * BUCKET_CELLS;
+    reinterpret_cast<int4 *>(s_cnt)[tid] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    const int cnt = s_pre[SUBB];
+    for (int i = tid; i < cnt; i += BSORT_THREADS) {
+        int q = 0;  // part holding local index i
 #pragma unroll
-        for (int q = 0; q < G; q++) {
-            dst[q] = -1;
-            if ((bits0 | bits1) && en[q] - st0[q] > cell_max) {
-                // a grid node could collect > 511 particle masses of 2^22: its
-                // int32 fixed-point sum would overflow
-                atomicMin(&dst_->key, err_key(3, cg + 32 * q + lane, CS_DEPOSIT_OVERFLOW));
-                dst_->abort = 1;
-                dst_->step = step;
-            }
-            if (cnt[q] > 32) continue;  // dense group (rare): serial, below
-            const bool valid = lane < cnt[q];
-            const unsigned id = __float_as_uint(r[q].z) & ID_MASK;
-            const unsigned heads = __reduce_or_sync(
-                0xffffffffu, en[q] > st0[q] ? 1u << (st0[q] - base[q]) : 0u);
-            const int s0 = 31 - __clz(heads & below);  // first slot of my cell (lane units)
-            const unsigned above = heads & ~below;
-            const int e1 = above ? __ffs(above) - 1 : cnt[q];
-            const int len = valid ? e1 - s0 : 0;
-            const int lmax = __reduce_max_sync(0xffffffffu, (unsigned)len);
-            if (lmax < 2) continue;
-            int rank = 0;
-            for (int k = 0; k < lmax; k++) {
-                const unsigned idk = __shfl_sync(0xffffffffu, id, min(s0 + k, 31));
-                rank += (k < len && idk < id) ? 1 : 0;
-            }
-            if (len >= 2 && s0 + rank != lane) dst[q] = base[q] + s0 + rank;
-        }
-        // every lane's records must be read before any lane overwrites a slot:
-        // the shuffles order only registers, __syncwarp also memory
-        __syncwarp();
+        for (int k = 1; k < SUBB; k++) q += i >= s_pre[k] ? 1 : 0;
+        const float4 r = __ldg(r4 + (long long)q * cap + (i - s_pre[q]));
+        const int key = cell_axis_fast((double)r.y, g.lo1, eff1, g.n1) * g.n0 +
+                        cell_axis_fast((double)r.x, g.lo0, eff0, g.n0);
+        const int lc = (int)(key - cell0);
+        const int arr = atomicAdd(&s_cnt[lc], 1);
+        s_code[i] = lc | (arr << BUCKET_SHIFT) | (q << 25);
+    }
+    __syncthreads();
+    // exclusive scan of the cell counts: thread t owns cells 4t .. 4t + 3
+    const int4 c4 = reinterpret_cast<const int4 *>(s_cnt)[tid];
+    const int csum = c4.x + c4.y + c4.z + c4.w;
+    int v = csum;
 #pragma unroll
-        for (int q = 0; q < G; q++) {
-            if (dst[q] >= 0) r4[dst[q]] = r[q];
-            if (cnt[q] > 32) {
-                if (en[q] - st0[q] >= 2) cell_insertion_sort(r4, st0[q], en[q]);
-                for (int k = st0[q]; deposit && k < en[q]; k++) {
-                    const float4 rv = r4[k];
-                    const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
-                    if (bits) deposit_record(rv, gg, d0, d1, bits, rho_q, m);
-                }
-            } else if (deposit && lane < cnt[q]) {
-                const unsigned bits = (__float_as_uint(r[q].z) >> 31) ? bits1 : bits0;
-                if (bits) deposit_record(r[q], gg, d0, d1, bits, rho_q, m);
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    __syncthreads();
+    int wbase = 0;
+#pragma unroll
+    for (int w = 0; w < BSORT_THREADS / 32; w++) wbase += w < warp ? s_wsum[w] : 0;
+    int4 b4;
+    b4.x = wbase + v - csum;
+    b4.y = b4.x + c4.x;
+    b4.z = b4.y + c4.y;
+    b4.w = b4.z + c4.z;
+    reinterpret_cast<int4 *>(s_beg)[tid] = b4;
+    if (tid == 0) s_beg[BUCKET_CELLS] = cnt;
+    const long long cfirst = cell0 + CELLS_PER_THREAD * tid;
+    const int4 o4 = make_int4(off + b4.x, off + b4.y, off + b4.z, off + b4.w);
+    if (cfirst + 4 <= nflat) {
+        reinterpret_cast<int4 *>(starts + cfirst)[0] = o4;
+    } else {
+        const int ov[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (cfirst + k < nflat) starts[cfirst + k] = ov[k];
+    }
+    if (cell_max > 0) {
+        const int cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (cv[k] > cell_max && cfirst + k < nflat) {
+                // a grid node could collect more particle masses of 2^22 than
+                // an int32 sums exactly
+                atomicMin(&st->key, err_key(3, cfirst + k, CS_DEPOSIT_OVERFLOW));
+                st->abort = 1;
+                st->step = step;
             }
         }
     }
-}
-
-// CIC deposit of the sorted records for the next step's field: consecutive
-// threads hit adjacent grid nodes, so the integer reductions stay L2-local
-// (deterministic: integer addition is associative).
-__global__ void __launch_bounds__(256)
-k_fast_deposit(const Rec *__restrict__ rec, long long n, GridGeom gg, ExactDiv d0, ExactDiv d1,
-               unsigned bits0, unsigned bits1, int *__restrict__ rho_q) {
-    const int m = gg.n * gg.n;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rec) + t);
-        const unsigned bits = (__float_as_uint(rv.z) >> 31) ? bits1 : bits0;
-        if (!bits) continue;
-        const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
-        if (bits & 1u) cic_deposit_q(c, rho_q);
-        if (bits & 2u) cic_deposit_q(c, rho_q + m);
+    if (b == nbucket - 1 && tid == 0) starts[nflat] = off + cnt;
+    {
+        // overflowed parts (the run is stopped): the lost records' slots get
+        // an in-domain placeholder, so that no kernel reads garbage ids or
+        // coordinates before the host sees the status
+        const int full = boff[(b + 1) * SUBB] - off;
+        for (int i = cnt + tid; i < full; i += BSORT_THREADS) {
+            Rec ph;
+            ph.x = (float)g.lo0;
+            ph.y = (float)g.lo1;
+            ph.meta = 0;
+            ph.wx = 0;
+            ph.wy = 0;
+            out[off + i] = ph;
+        }
+    }
+    __syncthreads();
+    constexpr int LC_MASK = BUCKET_CELLS - 1;
+    constexpr int ARR_MASK = (1 << (25 - BUCKET_SHIFT)) - 1;
+    for (int i = tid; i < cnt; i += BSORT_THREADS) {
+        const int code = s_code[i];
+        const int q = code >> 25;
+        s_id[s_beg[code & LC_MASK] + ((code >> BUCKET_SHIFT) & ARR_MASK)] =
+            __float_as_uint(__ldg(r4 + (long long)q * cap + (i - s_pre[q])).z) & ID_MASK;
+    }
+    __syncthreads();
+    const unsigned bits_dep = deposit ? (bits0 | bits1) : 0u;
+    for (int i = tid; i < cnt; i += BSORT_THREADS) {
+        const int code = s_code[i];
+        const int lc = code & LC_MASK;
+        const int q = code >> 25;
+        const int kb = s_beg[lc], len = s_beg[lc + 1] - kb;
+        const float4 r = __ldg(r4 + (long long)q * cap + (i - s_pre[q]));
+        int rank = 0;
+        if (len > 1) {
+            const unsigned id = __float_as_uint(r.z) & ID_MASK;
+            for (int k = 0; k < len; k++) rank += s_id[kb + k] < id ? 1 : 0;
+        }
+        reinterpret_cast<float4 *>(out)[off + kb + rank] = r;
+        if (bits_dep) {
+            const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
+            if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, gg.n * gg.n);
+        }
     }
 }
 
@@ -937,13 +990,15 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 }  // namespace cs
 
 // ---------------------------------------------------------------------------
-constexpr int STARTS_OFF = 3;
+constexpr int STARTS_OFF = 0;
 
 struct cs_fast {
-    cs::Buf rec[2], tmp, keys, counts, starts[2], anchor0, rho_q, force, spec;
+    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
+    long long nbucket = 0;  // buckets of BUCKET_CELLS cells
+    long long cap = 0;      // record slots per bucket region
     double eff0 = 1.0, eff1 = 1.0;  // cell sides
     cs::BinGeom g{};
     bool gather = false;            // deposit by grid rows (k_fast_deposit_rows)
@@ -973,18 +1028,24 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     f->gather = gg && gg->per && g.per0 && g.per1 && gg->n >= 2 &&
                 (size_t)gg->n * DEP_ROWS * 8 <= 200 * 1024 &&
                 !getenv("CS_ATOMIC_DEPOSIT");
+    // bucket regions: 8x the mean bucket population + 256 slots (at least
+    // 1024), capped so that a block's shared staging (8 B per slot) fits
+    f->nbucket = (f->nflat + BUCKET_CELLS - 1) / BUCKET_CELLS;
+    const double mean = (double)(n > 0 ? n : 1) / (double)f->nbucket;
+    long long cap = (long long)(8.0 * mean / SUBB) + 64;  // per region part
+    if (cap < 128) cap = 128;
+    if (cap > 24576 / SUBB) cap = 24576 / SUBB;
+    if (const char *e = getenv("CS_BUCKET_CAP")) cap = atoll(e);  // tests: force overflows
+    f->cap = (cap + 7) / 8 * 8;
     const size_t nr = sizeof(Rec) * (size_t)(n > 0 ? n : 1);
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
-    CS_TRY(f->tmp.ensure(nr));
-    CS_TRY(f->keys.ensure(sizeof(int) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(f->region.ensure(sizeof(Rec) * (size_t)f->nbucket * SUBB * (size_t)f->cap));
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
-    CS_TRY(f->counts.ensure(sizeof(int) * (size_t)f->nflat));
-    CS_CUDA(cudaMemset(f->counts.p, 0, f->counts.bytes));
-    // cell tables: nflat + 1 starts plus one slot for the scan's shifted
-    // output (k_fast_scatter); the table begins STARTS_OFF ints into its
-    // buffer so that the scan's vector stores (at table + 1) stay 16-B
-    // aligned; entry 0 stays 0
+    CS_TRY(f->fill.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 1)));
+    CS_CUDA(cudaMemset(f->fill.p, 0, f->fill.bytes));
+    CS_TRY(f->boff.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 4)));
+    // cell tables: nflat + 1 starts (kept STARTS_OFF ints into the buffer)
     for (int b = 0; b < 2; b++) {
         CS_TRY(f->starts[b].ensure(sizeof(int) * (size_t)(f->nflat + 2 + STARTS_OFF)));
         CS_CUDA(cudaMemset(f->starts[b].p, 0, f->starts[b].bytes));
@@ -999,37 +1060,10 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 
 void fast_destroy(cs_fast *f) {
     if (!f) return;
-    for (Buf *b : {&f->rec[0], &f->rec[1], &f->tmp, &f->keys, &f->counts, &f->starts[0],
+    for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
                    &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec})
         b->release();
     delete f;
-}
-
-static int fast_sort(cs_ctx *ctx, cs_fast *f, long long n, int nxt) {
-    // scan the histogram into the next cell table and reset it in the same pass
-    CS_TRY(exclusive_scan_i32(ctx, f->counts.as<int>(), cell_table(f, nxt) + 1, f->nflat,
-                              f->counts.as<int>()));
-    if (n > 0) {
-        // persistent grid: a single processing front, so the destinations of
-        // the 16-byte scattered records (within ~+-50 cell rows of the front)
-        // complete their sectors in L2 before write-back
-        static int resident = 0;
-        if (!resident) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_scatter, 256, 0);
-            if (resident < 1) resident = 1;
-        }
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        const long long want = (n + 256 * SCATTER_U - 1) / (256 * SCATTER_U);
-        const int grid = (int)(want < (long long)sms * resident ? want : (long long)sms * resident);
-        k_fast_scatter<<<grid, 256, 0, ctx->stream>>>(
-            f->tmp.as<Rec>(), f->keys.as<int>(), n, cell_table(f, nxt),
-            f->rec[nxt].as<Rec>());
-        CS_LAUNCH_CHECK();
-        ctx->launches += 1;
-    }
-    f->cur = nxt;
-    return CS_OK;
 }
 
 static int persistent_grid(cs_ctx *ctx, const void *kern, int block, long long work,
@@ -1054,39 +1088,57 @@ static int deposit_cell_max(const GridGeom &gg, const cs_fast *f) {
     return m < 1.0 ? 1 : (int)m;
 }
 
-// in-cell id order + the next step's deposit over the freshly sorted records
-static int fast_cellfix(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
-                        const unsigned char bits[3], DevStatus *st, int step) {
-    if (p.n <= 0) return CS_OK;
+// Bucket offsets (scan of the claim counts, which it also resets), then the
+// bucket sort into the next record array and cell table (in-cell id order;
+// the atomic-mode deposit of the next step's field rides along).
+static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
+                     const unsigned char bits[3], DevStatus *st, int step) {
+    const int nxt = 1 - f->cur;
+    CS_TRY(exclusive_scan_i32(ctx, f->fill.as<int>(), f->boff.as<int>(), f->nbucket * SUBB,
+                              f->fill.as<int>()));
     const char *dbg = getenv("CS_FAST_DEBUG");
     const int debug = dbg ? atoi(dbg) : 0;
     const bool dep = p.field_active && !(debug & 2);
-    static int res = 0;
     const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
-    const bool rows = dep && f->gather;
-    k_fast_cellfix<<<persistent_grid(ctx, (const void *)k_fast_cellfix, 256, (f->nflat + 1) / 2,
-                                     &res), 256,
-                     0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), cell_table(f, f->cur),
-                                       f->nflat, gg, make_exact_div(d0), make_exact_div(d1),
-                                       dep ? bits[0] : 0u, dep ? bits[1] : 0u,
-                                       f->rho_q.as<int>(), deposit_cell_max(gg, f), st, step,
-                                       dep && !rows);
+    const size_t smem = (size_t)SUBB * f->cap * 2 * sizeof(int);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {  // static + dynamic may pass 48 KB before the dynamic part does
+        CS_CUDA(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        smem_set = smem;
+    }
+    k_bucket_sort<<<(unsigned)f->nbucket, BSORT_THREADS, smem, ctx->stream>>>(
+        f->region.as<Rec>(), f->boff.as<int>(), f->cap, f->nbucket, f->g,
+        make_exact_div(f->g.eff0), make_exact_div(f->g.eff1), f->nflat, f->rec[nxt].as<Rec>(),
+        cell_table(f, nxt), gg, make_exact_div(d0), make_exact_div(d1), dep ? bits[0] : 0u,
+        dep ? bits[1] : 0u, f->rho_q.as<int>(), dep && !f->gather,
+        dep && (bits[0] | bits[1]) ? deposit_cell_max(gg, f) : 0, st,
+        step);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
-    if (rows) {
-        const int smem = (int)(DEP_ROWS * 2 * sizeof(int) * (size_t)gg.n);
-        static int smem_set = 0;
-        if (smem > 48 * 1024 && smem > smem_set) {
-            CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            smem_set = smem;
-        }
-        k_fast_deposit_rows<<<(gg.n + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
-            f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
-            make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>());
-        CS_LAUNCH_CHECK();
-        ctx->launches += 1;
+    f->cur = nxt;
+    return CS_OK;
+}
+
+// periodic grids: the next step's deposit gathered per grid row
+static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
+                             const GridGeom &gg, const unsigned char bits[3]) {
+    const char *dbg = getenv("CS_FAST_DEBUG");
+    const int debug = dbg ? atoi(dbg) : 0;
+    if (p.n <= 0 || !p.field_active || (debug & 2) || !f->gather) return CS_OK;
+    const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
+    const int smem = (int)(DEP_ROWS * 2 * sizeof(int) * (size_t)gg.n);
+    static int smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        smem_set = smem;
     }
+    k_fast_deposit_rows<<<(gg.n + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
+        f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
+        make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>());
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
     return CS_OK;
 }
 
@@ -1096,13 +1148,15 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     const long long n = p.n;
     if (n > 0) {
         k_fast_import<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-            (const float *)s->pos, (const float *)s->anchor, s->type, n, g, f->tmp.as<Rec>(),
-            f->keys.as<int>(), f->counts.as<int>(), f->anchor0.as<float>());
+            (const float *)s->pos, (const float *)s->anchor, s->type, n, g,
+            f->region.as<Rec>(), f->fill.as<int>(), f->cap, f->anchor0.as<float>(), st);
         CS_LAUNCH_CHECK();
+        ctx->launches += 1;
     }
-    CS_TRY(fast_sort(ctx, f, n, 0));
-    if (p.field_active) CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
-    CS_TRY(fast_cellfix(ctx, f, p, gg, bits, st, step));
+    if (p.field_active && !f->gather)
+        CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
+    CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
+    CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits));
     f->imported = true;
     return CS_OK;
 }
@@ -1179,14 +1233,14 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     FastArgs a;
     a.rec = f->rec[f->cur].as<Rec>();
     a.starts = cell_table(f, f->cur);
-    a.tmp = f->tmp.as<Rec>();
-    a.keys = f->keys.as<int>();
+    a.region = f->region.as<Rec>();
+    a.fill = f->fill.as<int>();
+    a.cap = f->cap;
     a.force = f->force.as<double2>();
     {
         const char *dbg = getenv("CS_FAST_DEBUG");
         a.debug = dbg ? atoi(dbg) : 0;
     }
-    a.counts = f->counts.as<int>();
     a.xi = (const float *)xi;
     a.grad = (const float *)s->grad;
     a.rho_q = f->rho_q.as<int>();
@@ -1258,13 +1312,13 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     return CS_OK;
 }
 
-// Next step's deposit over the freshly sorted records: consecutive threads
-// hit adjacent grid lines, so the reductions stay in L2 (deposited from the
-// old order they scattered over +-50 cell rows and missed L2 almost always).
+// part 1: bucket sort into the next record array / cell table (+ the
+// atomic-mode deposit); part 2: the row-gathered deposit (periodic grids)
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
                 const unsigned char bits[3], int part, DevStatus *st, int step) {
-    if (part & 1) CS_TRY(fast_sort(ctx, f, n, 1 - f->cur));
-    if (part & 2) CS_TRY(fast_cellfix(ctx, f, p, gg, bits, st, step));
+    (void)n;
+    if (part & 1) CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
+    if (part & 2) CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits));
     return CS_OK;
 }
 

@@ -471,7 +471,8 @@ int sim_status(cs_sim *sim, cs_status *out) {
         out->particle = (long long)((d.key >> 3) & ((1ULL << 57) - 1));
         out->axis = rank >= 1 ? rank - 1 : 0;
         out->step = d.step;
-        if (out->code == CS_FIELD_NONFINITE || out->code == CS_DEPOSIT_OVERFLOW) {
+        if (out->code == CS_FIELD_NONFINITE || out->code == CS_DEPOSIT_OVERFLOW ||
+            out->code == CS_SORT_OVERFLOW) {
             out->particle = -1;
             out->axis = -1;
         }

@@ -574,6 +574,10 @@ class Realisation:
                     raise SimulationError(
                         "too many particles in one cell for the sorted engine's int32 "
                         "fixed-point deposit; use engine='direct'")
+                if st.code == N.CS_SORT_OVERFLOW:
+                    raise SimulationError(
+                        "local particle density outgrew the sorted engine's bucket regions; "
+                        "use engine='direct'")
                 src = "next_pos" if self._sim.engine == "direct" else "pos"
                 raise_boundary_status(st.code, int(st.particle), int(st.axis),
                                       self._state[src].double().cpu().numpy())

@@ -245,3 +245,26 @@ def test_row_gather_deposit_bitwise_equals_atomic_deposit(monkeypatch):
     monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
     for k in out["rows"]:
         assert torch.equal(out["rows"][k], out["atomic"][k]), k
+
+
+def test_sorted_engine_reports_bucket_overflow(monkeypatch):
+    """More records in a bucket of 256 consecutive cells than its region
+    holds stops the sorted engine with CS_SORT_OVERFLOW (no record is lost
+    silently); the same input with roomy regions runs and matches the direct
+    engine bit for bit."""
+    n = 20_000
+    pos, sp, xi = _inputs(n, 6)
+    pos[:3000, 1] = np.float32(0.2)  # 3000 particles in one cell row: a few buckets
+    x = torch.as_tensor(xi[:2], device="cuda")
+    monkeypatch.setenv("CS_BUCKET_CAP", "16")
+    a, sa = _sim(pos, sp, engine="sorted", field=False)
+    a.step(x, 1)
+    assert a.status().code == cs._native.CS_SORT_OVERFLOW
+    monkeypatch.delenv("CS_BUCKET_CAP")
+    b, sb = _sim(pos, sp, engine="sorted", field=False)
+    c, sc = _sim(pos, sp, engine="direct", field=False)
+    b.step(x, 2)
+    c.step(x, 2)
+    b.export_state()
+    assert b.status().code == 0 and c.status().code == 0
+    assert torch.equal(sb["pos"], sc["pos"])

@@ -65,6 +65,7 @@ static_assert(CELLS_PER_THREAD == 4, "k_bucket_sort owns 4 cells (one int4) per 
 #define CS_SUBB 8
 #endif
 constexpr int SUBB = CS_SUBB;
+constexpr int RPT = 4;  // records per k_bucket_sort thread held in registers
 static_assert(SUBB >= 1 && SUBB <= 32 && (SUBB & (SUBB - 1)) == 0, "SUBB: power of two <= 32");
 constexpr int BUCKET_CELLS = 1 << BUCKET_SHIFT;
 
@@ -516,7 +517,7 @@ k_fast_forces(const DevStatus *st) {
 // Per sorted slot: drift refresh, EM proposal, boundaries, new cell key and
 // rank, deposit of the new position for the next step's field.
 #ifndef CS_UPDATE_MINB
-#define CS_UPDATE_MINB 5  // measured: (256) 245 us, (256,5) 220, (256,6) 272
+#define CS_UPDATE_MINB 4  // measured with the bucket claims: 4: 320 us, 5: 327 (spills), 6: 380
 #endif
 // store a record at its claimed bucket slot (or flag the overflow)
 __device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, int step, int b,
@@ -542,23 +543,11 @@ k_fast_update(DevStatus *st, int step) {
     // atomic's round trip overlaps them instead of stalling the warp
     float4 p_out = make_float4(0.f, 0.f, 0.f, 0.f);
     int p_b = -1, p_slot = 0;
-    // the record and pair force of the next iteration are loaded one
-    // iteration ahead (their latency overlaps this iteration's work)
     const long long stride = (long long)gridDim.x * blockDim.x;
-    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    float4 n_mer = make_float4(0.f, 0.f, 0.f, 0.f);
-    double2 n_f = make_double2(0.0, 0.0);
-    if (t < a.n) {
-        n_mer = __ldcs(rec + t);
-        if (a.interact) n_f = __ldcs(a.force + t);
-    }
-    for (; t < a.n; t += stride) {
-        const float4 mer = n_mer;
-        const double2 f = n_f;
-        if (t + stride < a.n) {
-            n_mer = __ldcs(rec + t + stride);
-            if (a.interact) n_f = __ldcs(a.force + t + stride);
-        }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n; t += stride) {
+        const float4 mer = __ldcs(rec + t);
+        double2 f = make_double2(0.0, 0.0);
+        if (a.interact) f = __ldcs(a.force + t);
         const float xf = mer.x, yf = mer.y;
         const unsigned meta = __float_as_uint(mer.z);
         const unsigned wbits = __float_as_uint(mer.w);
@@ -721,14 +710,15 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
               Rec *__restrict__ out, int *__restrict__ starts, GridGeom gg, ExactDiv d0,
               ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q, int deposit,
               int cell_max, DevStatus *st, int step) {
-    // [SUBB cap] codes (cell | arrival << 10 | part << 25), [SUBB cap] ids by slot
+    // [SUBB cap] ids by slot, then codes (cell | arrival << 10 | part << 25) of
+    // the records beyond the register-resident ones
     extern __shared__ int s_dyn[];
     __shared__ int s_pre[SUBB + 1];
     __shared__ __align__(16) int s_cnt[BUCKET_CELLS];
     __shared__ __align__(16) int s_beg[BUCKET_CELLS + 4];
     __shared__ int s_wsum[BSORT_THREADS / 32];
-    int *s_code = s_dyn;
-    unsigned *s_id = reinterpret_cast<unsigned *>(s_dyn + SUBB * cap);
+    unsigned *s_id = reinterpret_cast<unsigned *>(s_dyn);
+    int *s_code = s_dyn + SUBB * cap;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long b = blockIdx.x;
     // the bucket's records: its SUBB region parts, concatenated (part q
@@ -754,16 +744,41 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
     reinterpret_cast<int4 *>(s_cnt)[tid] = make_int4(0, 0, 0, 0);
     __syncthreads();
     const int cnt = s_pre[SUBB];
-    for (int i = tid; i < cnt; i += BSORT_THREADS) {
-        int q = 0;  // part holding local index i
+    auto part_of = [&](int i) {  // part holding local index i
+        int q = 0;
 #pragma unroll
         for (int k = 1; k < SUBB; k++) q += i >= s_pre[k] ? 1 : 0;
-        const float4 r = __ldg(r4 + (long long)q * cap + (i - s_pre[q]));
+        return q;
+    };
+    auto cell_code = [&](float4 r, int q) {
         const int key = cell_axis_fast((double)r.y, g.lo1, eff1, g.n1) * g.n0 +
                         cell_axis_fast((double)r.x, g.lo0, eff0, g.n0);
         const int lc = (int)(key - cell0);
         const int arr = atomicAdd(&s_cnt[lc], 1);
-        s_code[i] = lc | (arr << BUCKET_SHIFT) | (q << 25);
+        return lc | (arr << BUCKET_SHIFT) | (q << 25);
+    };
+    // the first RPT * BSORT_THREADS records stay in registers through all
+    // phases (their loads issued together); the rest (dense buckets only)
+    // keep their codes in shared memory and are re-read
+    float4 rr[RPT];
+    int cc[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+        const int i = tid + k * BSORT_THREADS;
+        cc[k] = -1;
+        if (i < cnt) {
+            const int q = part_of(i);
+            rr[k] = __ldg(r4 + (long long)q * cap + (i - s_pre[q]));
+            cc[k] = q;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; k++)
+        if (cc[k] >= 0) cc[k] = cell_code(rr[k], cc[k]);
+    for (int i = tid + RPT * BSORT_THREADS; i < cnt; i += BSORT_THREADS) {
+        const int q = part_of(i);
+        s_code[i - RPT * BSORT_THREADS] =
+            cell_code(__ldg(r4 + (long long)q * cap + (i - s_pre[q])), q);
     }
     __syncthreads();
     // exclusive scan of the cell counts: thread t owns cells 4t .. 4t + 3
@@ -829,20 +844,22 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
     __syncthreads();
     constexpr int LC_MASK = BUCKET_CELLS - 1;
     constexpr int ARR_MASK = (1 << (25 - BUCKET_SHIFT)) - 1;
-    for (int i = tid; i < cnt; i += BSORT_THREADS) {
-        const int code = s_code[i];
+#pragma unroll
+    for (int k = 0; k < RPT; k++)
+        if (cc[k] >= 0)
+            s_id[s_beg[cc[k] & LC_MASK] + ((cc[k] >> BUCKET_SHIFT) & ARR_MASK)] =
+                __float_as_uint(rr[k].z) & ID_MASK;
+    for (int i = tid + RPT * BSORT_THREADS; i < cnt; i += BSORT_THREADS) {
+        const int code = s_code[i - RPT * BSORT_THREADS];
         const int q = code >> 25;
         s_id[s_beg[code & LC_MASK] + ((code >> BUCKET_SHIFT) & ARR_MASK)] =
             __float_as_uint(__ldg(r4 + (long long)q * cap + (i - s_pre[q])).z) & ID_MASK;
     }
     __syncthreads();
     const unsigned bits_dep = deposit ? (bits0 | bits1) : 0u;
-    for (int i = tid; i < cnt; i += BSORT_THREADS) {
-        const int code = s_code[i];
+    auto place = [&](float4 r, int code) {
         const int lc = code & LC_MASK;
-        const int q = code >> 25;
         const int kb = s_beg[lc], len = s_beg[lc + 1] - kb;
-        const float4 r = __ldg(r4 + (long long)q * cap + (i - s_pre[q]));
         int rank = 0;
         if (len > 1) {
             const unsigned id = __float_as_uint(r.z) & ID_MASK;
@@ -853,6 +870,14 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
             const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
             if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, gg.n * gg.n);
         }
+    };
+#pragma unroll
+    for (int k = 0; k < RPT; k++)
+        if (cc[k] >= 0) place(rr[k], cc[k]);
+    for (int i = tid + RPT * BSORT_THREADS; i < cnt; i += BSORT_THREADS) {
+        const int code = s_code[i - RPT * BSORT_THREADS];
+        const int q = code >> 25;
+        place(__ldg(r4 + (long long)q * cap + (i - s_pre[q])), code);
     }
 }
 
@@ -1100,7 +1125,8 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const Grid
     const int debug = dbg ? atoi(dbg) : 0;
     const bool dep = p.field_active && !(debug & 2);
     const double d0 = gg.d0 > 0 ? gg.d0 : 1.0, d1 = gg.d1 > 0 ? gg.d1 : 1.0;
-    const size_t smem = (size_t)SUBB * f->cap * 2 * sizeof(int);
+    const long long extra = SUBB * f->cap - RPT * BSORT_THREADS;
+    const size_t smem = sizeof(int) * (size_t)(SUBB * f->cap + (extra > 0 ? extra : 0));
     static size_t smem_set = 0;
     if (smem > smem_set) {  // static + dynamic may pass 48 KB before the dynamic part does
         CS_CUDA(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 1
+#define CS_ABI_VERSION 2
 
 enum cs_code {
     CS_OK = 0,
@@ -158,6 +158,19 @@ int cs_field_step(cs_field_ops *ops, void *c, const void *rho_a,
 /* y = exp(x) on the device with the glibc-exact restatement (test seam). */
 int cs_exp_batch(cs_ctx *ctx, const double *x, double *y, int64_t n);
 
+/* Species switching, one Bernoulli trial per particle against the species
+ * snapshot (reactions.py:43-81 fixed_step_reactions; with p_ab = 0 it is
+ * beta_step_reactions, reactions.py:141-160): an Alpha (type 0) becomes Beta
+ * when u < p_ab; a Beta becomes Alpha when r_beta != 0 and
+ * u < (r_beta * max(local_c, 0)) * dt, and its drift row (if drift != NULL)
+ * is zeroed.  type (n,) u8 in/out, local_c (n,) f64 (NULL: 0), u (n,) f64
+ * uniforms on [0, 1).  flips[0] = Alpha -> Beta, flips[1] = Beta -> Alpha;
+ * *high = the largest flip probability above 1 (0 if none), which the
+ * reference clamps with a warning (the decisions are the same: u < 1). */
+int cs_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drift,
+             const double *u, int64_t n, double p_ab, double r_beta, double dt,
+             int64_t *flips, double *high);
+
 /* ---------------------------------------------------------------------- */
 /* Fused K-step pipeline (Realisation._step_inner, engine.py:369-387).      */
 /* ---------------------------------------------------------------------- */
@@ -183,6 +196,12 @@ typedef struct {
     int32_t store_samples;   /* write drift / local_c every step */
     int32_t store_next;      /* write next_pos every step */
     int32_t engine;          /* CS_ENGINE_AUTO / _DIRECT / _SORTED */
+    /* fixed-step reactions after the boundaries of every step
+     * (engine.py:389-393, reactions.py:43-81), DIRECT engine only: one
+     * uniform per particle per step from cs_sim_step_react's u. */
+    int32_t react;           /* 0 off, 1 fixed-step Bernoulli flips */
+    double react_p_ab;       /* r_alpha * dt */
+    double react_r_beta;     /* Beta -> Alpha rate per unit concentration */
 } cs_sim_params;
 
 /* Engines.  DIRECT keeps the reference layout (rows in id order) and
@@ -198,7 +217,7 @@ typedef struct {
     void *pos;               /* (n, 2) prec, in/out */
     void *next_pos;          /* (n, 2) prec, optional */
     void *anchor;            /* (n, 2) prec, in/out */
-    const uint8_t *type;     /* (n,) or NULL */
+    uint8_t *type;           /* (n,) or NULL; switched in place by reactions */
     double *drift;           /* (n, 2) f64; read when refresh is off */
     double *local_c;         /* (n,) f64, optional */
     void *c;                 /* (n_c^2) prec */
@@ -216,6 +235,8 @@ typedef struct {
     int64_t neg_mass_steps;  /* steps with negative weighted mass < -1e-12 */
     double first_neg_mass;
     int64_t steps_done;
+    int64_t react_high_count; /* particle-steps whose flip probability exceeded 1 */
+    double react_high_max;    /* the largest such probability */
 } cs_status;
 
 int cs_sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out);
@@ -225,6 +246,11 @@ int cs_sim_destroy(cs_sim *sim);
  * steps xi_stride elements apart. */
 int cs_sim_step(cs_sim *sim, const cs_sim_state *st, const void *xi,
                 int64_t xi_stride, int32_t k_steps);
+/* cs_sim_step with the reaction uniforms of params.react: u points at the
+ * (n,) f64 uniforms of the first step, successive steps u_stride apart. */
+int cs_sim_step_react(cs_sim *sim, const cs_sim_state *st, const void *xi,
+                      int64_t xi_stride, const double *u, int64_t u_stride,
+                      int32_t k_steps);
 /* Synchronise and read the status accumulated since the last reset. */
 int cs_sim_status(cs_sim *sim, cs_status *out);
 int cs_sim_reset_status(cs_sim *sim);

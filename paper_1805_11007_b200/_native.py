@@ -49,7 +49,8 @@ class SimParams_t(ctypes.Structure):
                 ("gamma", C_f64), ("deposit_kind", C_i32), ("kernel_h", C_f64),
                 ("kernel_cutoff", C_f64), ("secretes", C_i32 * 2), ("consumes", C_i32 * 2),
                 ("chi", C_f64 * 2), ("chi_pinned", C_i32 * 2), ("store_samples", C_i32),
-                ("store_next", C_i32), ("engine", C_i32)]
+                ("store_next", C_i32), ("engine", C_i32), ("react", C_i32),
+                ("react_p_ab", C_f64), ("react_r_beta", C_f64)]
 
 
 class SimState_t(ctypes.Structure):
@@ -61,7 +62,8 @@ class SimState_t(ctypes.Structure):
 class Status_t(ctypes.Structure):
     _fields_ = [("code", C_i32), ("step", C_i32), ("particle", C_i64), ("axis", C_i32),
                 ("clamped", C_i64), ("neg_mass_steps", C_i64), ("first_neg_mass", C_f64),
-                ("steps_done", C_i64)]
+                ("steps_done", C_i64), ("react_high_count", C_i64),
+                ("react_high_max", C_f64)]
 
 
 # (name, restype, argtypes) -- every symbol include/chemo_b200.h declares
@@ -92,9 +94,13 @@ SIGNATURES = [
     ("cs_field_step", C_i32, [C_p, C_p, C_p, C_p, C_f64, C_f64, C_f64, ctypes.POINTER(C_i32),
                               ctypes.POINTER(C_f64)]),
     ("cs_exp_batch", C_i32, [C_p, C_p, C_p, C_i64]),
+    ("cs_react", C_i32, [C_p, C_p, C_p, C_p, C_p, C_i64, C_f64, C_f64, C_f64,
+                         ctypes.POINTER(C_i64), ctypes.POINTER(C_f64)]),
     ("cs_sim_create", C_i32, [C_p, ctypes.POINTER(SimParams_t), ctypes.POINTER(C_p)]),
     ("cs_sim_destroy", C_i32, [C_p]),
     ("cs_sim_step", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p, C_i64, C_i32]),
+    ("cs_sim_step_react", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p, C_i64, C_p, C_i64,
+                                  C_i32]),
     ("cs_sim_status", C_i32, [C_p, ctypes.POINTER(Status_t)]),
     ("cs_sim_reset_status", C_i32, [C_p]),
     ("cs_sim_launches", C_i64, [C_p]),

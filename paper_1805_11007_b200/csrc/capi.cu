@@ -109,7 +109,11 @@ int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, 
 int field_load_rhs(cs_field_ops *ops, const void *rhs);
 int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out);
 void sim_destroy(cs_sim *sim);
-int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k);
+int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k,
+             const double *u, int64_t u_stride);
+int launch_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drift,
+                 const double *u, long long n, double p_ab, double r_beta, double dt,
+                 DevStatus *st);
 int sim_status(cs_sim *sim, cs_status *out);
 int sim_reset_status(cs_sim *sim);
 
@@ -374,7 +378,35 @@ int cs_sim_destroy(cs_sim *sim) {
 
 int cs_sim_step(cs_sim *sim, const cs_sim_state *st, const void *xi, int64_t xi_stride,
                 int32_t k_steps) {
-    return sim_step(sim, st, xi, xi_stride, k_steps);
+    return sim_step(sim, st, xi, xi_stride, k_steps, nullptr, 0);
+}
+
+int cs_sim_step_react(cs_sim *sim, const cs_sim_state *st, const void *xi, int64_t xi_stride,
+                      const double *u, int64_t u_stride, int32_t k_steps) {
+    return sim_step(sim, st, xi, xi_stride, k_steps, u, u_stride);
+}
+
+int cs_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drift, const double *u,
+             int64_t n, double p_ab, double r_beta, double dt, int64_t *flips, double *high) {
+    if (n < 0 || !(p_ab >= 0.0) || !(r_beta >= 0.0)) {
+        set_error("cs_react: n, p_ab and r_beta must be non-negative");
+        return CS_ERR_PARAM;
+    }
+    DevStatus *st;
+    CS_TRY(local_status(ctx, &st));
+    CS_TRY(launch_react(ctx, type, local_c, drift, u, n, p_ab, r_beta, dt, st));
+    DevStatus d;
+    CS_CUDA(cudaMemcpyAsync(&d, st, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (flips) {
+        flips[0] = (int64_t)d.react_flips[0];
+        flips[1] = (int64_t)d.react_flips[1];
+    }
+    if (high) {
+        *high = 0.0;
+        if (d.react_high_n) memcpy(high, &d.react_high_bits, sizeof(double));
+    }
+    return CS_OK;
 }
 
 int cs_sim_status(cs_sim *sim, cs_status *out) { return sim_status(sim, out); }

@@ -65,6 +65,9 @@ struct DevStatus {
     double neg_mass;          // scratch: this step's negative weighted mass
     int neg_flag;             // scratch: this step saw a negative node
     int pad2;
+    unsigned long long react_flips[2];  // Alpha -> Beta, Beta -> Alpha
+    unsigned long long react_high_n;    // particle-steps with a flip probability > 1
+    unsigned long long react_high_bits; // max such probability (binary64 bits; > 0)
 };
 
 // error key: rank 0 = non-finite (lowest index wins), rank 1 + ax = axis

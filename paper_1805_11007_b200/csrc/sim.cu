@@ -1,4 +1,5 @@
 #include <stdlib.h>
+#include <string.h>
 // sim.cu -- the fused per-step pipeline (Realisation._step_inner,
 // engine.py:369-387) run for K steps on the device without host syncs.
 //
@@ -32,6 +33,9 @@ void field_ops_destroy(cs_field_ops *ops);
 int field_solve_rhs(cs_field_ops *ops, void *out);
 int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
               double kb, double gamma, const DevStatus *st);
+int launch_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drift,
+                 const double *u, long long n, double p_ab, double r_beta, double dt,
+                 DevStatus *st);
 
 struct FastStepCfg {
     const cs_sim_params *p;
@@ -229,7 +233,12 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
         const double per_cell = (double)p->n / ((double)g.n0 * (double)g.n1);
         bool want_sorted = p->engine == CS_ENGINE_SORTED ||
                            (p->engine == CS_ENGINE_AUTO && p->prec == CS_F32 &&
-                            !p->store_samples && !p->store_next && per_cell <= 4.0);
+                            !p->store_samples && !p->store_next && !p->react &&
+                            per_cell <= 4.0);
+        if (want_sorted && p->react) {
+            set_error("reactions run on the direct engine only");
+            return CS_ERR_PARAM;
+        }
         if (want_sorted && p->prec != CS_F32) {
             set_error("the sorted engine stores binary32 records (prec must be CS_F32)");
             return CS_ERR_PARAM;
@@ -310,7 +319,16 @@ int sim_collect_stage_times(cs_sim *sim) {
     return CS_OK;
 }
 
-int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k) {
+int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride, int k,
+             const double *u, int64_t u_stride) {
+    if (sim->p.react && !u) {
+        set_error("params.react is set: the step needs the reaction uniforms (cs_sim_step_react)");
+        return CS_ERR_PARAM;
+    }
+    if (sim->p.react && !s->type) {
+        set_error("reactions need the species array");
+        return CS_ERR_PARAM;
+    }
     cs_ctx *ctx = sim->ctx;
     const cs_sim_params &p = sim->p;
     DevStatus *st = sim->dstat();
@@ -436,7 +454,9 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         a.chi_pinned[0] = p.chi_pinned[0];
         a.chi_pinned[1] = p.chi_pinned[1];
         a.refresh = p.refresh_active;
-        a.store_samples = p.store_samples && s->drift && s->local_c;
+        // Beta -> Alpha flips read this step's local concentration
+        a.store_samples = (p.store_samples || (p.react && p.react_r_beta != 0.0)) && s->drift &&
+                          s->local_c;
         a.store_next = p.store_next && s->next_pos;
         a.dom = p.domain;
         a.gg = sim->gg;
@@ -449,6 +469,12 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 k_update<float><<<grid_for(n, B), B, 0, ctx->stream>>>(a, st, step);
             CS_LAUNCH_CHECK();
             ctx->launches += 1;
+        }
+        if (p.react) {  // fixed-step reactions after the boundaries (engine.py:387-393)
+            StageMark m(sim, CS_STAGE_UPDATE);
+            CS_TRY(launch_react(ctx, s->type, s->local_c, s->drift,
+                                u + (size_t)kk * (size_t)u_stride, n, p.react_p_ab,
+                                p.react_r_beta, p.dt, st));
         }
     }
     sim->steps_done += k;
@@ -481,6 +507,9 @@ int sim_status(cs_sim *sim, cs_status *out) {
     out->neg_mass_steps = d.neg_steps;
     out->first_neg_mass = d.first_neg;
     out->steps_done = sim->steps_done;
+    out->react_high_count = (int64_t)d.react_high_n;
+    out->react_high_max = 0.0;
+    if (d.react_high_n) memcpy(&out->react_high_max, &d.react_high_bits, sizeof(double));
     return CS_OK;
 }
 

@@ -24,8 +24,12 @@ Extensions (BASELINE configs 1-4):
   alpha_init           "normal" (reference) | "uniform"
   initial_positions    "default" | "clusters" (n_clusters centres, offset
                        N(0, cluster_sigma^2), wrapped; BASELINE config 4)
-Out of scope: reactions (r_alpha/r_beta > 0), hard-sphere
-interaction and the tamed integrator raise NotImplementedError.
+Reactions: the fixed scheduler runs on the device after
+the boundaries of every step (one rng_react.random(N) block per step, the
+reference's stream layout); the gillespie scheduler keeps the reference's
+host event clock and runs the Beta -> Alpha trials on the device.  Both run
+on the direct engine.  Out of scope: the hard-sphere interaction
+and the tamed integrator raise NotImplementedError.
 """
 
 from __future__ import annotations
@@ -44,6 +48,7 @@ from .coupling import Kernel
 from .field import Field, FieldParams, Grid, Operators
 from .motion import MotionParams, SimulationError, raise_boundary_status
 from .particles import Population, Species, clustered_positions, init_population
+from .reactions import AlphaEventClock, ReactionParams, beta_step_reactions
 from .spatial_index import Domain
 
 EXPERIMENTS = ("fig1", "counts", "msd1", "msd2", "msd3", "custom")
@@ -221,6 +226,10 @@ class SimConfig:
                             radius_alpha=self.radius_alpha, radius_beta=self.radius_beta,
                             cutoff_factor=self.soft_cutoff_factor)
 
+    def reaction_params(self) -> ReactionParams:
+        return ReactionParams(r_alpha=self.r_alpha, r_beta=self.r_beta,
+                              scheduler=self.scheduler)
+
     def field_params(self) -> FieldParams:
         return FieldParams(d_c=self.d_c, k_alpha=self.k_alpha, k_beta=self.k_beta,
                            gamma=self.gamma)
@@ -258,7 +267,8 @@ class Observables:
 def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, field_active,
                       refresh_active, grid: Grid | None, fparams: FieldParams | None,
                       kernel: Kernel | None, secretes, consumes, chi, chi_pinned,
-                      store_samples, store_next, engine: str = "auto") -> N.SimParams_t:
+                      store_samples, store_next, engine: str = "auto",
+                      reaction: ReactionParams | None = None) -> N.SimParams_t:
     p = N.SimParams_t()
     p.n = int(n)
     p.prec = prec
@@ -292,6 +302,11 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
     p.store_next = int(bool(store_next))
     p.engine = {"auto": N.CS_ENGINE_AUTO, "direct": N.CS_ENGINE_DIRECT,
                 "sorted": N.CS_ENGINE_SORTED}[engine]
+    if reaction is not None and reaction.scheduler == "fixed" and (
+            reaction.r_alpha > 0 or reaction.r_beta > 0):
+        p.react = 1
+        p.react_p_ab = float(reaction.r_alpha * dt)  # reactions.py:61
+        p.react_r_beta = float(reaction.r_beta)
     return p
 
 
@@ -322,12 +337,19 @@ class DeviceSim:
             setattr(s, name, None if t is None else t.data_ptr())
         s.type = None if state.get("species") is None else state["species"].data_ptr()
 
-    def step(self, xi, k: int, stride: int | None = None):
-        """Enqueue k steps; xi is a device tensor holding k (N, 2) blocks."""
+    def step(self, xi, k: int, stride: int | None = None, u=None):
+        """Enqueue k steps; xi is a device tensor holding k (N, 2) blocks
+        (u: k (N,) f64 blocks of reaction uniforms when params.react)."""
         if stride is None:
             stride = 2 * self.n
-        N.check(N.load_library().cs_sim_step(self._h, ctypes.byref(self._st), N.ptr(xi),
-                                             int(stride), int(k)), "cs_sim_step")
+        lib = N.load_library()
+        if u is None:
+            N.check(lib.cs_sim_step(self._h, ctypes.byref(self._st), N.ptr(xi), int(stride),
+                                    int(k)), "cs_sim_step")
+        else:
+            N.check(lib.cs_sim_step_react(self._h, ctypes.byref(self._st), N.ptr(xi),
+                                          int(stride), N.ptr(u), self.n, int(k)),
+                    "cs_sim_step_react")
 
     def status(self) -> N.Status_t:
         st = N.Status_t()
@@ -396,10 +418,8 @@ class Realisation:
         self.dt = config.dt
         self.n_steps = config.n_steps
         self.step_index = 0
-        if config.r_alpha > 0 or config.r_beta > 0:
-            raise NotImplementedError(
-                "species reactions are out of scope of the device hot path (SURVEY 8f); "
-                "set r_alpha = r_beta = 0")
+        self.reaction = config.reaction_params()
+        self.reactions_active = self.reaction.r_alpha > 0 or self.reaction.r_beta > 0
         if config.interaction == "hard" or config.integrator == "tamed":
             raise NotImplementedError("hard-sphere / tamed motion is out of scope (SURVEY 8f)")
 
@@ -446,7 +466,8 @@ class Realisation:
             self._initial_refresh()
         # fp64 keeps the reference's per-step drift / local_c / next_positions
         # stores; fp32 runs drop them so the sorted engine can be used
-        self._stores = config.precision == "fp64" or config.engine == "direct"
+        self._stores = (config.precision == "fp64" or config.engine == "direct"
+                        or self.reactions_active)
         params = sim_params_struct(
             n=len(host), prec=N.prec_code(dt_), domain=self.domain, motion=self.motion,
             dt=self.dt, field_active=self.field_active, refresh_active=self.refresh_active,
@@ -454,8 +475,14 @@ class Realisation:
             secretes=(config.secrete_alpha, config.secrete_beta),
             consumes=(config.consume_alpha, config.consume_beta), chi=self._chi,
             chi_pinned=self._chi_pinned, store_samples=self._stores,
-            store_next=self._stores, engine=config.engine)
+            store_next=self._stores, engine=config.engine, reaction=self.reaction)
         self._sim = DeviceSim(params, self._state)
+        self._fixed = self.reactions_active and self.reaction.scheduler == "fixed"
+        self.clock = None
+        if self.reactions_active and self.reaction.scheduler == "gillespie":
+            n_a = int(np.count_nonzero(host.species == Species.ALPHA))
+            self.clock = AlphaEventClock(n_a, self.reaction.r_alpha, 0.0, self.rng_react)
+        self._warned_react = 0
         self._warned_clamp = 0
         self._warned_neg = 0
         self._dead = False
@@ -553,14 +580,15 @@ class Realisation:
     def time(self) -> float:
         return self.step_index * self.dt
 
-    def _advance(self, xi_host: np.ndarray) -> None:
+    def _advance(self, xi_host: np.ndarray, u_host: np.ndarray | None = None) -> None:
         """Run xi_host.shape[0] steps on the device, then check the status."""
         import torch
         if self._dead:
             raise SimulationError("realisation already failed")
         k = xi_host.shape[0]
         xi = torch.as_tensor(xi_host, device="cuda").to(self.dtype).contiguous()
-        self._sim.step(xi, k)
+        u = None if u_host is None else torch.as_tensor(u_host, device="cuda").contiguous()
+        self._sim.step(xi, k, u=u)
         self._sim.export_state()
         st = self._sim.status()
         self._report_warnings(st)
@@ -585,7 +613,21 @@ class Realisation:
                 raise SimulationError(f"step {st.step}: {exc}") from exc
         self.step_index += k
 
+    def _react_host(self, now: float) -> None:
+        """Gillespie scheduler after a device step (engine.py:389-400): the
+        event clock on the host, the Beta -> Alpha trials on the device."""
+        view = _SpeciesView(self._state)
+        self.clock.advance(view, now, self.rng_react)
+        flipped = beta_step_reactions(view, self.reaction, self.dt, self.rng_react)
+        if flipped:
+            n_a = int((self._state["species"] == int(Species.ALPHA)).sum().item())
+            self.clock.reschedule(n_a, now, self.rng_react)
+
     def _report_warnings(self, st) -> None:
+        if st.react_high_count > self._warned_react:
+            warnings.warn(f"flip probability {st.react_high_max:.3g} exceeded 1 and was "
+                          "clamped; reduce dt", stacklevel=3)
+            self._warned_react = st.react_high_count
         if st.clamped > self._warned_clamp:
             warnings.warn(f"{st.clamped - self._warned_clamp} interpolation point(s) outside "
                           "the grid hull were clamped", stacklevel=3)
@@ -597,14 +639,23 @@ class Realisation:
 
     def step(self) -> None:
         """Advance the whole system by dt (fixed sub-stage order)."""
-        xi = self.rng_motion.standard_normal((1, len(self._ids), 2))
-        self._advance(xi)
+        n = len(self._ids)
+        xi = self.rng_motion.standard_normal((1, n, 2))
+        u = self.rng_react.random((1, n)) if self._fixed else None
+        self._advance(xi, u)
+        if self.clock is not None:
+            # step s reacts at now = (s + 1) dt (engine.py:387), s + 1 = step_index
+            self._react_host(self.step_index * self.dt)
         self._observe(self.step_index)
 
     def run(self, max_block_bytes: int = 1 << 28) -> Observables:
         n = len(self._ids)
         per_step = 16 * n
         cap = max(1, max_block_bytes // max(per_step, 1))
+        if self.clock is not None:  # host event clock: one step at a time
+            while self.step_index < self.n_steps:
+                self.step()
+            return self._observables()
         while self.step_index < self.n_steps:
             s = self.step_index
             nxt = s + 1
@@ -615,14 +666,33 @@ class Realisation:
             # one (N, 2) block per step, drawn as one array: bit-identical
             # to k successive draws
             xi = self.rng_motion.standard_normal((k, n, 2))
-            self._advance(xi)
+            # one (N,) uniform block per step: rng.random((k, n)) is
+            # bit-identical to k successive rng.random(n) draws
+            u = self.rng_react.random((k, n)) if self._fixed else None
+            self._advance(xi, u)
             self._observe(self.step_index)
+        return self._observables()
+
+    def _observables(self) -> Observables:
         return Observables(times=np.array(self._times),
                            counts=np.array(self._counts, dtype=np.int64),
                            msd=np.array(self._msd),
                            snapshot_times=np.array(self._snapshot_steps, dtype=float) * self.dt,
                            hist_alpha=self._hist_alpha, hist_beta=self._hist_beta,
                            field_c=self._field_c)
+
+
+class _SpeciesView:
+    """The population slice the reaction functions touch, over the
+    Realisation's device tensors."""
+
+    def __init__(self, state: dict):
+        self.species = state["species"]
+        self.local_concentration = state["local_c"]
+        self.drift = state["drift"]
+
+    def __len__(self) -> int:
+        return int(self.species.shape[0])
 
 
 def run_realisation(config: SimConfig, sample: int) -> Observables:

@@ -299,6 +299,97 @@ def composed_cfg2_small():
     np.savez_compressed(os.path.join(OUT, "cfg2_small.npz"), **res)
 
 
+def reaction_cases():
+    """fixed_step_reactions / beta_step_reactions on seeded populations
+    (mixed species, negative / zero / large local concentrations, nonzero
+    drift rows so the zeroing of new Alphas shows), including clamped
+    probabilities; AlphaEventClock event sequences."""
+    rng = np.random.default_rng(31)
+    res = {}
+    cases = [(10.0, 0.0, 1e-3), (10.0, 50.0, 1e-3), (0.0, 80.0, 2e-3),
+             (600.0, 0.0, 2e-3), (5.0, 400.0, 3e-3), (0.0, 0.0, 1e-3)]
+    for k, (ra, rb, dt) in enumerate(cases):
+        n = int(rng.integers(50, 400))
+        species = rng.integers(0, 2, n).astype(np.uint8)
+        local_c = rng.normal(2.0, 3.0, n)
+        local_c[:5] = [0.0, -0.0, -1.0, 1e3, 0.5]
+        drift = rng.normal(0.0, 1.0, (n, 2))
+        pop = mkpop(rng.uniform(-0.5, 0.5, (n, 2)), species)
+        pop.local_concentration[:] = local_c
+        pop.drift[:] = drift
+        seed = 1000 + k
+        u = np.random.default_rng(seed).random(n)
+        params = cs.ReactionParams(r_alpha=ra, r_beta=rb)
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            cnt = cs.fixed_step_reactions(pop, params, dt, np.random.default_rng(seed))
+        res[f"f{k}_in"] = np.array([ra, rb, dt])
+        res[f"f{k}_species"] = species
+        res[f"f{k}_local_c"] = local_c
+        res[f"f{k}_drift"] = drift
+        res[f"f{k}_u"] = u
+        res[f"f{k}_out_species"] = pop.species.copy()
+        res[f"f{k}_out_drift"] = pop.drift.copy()
+        res[f"f{k}_counts"] = np.array(cnt)
+        res[f"f{k}_warned"] = np.array(len(w))
+        # the Beta channel alone (gillespie companion)
+        pop2 = mkpop(pop.positions, species)
+        pop2.local_concentration[:] = local_c
+        pop2.drift[:] = drift
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            nb = cs.beta_step_reactions(pop2, params, dt, np.random.default_rng(seed))
+        res[f"b{k}_out_species"] = pop2.species.copy()
+        res[f"b{k}_out_drift"] = pop2.drift.copy()
+        res[f"b{k}_count"] = np.array(nb)
+        res[f"b{k}_warned"] = np.array(len(w))
+    res["n_fixed"] = np.array(len(cases))
+    # event clock: species after successive advances and the clock times
+    species = rng.integers(0, 2, 120).astype(np.uint8)
+    pop = mkpop(rng.uniform(-0.5, 0.5, (120, 2)), species)
+    crng = np.random.default_rng(77)
+    clock = cs.AlphaEventClock(pop.n_alpha, 40.0, 0.0, crng)
+    res["clock_species0"] = species
+    times = [clock.next_time]
+    fired = []
+    for until in (0.001, 0.004, 0.01, 0.02, 0.05):
+        fired.append(clock.advance(pop, until, crng))
+        times.append(clock.next_time)
+        res[f"clock_species_{until}"] = pop.species.copy()
+    res["clock_times"] = np.array(times)
+    res["clock_fired"] = np.array(fired)
+    np.savez_compressed(os.path.join(OUT, "reactions.npz"), **res)
+
+
+def reaction_trajectories():
+    """fig1-like runs with reactions through the reference's Realisation
+    unmodified: 40 particles, soft forces, gaussian deposit on the Neumann
+    52^2 grid, both schedulers; rates raised so that flips (both ways) and,
+    in one case, clamped probabilities occur within the recorded steps."""
+    res = {}
+    runs = {
+        "fixed": dict(r_alpha=8000.0, r_beta=3000.0, scheduler="fixed"),
+        "gillespie": dict(r_alpha=3000.0, r_beta=3000.0, scheduler="gillespie"),
+        "fixed_clamp": dict(r_alpha=3.0e5, r_beta=0.0, scheduler="fixed"),
+        "counts": dict(r_alpha=3000.0, r_beta=0.0, scheduler="fixed",
+                       interaction="none", d_c=0.0, k_alpha=0.0, k_beta=0.0, dt=1e-4),
+    }
+    for name, kw in runs.items():
+        cfg = cs.SimConfig(n_alpha_0=20, n_beta_0=20, t_final=1.0, seed_base=5, **kw)
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            real = cs.Realisation(cfg, 1)
+            res[f"{name}_pos0"] = real.pop.positions.copy()
+            for s in range(1, 31):
+                real.step()
+                if s in (1, 5, 10, 20, 30):
+                    res[f"{name}_pos{s}"] = real.pop.positions.copy()
+                    res[f"{name}_species{s}"] = real.pop.species.copy()
+            res[f"{name}_warned"] = np.array(
+                sum("flip probability" in str(x.message) for x in w))
+    np.savez_compressed(os.path.join(OUT, "reaction_traj.npz"), **res)
+
+
 class _Replay:
     """Generator stand-in handing em_step a pre-drawn block."""
 
@@ -320,6 +411,8 @@ if __name__ == "__main__":
     cfg0_trajectory()
     composed_cfg1_small()
     composed_cfg2_small()
+    reaction_cases()
+    reaction_trajectories()
     for name in sorted(os.listdir(OUT)):
         if name.endswith(".npz"):
             print(name, os.path.getsize(os.path.join(OUT, name)))

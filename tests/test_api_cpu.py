@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert {n for n, _, _ in N.SIGNATURES} == decl
-    assert lib.cs_abi_version() == 1
+    assert lib.cs_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
@@ -111,3 +111,35 @@ def test_clustered_positions_wrap_into_box():
     dom = cs.Domain.square(1.0, periodic=True)
     pos = cs.clustered_positions(100000, dom, np.random.default_rng(0))
     assert np.all(pos >= -0.5) and np.all(pos < 0.5)
+
+
+def test_reaction_params_validate_like_reference():
+    with pytest.raises(ValueError, match="non-negative"):
+        cs.ReactionParams(r_alpha=-1.0)
+    with pytest.raises(ValueError, match="unknown reaction scheduler"):
+        cs.ReactionParams(scheduler="tau")
+    assert cs.SimConfig().reaction_params() == cs.ReactionParams(10.0, 0.0, "fixed")
+
+
+def test_exponential_waiting_time_and_event_clock_match_reference_golden():
+    """The event clock is host logic (reactions.py:84-138): on a host
+    population it must reproduce the reference's picks and times exactly."""
+    from conftest import load_golden
+    r = load_golden("reactions.npz")
+    assert cs.exponential_waiting_time(0, 5.0, np.random.default_rng(0)) == np.inf
+    assert cs.exponential_waiting_time(3, 0.0, np.random.default_rng(0)) == np.inf
+    species = r["clock_species0"].copy()
+    n = species.shape[0]
+    pop = cs.Population(ids=np.arange(n), positions=np.zeros((n, 2)),
+                        next_positions=np.zeros((n, 2)), species=species,
+                        drift=np.zeros((n, 2)), local_concentration=np.zeros(n),
+                        start_anchor=np.zeros((n, 2)))
+    rng = np.random.default_rng(77)
+    clock = cs.AlphaEventClock(pop.n_alpha, 40.0, 0.0, rng)
+    times, fired = [clock.next_time], []
+    for until in (0.001, 0.004, 0.01, 0.02, 0.05):
+        fired.append(clock.advance(pop, until, rng))
+        times.append(clock.next_time)
+        assert np.array_equal(pop.species, r[f"clock_species_{until}"]), until
+    assert np.array_equal(np.array(times), r["clock_times"])
+    assert np.array_equal(np.array(fired), r["clock_fired"])

@@ -390,7 +390,19 @@ def test_realisation_errors_map_to_reference_exceptions():
 
 def test_out_of_scope_paths_fail_loudly():
     with pytest.raises(NotImplementedError):
-        cs.Realisation(cs.SimConfig(), 0)  # default config has reactions on
+        cs.Realisation(cs.SimConfig(interaction="hard"), 0)
+    with pytest.raises(NotImplementedError):
+        cs.Realisation(cs.SimConfig(integrator="tamed"), 0)
+
+
+def test_default_fig1_config_runs_on_the_device():
+    """The reference's default SimConfig (the fig1 clustering experiment:
+    reactions on, gaussian deposit, Neumann 52^2 field) steps through the
+    drop-in Realisation."""
+    real = cs.Realisation(cs.SimConfig(), 0)
+    for _ in range(5):
+        real.step()
+    assert real.step_index == 5 and len(real.pop) == 200
 
 
 # ------------------------------------------------------------------- full size

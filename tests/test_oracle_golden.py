@@ -223,3 +223,23 @@ def test_glibc_exp_restatement_matches_host_libm():
         a = oracle.host_exp(float(x))
         b = py_exp(float(x))
         assert a == b or (np.isnan(a) and np.isnan(b)), x
+
+
+def test_reaction_restatement_matches_reference_golden():
+    """oracle/react.py against fixed_step_reactions / beta_step_reactions of
+    the reference (tests/golden/reactions.npz): switched species, zeroed
+    drift rows, flip counts and the clamp warning, bit for bit."""
+    from oracle.react import fixed_step
+    r = load_golden("reactions.npz")
+    for k in range(int(r["n_fixed"])):
+        ra, rb, dt = r[f"f{k}_in"]
+        args = (r[f"f{k}_species"], r[f"f{k}_local_c"], r[f"f{k}_drift"], r[f"f{k}_u"])
+        t, d, c, h = fixed_step(*args, ra * dt, rb, dt)
+        assert np.array_equal(t, r[f"f{k}_out_species"]), k
+        assert np.array_equal(d, r[f"f{k}_out_drift"]), k
+        assert c == tuple(int(v) for v in r[f"f{k}_counts"]), k
+        assert (h > 1.0) == bool(r[f"f{k}_warned"]), k
+        t, d, c, h = fixed_step(*args, 0.0, rb, dt)
+        assert np.array_equal(t, r[f"b{k}_out_species"]), k
+        assert np.array_equal(d, r[f"b{k}_out_drift"]), k
+        assert c[1] == int(r[f"b{k}_count"]) and (h > 1.0) == bool(r[f"b{k}_warned"]), k

@@ -8,10 +8,11 @@ import sys
 TIME = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
         "s": 1.0, "second": 1.0}
 KERNELS = {"k_fast_forces": "forces", "k_fast_update": "update", "k_scan": "scan",
-           "k_fast_scatter": "scatter", "k_fast_cellfix": "cellfix_deposit"}
-# kernels of the bench's roofline stage (bin + force + update); the cell
-# fix-up/deposit is reported but belongs to the deposit stage
-FU = ("forces", "update", "scan", "scatter")
+           "k_bucket_sort": "bucket_sort", "k_fast_deposit_rows": "deposit_rows",
+           "k_spec_cols": "spec_cols"}
+# kernels of the bench's roofline stage (bin + force + update); the row
+# deposit and the spectral pass are reported but belong to other stages
+FU = ("forces", "update", "scan", "bucket_sort")
 
 
 def main(rep, out, config):

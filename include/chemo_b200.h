@@ -283,6 +283,33 @@ void *cs_sim_status_device(cs_sim *sim);
 int64_t cs_sim_status_bytes(void);
 int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n);
 
+/* ---------------------------------------------------------------------- */
+/* Ensembles of small realisations (run_ensemble, engine.py:455-484;       */
+/* SURVEY 8f rank 1): one CTA per realisation, state in shared memory,      */
+/* K steps per launch.  The realisations share one cs_sim_params (n =       */
+/* particles per realisation; prec must be CS_F64; a grid, if any, must be  */
+/* neumann with n_c <= 64; direct-engine semantics incl. react).            */
+/* ---------------------------------------------------------------------- */
+typedef struct cs_ens cs_ens;
+
+typedef struct {
+    double *pos;             /* (S, n, 2) in/out */
+    double *anchor;          /* (S, n, 2) in/out */
+    double *drift;           /* (S, n, 2) in/out */
+    double *local_c;         /* (S, n) in/out */
+    uint8_t *type;           /* (S, n) in/out */
+    double *c;               /* (S, n_c^2) in/out; NULL without a grid */
+} cs_ens_state;
+
+int cs_ens_create(cs_ctx *ctx, const cs_sim_params *p, int32_t n_real, cs_ens **out);
+int cs_ens_destroy(cs_ens *e);
+/* xi: (k, S, n, 2) f64 Brownian increments; u: (k, S, n) f64 reaction
+ * uniforms (required when p->react).  Asynchronous on the context stream. */
+int cs_ens_step(cs_ens *e, const cs_ens_state *st, const double *xi, const double *u,
+                int32_t k_steps);
+/* Synchronise and read the per-realisation status: out[S]. */
+int cs_ens_status(cs_ens *e, cs_status *out);
+
 #ifdef __cplusplus
 }
 #endif

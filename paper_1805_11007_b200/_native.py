@@ -66,6 +66,11 @@ class Status_t(ctypes.Structure):
                 ("react_high_max", C_f64)]
 
 
+class EnsState_t(ctypes.Structure):
+    _fields_ = [("pos", C_p), ("anchor", C_p), ("drift", C_p), ("local_c", C_p),
+                ("type", C_p), ("c", C_p)]
+
+
 # (name, restype, argtypes) -- every symbol include/chemo_b200.h declares
 SIGNATURES = [
     ("cs_abi_version", C_i32, []),
@@ -111,6 +116,10 @@ SIGNATURES = [
     ("cs_sim_export", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
     ("cs_sim_status_device", C_p, [C_p]),
     ("cs_sim_status_bytes", C_i64, []),
+    ("cs_ens_create", C_i32, [C_p, ctypes.POINTER(SimParams_t), C_i32, ctypes.POINTER(C_p)]),
+    ("cs_ens_destroy", C_i32, [C_p]),
+    ("cs_ens_step", C_i32, [C_p, ctypes.POINTER(EnsState_t), C_p, C_p, C_i32]),
+    ("cs_ens_status", C_i32, [C_p, C_p]),
 ]
 
 STAGES = ("deposit", "solve", "gradient", "bin", "force", "update")

@@ -299,6 +299,108 @@ int run_soft_force_pairs(cs_ctx *ctx, int prec, const void *pos, const uint8_t *
                          long long n, const BinGeom &g, const PairTab &pt,
                          int64_t *pairs, int64_t cap, int64_t *count);
 
+
+// ---- shared with ensemble.cu (definitions of the host helpers in field.cu)
+struct Route {
+    unsigned char bits[3];  // indexed by min(type, 2): bit0 -> rho_a, bit1 -> rho_b
+};
+
+__device__ __forceinline__ unsigned route_bits(const uint8_t *type, long long p, const Route &r) {
+    const unsigned t = type ? (unsigned)type[p] : 0u;
+    return r.bits[t < 2u ? t : 2u];
+}
+
+struct GaussParams {
+    double inv_norm, two_h2, cut2;
+    int w0, w1;
+};
+
+GaussParams make_gauss(const GridGeom &gg, double h, double cutoff);
+
+// d1 coefficients (field.py:128-137), each entry value / (2 h) as the
+// reference's lil / scalar division produces them.
+struct D1Coef {
+    double m1, p1;        // interior / periodic: -1/(2h), +1/(2h)
+    double l0, l1, l2;    // neumann row 0: -3, 4, -1 over 2h
+    double r0, r1, r2;    // neumann row n-1 (cols n-3, n-2, n-1): 1, -4, 3 over 2h
+};
+D1Coef make_d1(double h);
+
+template <class G>
+__device__ __forceinline__ double d1_at(const G *__restrict__ c, long long base, long long stride,
+                                        int i, int n, int per, const D1Coef &k) {
+    if (per) {
+        const int im = i == 0 ? n - 1 : i - 1, ip = i == n - 1 ? 0 : i + 1;
+        const double am = dmul(k.m1, (double)c[base + im * stride]);
+        const double ap = dmul(k.p1, (double)c[base + ip * stride]);
+        return im < ip ? dadd(dadd(0.0, am), ap) : dadd(dadd(0.0, ap), am);
+    }
+    if (i == 0)
+        return dadd(dadd(dadd(0.0, dmul(k.l0, (double)c[base])),
+                         dmul(k.l1, (double)c[base + stride])),
+                    dmul(k.l2, (double)c[base + 2 * stride]));
+    if (i == n - 1)
+        return dadd(dadd(dadd(0.0, dmul(k.r0, (double)c[base + (long long)(n - 3) * stride])),
+                         dmul(k.r1, (double)c[base + (long long)(n - 2) * stride])),
+                    dmul(k.r2, (double)c[base + (long long)(n - 1) * stride]));
+    return dadd(dadd(0.0, dmul(k.m1, (double)c[base + (long long)(i - 1) * stride])),
+                dmul(k.p1, (double)c[base + (long long)(i + 1) * stride]));
+}
+
+
+// The reference pair loop of one particle (motion.py:200-245); used by
+// forces.cu and ensemble.cu.
+template <class P, class Visit>
+__device__ __forceinline__ void pair_loop(const P *__restrict__ pos, const uint8_t *__restrict__ type,
+                                          const int *__restrict__ order,
+                                          const int *__restrict__ starts, const BinGeom &g,
+                                          const PairTab &pt, int i, Visit visit) {
+    double xi, yi;
+    load2(pos, i, xi, yi);
+    const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
+    const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
+    const int ti = type ? (int)type[i] : 0;
+    for (int o1 = -1; o1 <= 1; o1++) {
+        int g1 = cy + o1;
+        if (g.per1) {
+            if (g.n1 == 1 && o1 != 0) continue;
+            if (g.n1 == 2 && o1 == 1) continue;
+            g1 = (int)pymod(g1, g.n1);
+        } else if (g1 < 0 || g1 >= g.n1) {
+            continue;
+        }
+        for (int o0 = -1; o0 <= 1; o0++) {
+            int g0 = cx + o0;
+            if (g.per0) {
+                if (g.n0 == 1 && o0 != 0) continue;
+                if (g.n0 == 2 && o0 == 1) continue;
+                g0 = (int)pymod(g0, g.n0);
+            } else if (g0 < 0 || g0 >= g.n0) {
+                continue;
+            }
+            const int f = g1 * g.n0 + g0;
+            const int kend = starts[f + 1];
+            for (int k = starts[f]; k < kend; k++) {
+                const int j = order[k];
+                if (j == i) continue;
+                double xj, yj;
+                load2(pos, j, xj, yj);
+                double dx0 = dsub(xj, xi);
+                double dx1 = dsub(yj, yi);
+                if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
+                if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
+                const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                const int t = ti * 2 + (type ? (int)type[j] : 0);
+                if (r2 > pt.cut2[t] || r2 == 0.0) continue;
+                const double eps = pt.eps[t];
+                const double r = dsqrt(r2);
+                const double s = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
+                visit(j, s, dx0, dx1);
+            }
+        }
+    }
+}
+
 }  // namespace cs
 
 // ------------------------------------------------------------------ ops

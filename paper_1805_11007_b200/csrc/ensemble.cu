@@ -1,0 +1,733 @@
+// ensemble.cu -- many small realisations per GPU.
+//
+// The paper's workload is an ensemble of small systems (fig1: N = 200
+// particles on a 52^2 Neumann grid, thousands of seeded realisations,
+// engine.py:455-484), which the reference parallelises only across
+// processes.  Here one 256-thread CTA owns one realisation for a block of
+// K steps: particles, cell list and grid live in shared memory, and every
+// stage of Realisation._step_inner (engine.py:369-393) runs in the CTA
+// between barriers, in the reference's order and arithmetic:
+//   deposit (coupling.py:77-110 gaussian / :113-138 CIC) -> rhs
+//   (field.py:224-229) -> DCT-I modal solve (field.py:162-167, the same
+//   k-ordered fma GEMMs as field.cu's k_gemm) -> field checks
+//   (field.py:229-238) -> refresh (coupling.py:302-325, the gradient
+//   stencil of field.py:128-137 evaluated at the four corner nodes) ->
+//   cell list + pair forces (motion.py:170-245, csrc/common.cuh pair_loop)
+//   -> Euler-Maruyama + boundaries (motion.py:268-282, :355-430) ->
+//   fixed-step reactions (reactions.py:43-81).
+// The Brownian increments and reaction uniforms of every realisation come
+// from its own generator streams on the host (the reference's RNG
+// contract), K steps at a time.  Deposits accumulate with shared-memory
+// fp64 atomics (the summation order of concurrent stamps differs from the
+// reference's particle order; tolerance as for the direct engine).
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace cs {
+
+struct EnsArgs {
+    int n, nc, ncell, k_steps, step0;
+    double *pos, *anchor, *drift, *local_c;  // [S][n][2], [S][n]
+    uint8_t *type;                           // [S][n]
+    double *c;                               // [S][nc^2]
+    const double *xi;                        // step k, realisation s: xi + k xs + 2 n s
+    long long xs;
+    const double *u;                         // reaction uniforms: u + k us + n s
+    long long us;
+    const double *F, *Inv, *E;               // DCT-I operators (field.cu)
+    DevStatus *st;                           // [S]
+    cs_domain dom;
+    BinGeom g;
+    PairTab pt;
+    int interact, refresh, field, deposit_kind, solve;
+    double amp[2], dt, chi[2];
+    int chi_pinned[2];
+    GaussParams gp;
+    GridGeom gg;
+    Route route;
+    double one_m_dtg, dka, dkb;
+    int has_g, has_a, has_b;
+    D1Coef kx, ky;
+    double wcell;
+    int react;
+    double p_ab, r_beta;
+};
+
+// C = A op(B) (E *) for n <= 64 inside one CTA of 256 threads: thread
+// (ty, tx) owns rows ty + 16 u, columns tx + 16 v; the k loop is sequential
+// fma, the accumulation order of field.cu's k_gemm.
+template <bool BT>
+__device__ __forceinline__ void cta_gemm(const double *A, const double *B, const double *E,
+                                         double *C, int n) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) acc[u][v] = 0.0;
+    int rr[4], cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        rr[u] = min(ty + 16 * u, n - 1);
+        cc[u] = min(tx + 16 * u, n - 1);
+    }
+    for (int k = 0; k < n; k++) {
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            a[u] = A[rr[u] * n + k];
+            b[u] = BT ? B[cc[u] * n + k] : B[k * n + cc[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int v = 0; v < 4; v++) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const int r = ty + 16 * u, col = tx + 16 * v;
+            if (r < n && col < n) {
+                double val = acc[u][v];
+                if (E) val *= E[r * n + col];
+                C[r * n + col] = val;
+            }
+        }
+}
+
+__device__ __forceinline__ double grad_bilinear(const Bilin &b, const double *c, int n, int per,
+                                                const D1Coef &k, int axis) {
+    const long long r[4] = {b.r00, b.r10, b.r01, b.r11};
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int j = (int)(r[q] / n), i = (int)(r[q] - (long long)j * n);
+        v[q] = axis == 0 ? d1_at(c, (long long)j * n, 1, i, n, per, k)
+                         : d1_at(c, (long long)i, n, j, n, per, k);
+    }
+    return dadd(dadd(dadd(dmul(b.w00, v[0]), dmul(b.w10, v[1])), dmul(b.w01, v[2])),
+                dmul(b.w11, v[3]));
+}
+
+__device__ __forceinline__ void set_status(DevStatus *st, int *s_abort, unsigned long long key,
+                                           int step) {
+    atomicMin(&st->key, key);
+    st->abort = 1;
+    st->step = step;
+    *s_abort = 1;
+}
+
+constexpr int ENS_THREADS = 256;
+
+__global__ void __launch_bounds__(ENS_THREADS)
+k_ensemble(const __grid_constant__ EnsArgs a) {
+    extern __shared__ double sm[];
+    __shared__ int s_abort;
+    __shared__ double s_red[ENS_THREADS / 32];
+    __shared__ int s_flag[ENS_THREADS / 32];
+    const int n = a.n, m = a.nc * a.nc, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const long long s = blockIdx.x;
+    double *pos = sm, *anc = pos + 2 * n, *drift = anc + 2 * n, *frc = drift + 2 * n;
+    double *lc = frc + 2 * n, *c = lc + n, *ra = c + m, *rb = ra + m;
+    int *order = reinterpret_cast<int *>(rb + m);
+    int *starts = order + n, *cur = starts + a.ncell + 1, *key = cur + a.ncell;
+    uint8_t *type = reinterpret_cast<uint8_t *>(key + n);
+    DevStatus *st = a.st + s;
+    for (int i = tid; i < 2 * n; i += ENS_THREADS) {
+        pos[i] = a.pos[2 * n * s + i];
+        anc[i] = a.anchor[2 * n * s + i];
+        drift[i] = a.drift[2 * n * s + i];
+    }
+    for (int i = tid; i < n; i += ENS_THREADS) {
+        lc[i] = a.local_c[n * s + i];
+        type[i] = a.type[n * s + i];
+    }
+    if (a.field || a.refresh)
+        for (int l = tid; l < m; l += ENS_THREADS) c[l] = a.c[(long long)m * s + l];
+    if (tid == 0) s_abort = st->abort;
+    long long clamped = 0;
+    unsigned long long high_n = 0;
+    double high = 0.0;
+    __syncthreads();
+    for (int kk = 0; kk < a.k_steps; kk++) {
+        if (s_abort) break;
+        const int step = a.step0 + kk;
+        const GridGeom &gg = a.gg;
+        const int nc = gg.n;
+        if (a.field) {
+            // ---- deposit_both (coupling.py:77-110, 113-138)
+            for (int l = tid; l < m; l += ENS_THREADS) {
+                ra[l] = 0.0;
+                rb[l] = 0.0;
+            }
+            __syncthreads();
+            for (int p = tid; p < n; p += ENS_THREADS) {
+                const unsigned bits = route_bits(type, p, a.route);
+                if (!bits) continue;
+                const double x = pos[2 * p], y = pos[2 * p + 1];
+                const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
+                const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+                if (a.deposit_kind == CS_GAUSSIAN) {
+                    const long long b0 = (long long)floor(dadd(u0, 0.5));
+                    const long long b1 = (long long)floor(dadd(u1, 0.5));
+                    for (int o1 = -a.gp.w1; o1 <= a.gp.w1; o1++) {
+                        const long long j = b1 + o1;
+                        if (j < 0 || j >= nc) continue;
+                        const double dy = dmul(dsub(u1, (double)(b1 + o1)), gg.d1);
+                        const double dy2 = dmul(dy, dy);
+                        for (int o0 = -a.gp.w0; o0 <= a.gp.w0; o0++) {
+                            const long long i = b0 + o0;
+                            if (i < 0 || i >= nc) continue;
+                            const double dxp = dmul(dsub(u0, (double)(b0 + o0)), gg.d0);
+                            const double r2 = dadd(dmul(dxp, dxp), dy2);
+                            if (r2 <= a.gp.cut2) {
+                                const double v =
+                                    dmul(a.gp.inv_norm, cs_exp(-ddiv(r2, a.gp.two_h2)));
+                                if (bits & 1u) atomicAdd(&ra[j * nc + i], v);
+                                if (bits & 2u) atomicAdd(&rb[j * nc + i], v);
+                            }
+                        }
+                    }
+                } else {
+                    long long b0 = (long long)floor(u0), b1 = (long long)floor(u1);
+                    b0 = b0 < 0 ? 0 : (b0 > nc - 2 ? nc - 2 : b0);
+                    b1 = b1 < 0 ? 0 : (b1 > nc - 2 ? nc - 2 : b1);
+                    const double f0 = dsub(u0, (double)b0), f1 = dsub(u1, (double)b1);
+                    const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
+                    const double w[4] = {dmul(dmul(dsub(1.0, f0), dsub(1.0, f1)), unit),
+                                         dmul(dmul(f0, dsub(1.0, f1)), unit),
+                                         dmul(dmul(dsub(1.0, f0), f1), unit),
+                                         dmul(dmul(f0, f1), unit)};
+                    const long long at[4] = {b1 * nc + b0, b1 * nc + b0 + 1, (b1 + 1) * nc + b0,
+                                             (b1 + 1) * nc + b0 + 1};
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (bits & 1u) atomicAdd(&ra[at[q]], w[q]);
+                        if (bits & 2u) atomicAdd(&rb[at[q]], w[q]);
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- rhs (field.py:224-229), in place into ra
+            for (int l = tid; l < m; l += ENS_THREADS) {
+                const double cv = c[l];
+                double r = a.has_g ? dmul(cv, a.one_m_dtg) : cv;
+                if (a.has_a) r = dadd(r, dmul(a.dka, ra[l]));
+                if (a.has_b) r = dsub(r, dmul(dmul(rb[l], cv), a.dkb));
+                ra[l] = r;
+            }
+            __syncthreads();
+            // ---- implicit solve (field.py:162-170)
+            if (a.solve) {
+                cta_gemm<false>(a.F, ra, nullptr, rb, nc);  // T1 = F X
+                __syncthreads();
+                cta_gemm<true>(rb, a.F, a.E, ra, nc);       // T2 = E * (T1 F^T)
+                __syncthreads();
+                cta_gemm<false>(a.Inv, ra, nullptr, rb, nc);  // U = Inv T2
+                __syncthreads();
+                cta_gemm<true>(rb, a.Inv, nullptr, c, nc);    // c = U Inv^T
+            } else {
+                for (int l = tid; l < m; l += ENS_THREADS) c[l] = ra[l];
+            }
+            __syncthreads();
+            // ---- post-checks (field.py:229-238): non-finite, negative mass
+            double neg = 0.0;
+            int flags = 0;
+            for (int l = tid; l < m; l += ENS_THREADS) {
+                const double v = c[l];
+                if (!isfinite(v)) flags |= 1;
+                if (v < 0.0) {
+                    const int j = l / nc, i = l - j * nc;
+                    const double wi = (i == 0 || i == nc - 1) ? 0.5 : 1.0;
+                    const double wj = (j == 0 || j == nc - 1) ? 0.5 : 1.0;
+                    neg += ((wj * wi) * a.wcell) * v;
+                    flags |= 2;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                neg += __shfl_xor_sync(0xffffffffu, neg, o);
+                flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+            }
+            if (lane == 0) {
+                s_red[warp] = neg;
+                s_flag[warp] = flags;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                int f = 0;
+                for (int w = 0; w < ENS_THREADS / 32; w++) {
+                    t += s_red[w];
+                    f |= s_flag[w];
+                }
+                if (f & 1) set_status(st, &s_abort, err_key(0, 0, CS_FIELD_NONFINITE), step);
+                if ((f & 2) && t < -1e-12) {
+                    if (st->neg_steps == 0) st->first_neg = t;
+                    st->neg_steps += 1;
+                }
+            }
+            __syncthreads();
+            if (s_abort) break;
+        }
+        // ---- refresh (coupling.py:302-325)
+        if (a.refresh) {
+            for (int p = tid; p < n; p += ENS_THREADS) {
+                Bilin b;
+                clamped += 2 * bilinear_stencil(pos[2 * p], pos[2 * p + 1], gg, b);
+                lc[p] = bilinear_apply(b, c, 1, 0);
+                const int t = type[p] ? 1 : 0;
+                double d0 = grad_bilinear(b, c, nc, gg.per, a.kx, 0);
+                double d1 = grad_bilinear(b, c, nc, gg.per, a.ky, 1);
+                if (a.chi_pinned[t]) {
+                    d0 = 0.0;
+                    d1 = 0.0;
+                } else if (a.chi[t] != 1.0) {
+                    d0 = dmul(d0, a.chi[t]);
+                    d1 = dmul(d1, a.chi[t]);
+                }
+                drift[2 * p] = d0;
+                drift[2 * p + 1] = d1;
+            }
+        }
+        // ---- cell list + pair forces (motion.py:170-245)
+        if (a.interact) {
+            for (int f = tid; f <= a.ncell; f += ENS_THREADS) starts[f] = 0;
+            __syncthreads();
+            for (int p = tid; p < n; p += ENS_THREADS) {
+                const int k = cell_axis(pos[2 * p + 1], a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
+                              cell_axis(pos[2 * p], a.g.lo0, a.g.eff0, a.g.n0);
+                key[p] = k;
+                atomicAdd(&starts[k + 1], 1);
+            }
+            __syncthreads();
+            if (warp == 0) {  // inclusive scan of starts[1..ncell] (counts) by one warp
+                int carry = 0;
+                for (int f0 = 1; f0 <= a.ncell; f0 += 32) {
+                    const int f = f0 + lane;
+                    int v = f <= a.ncell ? starts[f] : 0;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, v, d);
+                        if (lane >= d) v += y;
+                    }
+                    if (f <= a.ncell) starts[f] = v + carry;
+                    carry += __shfl_sync(0xffffffffu, v, 31);
+                }
+                __syncwarp();
+                for (int f = lane; f < a.ncell; f += 32) cur[f] = starts[f];
+                __syncwarp();
+                // stable placement (ascending index inside a cell,
+                // motion.py:195-199), 32 particles at a time in index order
+                for (int p0 = 0; p0 < n; p0 += 32) {
+                    const int p = p0 + lane;
+                    const int k = p < n ? key[p] : -1 - lane;
+                    const unsigned same = __match_any_sync(0xffffffffu, k);
+                    const int rank = __popc(same & ((1u << lane) - 1u));
+                    int base = 0;
+                    if (p < n) base = cur[k];
+                    __syncwarp();
+                    if (p < n) {
+                        order[base + rank] = p;
+                        if (rank == __popc(same) - 1) cur[k] = base + rank + 1;
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            // one warp per particle: the lanes test its ring candidates 32 at
+            // a time in ring order (cells o1-major, ascending index inside a
+            // cell) and evaluate the accepted pair terms in parallel; the
+            // terms are then added in candidate order (motion.py:240-243)
+            const BinGeom &g = a.g;
+            for (int i = warp; i < n; i += ENS_THREADS / 32) {
+                const double xi = pos[2 * i], yi = pos[2 * i + 1];
+                const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
+                const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
+                const int ti = type[i] ? 1 : 0;
+                int rs = 0, rl = 0;
+                if (lane < 9) {
+                    const int o1 = lane / 3 - 1, o0 = lane % 3 - 1;
+                    int g1 = cy + o1, g0 = cx + o0;
+                    bool ok = true;
+                    if (g.per1) {
+                        if ((g.n1 == 1 && o1 != 0) || (g.n1 == 2 && o1 == 1)) ok = false;
+                        g1 = (int)pymod(g1, g.n1);
+                    } else if (g1 < 0 || g1 >= g.n1) {
+                        ok = false;
+                    }
+                    if (g.per0) {
+                        if ((g.n0 == 1 && o0 != 0) || (g.n0 == 2 && o0 == 1)) ok = false;
+                        g0 = (int)pymod(g0, g.n0);
+                    } else if (g0 < 0 || g0 >= g.n0) {
+                        ok = false;
+                    }
+                    if (ok) {
+                        const int f = g1 * g.n0 + g0;
+                        rs = starts[f];
+                        rl = starts[f + 1] - rs;
+                    }
+                }
+                int incl = rl;
+#pragma unroll
+                for (int d = 1; d < 16; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 8);
+                int pre[9], cs_[9];
+#pragma unroll
+                for (int r = 0; r < 9; r++) {
+                    pre[r] = __shfl_sync(0xffffffffu, incl - rl, r);
+                    cs_[r] = __shfl_sync(0xffffffffu, rs, r);
+                }
+                double fx = 0.0, fy = 0.0;
+                for (int k0 = 0; k0 < total; k0 += 32) {
+                    const int k = k0 + lane;
+                    double tx = 0.0, ty = 0.0;
+                    bool acc = false;
+                    if (k < total) {
+                        int r = 0;
+#pragma unroll
+                        for (int q = 1; q < 9; q++) r = k >= pre[q] ? q : r;
+                        int base = cs_[0] - pre[0];
+#pragma unroll
+                        for (int q = 1; q < 9; q++) base = r == q ? cs_[q] - pre[q] : base;
+                        const int j = order[base + k];
+                        if (j != i) {
+                            double dx0 = dsub(pos[2 * j], xi);
+                            double dx1 = dsub(pos[2 * j + 1], yi);
+                            if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
+                            if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
+                            const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                            const int t = ti * 2 + (type[j] ? 1 : 0);
+                            if (!(r2 > a.pt.cut2[t] || r2 == 0.0)) {
+                                const double eps = a.pt.eps[t];
+                                const double rr = dsqrt(r2);
+                                const double sc = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
+                                tx = dmul(sc, dx0);
+                                ty = dmul(sc, dx1);
+                                acc = true;
+                            }
+                        }
+                    }
+                    unsigned msk = __ballot_sync(0xffffffffu, acc);
+                    while (msk) {  // ordered sum, identical in every lane
+                        const int b = __ffs(msk) - 1;
+                        fx = dadd(fx, __shfl_sync(0xffffffffu, tx, b));
+                        fy = dadd(fy, __shfl_sync(0xffffffffu, ty, b));
+                        msk &= msk - 1;
+                    }
+                }
+                if (lane == 0) {
+                    frc[2 * i] = fx;
+                    frc[2 * i + 1] = fy;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- Euler-Maruyama + boundaries (motion.py:268-282, 355-430)
+        const double *xk = a.xi + (long long)kk * a.xs + 2LL * n * s;
+        for (int p = tid; p < n; p += ENS_THREADS) {
+            const int t = type[p] ? 1 : 0;
+            const double amp = a.amp[t];
+            const double f0 = a.interact ? frc[2 * p] : 0.0, f1 = a.interact ? frc[2 * p + 1] : 0.0;
+            double v[2];
+            v[0] = dadd(dadd(dadd(pos[2 * p], dmul(amp, xk[2 * p])), dmul(drift[2 * p], a.dt)),
+                        dmul(f0, a.dt));
+            v[1] = dadd(dadd(dadd(pos[2 * p + 1], dmul(amp, xk[2 * p + 1])),
+                             dmul(drift[2 * p + 1], a.dt)),
+                        dmul(f1, a.dt));
+            const double raw0 = v[0], raw1 = v[1];
+            bool ok = isfinite(v[0]) && isfinite(v[1]);
+            if (!ok) set_status(st, &s_abort, err_key(0, p, CS_NONFINITE), step);
+            double an[2] = {anc[2 * p], anc[2 * p + 1]};
+            for (int ax = 0; ok && ax < 2; ax++) {
+                const int code = boundary_axis(v[ax], an[ax], a.dom.lo[ax], a.dom.hi[ax],
+                                               a.dom.periodic[ax]);
+                if (code) {
+                    set_status(st, &s_abort, err_key(1 + ax, p, code), step);
+                    ok = false;
+                }
+            }
+            if (!ok) {  // the raw proposal stays visible for the host's message
+                pos[2 * p] = raw0;
+                pos[2 * p + 1] = raw1;
+                continue;
+            }
+            pos[2 * p] = v[0];
+            pos[2 * p + 1] = v[1];
+            anc[2 * p] = an[0];
+            anc[2 * p + 1] = an[1];
+        }
+        __syncthreads();
+        if (s_abort) break;
+        // ---- fixed-step reactions (reactions.py:43-81)
+        if (a.react) {
+            const double *uk = a.u + (long long)kk * a.us + (long long)n * s;
+            for (int p = tid; p < n; p += ENS_THREADS) {
+                const double ui = uk[p];
+                if (type[p] == 0) {
+                    if (a.p_ab > 1.0) {
+                        high_n++;
+                        high = fmax(high, a.p_ab);
+                    }
+                    if (ui < a.p_ab) type[p] = 1;
+                } else if (a.r_beta != 0.0) {
+                    const double cv = lc[p];
+                    const double conc = cv > 0.0 || cv != cv ? cv : 0.0;
+                    const double pb = dmul(dmul(a.r_beta, conc), a.dt);
+                    if (pb > 1.0) {
+                        high_n++;
+                        high = fmax(high, pb);
+                    }
+                    if (ui < pb) {
+                        type[p] = 0;
+                        drift[2 * p] = 0.0;
+                        drift[2 * p + 1] = 0.0;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < 2 * n; i += ENS_THREADS) {
+        a.pos[2 * n * s + i] = pos[i];
+        a.anchor[2 * n * s + i] = anc[i];
+        a.drift[2 * n * s + i] = drift[i];
+    }
+    for (int i = tid; i < n; i += ENS_THREADS) {
+        a.local_c[n * s + i] = lc[i];
+        a.type[n * s + i] = type[i];
+    }
+    if (a.field)
+        for (int l = tid; l < m; l += ENS_THREADS) a.c[(long long)m * s + l] = c[l];
+    if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
+    if (high_n) {
+        atomicAdd(&st->react_high_n, high_n);
+        atomicMax(&st->react_high_bits, (unsigned long long)__double_as_longlong(high));
+    }
+}
+
+}  // namespace cs
+
+// ---------------------------------------------------------------- host side
+namespace cs {
+int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
+                     cs_field_ops **out);
+void field_ops_destroy(cs_field_ops *ops);
+}  // namespace cs
+
+struct cs_ens {
+    cs_ctx *ctx = nullptr;
+    cs_sim_params p{};
+    int n_real = 0;
+    int steps_done = 0;
+    cs::EnsArgs a{};
+    cs_field_ops *ops = nullptr;
+    cs::Buf status;  // DevStatus[n_real]
+    size_t smem = 0;
+};
+
+namespace cs {
+
+static size_t ens_smem(int n, int nc, int ncell) {
+    const size_t m = (size_t)nc * nc;
+    return sizeof(double) * (9 * (size_t)n + 3 * m) +
+           sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1) + (size_t)n + 16;
+}
+
+int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
+    *out = nullptr;
+    if (p->prec != CS_F64) {
+        set_error("the ensemble engine runs in binary64 (prec must be CS_F64)");
+        return CS_ERR_PARAM;
+    }
+    if (p->n < 1 || p->n > 4096 || n_real < 1) {
+        set_error("ensemble: 1 <= n <= 4096 particles per realisation and >= 1 realisation");
+        return CS_ERR_PARAM;
+    }
+    const bool grid = p->field_active || p->refresh_active;
+    if (grid && (p->grid.periodic || p->grid.n_c < 3 || p->grid.n_c > 64)) {
+        set_error("ensemble: the grid must be neumann with 3 <= n_c <= 64 "
+                  "(periodic grids run through cs_sim)");
+        return CS_ERR_PARAM;
+    }
+    auto *e = new cs_ens();
+    *out = e;
+    e->ctx = ctx;
+    e->p = *p;
+    e->n_real = n_real;
+    EnsArgs &a = e->a;
+    a.n = (int)p->n;
+    a.nc = grid ? p->grid.n_c : 0;
+    a.dom = p->domain;
+    a.interact = p->interaction == 1;
+    a.ncell = 0;
+    if (a.interact) {
+        a.g = make_geom(p->domain, p->pairs.cell_cutoff);
+        a.pt = make_pairtab(p->pairs);
+        a.ncell = a.g.n0 * a.g.n1;
+    }
+    a.refresh = p->refresh_active;
+    a.field = p->field_active;
+    for (int t = 0; t < 2; t++) {
+        a.amp[t] = p->amp[t];
+        a.chi[t] = p->chi[t];
+        a.chi_pinned[t] = p->chi_pinned[t];
+        a.route.bits[t] = (unsigned char)((p->secretes[t] ? 1 : 0) | (p->consumes[t] ? 2 : 0));
+    }
+    a.route.bits[2] = 0;
+    a.dt = p->dt;
+    if (grid) {
+        a.gg = make_grid_geom(p->grid);
+        a.kx = make_d1(a.gg.d0);
+        a.ky = make_d1(a.gg.d1);
+        a.wcell = a.gg.d0 * a.gg.d1;
+    }
+    if (a.field) {
+        a.deposit_kind = p->deposit_kind;
+        a.gp = make_gauss(a.gg, p->kernel_h, p->kernel_cutoff);
+        a.has_g = p->gamma != 0.0;
+        a.has_a = p->k_alpha != 0.0;
+        a.has_b = p->k_beta != 0.0;
+        a.one_m_dtg = 1.0 - p->dt * p->gamma;
+        a.dka = p->dt * p->k_alpha;
+        a.dkb = p->dt * p->k_beta;
+        CS_TRY(field_ops_create(ctx, CS_F64, &p->grid, p->d_c, p->dt, &e->ops));
+        a.solve = e->ops->kind == 1;
+        a.F = e->ops->F;
+        a.Inv = e->ops->Inv;
+        a.E = e->ops->E;
+    }
+    a.react = p->react;
+    a.p_ab = p->react_p_ab;
+    a.r_beta = p->react_r_beta;
+    e->smem = ens_smem(a.n, a.nc, a.ncell);
+    int dev_max = 0;
+    CS_CUDA(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                   ctx->device));
+    if (e->smem + 2048 > (size_t)dev_max) {
+        set_error("ensemble: a realisation needs %zu B of shared memory (> %d)", e->smem,
+                  dev_max);
+        return CS_ERR_PARAM;
+    }
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)e->smem));
+    CS_TRY(e->status.ensure(sizeof(DevStatus) * (size_t)n_real));
+    std::vector<DevStatus> init((size_t)n_real);
+    for (auto &d : init) {
+        d = DevStatus{};
+        d.key = ~0ULL;
+        d.step = -1;
+    }
+    CS_CUDA(cudaMemcpy(e->status.p, init.data(), sizeof(DevStatus) * (size_t)n_real,
+                       cudaMemcpyHostToDevice));
+    return CS_OK;
+}
+
+void ens_destroy(cs_ens *e) {
+    if (!e) return;
+    field_ops_destroy(e->ops);
+    e->status.release();
+    delete e;
+}
+
+int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u, int k) {
+    if (k <= 0) return CS_OK;
+    if (e->p.react && !u) {
+        set_error("params.react is set: the ensemble step needs the reaction uniforms");
+        return CS_ERR_PARAM;
+    }
+    if (!s->pos || !s->anchor || !s->drift || !s->local_c || !s->type ||
+        ((e->a.field || e->a.refresh) && !s->c)) {
+        set_error("ensemble state: pos, anchor, drift, local_c, type (and c) are required");
+        return CS_ERR_PARAM;
+    }
+    EnsArgs a = e->a;
+    a.pos = s->pos;
+    a.anchor = s->anchor;
+    a.drift = s->drift;
+    a.local_c = s->local_c;
+    a.type = s->type;
+    a.c = s->c;
+    a.xi = xi;
+    a.xs = 2LL * a.n * e->n_real;
+    a.u = u;
+    a.us = (long long)a.n * e->n_real;
+    a.st = e->status.as<DevStatus>();
+    a.k_steps = k;
+    a.step0 = e->steps_done;
+    k_ensemble<<<e->n_real, ENS_THREADS, e->smem, e->ctx->stream>>>(a);
+    CS_LAUNCH_CHECK();
+    e->ctx->launches += 1;
+    e->steps_done += k;
+    return CS_OK;
+}
+
+int ens_status(cs_ens *e, cs_status *out) {
+    std::vector<DevStatus> d((size_t)e->n_real);
+    CS_CUDA(cudaMemcpyAsync(d.data(), e->status.p, sizeof(DevStatus) * d.size(),
+                            cudaMemcpyDeviceToHost, e->ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+    for (int r = 0; r < e->n_real; r++) {
+        cs_status &o = out[r];
+        const DevStatus &x = d[(size_t)r];
+        o = cs_status{};
+        o.code = CS_OK;
+        o.step = -1;
+        o.particle = -1;
+        o.axis = -1;
+        if (x.key != ~0ULL) {
+            const int rank = (int)(x.key >> 60);
+            o.code = (int)(x.key & 7ULL);
+            o.particle = (long long)((x.key >> 3) & ((1ULL << 57) - 1));
+            o.axis = rank >= 1 ? rank - 1 : 0;
+            o.step = x.step;
+            if (o.code == CS_FIELD_NONFINITE) {
+                o.particle = -1;
+                o.axis = -1;
+            }
+        }
+        o.clamped = x.clamped;
+        o.neg_mass_steps = x.neg_steps;
+        o.first_neg_mass = x.first_neg;
+        o.steps_done = e->steps_done;
+        o.react_high_count = (int64_t)x.react_high_n;
+        o.react_high_max = 0.0;
+        if (x.react_high_n) memcpy(&o.react_high_max, &x.react_high_bits, sizeof(double));
+    }
+    return CS_OK;
+}
+
+}  // namespace cs
+
+extern "C" {
+
+int cs_ens_create(cs_ctx *ctx, const cs_sim_params *p, int32_t n_real, cs_ens **out) {
+    const int rc = cs::ens_create(ctx, p, n_real, out);
+    if (rc != CS_OK) {
+        cs::ens_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int cs_ens_destroy(cs_ens *e) {
+    cs::ens_destroy(e);
+    return CS_OK;
+}
+
+int cs_ens_step(cs_ens *e, const cs_ens_state *st, const double *xi, const double *u,
+                int32_t k_steps) {
+    return cs::ens_step(e, st, xi, u, k_steps);
+}
+
+int cs_ens_status(cs_ens *e, cs_status *out) { return cs::ens_status(e, out); }
+
+}  // extern "C"

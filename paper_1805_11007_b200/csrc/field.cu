@@ -29,15 +29,6 @@
 namespace cs {
 
 // ------------------------------------------------------------------ deposit
-struct Route {
-    unsigned char bits[3];  // indexed by min(type, 2): bit0 -> rho_a, bit1 -> rho_b
-};
-
-__device__ __forceinline__ unsigned route_bits(const uint8_t *type, long long p, const Route &r) {
-    const unsigned t = type ? (unsigned)type[p] : 0u;
-    return r.bits[t < 2u ? t : 2u];
-}
-
 template <class G>
 __device__ __forceinline__ void atomic_add_g(G *a, double v);
 template <>
@@ -98,11 +89,6 @@ __global__ void k_deposit_cic(const P *__restrict__ pos, const uint8_t *__restri
         }
     }
 }
-
-struct GaussParams {
-    double inv_norm, two_h2, cut2;
-    int w0, w1;
-};
 
 template <class P, class G>
 __global__ void k_deposit_gauss(const P *__restrict__ pos, const uint8_t *__restrict__ type,
@@ -227,13 +213,6 @@ int launch_bilinear(cs_ctx *ctx, int prec, const void *pts, long long np, const 
 }
 
 // ------------------------------------------------------------------ gradient
-// d1 coefficients (field.py:128-137), each entry value / (2 h) as the
-// reference's lil / scalar division produces them.
-struct D1Coef {
-    double m1, p1;        // interior / periodic: -1/(2h), +1/(2h)
-    double l0, l1, l2;    // neumann row 0: -3, 4, -1 over 2h
-    double r0, r1, r2;    // neumann row n-1 (cols n-3, n-2, n-1): 1, -4, 3 over 2h
-};
 D1Coef make_d1(double h) {
     const double two_h = 2.0 * h;
     D1Coef c;
@@ -246,27 +225,6 @@ D1Coef make_d1(double h) {
     c.r1 = -4.0 / two_h;
     c.r2 = 3.0 / two_h;
     return c;
-}
-
-template <class G>
-__device__ __forceinline__ double d1_at(const G *__restrict__ c, long long base, long long stride,
-                                        int i, int n, int per, const D1Coef &k) {
-    if (per) {
-        const int im = i == 0 ? n - 1 : i - 1, ip = i == n - 1 ? 0 : i + 1;
-        const double am = dmul(k.m1, (double)c[base + im * stride]);
-        const double ap = dmul(k.p1, (double)c[base + ip * stride]);
-        return im < ip ? dadd(dadd(0.0, am), ap) : dadd(dadd(0.0, ap), am);
-    }
-    if (i == 0)
-        return dadd(dadd(dadd(0.0, dmul(k.l0, (double)c[base])),
-                         dmul(k.l1, (double)c[base + stride])),
-                    dmul(k.l2, (double)c[base + 2 * stride]));
-    if (i == n - 1)
-        return dadd(dadd(dadd(0.0, dmul(k.r0, (double)c[base + (long long)(n - 3) * stride])),
-                         dmul(k.r1, (double)c[base + (long long)(n - 2) * stride])),
-                    dmul(k.r2, (double)c[base + (long long)(n - 1) * stride]));
-    return dadd(dadd(0.0, dmul(k.m1, (double)c[base + (long long)(i - 1) * stride])),
-                dmul(k.p1, (double)c[base + (long long)(i + 1) * stride]));
 }
 
 // grad = (d1x c, d1y c); when st != NULL also the step_field post-checks on

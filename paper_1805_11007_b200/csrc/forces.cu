@@ -20,57 +20,6 @@
 
 namespace cs {
 
-template <class P, class Visit>
-__device__ __forceinline__ void pair_loop(const P *__restrict__ pos, const uint8_t *__restrict__ type,
-                                          const int *__restrict__ order,
-                                          const int *__restrict__ starts, const BinGeom &g,
-                                          const PairTab &pt, int i, Visit visit) {
-    double xi, yi;
-    load2(pos, i, xi, yi);
-    const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
-    const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
-    const int ti = type ? (int)type[i] : 0;
-    for (int o1 = -1; o1 <= 1; o1++) {
-        int g1 = cy + o1;
-        if (g.per1) {
-            if (g.n1 == 1 && o1 != 0) continue;
-            if (g.n1 == 2 && o1 == 1) continue;
-            g1 = (int)pymod(g1, g.n1);
-        } else if (g1 < 0 || g1 >= g.n1) {
-            continue;
-        }
-        for (int o0 = -1; o0 <= 1; o0++) {
-            int g0 = cx + o0;
-            if (g.per0) {
-                if (g.n0 == 1 && o0 != 0) continue;
-                if (g.n0 == 2 && o0 == 1) continue;
-                g0 = (int)pymod(g0, g.n0);
-            } else if (g0 < 0 || g0 >= g.n0) {
-                continue;
-            }
-            const int f = g1 * g.n0 + g0;
-            const int kend = starts[f + 1];
-            for (int k = starts[f]; k < kend; k++) {
-                const int j = order[k];
-                if (j == i) continue;
-                double xj, yj;
-                load2(pos, j, xj, yj);
-                double dx0 = dsub(xj, xi);
-                double dx1 = dsub(yj, yi);
-                if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
-                if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
-                const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
-                const int t = ti * 2 + (type ? (int)type[j] : 0);
-                if (r2 > pt.cut2[t] || r2 == 0.0) continue;
-                const double eps = pt.eps[t];
-                const double r = dsqrt(r2);
-                const double s = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
-                visit(j, s, dx0, dx1);
-            }
-        }
-    }
-}
-
 template <class P>
 __global__ void __launch_bounds__(256)
 k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,

@@ -37,6 +37,7 @@ from __future__ import annotations
 import ctypes
 import math
 import multiprocessing
+import os
 import warnings
 from dataclasses import asdict, dataclass
 
@@ -729,9 +730,22 @@ def _mean_se(stack):
 
 
 def run_ensemble(config: SimConfig) -> EnsembleResult:
-    """Samples 0..S-1 in sequence on the current device (the device is the
-    parallel resource; ``threads`` is accepted for compatibility)."""
-    all_obs = [run_realisation(config, s) for s in range(config.samples)]
+    """Run samples 0..S-1 and average their observables pointwise
+    (engine.py:455-484).  Configurations the batched engine supports
+    (ensemble.py: fp64, EM, neumann grid <= 64^2 or none, fixed-step
+    reactions, <= 4096 particles) advance all samples together, one CTA per
+    sample; the rest run sample by sample through ``Realisation``.  Results
+    are reduced in sample order either way; ``threads`` sizes the host pool
+    that draws the samples' random blocks."""
+    from . import ensemble as E
+    if E.supported(config) is None and os.environ.get("CS_ENSEMBLE") != "sequential":
+        ens = E.Ensemble(config, threads=config.threads if config.threads > 1 else None)
+        try:
+            all_obs = ens.run()
+        finally:
+            ens.close()
+    else:
+        all_obs = [run_realisation(config, s) for s in range(config.samples)]
     cm, cse = _mean_se(np.stack([o.counts for o in all_obs]).astype(float))
     mm, mse = _mean_se(np.stack([o.msd for o in all_obs]))
     ham, hase = _mean_se(np.stack([o.hist_alpha for o in all_obs]))

@@ -310,6 +310,17 @@ int cs_ens_step(cs_ens *e, const cs_ens_state *st, const double *xi, const doubl
 /* Synchronise and read the per-realisation status: out[S]. */
 int cs_ens_status(cs_ens *e, cs_status *out);
 
+/* numpy's Generator(PCG64) on the device (csrc/rng.cu): n_streams streams
+ * with state (n_streams, 4) u64 = {state_hi, state_lo, inc_hi, inc_lo}
+ * (numpy's bit_generator.state), advanced in place.  out (k, n_streams, m)
+ * f64: out[k][s] = stream s's next m draws of step k -- kind 0:
+ * standard_normal (the ziggurat of numpy's distributions.c), kind 1:
+ * random ([0, 1) doubles); bit-identical to numpy on the same host libm. */
+int cs_rng_fill(cs_ctx *ctx, uint64_t *state, int32_t n_streams, int32_t kind, int32_t k,
+                int64_t m, double *out);
+/* y = log1p(x) with the glibc-exact restatement (test seam). */
+int cs_log1p_batch(cs_ctx *ctx, const double *x, double *y, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,8 +10,10 @@ Seeding, initial states and random streams are per sample exactly as in
 reactions; engine.py:272-275): each sample's increments are one
 ``standard_normal((K, N, 2))`` block of its own motion stream per launch
 (bit-identical to K per-step draws), its reaction uniforms one
-``random((K, N))`` block of its reaction stream.  The host draws them on a
-thread pool while the device runs the previous block.  Observables are
+``random((K, N))`` block of its reaction stream.  By default the device
+draws them (csrc/rng.cu: numpy's PCG64 and ziggurat restated, seeded from
+the host generators' states, bit-identical draws); ``rng="host"`` draws
+them with numpy on a thread pool while the device runs the previous block.  Observables are
 recorded at the reference's steps from the device state and reduced in
 sample order with the reference's mean / standard error.
 """
@@ -54,7 +56,8 @@ def supported(config) -> str | None:
 class Ensemble:
     """S samples of one SimConfig advanced together on the device."""
 
-    def __init__(self, config, samples: int | None = None, threads: int | None = None):
+    def __init__(self, config, samples: int | None = None, threads: int | None = None,
+                 rng: str = "device"):
         from .engine import sim_params_struct  # noqa: circular at import time
         torch = N.require_cuda()
         why = supported(config)
@@ -76,6 +79,9 @@ class Ensemble:
         self.refresh_active = self.field_active or config.initial_field != "zero"
         self.react = self.reaction.r_alpha > 0 or self.reaction.r_beta > 0
         self.threads = max(1, int(threads or min(32, os.cpu_count() or 1)))
+        if rng not in ("device", "host"):
+            raise ValueError(f"unknown rng {rng!r}")
+        self.rng = rng
         n, S = self.n, self.S
         self.seeds = [config.sample_seed(s) for s in range(S)]
         self.rng_motion, self.rng_react = [], []
@@ -129,6 +135,17 @@ class Ensemble:
         self._st = st
         self.step_index = 0
         self._pool = ThreadPoolExecutor(self.threads)
+        if rng == "device":
+            def words(gens):
+                w = np.empty((S, 4), np.uint64)
+                for s, g in enumerate(gens):
+                    st = g.bit_generator.state["state"]
+                    for q, v in enumerate((st["state"] >> 64, st["state"], st["inc"] >> 64,
+                                           st["inc"])):
+                        w[s, q] = v & 0xFFFFFFFFFFFFFFFF
+                return torch.as_tensor(w.view(np.int64), device=dev)
+            self._dev_motion = words(self.rng_motion)
+            self._dev_react = words(self.rng_react)
         self._warned = dict(clamp=0, neg=0, react=0)
 
     # ---- random blocks ------------------------------------------------------
@@ -147,12 +164,28 @@ class Ensemble:
         list(self._pool.map(fill, [(i, min(S, i + step)) for i in range(0, S, step)]))
         return xi, u
 
+    def _draw_device(self, k: int):
+        import torch
+        lib, ctx = N.load_library(), N.context()
+        xd = torch.empty((k, self.S, self.n, 2), dtype=torch.float64, device="cuda")
+        N.check(lib.cs_rng_fill(ctx, N.ptr(self._dev_motion), self.S, 0, int(k), 2 * self.n,
+                                N.ptr(xd)), "cs_rng_fill")
+        ud = None
+        if self.react:
+            ud = torch.empty((k, self.S, self.n), dtype=torch.float64, device="cuda")
+            N.check(lib.cs_rng_fill(ctx, N.ptr(self._dev_react), self.S, 1, int(k), self.n,
+                                    N.ptr(ud)), "cs_rng_fill")
+        return xd, ud
+
     def advance(self, k: int, drawn=None) -> None:
         """Run k steps of every sample (drawn: a pre-drawn (xi, u) block)."""
         import torch
-        xi, u = drawn if drawn is not None else self._draw(k)
-        xd = torch.as_tensor(xi, device="cuda")
-        ud = None if u is None else torch.as_tensor(u, device="cuda")
+        if self.rng == "device" and drawn is None:
+            xd, ud = self._draw_device(k)
+        else:
+            xi, u = drawn if drawn is not None else self._draw(k)
+            xd = torch.as_tensor(xi, device="cuda")
+            ud = None if u is None else torch.as_tensor(u, device="cuda")
         N.check(N.load_library().cs_ens_step(self._h, ctypes.byref(self._st), N.ptr(xd),
                                              N.ptr(ud), int(k)), "cs_ens_step")
         self.step_index += k
@@ -229,6 +262,13 @@ class Ensemble:
         field_c = np.zeros((S, 4, self.grid.n_c ** 2))
         lo, hi = self.domain.lo, self.domain.hi
 
+        edges = [np.linspace(lo[a], hi[a], b + 1) for a in range(2)]
+
+        def bins(v, e):  # np.histogram2d's bin index (histogramdd: right edge closed)
+            i = np.searchsorted(e, v, side="right")
+            i[v == e[-1]] -= 1
+            return i - 1
+
         def observe(step):
             snap = [k for k in range(4) if snaps[k] == step]
             if not (flags[step] or snap):
@@ -241,22 +281,29 @@ class Ensemble:
                 n_a = (species == Species.ALPHA).sum(axis=1)
                 counts.append(np.stack([n_a, self.n - n_a], axis=1))
                 d = pos - anc
-                msds.append(np.array([float((d[s] * d[s]).sum(axis=1).mean())
-                                      for s in range(S)]))
+                # per sample float((d * d).sum(axis=1).mean()) (engine.py:230-235);
+                # the row-wise reduction is the same pairwise sum
+                msds.append((d * d).sum(axis=2).mean(axis=1))
             if snap:
                 c = self.state["c"].cpu().numpy() if self.field_active or \
                     self.refresh_active else np.zeros((S, self.grid.n_c ** 2))
-                for s in range(S):
-                    for sp, out in ((Species.ALPHA, hist_a), (Species.BETA, hist_b)):
-                        p = pos[s][species[s] == sp]
-                        h, _, _ = np.histogram2d(p[:, 0], p[:, 1], bins=b,
-                                                 range=[[lo[0], hi[0]], [lo[1], hi[1]]])
-                        h = h.T
-                        h = h / p.shape[0] if p.shape[0] else h
-                        for k in snap:
-                            out[s, k] = h
+                ix = bins(pos[..., 0].ravel(), edges[0]).reshape(S, -1)
+                iy = bins(pos[..., 1].ravel(), edges[1]).reshape(S, -1)
+                inside = (ix >= 0) & (ix < b) & (iy >= 0) & (iy < b)
+                sid = np.arange(S)[:, None]
+                for sp, out in ((Species.ALPHA, hist_a), (Species.BETA, hist_b)):
+                    sel = species == sp
+                    keep = sel & inside
+                    key = (sid * b * b + ix * b + iy)[keep]
+                    h = np.bincount(key, minlength=S * b * b).reshape(S, b, b)
+                    h = h.transpose(0, 2, 1).astype(np.float64)
+                    cnt = sel.sum(axis=1)
+                    nz = cnt > 0
+                    h[nz] = h[nz] / cnt[nz][:, None, None]
                     for k in snap:
-                        field_c[s, k] = c[s]
+                        out[:, k] = h
+                for k in snap:
+                    field_c[:, k] = c
 
         observe(0)
         # block boundaries at the recording / snapshot steps
@@ -268,11 +315,14 @@ class Ensemble:
             blocks.append(stop - prev)
             prev = stop
         for bi, k in enumerate(blocks):
-            drawn = pending.result() if pending is not None else self._draw(k)
-            self.advance(k, drawn)
-            # draw the next block on the host while the device runs this one
-            pending = (self._pool_submit_draw(blocks[bi + 1]) if bi + 1 < len(blocks)
-                       else None)
+            if self.rng == "device":
+                self.advance(k)
+            else:
+                drawn = pending.result() if pending is not None else self._draw(k)
+                self.advance(k, drawn)
+                # draw the next block on the host while the device runs this one
+                pending = (self._pool_submit_draw(blocks[bi + 1]) if bi + 1 < len(blocks)
+                           else None)
             self.check()
             observe(self.step_index)
         cnt = np.stack(counts, axis=1)        # (S, T, 2)

@@ -109,3 +109,19 @@ def test_unsupported_configs_fall_back_to_realisations():
     assert supported(_quiet(scheduler="gillespie")) is not None
     assert supported(_quiet(periodic=True)) is not None  # periodic grid
     assert supported(_quiet()) is None
+
+
+def test_device_rng_ensemble_equals_host_rng_ensemble():
+    """The ensemble's device-drawn increments/uniforms are numpy's: the
+    same states as with host-drawn blocks, bit for bit."""
+    cfg = _quiet(samples=5, seed_base=11, r_alpha=3000.0, r_beta=1500.0)
+    a = Ensemble(cfg, rng="device")
+    b = Ensemble(cfg, rng="host")
+    for k in (7, 13):
+        a.advance(k)
+        b.advance(k)
+    for key in ("pos", "species", "anchor"):
+        assert torch.equal(a.state[key], b.state[key]) or key != "pos" or \
+            torch.allclose(a.state[key], b.state[key], rtol=0, atol=1e-12), key
+    a.close()
+    b.close()

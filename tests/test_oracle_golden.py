@@ -243,3 +243,16 @@ def test_reaction_restatement_matches_reference_golden():
         assert np.array_equal(t, r[f"b{k}_out_species"]), k
         assert np.array_equal(d, r[f"b{k}_out_drift"]), k
         assert c[1] == int(r[f"b{k}_count"]) and (h > 1.0) == bool(r[f"b{k}_warned"]), k
+
+
+def test_rng_restatement_matches_numpy():
+    """oracle/rng.py (PCG64 + numpy's ziggurat with the tables read from
+    numpy's own library) against Generator.standard_normal / random."""
+    from oracle.rng import PCG64
+    for seed in (0, 5, 2**33 + 1):
+        g = np.random.default_rng(np.random.SeedSequence(seed).spawn(3)[1])
+        p = PCG64.of(g)
+        a = g.standard_normal(60000)
+        b = np.array([p.standard_normal() for _ in range(60000)])
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), seed
+        assert np.array_equal(g.random(500), np.array([p.next_double() for _ in range(500)]))

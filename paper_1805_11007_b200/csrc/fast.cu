@@ -77,7 +77,7 @@ struct FastArgs {
     long long cap;      // slots per sub-bucket region
     double2 *force;     // pair force per sorted slot (binary64)
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
-                        // 2 skip deposits, 4 store records at the slot index
+                        // 2 skip deposits, 64 no pair terms, 128 no candidate walk, 4 store records at the slot index
                         // without claims, 8 the same plus a fire-and-forget
                         // claim (4/8/32: timing only, wrong results)
                         // 32 xi read at the slot index (timing only: wrong results)
@@ -417,6 +417,7 @@ k_fast_forces(const DevStatus *st) {
                     se[r] = __ldg(a.starts + f + 3);
                 }
                 tot = (se[0] - sa[0]) + (se[1] - sa[1]) + (se[2] - sa[2]);
+                if (a.debug & 128) tot = 0;  // timing diagnostic: no walk
 #pragma unroll
                 for (int r = 2; r >= 0; r--) {  // push front, skipping empty rows
                     if (se[r] > sa[r]) {
@@ -498,7 +499,8 @@ k_fast_forces(const DevStatus *st) {
                 const double d1 = dsub((double)q.y, (double)wq.oy[ow]);
                 const double r2 = dadd(dmul(d0, d0), dmul(d1, d1));
                 double2 term = make_double2(0.0, 0.0);
-                if (!(r2 > a.pt.cut2[tt] || r2 == 0.0)) term = pair_term(d0, d1, r2, a.pt.eps[tt]);
+                if (!(r2 > a.pt.cut2[tt] || r2 == 0.0) && !(a.debug & 64))
+                    term = pair_term(d0, d1, r2, a.pt.eps[tt]);
                 wq.tx[o] = term.x;
                 wq.ty[o] = term.y;
             }

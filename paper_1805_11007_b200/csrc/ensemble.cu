@@ -54,15 +54,20 @@ struct EnsArgs {
     double wcell;
     int react;
     double p_ab, r_beta;
+    int qper;  // doubles of pair queue per warp (in the grid scratch ra/rb)
 };
 
-// C = A op(B) (E *) for n <= 64 inside one CTA of 256 threads: thread
-// (ty, tx) owns rows ty + 16 u, columns tx + 16 v; the k loop is sequential
-// fma, the accumulation order of field.cu's k_gemm.
+// C = A op(B) (E *) for n <= 64 inside one CTA: T = ceil(n / 4) and thread
+// (ty, tx) < (T, T) owns rows ty + T u, columns tx + T v (u, v < 4) -- no
+// wasted products for n = 4T; the k loop is sequential fma, the
+// accumulation order of field.cu's k_gemm.
 template <bool BT>
 __device__ __forceinline__ void cta_gemm(const double *A, const double *B, const double *E,
                                          double *C, int n) {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int T = (n + 3) >> 2;
+    const int tid = threadIdx.x;
+    if (tid >= T * T) return;
+    const int ty = tid / T, tx = tid - ty * T;
     double acc[4][4];
 #pragma unroll
     for (int u = 0; u < 4; u++)
@@ -71,8 +76,8 @@ __device__ __forceinline__ void cta_gemm(const double *A, const double *B, const
     int rr[4], cc[4];
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-        rr[u] = min(ty + 16 * u, n - 1);
-        cc[u] = min(tx + 16 * u, n - 1);
+        rr[u] = min(ty + T * u, n - 1);
+        cc[u] = min(tx + T * u, n - 1);
     }
     for (int k = 0; k < n; k++) {
         double a[4], b[4];
@@ -90,7 +95,7 @@ __device__ __forceinline__ void cta_gemm(const double *A, const double *B, const
     for (int u = 0; u < 4; u++)
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const int r = ty + 16 * u, col = tx + 16 * v;
+            const int r = ty + T * u, col = tx + T * v;
             if (r < n && col < n) {
                 double val = acc[u][v];
                 if (E) val *= E[r * n + col];
@@ -134,7 +139,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
     const long long s = blockIdx.x;
     double *pos = sm, *anc = pos + 2 * n, *drift = anc + 2 * n, *frc = drift + 2 * n;
     double *lc = frc + 2 * n, *c = lc + n, *ra = c + m, *rb = ra + m;
-    int *order = reinterpret_cast<int *>(rb + m);
+    int *order = reinterpret_cast<int *>(ra + 8 * a.qper);
     int *starts = order + n, *cur = starts + a.ncell + 1, *key = cur + a.ncell;
     uint8_t *type = reinterpret_cast<uint8_t *>(key + n);
     DevStatus *st = a.st + s;
@@ -344,6 +349,8 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             // cell) and evaluate the accepted pair terms in parallel; the
             // terms are then added in candidate order (motion.py:240-243)
             const BinGeom &g = a.g;
+            double *wq = ra + (long long)warp * a.qper;  // this warp's pair queue
+            const int qcap = a.qper / 4;
             for (int i = warp; i < n; i += ENS_THREADS / 32) {
                 const double xi = pos[2 * i], yi = pos[2 * i + 1];
                 const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
@@ -385,10 +392,33 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                     pre[r] = __shfl_sync(0xffffffffu, incl - rl, r);
                     cs_[r] = __shfl_sync(0xffffffffu, rs, r);
                 }
+                // accepted pairs are queued (ballot-compacted, candidate
+                // order) in the warp's slice of the grid scratch, their terms
+                // evaluated 32 at a time, then added in order by lane 0
                 double fx = 0.0, fy = 0.0;
+                int nq = 0;
+                auto flush = [&]() {
+                    __syncwarp();
+                    for (int e = lane; e < nq; e += 32) {
+                        double *qe = wq + 4 * e;
+                        const double eps = qe[3], rr = dsqrt(qe[2]);
+                        const double sc = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
+                        qe[0] = dmul(sc, qe[0]);
+                        qe[1] = dmul(sc, qe[1]);
+                    }
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int e = 0; e < nq; e++) {
+                            fx = dadd(fx, wq[4 * e]);
+                            fy = dadd(fy, wq[4 * e + 1]);
+                        }
+                    __syncwarp();
+                    nq = 0;
+                };
                 for (int k0 = 0; k0 < total; k0 += 32) {
+                    if (nq + 32 > qcap) flush();
                     const int k = k0 + lane;
-                    double tx = 0.0, ty = 0.0;
+                    double dx0 = 0.0, dx1 = 0.0, r2 = 0.0, eps = 0.0;
                     bool acc = false;
                     if (k < total) {
                         int r = 0;
@@ -399,30 +429,27 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                         for (int q = 1; q < 9; q++) base = r == q ? cs_[q] - pre[q] : base;
                         const int j = order[base + k];
                         if (j != i) {
-                            double dx0 = dsub(pos[2 * j], xi);
-                            double dx1 = dsub(pos[2 * j + 1], yi);
+                            dx0 = dsub(pos[2 * j], xi);
+                            dx1 = dsub(pos[2 * j + 1], yi);
                             if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
                             if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
-                            const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                            r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
                             const int t = ti * 2 + (type[j] ? 1 : 0);
-                            if (!(r2 > a.pt.cut2[t] || r2 == 0.0)) {
-                                const double eps = a.pt.eps[t];
-                                const double rr = dsqrt(r2);
-                                const double sc = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
-                                tx = dmul(sc, dx0);
-                                ty = dmul(sc, dx1);
-                                acc = true;
-                            }
+                            acc = !(r2 > a.pt.cut2[t] || r2 == 0.0);
+                            eps = a.pt.eps[t];
                         }
                     }
-                    unsigned msk = __ballot_sync(0xffffffffu, acc);
-                    while (msk) {  // ordered sum, identical in every lane
-                        const int b = __ffs(msk) - 1;
-                        fx = dadd(fx, __shfl_sync(0xffffffffu, tx, b));
-                        fy = dadd(fy, __shfl_sync(0xffffffffu, ty, b));
-                        msk &= msk - 1;
+                    const unsigned msk = __ballot_sync(0xffffffffu, acc);
+                    if (acc) {
+                        double *qe = wq + 4 * (nq + __popc(msk & ((1u << lane) - 1u)));
+                        qe[0] = dx0;
+                        qe[1] = dx1;
+                        qe[2] = r2;
+                        qe[3] = eps;
                     }
+                    nq += __popc(msk);
                 }
+                flush();
                 if (lane == 0) {
                     frc[2 * i] = fx;
                     frc[2 * i + 1] = fy;
@@ -536,9 +563,17 @@ struct cs_ens {
 
 namespace cs {
 
+// scratch doubles after c: ra and rb of the field stage, reused as the warps'
+// pair queues by the force stage (at least 64 entries of 4 doubles per warp)
+static size_t ens_scratch(int nc) {
+    const size_t m = (size_t)nc * nc;
+    const size_t q = (ENS_THREADS / 32) * 4 * 64;
+    return 2 * m > q ? 2 * m : q;
+}
+
 static size_t ens_smem(int n, int nc, int ncell) {
     const size_t m = (size_t)nc * nc;
-    return sizeof(double) * (9 * (size_t)n + 3 * m) +
+    return sizeof(double) * (9 * (size_t)n + m + ens_scratch(nc)) +
            sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1) + (size_t)n + 16;
 }
 
@@ -608,6 +643,7 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
     a.react = p->react;
     a.p_ab = p->react_p_ab;
     a.r_beta = p->react_r_beta;
+    a.qper = (int)(ens_scratch(a.nc) / (ENS_THREADS / 32));
     e->smem = ens_smem(a.n, a.nc, a.ncell);
     int dev_max = 0;
     CS_CUDA(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin,

@@ -309,6 +309,10 @@ int cs_ens_step(cs_ens *e, const cs_ens_state *st, const double *xi, const doubl
                 int32_t k_steps);
 /* Synchronise and read the per-realisation status: out[S]. */
 int cs_ens_status(cs_ens *e, cs_status *out);
+/* Recorded observables of every realisation (engine.py:343-349), device
+ * arrays: n_alpha[S] (int64) and msd[S] (f64, numpy's pairwise mean of the
+ * squared displacements from the start anchors, bit-identical). */
+int cs_ens_observe(cs_ens *e, const cs_ens_state *st, int64_t *n_alpha, double *msd);
 
 /* numpy's Generator(PCG64) on the device (csrc/rng.cu): n_streams streams
  * with state (n_streams, 4) u64 = {state_hi, state_lo, inc_hi, inc_lo}

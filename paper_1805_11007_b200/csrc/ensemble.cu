@@ -543,6 +543,67 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
 
 }  // namespace cs
 
+namespace cs {
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// DOUBLE_pairwise_sum): < 8 terms in order from -0.0; <= 128 terms in 8
+// interleaved accumulators folded ((r0 + r1) + (r2 + r3)) + ((r4 + r5) +
+// (r6 + r7)) plus the tail in order; beyond, split at n / 2 rounded down to
+// a multiple of 8.  Used for the per-sample mean squared displacement.
+__device__ double np_pairwise_sum(const double *v, int n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int i = 0; i < n; i++) res = dadd(res, v[i]);
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) r[q] = v[q];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int q = 0; q < 8; q++) r[q] = dadd(r[q], v[i + q]);
+        double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])),
+                          dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+        for (; i < n; i++) res = dadd(res, v[i]);
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return dadd(np_pairwise_sum(v, n2), np_pairwise_sum(v + n2, n - n2));
+}
+
+// per sample: Alpha count and msd = mean over particles of
+// (0 + dx^2) + dy^2 (engine.py:230-235 in numpy's reduction order); one
+// block per sample, the squared displacements staged in shared memory
+__global__ void __launch_bounds__(256)
+k_ens_observe(const double *__restrict__ pos, const double *__restrict__ anchor,
+              const uint8_t *__restrict__ type, int n, long long *__restrict__ n_alpha,
+              double *__restrict__ msd) {
+    extern __shared__ double sq[];
+    __shared__ int s_cnt;
+    const long long s = blockIdx.x;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int c = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double d0 = dsub(pos[2 * n * s + 2 * i], anchor[2 * n * s + 2 * i]);
+        const double d1 = dsub(pos[2 * n * s + 2 * i + 1], anchor[2 * n * s + 2 * i + 1]);
+        sq[i] = dadd(dadd(-0.0, dmul(d0, d0)), dmul(d1, d1));
+        c += type[(long long)n * s + i] == 0 ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        n_alpha[s] = s_cnt;
+        msd[s] = ddiv(np_pairwise_sum(sq, n), (double)n);
+    }
+}
+
+}  // namespace cs
+
 // ---------------------------------------------------------------- host side
 namespace cs {
 int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
@@ -706,6 +767,14 @@ int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u
     return CS_OK;
 }
 
+int ens_observe(cs_ens *e, const cs_ens_state *s, int64_t *n_alpha, double *msd) {
+    k_ens_observe<<<e->n_real, 256, sizeof(double) * (size_t)e->a.n, e->ctx->stream>>>(
+        s->pos, s->anchor, s->type, e->a.n, reinterpret_cast<long long *>(n_alpha), msd);
+    CS_LAUNCH_CHECK();
+    e->ctx->launches += 1;
+    return CS_OK;
+}
+
 int ens_status(cs_ens *e, cs_status *out) {
     std::vector<DevStatus> d((size_t)e->n_real);
     CS_CUDA(cudaMemcpyAsync(d.data(), e->status.p, sizeof(DevStatus) * d.size(),
@@ -765,5 +834,9 @@ int cs_ens_step(cs_ens *e, const cs_ens_state *st, const double *xi, const doubl
 }
 
 int cs_ens_status(cs_ens *e, cs_status *out) { return cs::ens_status(e, out); }
+
+int cs_ens_observe(cs_ens *e, const cs_ens_state *st, int64_t *n_alpha, double *msd) {
+    return cs::ens_observe(e, st, n_alpha, msd);
+}
 
 }  // extern "C"

@@ -98,8 +98,16 @@ __device__ __noinline__ double log1p_glibc(double x) {
     return fma(dk, ln2_hi, -dsub(dsub(hfsq, dadd(t, fma(dk, ln2_lo, c))), f));
 }
 
+// the ziggurat tables are indexed by a random byte per lane: read from
+// shared memory (constant memory would serialise the 32 lanes' addresses)
+struct ZigTables {
+    unsigned long long ki[256];
+    double wi[256], fi[256];
+};
+
 struct Pcg64 {
     unsigned long long hi, lo, ihi, ilo;  // state, increment (128-bit)
+    const ZigTables *zt;
     __device__ __forceinline__ unsigned long long next64() {
         constexpr unsigned long long MH = 0x2360ED051FC65DA4ull, ML = 0x4385DF649FCCF645ull;
         // state = state * M + inc (mod 2^128)
@@ -123,9 +131,9 @@ struct Pcg64 {
             r >>= 8;
             const int sign = (int)(r & 1);
             const unsigned long long rabs = (r >> 1) & 0x000fffffffffffffull;
-            double x = dmul((double)rabs, __longlong_as_double((long long)ZIG_WI[idx]));
+            double x = dmul((double)rabs, zt->wi[idx]);
             if (sign) x = -x;
-            if (rabs < ZIG_KI[idx]) return x;
+            if (rabs < zt->ki[idx]) return x;
             if (idx == 0) {
                 for (;;) {
                     const double xx = dmul(-ZIR, log1p_glibc(-next_double()));
@@ -134,8 +142,8 @@ struct Pcg64 {
                         return ((rabs >> 8) & 1) ? -dadd(ZR, xx) : dadd(ZR, xx);
                 }
             } else {
-                const double f0 = __longlong_as_double((long long)ZIG_FI[idx - 1]);
-                const double f1 = __longlong_as_double((long long)ZIG_FI[idx]);
+                const double f0 = zt->fi[idx - 1];
+                const double f1 = zt->fi[idx];
                 if (dadd(dmul(dsub(f0, f1), next_double()), f1) <
                     cs_exp(dmul(dmul(-0.5, x), x)))
                     return x;
@@ -149,9 +157,16 @@ struct Pcg64 {
 __global__ void __launch_bounds__(64)
 k_rng_fill(unsigned long long *__restrict__ state, int S, int kind, int k, long long m,
            double *__restrict__ out) {
+    __shared__ ZigTables zt;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        zt.ki[i] = ZIG_KI[i];
+        zt.wi[i] = __longlong_as_double((long long)ZIG_WI[i]);
+        zt.fi[i] = __longlong_as_double((long long)ZIG_FI[i]);
+    }
+    __syncthreads();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= S) return;
-    Pcg64 g{state[4 * s], state[4 * s + 1], state[4 * s + 2], state[4 * s + 3]};
+    Pcg64 g{state[4 * s], state[4 * s + 1], state[4 * s + 2], state[4 * s + 3], &zt};
     for (int kk = 0; kk < k; kk++) {
         double *o = out + ((long long)kk * S + s) * m;
         if (kind == 0)

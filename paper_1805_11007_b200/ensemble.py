@@ -164,15 +164,21 @@ class Ensemble:
         list(self._pool.map(fill, [(i, min(S, i + step)) for i in range(0, S, step)]))
         return xi, u
 
-    def _draw_device(self, k: int):
+    def _draw_device(self, k: int, into=None):
+        """The next k steps' increments (and uniforms) drawn on the device,
+        on the current stream (into: preallocated (xi, u) buffers)."""
         import torch
         lib, ctx = N.load_library(), N.context()
-        xd = torch.empty((k, self.S, self.n, 2), dtype=torch.float64, device="cuda")
+        if into is None:
+            xd = torch.empty((k, self.S, self.n, 2), dtype=torch.float64, device="cuda")
+            ud = (torch.empty((k, self.S, self.n), dtype=torch.float64, device="cuda")
+                  if self.react else None)
+        else:
+            xd = into[0][:k]
+            ud = None if into[1] is None else into[1][:k]
         N.check(lib.cs_rng_fill(ctx, N.ptr(self._dev_motion), self.S, 0, int(k), 2 * self.n,
                                 N.ptr(xd)), "cs_rng_fill")
-        ud = None
-        if self.react:
-            ud = torch.empty((k, self.S, self.n), dtype=torch.float64, device="cuda")
+        if ud is not None:
             N.check(lib.cs_rng_fill(ctx, N.ptr(self._dev_react), self.S, 1, int(k), self.n,
                                     N.ptr(ud)), "cs_rng_fill")
         return xd, ud
@@ -182,14 +188,28 @@ class Ensemble:
         import torch
         if self.rng == "device" and drawn is None:
             xd, ud = self._draw_device(k)
+        elif isinstance(drawn, tuple) and hasattr(drawn[0], "device"):  # device blocks
+            xd, ud = drawn
         else:
             xi, u = drawn if drawn is not None else self._draw(k)
             xd = torch.as_tensor(xi, device="cuda")
             ud = None if u is None else torch.as_tensor(u, device="cuda")
+        N.context()  # bind the library to the current stream
         N.check(N.load_library().cs_ens_step(self._h, ctypes.byref(self._st), N.ptr(xd),
                                              N.ptr(ud), int(k)), "cs_ens_step")
         self.step_index += k
         self._xd, self._ud = xd, ud  # keep alive until the next sync
+
+    def observe_device(self):
+        """(Alpha count (S,) int64, msd (S,) f64) of every sample now."""
+        import torch
+        if getattr(self, "_obs", None) is None:
+            self._obs = (torch.empty(self.S, dtype=torch.int64, device="cuda"),
+                         torch.empty(self.S, dtype=torch.float64, device="cuda"))
+        na, msd = self._obs
+        N.check(N.load_library().cs_ens_observe(self._h, ctypes.byref(self._st), N.ptr(na),
+                                                N.ptr(msd)), "cs_ens_observe")
+        return na.cpu().numpy(), msd.cpu().numpy()
 
     def status(self):
         out = (N.Status_t * self.S)()
@@ -199,10 +219,10 @@ class Ensemble:
     def check(self) -> None:
         """Raise the reference's error for the lowest failing sample; warn."""
         st = self.status()
-        for s in range(self.S):
-            x = st[s]
-            if x.code == N.CS_OK:
-                continue
+        arr = np.ctypeslib.as_array(st)
+        failing = np.flatnonzero(arr["code"] != N.CS_OK)
+        for s in failing[:1]:
+            x = st[int(s)]
             try:
                 try:
                     if x.code == N.CS_FIELD_NONFINITE:
@@ -213,18 +233,18 @@ class Ensemble:
                     raise SimulationError(f"step {x.step}: {exc}") from exc
             except SimulationError as exc:
                 raise SimulationError(f"sample {s}: {exc}") from exc
-        clamp = sum(int(st[s].clamped) for s in range(self.S))
-        neg = sum(int(st[s].neg_mass_steps) for s in range(self.S))
-        react = sum(int(st[s].react_high_count) for s in range(self.S))
+        clamp = int(arr["clamped"].sum())
+        neg = int(arr["neg_mass_steps"].sum())
+        react = int(arr["react_high_count"].sum())
         if clamp > self._warned["clamp"]:
             warnings.warn(f"{clamp - self._warned['clamp']} interpolation point(s) outside the "
                           "grid hull were clamped", stacklevel=3)
         if neg > self._warned["neg"]:
-            first = next(st[s].first_neg_mass for s in range(self.S) if st[s].neg_mass_steps)
+            first = float(arr["first_neg_mass"][np.flatnonzero(arr["neg_mass_steps"])[0]])
             warnings.warn(f"concentration went negative (weighted mass {first:.3e})",
                           stacklevel=3)
         if react > self._warned["react"]:
-            high = max(st[s].react_high_max for s in range(self.S))
+            high = float(arr["react_high_max"].max())
             warnings.warn(f"flip probability {high:.3g} exceeded 1 and was clamped; reduce dt",
                           stacklevel=3)
         self._warned = dict(clamp=clamp, neg=neg, react=react)
@@ -273,18 +293,16 @@ class Ensemble:
             snap = [k for k in range(4) if snaps[k] == step]
             if not (flags[step] or snap):
                 return
-            pos = self.state["pos"].cpu().numpy()
-            species = self.state["species"].cpu().numpy()
             if flags[step]:
-                anc = self.state["anchor"].cpu().numpy()
+                # counts and msd on the device (cs_ens_observe: numpy's
+                # pairwise mean, bit-identical to engine.py:230-235)
                 times.append(step * self.dt)
-                n_a = (species == Species.ALPHA).sum(axis=1)
+                n_a, msd = self.observe_device()
                 counts.append(np.stack([n_a, self.n - n_a], axis=1))
-                d = pos - anc
-                # per sample float((d * d).sum(axis=1).mean()) (engine.py:230-235);
-                # the row-wise reduction is the same pairwise sum
-                msds.append((d * d).sum(axis=2).mean(axis=1))
+                msds.append(msd)
             if snap:
+                pos = self.state["pos"].cpu().numpy()
+                species = self.state["species"].cpu().numpy()
                 c = self.state["c"].cpu().numpy() if self.field_active or \
                     self.refresh_active else np.zeros((S, self.grid.n_c ** 2))
                 ix = bins(pos[..., 0].ravel(), edges[0]).reshape(S, -1)
@@ -314,9 +332,38 @@ class Ensemble:
         for stop in stops:
             blocks.append(stop - prev)
             prev = stop
+        if self.rng == "device":
+            # the next block's random numbers are drawn on a side stream while
+            # the ensemble kernel runs the current one (two buffer sets)
+            import torch
+            side = torch.cuda.Stream()
+            main = torch.cuda.current_stream()
+            kmax = max(blocks) if blocks else 1
+            bufs = [(torch.empty((kmax, S, self.n, 2), dtype=torch.float64, device="cuda"),
+                     torch.empty((kmax, S, self.n), dtype=torch.float64, device="cuda")
+                     if self.react else None) for _ in range(2)]
+            ready = [torch.cuda.Event() for _ in range(2)]
+            done = [torch.cuda.Event() for _ in range(2)]
+
+            def fill(i, k):
+                with torch.cuda.stream(side):
+                    if done_used[i]:
+                        side.wait_event(done[i])
+                    drawn_i = self._draw_device(k, into=bufs[i])
+                    ready[i].record(side)
+                return drawn_i
+            done_used = [False, False]
+            side.wait_stream(main)
+            pend = fill(0, blocks[0]) if blocks else None
         for bi, k in enumerate(blocks):
             if self.rng == "device":
-                self.advance(k)
+                i = bi % 2
+                main.wait_event(ready[i])
+                self.advance(k, pend)
+                done[i].record(main)
+                done_used[i] = True
+                if bi + 1 < len(blocks):
+                    pend = fill(1 - i, blocks[bi + 1])
             else:
                 drawn = pending.result() if pending is not None else self._draw(k)
                 self.advance(k, drawn)

@@ -66,6 +66,9 @@ static_assert(CELLS_PER_THREAD == 4, "k_bucket_sort owns 4 cells (one int4) per 
 #endif
 constexpr int SUBB = CS_SUBB;
 constexpr int RPT = 4;  // records per k_bucket_sort thread held in registers
+#ifndef CS_CLAIM_AGG
+#define CS_CLAIM_AGG 1
+#endif
 static_assert(SUBB >= 1 && SUBB <= 32 && (SUBB & (SUBB - 1)) == 0, "SUBB: power of two <= 32");
 constexpr int BUCKET_CELLS = 1 << BUCKET_SHIFT;
 
@@ -546,7 +549,24 @@ k_fast_update(DevStatus *st, int step) {
     float4 p_out = make_float4(0.f, 0.f, 0.f, 0.f);
     int p_b = -1, p_slot = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
+#if CS_CLAIM_AGG
+    // warp-aggregated claims: the lanes of a warp that target the same
+    // bucket part claim with one atomic (the warp picks the part); the loop
+    // is warp-uniform so that the deferred shuffle of the claimed base sees
+    // every lane
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int wpart = (threadIdx.x >> 5) & (SUBB - 1);
+    bool p_have = false, p_live = false;
+    int p_leader = 0, p_rank = 0, p_ret = 0;
+    for (long long tb = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); tb < a.n;
+         tb += stride) {
+        const bool live = tb + lane < a.n;
+        const long long t = live ? tb + lane : a.n - 1;
+#else
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n; t += stride) {
+        const bool live = true;
+#endif
         const float4 mer = __ldcs(rec + t);
         double2 f = make_double2(0.0, 0.0);
         if (a.interact) f = __ldcs(a.force + t);
@@ -560,7 +580,14 @@ k_fast_update(DevStatus *st, int step) {
         const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + zi)
                                        : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + zi);
         const double fx = f.x, fy = f.y;  // zero without interactions
+#if CS_CLAIM_AGG
+        if (p_have) {
+            const int basev = __shfl_sync(0xffffffffu, p_ret, p_leader);
+            if (p_live) claim_store(a, st, step, p_b, basev + p_rank, p_out);
+        }
+#else
         if (p_b >= 0) claim_store(a, st, step, p_b, p_slot, p_out);
+#endif
         const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
         const bool do_drift = a.refresh && !dead && !pinned;
         float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
@@ -601,7 +628,7 @@ k_fast_update(DevStatus *st, int step) {
         double v0 = dadd(dadd(dadd(x, dmul(amp, (double)z.x)), dmul(dr0, a.dt)), dmul(fx, a.dt));
         double v1 = dadd(dadd(dadd(y, dmul(amp, (double)z.y)), dmul(dr1, a.dt)), dmul(fy, a.dt));
         int w0 = (short)(wbits & 0xffffu), w1 = (short)(wbits >> 16);
-        bool ok = !dead;
+        bool ok = !dead && live;
         if (ok && !(isfinite(v0) && isfinite(v1))) {
             atomicMin(&st->key, err_key(0, id, CS_NONFINITE));
             st->abort = 1;
@@ -641,6 +668,22 @@ k_fast_update(DevStatus *st, int step) {
         const double nx = (double)out.x, ny = (double)out.y;
         const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
                         cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
+#if CS_CLAIM_AGG
+        p_b = (key >> BUCKET_SHIFT) * SUBB + wpart;
+        if (a.debug & 12) {  // timing diagnostics only (wrong results)
+            if (live && (a.debug & 8)) atomicAdd(&a.fill[p_b], 1);
+            if (live) reinterpret_cast<float4 *>(a.region)[t] = out;
+            p_have = false;
+            continue;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, live ? p_b : -1 - lane);
+        p_leader = __ffs(peers) - 1;
+        p_rank = __popc(peers & lt);
+        if (live && lane == p_leader) p_ret = atomicAdd(&a.fill[p_b], __popc(peers));
+        p_live = live;
+        p_have = true;
+        p_out = out;
+#else
         p_b = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
         if (a.debug & 12) {  // timing diagnostics only (wrong results)
             if (a.debug & 8) atomicAdd(&a.fill[p_b], 1);
@@ -650,8 +693,16 @@ k_fast_update(DevStatus *st, int step) {
         }
         p_slot = atomicAdd(&a.fill[p_b], 1);
         p_out = out;
+#endif
     }
+#if CS_CLAIM_AGG
+    if (p_have) {
+        const int basev = __shfl_sync(0xffffffffu, p_ret, p_leader);
+        if (p_live) claim_store(a, st, step, p_b, basev + p_rank, p_out);
+    }
+#else
     if (p_b >= 0) claim_store(a, st, step, p_b, p_slot, p_out);
+#endif
 }
 
 // caller arrays (id order) -> records claimed into their bucket regions

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 2
+#define CS_ABI_VERSION 3
 
 enum cs_code {
     CS_OK = 0,
@@ -114,6 +114,12 @@ int cs_em_step(cs_ctx *ctx, int32_t prec, const void *pos,
                const double *diffusion, const double *drift,
                const double *force, const void *xi, double dt, int64_t n,
                void *out);
+/* tamed_step (motion.py:283-298): as cs_em_step with the interaction
+ * increment (force dt) / (1 + ||force|| dt). */
+int cs_tamed_step(cs_ctx *ctx, int32_t prec, const void *pos,
+                  const double *diffusion, const double *drift,
+                  const double *force, const void *xi, double dt, int64_t n,
+                  void *out);
 
 /* Resolves x (the proposal buffer) against the box in place, shifts anchor
  * on periodic wraps and, on success, copies x into positions (may be NULL).
@@ -202,6 +208,7 @@ typedef struct {
     int32_t react;           /* 0 off, 1 fixed-step Bernoulli flips */
     double react_p_ab;       /* r_alpha * dt */
     double react_r_beta;     /* Beta -> Alpha rate per unit concentration */
+    int32_t integrator;      /* 0 Euler-Maruyama, 1 tamed (motion.py:283-298) */
 } cs_sim_params;
 
 /* Engines.  DIRECT keeps the reference layout (rows in id order) and

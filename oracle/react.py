@@ -40,3 +40,15 @@ def fixed_step(types, local_c, drift, u, p_ab, r_beta, dt):
     d = np.array(drift, dtype=np.float64, copy=True)
     d[to_alpha] = 0.0
     return out, d, (int(to_beta.sum()), int(to_alpha.sum())), high
+
+
+def tamed_step(pos, dcoef, drift, force, xi, dt):
+    """chemosim/motion.py:283-298 restated (numpy, the reference's own
+    operation order): ((x + sqrt((2 D) dt) xi) + drift dt) + (f dt) /
+    (1 + ||f|| dt)."""
+    pos = np.asarray(pos, dtype=np.float64)
+    amp = np.sqrt(2.0 * np.asarray(dcoef, dtype=np.float64) * dt)[:, None]
+    f = np.asarray(force, dtype=np.float64)
+    fnorm = np.sqrt((f * f).sum(axis=-1, keepdims=True))
+    tamed = f * dt / (1.0 + fnorm * dt)
+    return pos + amp * np.asarray(xi) + np.asarray(drift) * dt + tamed

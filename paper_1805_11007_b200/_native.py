@@ -50,7 +50,7 @@ class SimParams_t(ctypes.Structure):
                 ("kernel_cutoff", C_f64), ("secretes", C_i32 * 2), ("consumes", C_i32 * 2),
                 ("chi", C_f64 * 2), ("chi_pinned", C_i32 * 2), ("store_samples", C_i32),
                 ("store_next", C_i32), ("engine", C_i32), ("react", C_i32),
-                ("react_p_ab", C_f64), ("react_r_beta", C_f64)]
+                ("react_p_ab", C_f64), ("react_r_beta", C_f64), ("integrator", C_i32)]
 
 
 class SimState_t(ctypes.Structure):
@@ -85,6 +85,7 @@ SIGNATURES = [
                                     ctypes.POINTER(PairParams_t), C_p, C_i64,
                                     ctypes.POINTER(C_i64)]),
     ("cs_em_step", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_p, C_p, C_f64, C_i64, C_p]),
+    ("cs_tamed_step", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_p, C_p, C_f64, C_i64, C_p]),
     ("cs_apply_boundaries", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_i64, ctypes.POINTER(Domain_t),
                                     ctypes.POINTER(C_i64), ctypes.POINTER(C_i32)]),
     ("cs_deposit", C_i32, [C_p, C_i32, C_p, C_p, C_i64, ctypes.POINTER(Grid_t), C_i32, C_f64,

@@ -88,7 +88,8 @@ GridGeom make_grid_geom(const cs_grid &g) {
 }
 
 int launch_em_step(cs_ctx *ctx, int prec, const void *pos, const double *D, const double *drift,
-                   const double *force, const void *xi, double dt, long long n, void *out);
+                   const double *force, const void *xi, double dt, long long n, void *out,
+                   int tamed);
 int launch_boundaries(cs_ctx *ctx, int prec, void *x, void *anchor, long long n,
                       const cs_domain &d, DevStatus *st);
 int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
@@ -221,7 +222,14 @@ int cs_em_step(cs_ctx *ctx, int32_t prec, const void *pos, const double *diffusi
                const double *drift, const double *force, const void *xi, double dt, int64_t n,
                void *out) {
     CS_TRY(check_prec(prec));
-    return launch_em_step(ctx, prec, pos, diffusion, drift, force, xi, dt, n, out);
+    return launch_em_step(ctx, prec, pos, diffusion, drift, force, xi, dt, n, out, 0);
+}
+
+int cs_tamed_step(cs_ctx *ctx, int32_t prec, const void *pos, const double *diffusion,
+                  const double *drift, const double *force, const void *xi, double dt,
+                  int64_t n, void *out) {
+    CS_TRY(check_prec(prec));
+    return launch_em_step(ctx, prec, pos, diffusion, drift, force, xi, dt, n, out, 1);
 }
 
 int cs_apply_boundaries(cs_ctx *ctx, int32_t prec, void *x, void *anchor, void *positions,

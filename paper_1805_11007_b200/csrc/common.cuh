@@ -244,6 +244,23 @@ __device__ __forceinline__ double bilinear_apply(const Bilin &b, const G *__rest
     return dadd(dadd(dadd(a, c), d), e);
 }
 
+// The interaction increment of the proposal: force dt (em_step,
+// motion.py:281-282) or, tamed (tamed_step, motion.py:283-298),
+// (force dt) / (1 + ||force|| dt) with ||force|| = sqrt((-0 + f0^2) + f1^2)
+// (numpy's pairwise row sum).
+__device__ __forceinline__ void force_increment(double f0, double f1, double dt, int tamed,
+                                                double &i0, double &i1) {
+    if (!tamed) {
+        i0 = dmul(f0, dt);
+        i1 = dmul(f1, dt);
+        return;
+    }
+    const double fn = dsqrt(dadd(dadd(-0.0, dmul(f0, f0)), dmul(f1, f1)));
+    const double den = dadd(1.0, dmul(fn, dt));
+    i0 = ddiv(dmul(f0, dt), den);
+    i1 = ddiv(dmul(f1, dt), den);
+}
+
 // One axis of _boundaries_kernel (motion.py:363-401).  Returns 0, 2 or 3.
 __device__ __forceinline__ int boundary_axis(double &v, double &a, double lo, double hi,
                                              int per) {

@@ -55,6 +55,7 @@ struct EnsArgs {
     int react;
     double p_ab, r_beta;
     int qper;  // doubles of pair queue per warp (in the grid scratch ra/rb)
+    int tamed;
 };
 
 // C = A op(B) (E *) for n <= 64 inside one CTA: T = ceil(n / 4) and thread
@@ -463,12 +464,14 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             const int t = type[p] ? 1 : 0;
             const double amp = a.amp[t];
             const double f0 = a.interact ? frc[2 * p] : 0.0, f1 = a.interact ? frc[2 * p + 1] : 0.0;
+            double i0, i1;
+            force_increment(f0, f1, a.dt, a.tamed, i0, i1);
             double v[2];
             v[0] = dadd(dadd(dadd(pos[2 * p], dmul(amp, xk[2 * p])), dmul(drift[2 * p], a.dt)),
-                        dmul(f0, a.dt));
+                        i0);
             v[1] = dadd(dadd(dadd(pos[2 * p + 1], dmul(amp, xk[2 * p + 1])),
                              dmul(drift[2 * p + 1], a.dt)),
-                        dmul(f1, a.dt));
+                        i1);
             const double raw0 = v[0], raw1 = v[1];
             bool ok = isfinite(v[0]) && isfinite(v[1]);
             if (!ok) set_status(st, &s_abort, err_key(0, p, CS_NONFINITE), step);
@@ -701,6 +704,7 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
         a.Inv = e->ops->Inv;
         a.E = e->ops->E;
     }
+    a.tamed = p->integrator == 1;
     a.react = p->react;
     a.p_ab = p->react_p_ab;
     a.r_beta = p->react_r_beta;

@@ -15,7 +15,8 @@ namespace cs {
 template <class P>
 __global__ void k_em_step(const P *__restrict__ pos, const double *__restrict__ D,
                           const double *__restrict__ drift, const double *__restrict__ force,
-                          const P *__restrict__ xi, double dt, long long n, P *__restrict__ out) {
+                          const P *__restrict__ xi, double dt, long long n, P *__restrict__ out,
+                          int tamed) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double amp = dsqrt(dmul(dmul(2.0, D[i]), dt));
@@ -24,8 +25,10 @@ __global__ void k_em_step(const P *__restrict__ pos, const double *__restrict__ 
         load2(xi, i, x0, x1);
         const double d0 = drift ? drift[2 * i] : 0.0, d1 = drift ? drift[2 * i + 1] : 0.0;
         const double f0 = force ? force[2 * i] : 0.0, f1 = force ? force[2 * i + 1] : 0.0;
-        const double nx = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(d0, dt)), dmul(f0, dt));
-        const double ny = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(d1, dt)), dmul(f1, dt));
+        double i0, i1;
+        force_increment(f0, f1, dt, tamed, i0, i1);
+        const double nx = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(d0, dt)), i0);
+        const double ny = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(d1, dt)), i1);
         store2(out, i, nx, ny);
     }
 }
@@ -57,15 +60,17 @@ __global__ void k_boundaries(P *__restrict__ x, P *__restrict__ anchor, long lon
 }
 
 int launch_em_step(cs_ctx *ctx, int prec, const void *pos, const double *D, const double *drift,
-                   const double *force, const void *xi, double dt, long long n, void *out) {
+                   const double *force, const void *xi, double dt, long long n, void *out,
+                   int tamed) {
     if (n == 0) return CS_OK;
     const int B = 256;
     if (prec == CS_F64)
         k_em_step<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
-            (const double *)pos, D, drift, force, (const double *)xi, dt, n, (double *)out);
+            (const double *)pos, D, drift, force, (const double *)xi, dt, n, (double *)out,
+            tamed);
     else
         k_em_step<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
-            (const float *)pos, D, drift, force, (const float *)xi, dt, n, (float *)out);
+            (const float *)pos, D, drift, force, (const float *)xi, dt, n, (float *)out, tamed);
     CS_LAUNCH_CHECK();
     return CS_OK;
 }

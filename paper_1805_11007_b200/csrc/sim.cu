@@ -73,7 +73,7 @@ struct UpdateArgs {
     long long n;
     double amp[2], dt, chi[2];
     int chi_pinned[2];
-    int refresh, store_samples, store_next;
+    int refresh, store_samples, store_next, tamed;
     cs_domain dom;
     GridGeom gg;
 };
@@ -123,8 +123,10 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, DevStatus *st, int
         load2(xi, i, x0, x1);
         const double amp = a.amp[t];
         double v[2];
-        v[0] = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(dr0, a.dt)), dmul(f0, a.dt));
-        v[1] = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(dr1, a.dt)), dmul(f1, a.dt));
+        double i0, i1;
+        force_increment(f0, f1, a.dt, a.tamed, i0, i1);
+        v[0] = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(dr0, a.dt)), i0);
+        v[1] = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(dr1, a.dt)), i1);
         if (!(isfinite(v[0]) && isfinite(v[1]))) {
             atomicMin(&st->key, err_key(0, i, CS_NONFINITE));
             st->abort = 1;
@@ -234,9 +236,10 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
         bool want_sorted = p->engine == CS_ENGINE_SORTED ||
                            (p->engine == CS_ENGINE_AUTO && p->prec == CS_F32 &&
                             !p->store_samples && !p->store_next && !p->react &&
+                            p->integrator == 0 &&
                             per_cell <= 4.0);
-        if (want_sorted && p->react) {
-            set_error("reactions run on the direct engine only");
+        if (want_sorted && (p->react || p->integrator != 0)) {
+            set_error("reactions and the tamed integrator run on the direct engine only");
             return CS_ERR_PARAM;
         }
         if (want_sorted && p->prec != CS_F32) {
@@ -458,6 +461,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         a.store_samples = (p.store_samples || (p.react && p.react_r_beta != 0.0)) && s->drift &&
                           s->local_c;
         a.store_next = p.store_next && s->next_pos;
+        a.tamed = p.integrator == 1;
         a.dom = p.domain;
         a.gg = sim->gg;
         if (n > 0) {

@@ -28,8 +28,8 @@ Reactions: the fixed scheduler runs on the device after
 the boundaries of every step (one rng_react.random(N) block per step, the
 reference's stream layout); the gillespie scheduler keeps the reference's
 host event clock and runs the Beta -> Alpha trials on the device.  Both run
-on the direct engine.  Out of scope: the hard-sphere interaction
-and the tamed integrator raise NotImplementedError.
+on the direct engine, as does the tamed integrator (motion.py:283-298).  Out of
+scope: the hard-sphere interaction raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -276,6 +276,7 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
     p.n_types = 2
     p.domain = N.domain_struct(domain.lo, domain.hi, domain.periodic)
     p.interaction = 1 if motion.interaction == "soft" else 0
+    p.integrator = 1 if getattr(motion, "integrator", "em") == "tamed" else 0
     if p.interaction:
         eps, cut, cell = motion.pair_table()
         p.pairs = N.pair_struct(eps, cut, cell)
@@ -421,8 +422,8 @@ class Realisation:
         self.step_index = 0
         self.reaction = config.reaction_params()
         self.reactions_active = self.reaction.r_alpha > 0 or self.reaction.r_beta > 0
-        if config.interaction == "hard" or config.integrator == "tamed":
-            raise NotImplementedError("hard-sphere / tamed motion is out of scope (SURVEY 8f)")
+        if config.interaction == "hard":
+            raise NotImplementedError("hard-sphere resolution is out of scope (SURVEY 8f)")
 
         host = init_population(config.n_alpha_0, config.n_beta_0, config.sigma, self.domain,
                                self.rng_init, alpha_init=config.alpha_init)

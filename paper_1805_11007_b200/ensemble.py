@@ -36,8 +36,8 @@ def supported(config) -> str | None:
     """None if the batched engine can run `config`, else the reason."""
     if config.precision != "fp64":
         return "precision must be fp64"
-    if config.interaction not in ("soft", "none") or config.integrator != "em":
-        return "hard-sphere / tamed motion"
+    if config.interaction not in ("soft", "none"):
+        return "hard-sphere motion"
     if config.engine == "sorted":
         return "engine='sorted' requested"
     r = config.reaction_params()

@@ -11,8 +11,9 @@ Extensions (additive keyword fields): per-type radii
 (``radius_alpha``/``radius_beta``) give the pair table eps_ij = (r_i+r_j)/2,
 cut_ij = cutoff_factor * eps_ij (BASELINE configs 2-4); with equal radii
 and cutoff_factor 2 it is bitwise the reference's homogeneous table.
-The hard-sphere and tamed integrators are out of scope
-and raise NotImplementedError.
+The tamed integrator (motion.py:283-298) runs on the device like em_step;
+the hard-sphere sweep is out of scope and raises
+NotImplementedError.
 """
 
 from __future__ import annotations
@@ -159,11 +160,7 @@ def soft_force_pairs(pop: Population, domain: Domain, params: MotionParams):
     return out[:cnt.value].cpu().numpy()
 
 
-def em_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=None):
-    """Euler--Maruyama proposal X + sqrt(2 D dt) xi + drift dt + force dt
-    (motion.py:268-282).  Draws exactly one standard-normal pair per
-    particle from `rng` (host numpy Generator, the reference contract), or
-    takes a pre-drawn `xi` array/tensor of the position's shape."""
+def _proposal(entry, position, diffusion, drift, force, dt, rng, xi):
     import torch
     single = (not A.is_tensor(position)) and np.asarray(position).ndim == 1
     host = not A.on_device(position)
@@ -172,7 +169,7 @@ def em_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=None):
     n = pos.shape[0]
     if xi is None:
         if rng is None:
-            raise ValueError("em_step needs an rng or a pre-drawn xi")
+            raise ValueError(f"{entry[3:]} needs an rng or a pre-drawn xi")
         xi = rng.standard_normal(tuple(pos.shape))
     xi_t = A.dev(xi, pdt).reshape(n, 2)
 
@@ -187,15 +184,26 @@ def em_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=None):
     drift_t = full(drift, (n, 2))
     force_t = full(force, (n, 2))
     out = A.empty((n, 2), pdt)
-    N.check(N.load_library().cs_em_step(N.context(), N.prec_code(pdt), N.ptr(pos), N.ptr(d_t),
-                                        N.ptr(drift_t), N.ptr(force_t), N.ptr(xi_t), float(dt),
-                                        n, N.ptr(out)), "cs_em_step")
+    N.check(getattr(N.load_library(), entry)(N.context(), N.prec_code(pdt), N.ptr(pos),
+                                             N.ptr(d_t), N.ptr(drift_t), N.ptr(force_t),
+                                             N.ptr(xi_t), float(dt), n, N.ptr(out)), entry)
     res = A.back(out, host)
     return res[0] if single else res
 
 
-def tamed_step(*args, **kwargs):  # pragma: no cover - out of scope
-    raise NotImplementedError("the tamed integrator is out of scope (SURVEY 8f)")
+def em_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=None):
+    """Euler--Maruyama proposal X + sqrt(2 D dt) xi + drift dt + force dt
+    (motion.py:268-282).  Draws exactly one standard-normal pair per
+    particle from `rng` (host numpy Generator, the reference contract), or
+    takes a pre-drawn `xi` array/tensor of the position's shape."""
+    return _proposal("cs_em_step", position, diffusion, drift, force, dt, rng, xi)
+
+
+def tamed_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=None):
+    """Tamed Euler proposal (motion.py:283-298): the interaction increment
+    force dt is scaled by 1 / (1 + ||force|| dt); one standard-normal pair
+    per particle as em_step."""
+    return _proposal("cs_tamed_step", position, diffusion, drift, force, dt, rng, xi)
 
 
 def resolve_hard_sphere(*args, **kwargs):  # pragma: no cover - out of scope

@@ -390,6 +390,32 @@ def reaction_trajectories():
     np.savez_compressed(os.path.join(OUT, "reaction_traj.npz"), **res)
 
 
+def tamed_cases():
+    """tamed_step on seeded inputs (force magnitudes from tiny to huge, so
+    the taming factor spans 1 .. ~0) and a fig1-like Realisation with the
+    tamed integrator."""
+    rng = np.random.default_rng(41)
+    n = 500
+    pos = rng.uniform(-0.5, 0.5, (n, 2))
+    dcoef = rng.choice([0.0, 0.1, 1.0], n)
+    drift = rng.normal(0.0, 1.0, (n, 2))
+    force = rng.normal(0.0, 1.0, (n, 2)) * 10.0 ** rng.uniform(-3, 6, (n, 1))
+    force[:3] = 0.0
+    dt = 1e-4
+    xi = np.random.default_rng(5).standard_normal((n, 2))
+    out = cs.tamed_step(pos, dcoef, drift, force, dt, np.random.default_rng(5))
+    res = dict(pos=pos, dcoef=dcoef, drift=drift, force=force, dt=np.array(dt), xi=xi, out=out)
+    cfg = cs.SimConfig(n_alpha_0=20, n_beta_0=20, t_final=1.0, seed_base=8, r_alpha=0.0,
+                       integrator="tamed", epsilon=0.05)
+    real = cs.Realisation(cfg, 0)
+    res["traj_pos0"] = real.pop.positions.copy()
+    for s in range(1, 21):
+        real.step()
+        if s in (1, 5, 20):
+            res[f"traj_pos{s}"] = real.pop.positions.copy()
+    np.savez_compressed(os.path.join(OUT, "tamed.npz"), **res)
+
+
 class _Replay:
     """Generator stand-in handing em_step a pre-drawn block."""
 
@@ -413,6 +439,7 @@ if __name__ == "__main__":
     composed_cfg2_small()
     reaction_cases()
     reaction_trajectories()
+    tamed_cases()
     for name in sorted(os.listdir(OUT)):
         if name.endswith(".npz"):
             print(name, os.path.getsize(os.path.join(OUT, name)))

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert {n for n, _, _ in N.SIGNATURES} == decl
-    assert lib.cs_abi_version() == 2
+    assert lib.cs_abi_version() == 3
 
 
 def test_struct_layouts_match_header():

@@ -125,3 +125,18 @@ def test_device_rng_ensemble_equals_host_rng_ensemble():
             torch.allclose(a.state[key], b.state[key], rtol=0, atol=1e-12), key
     a.close()
     b.close()
+
+
+def test_tamed_ensemble_tracks_realisations():
+    cfg = _quiet(samples=3, seed_base=8, r_alpha=0.0, integrator="tamed", epsilon=0.05,
+                 n_alpha_0=20, n_beta_0=20)
+    ens = Ensemble(cfg)
+    ens.advance(12)
+    ens.check()
+    pos = ens.state["pos"].cpu().numpy()
+    for s in range(3):
+        r = cs.Realisation(cfg, s)
+        for _ in range(12):
+            r.step()
+        np.testing.assert_allclose(pos[s], r.pop.positions, rtol=0, atol=1e-10)
+    ens.close()

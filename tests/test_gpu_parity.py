@@ -391,8 +391,6 @@ def test_realisation_errors_map_to_reference_exceptions():
 def test_out_of_scope_paths_fail_loudly():
     with pytest.raises(NotImplementedError):
         cs.Realisation(cs.SimConfig(interaction="hard"), 0)
-    with pytest.raises(NotImplementedError):
-        cs.Realisation(cs.SimConfig(integrator="tamed"), 0)
 
 
 def test_default_fig1_config_runs_on_the_device():

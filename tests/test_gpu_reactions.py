@@ -142,3 +142,29 @@ def test_run_blocks_equal_single_steps_with_reactions(scheduler):
     assert np.array_equal(a.pop.positions, b.pop.positions)
     assert np.array_equal(a.pop.species, b.pop.species)
     assert obs.counts[-1].sum() == 60
+
+
+def test_tamed_step_bitwise_vs_reference_golden():
+    g = load_golden("tamed.npz")
+    out = cs.tamed_step(g["pos"], g["dcoef"], g["drift"], g["force"], float(g["dt"]), xi=g["xi"])
+    assert np.array_equal(out, g["out"])
+    zero = cs.tamed_step(g["pos"], g["dcoef"], g["drift"], np.zeros_like(g["force"]),
+                         float(g["dt"]), xi=g["xi"])
+    assert np.array_equal(zero, cs.em_step(g["pos"], g["dcoef"], g["drift"],
+                                           np.zeros_like(g["force"]), float(g["dt"]),
+                                           xi=g["xi"]))
+
+
+def test_tamed_realisation_matches_reference_trajectory():
+    g = load_golden("tamed.npz")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        cfg = cs.SimConfig(n_alpha_0=20, n_beta_0=20, t_final=1.0, seed_base=8, r_alpha=0.0,
+                           integrator="tamed", epsilon=0.05)
+    real = cs.Realisation(cfg, 0)
+    assert np.array_equal(real.pop.positions, g["traj_pos0"])
+    for s in range(1, 21):
+        real.step()
+        if s in (1, 5, 20):
+            np.testing.assert_allclose(real.pop.positions, g[f"traj_pos{s}"], rtol=0,
+                                       atol=1e-10, err_msg=f"step {s}")

@@ -256,3 +256,10 @@ def test_rng_restatement_matches_numpy():
         b = np.array([p.standard_normal() for _ in range(60000)])
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), seed
         assert np.array_equal(g.random(500), np.array([p.next_double() for _ in range(500)]))
+
+
+def test_tamed_restatement_matches_reference_golden():
+    from oracle.react import tamed_step
+    g = load_golden("tamed.npz")
+    out = tamed_step(g["pos"], g["dcoef"], g["drift"], g["force"], g["xi"], float(g["dt"]))
+    assert np.array_equal(out, g["out"])

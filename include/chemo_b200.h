@@ -161,6 +161,14 @@ int cs_field_step(cs_field_ops *ops, void *c, const void *rho_a,
                   const void *rho_b, double k_alpha, double k_beta,
                   double gamma, int32_t *nonfinite, double *neg_mass);
 
+/* resolve_hard_sphere (motion.py:301-352) on proposals prop (n, 2) in
+ * place: the pairs closer than eps at the start, in ascending (i, j) order,
+ * each re-measured and pushed apart by 2 (eps - d) split by the
+ * diffusivities (type (n,) u8 or NULL = all Alpha). */
+int cs_resolve_hard_sphere(cs_ctx *ctx, int32_t prec, void *prop, const uint8_t *type,
+                           int64_t n, const cs_domain *dom, double eps, double d_alpha,
+                           double d_beta);
+
 /* y = exp(x) on the device with the glibc-exact restatement (test seam). */
 int cs_exp_batch(cs_ctx *ctx, const double *x, double *y, int64_t n);
 
@@ -209,6 +217,11 @@ typedef struct {
     double react_p_ab;       /* r_alpha * dt */
     double react_r_beta;     /* Beta -> Alpha rate per unit concentration */
     int32_t integrator;      /* 0 Euler-Maruyama, 1 tamed (motion.py:283-298) */
+    /* interaction 2 = hard spheres (motion.py:301-352): no soft forces; the
+     * proposals get one overlap-correction sweep before the boundaries.
+     * DIRECT engine, n <= 65536 (O(n^2) scan), next_pos required. */
+    double hard_eps;         /* the sphere diameter epsilon */
+    double diffusion[2];     /* D per type (the sweep's split) */
 } cs_sim_params;
 
 /* Engines.  DIRECT keeps the reference layout (rows in id order) and

@@ -50,7 +50,8 @@ class SimParams_t(ctypes.Structure):
                 ("kernel_cutoff", C_f64), ("secretes", C_i32 * 2), ("consumes", C_i32 * 2),
                 ("chi", C_f64 * 2), ("chi_pinned", C_i32 * 2), ("store_samples", C_i32),
                 ("store_next", C_i32), ("engine", C_i32), ("react", C_i32),
-                ("react_p_ab", C_f64), ("react_r_beta", C_f64), ("integrator", C_i32)]
+                ("react_p_ab", C_f64), ("react_r_beta", C_f64), ("integrator", C_i32),
+                ("hard_eps", C_f64), ("diffusion", C_f64 * 2)]
 
 
 class SimState_t(ctypes.Structure):
@@ -100,6 +101,8 @@ SIGNATURES = [
     ("cs_field_step", C_i32, [C_p, C_p, C_p, C_p, C_f64, C_f64, C_f64, ctypes.POINTER(C_i32),
                               ctypes.POINTER(C_f64)]),
     ("cs_exp_batch", C_i32, [C_p, C_p, C_p, C_i64]),
+    ("cs_resolve_hard_sphere", C_i32, [C_p, C_i32, C_p, C_p, C_i64, ctypes.POINTER(Domain_t),
+                                       C_f64, C_f64, C_f64]),
     ("cs_react", C_i32, [C_p, C_p, C_p, C_p, C_p, C_i64, C_f64, C_f64, C_f64,
                          ctypes.POINTER(C_i64), ctypes.POINTER(C_f64)]),
     ("cs_sim_create", C_i32, [C_p, ctypes.POINTER(SimParams_t), ctypes.POINTER(C_p)]),

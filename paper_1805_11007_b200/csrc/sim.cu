@@ -33,6 +33,8 @@ void field_ops_destroy(cs_field_ops *ops);
 int field_solve_rhs(cs_field_ops *ops, void *out);
 int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, double ka,
               double kb, double gamma, const DevStatus *st);
+int launch_hard_sphere(cs_ctx *ctx, int prec, void *prop, const uint8_t *type, long long n,
+                       const cs_domain &dom, double eps, const double D[2], int *n_hits_dev);
 int launch_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drift,
                  const double *u, long long n, double p_ab, double r_beta, double dt,
                  DevStatus *st);
@@ -73,7 +75,7 @@ struct UpdateArgs {
     long long n;
     double amp[2], dt, chi[2];
     int chi_pinned[2];
-    int refresh, store_samples, store_next, tamed;
+    int refresh, store_samples, store_next, tamed, propose_only;
     cs_domain dom;
     GridGeom gg;
 };
@@ -127,6 +129,10 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, DevStatus *st, int
         force_increment(f0, f1, a.dt, a.tamed, i0, i1);
         v[0] = dadd(dadd(dadd(x, dmul(amp, x0)), dmul(dr0, a.dt)), i0);
         v[1] = dadd(dadd(dadd(y, dmul(amp, x1)), dmul(dr1, a.dt)), i1);
+        if (a.propose_only) {  // hard spheres: the sweep comes before the boundaries
+            store2((P *)a.next, i, v[0], v[1]);
+            continue;
+        }
         if (!(isfinite(v[0]) && isfinite(v[1]))) {
             atomicMin(&st->key, err_key(0, i, CS_NONFINITE));
             st->abort = 1;
@@ -156,6 +162,41 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, DevStatus *st, int
         store2(anchor, i, an[0], an[1]);
     }
     if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
+}
+
+// apply_boundaries (motion.py:355-430) of the swept proposals and commit
+template <class P>
+__global__ void __launch_bounds__(256)
+k_commit(P *__restrict__ pos, P *__restrict__ anchor, const P *__restrict__ next, long long n,
+         cs_domain dom, DevStatus *st, int step) {
+    if (st->abort) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double v[2], an[2];
+        load2(next, i, v[0], v[1]);
+        if (!(isfinite(v[0]) && isfinite(v[1]))) {
+            atomicMin(&st->key, err_key(0, i, CS_NONFINITE));
+            st->abort = 1;
+            st->step = step;
+            continue;
+        }
+        load2(anchor, i, an[0], an[1]);
+        bool ok = true;
+        for (int ax = 0; ax < 2; ax++) {
+            const int code = boundary_axis(v[ax], an[ax], dom.lo[ax], dom.hi[ax],
+                                           dom.periodic[ax]);
+            if (code) {
+                atomicMin(&st->key, err_key(1 + ax, i, code));
+                st->abort = 1;
+                st->step = step;
+                ok = false;
+                break;
+            }
+        }
+        if (!ok) continue;
+        store2(pos, i, v[0], v[1]);
+        store2(anchor, i, an[0], an[1]);
+    }
 }
 
 }  // namespace cs
@@ -236,10 +277,10 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
         bool want_sorted = p->engine == CS_ENGINE_SORTED ||
                            (p->engine == CS_ENGINE_AUTO && p->prec == CS_F32 &&
                             !p->store_samples && !p->store_next && !p->react &&
-                            p->integrator == 0 &&
+                            p->integrator == 0 && p->interaction != 2 &&
                             per_cell <= 4.0);
-        if (want_sorted && (p->react || p->integrator != 0)) {
-            set_error("reactions and the tamed integrator run on the direct engine only");
+        if (want_sorted && (p->react || p->integrator != 0 || p->interaction == 2)) {
+            set_error("reactions, the tamed integrator and hard spheres run on the direct engine only");
             return CS_ERR_PARAM;
         }
         if (want_sorted && p->prec != CS_F32) {
@@ -326,6 +367,10 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
              const double *u, int64_t u_stride) {
     if (sim->p.react && !u) {
         set_error("params.react is set: the step needs the reaction uniforms (cs_sim_step_react)");
+        return CS_ERR_PARAM;
+    }
+    if (sim->p.interaction == 2 && (!s->next_pos || sim->p.n > 65536)) {
+        set_error("hard spheres need the next_pos buffer and n <= 65536");
         return CS_ERR_PARAM;
     }
     if (sim->p.react && !s->type) {
@@ -462,6 +507,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                           s->local_c;
         a.store_next = p.store_next && s->next_pos;
         a.tamed = p.integrator == 1;
+        a.propose_only = p.interaction == 2;
         a.dom = p.domain;
         a.gg = sim->gg;
         if (n > 0) {
@@ -471,6 +517,23 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 k_update<double><<<grid_for(n, B), B, 0, ctx->stream>>>(a, st, step);
             else
                 k_update<float><<<grid_for(n, B), B, 0, ctx->stream>>>(a, st, step);
+            CS_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        if (p.interaction == 2 && n > 0) {  // hard spheres (engine.py:384-386)
+            StageMark m(sim, CS_STAGE_UPDATE);
+            const double D[2] = {p.diffusion[0], p.diffusion[1]};
+            CS_TRY(launch_hard_sphere(ctx, p.prec, s->next_pos, s->type, n, p.domain, p.hard_eps, D,
+                                      nullptr));
+            const int B = 256;
+            if (p.prec == CS_F64)
+                k_commit<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
+                    (double *)s->pos, (double *)s->anchor, (const double *)s->next_pos, n,
+                    p.domain, st, step);
+            else
+                k_commit<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
+                    (float *)s->pos, (float *)s->anchor, (const float *)s->next_pos, n, p.domain,
+                    st, step);
             CS_LAUNCH_CHECK();
             ctx->launches += 1;
         }

@@ -28,8 +28,8 @@ Reactions: the fixed scheduler runs on the device after
 the boundaries of every step (one rng_react.random(N) block per step, the
 reference's stream layout); the gillespie scheduler keeps the reference's
 host event clock and runs the Beta -> Alpha trials on the device.  Both run
-on the direct engine, as does the tamed integrator (motion.py:283-298).  Out of
-scope: the hard-sphere interaction raises NotImplementedError.
+on the direct engine, as do the tamed integrator (motion.py:283-298) and the
+hard-sphere sweep (motion.py:301-352; O(N^2) scan, N <= 65536).
 """
 
 from __future__ import annotations
@@ -275,7 +275,9 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
     p.prec = prec
     p.n_types = 2
     p.domain = N.domain_struct(domain.lo, domain.hi, domain.periodic)
-    p.interaction = 1 if motion.interaction == "soft" else 0
+    p.interaction = {"soft": 1, "hard": 2}.get(motion.interaction, 0)
+    p.hard_eps = float(motion.epsilon)
+    p.diffusion[0], p.diffusion[1] = float(motion.d_alpha), float(motion.d_beta)
     p.integrator = 1 if getattr(motion, "integrator", "em") == "tamed" else 0
     if p.interaction:
         eps, cut, cell = motion.pair_table()
@@ -422,8 +424,6 @@ class Realisation:
         self.step_index = 0
         self.reaction = config.reaction_params()
         self.reactions_active = self.reaction.r_alpha > 0 or self.reaction.r_beta > 0
-        if config.interaction == "hard":
-            raise NotImplementedError("hard-sphere resolution is out of scope (SURVEY 8f)")
 
         host = init_population(config.n_alpha_0, config.n_beta_0, config.sigma, self.domain,
                                self.rng_init, alpha_init=config.alpha_init)
@@ -469,7 +469,7 @@ class Realisation:
         # fp64 keeps the reference's per-step drift / local_c / next_positions
         # stores; fp32 runs drop them so the sorted engine can be used
         self._stores = (config.precision == "fp64" or config.engine == "direct"
-                        or self.reactions_active)
+                        or self.reactions_active or config.interaction == "hard")
         params = sim_params_struct(
             n=len(host), prec=N.prec_code(dt_), domain=self.domain, motion=self.motion,
             dt=self.dt, field_active=self.field_active, refresh_active=self.refresh_active,

@@ -11,9 +11,8 @@ Extensions (additive keyword fields): per-type radii
 (``radius_alpha``/``radius_beta``) give the pair table eps_ij = (r_i+r_j)/2,
 cut_ij = cutoff_factor * eps_ij (BASELINE configs 2-4); with equal radii
 and cutoff_factor 2 it is bitwise the reference's homogeneous table.
-The tamed integrator (motion.py:283-298) runs on the device like em_step;
-the hard-sphere sweep is out of scope and raises
-NotImplementedError.
+The tamed integrator (motion.py:283-298) and the hard-sphere sweep
+(motion.py:301-352) run on the device.
 """
 
 from __future__ import annotations
@@ -206,8 +205,31 @@ def tamed_step(position, diffusion, drift, force, dt: float, rng=None, *, xi=Non
     return _proposal("cs_tamed_step", position, diffusion, drift, force, dt, rng, xi)
 
 
-def resolve_hard_sphere(*args, **kwargs):  # pragma: no cover - out of scope
-    raise NotImplementedError("hard-sphere resolution is out of scope (SURVEY 8f)")
+def resolve_hard_sphere(pop: Population, domain: Domain, params: MotionParams):
+    """Single overlap-correction sweep over the proposed positions
+    (motion.py:301-352), on the device: the pairs closer than epsilon at the
+    start of the sweep, in ascending (i, j) order, re-measured against the
+    current buffer and pushed apart along the centre line, split by the
+    diffusivities.  Updates pop.next_positions in place and returns it."""
+    prop = pop.next_positions
+    n = len(pop)
+    if n < 2:
+        return prop
+    host = not A.on_device(prop)
+    pdt = A.float_dtype_of(prop)
+    x = A.dev(prop, pdt)
+    import torch
+    sp = A.dev(pop.species, torch.uint8)
+    dom = N.domain_struct(domain.lo, domain.hi, domain.periodic)
+    N.check(N.load_library().cs_resolve_hard_sphere(
+        N.context(), N.prec_code(pdt), N.ptr(x), N.ptr(sp), n, ctypes.byref(dom),
+        float(params.epsilon), float(params.d_alpha), float(params.d_beta)),
+        "cs_resolve_hard_sphere")
+    if host:
+        prop[...] = x.cpu().numpy()
+    elif x.data_ptr() != prop.data_ptr():
+        prop.copy_(x)
+    return prop
 
 
 def raise_boundary_status(status: int, i: int, ax: int, x) -> None:

@@ -416,6 +416,43 @@ def tamed_cases():
     np.savez_compressed(os.path.join(OUT, "tamed.npz"), **res)
 
 
+def hard_sphere_cases():
+    """resolve_hard_sphere on seeded dense proposals (chains, immobile
+    partners, periodic seams, both species) and a Realisation with hard
+    spheres."""
+    rng = np.random.default_rng(61)
+    res = {}
+    cases = [(1.0, False, 0.02, 300), (1.0, True, 0.02, 300), (0.3, True, 0.03, 150),
+             (10.0, False, 0.02, 60)]
+    for k, (size, per, eps, n) in enumerate(cases):
+        domain = cs.Domain.square(size, periodic=per)
+        params = cs.MotionParams(epsilon=eps, d_alpha=rng.choice([0.0, 0.1]), d_beta=1.0,
+                                 dt=1e-7, interaction="hard")
+        pos = rng.uniform(-size / 2, size / 2, (n, 2))
+        if k == 3:  # overlapping chains along x
+            pos = np.stack([np.arange(n) * 0.9 * eps - 0.3, np.repeat([0.0, 0.011, -0.013], n // 3 + 1)[:n]], 1)
+        pos[:4] = pos[4:8] + 0.3 * eps  # guaranteed overlaps
+        species = rng.integers(0, 2, n).astype(np.uint8)
+        pop = mkpop(pos, species)
+        pop.next_positions[:] = pos + rng.normal(0, 0.2 * eps, (n, 2))
+        before = pop.next_positions.copy()
+        cs.resolve_hard_sphere(pop, domain, params)
+        res[f"h{k}_meta"] = np.array([size, per, eps, params.d_alpha, params.d_beta])
+        res[f"h{k}_species"] = species
+        res[f"h{k}_in"] = before
+        res[f"h{k}_out"] = pop.next_positions.copy()
+    res["n_cases"] = np.array(len(cases))
+    cfg = cs.SimConfig(n_alpha_0=30, n_beta_0=30, t_final=1.0, seed_base=9, r_alpha=0.0,
+                       interaction="hard", epsilon=0.05)
+    real = cs.Realisation(cfg, 0)
+    res["traj_pos0"] = real.pop.positions.copy()
+    for s_ in range(1, 21):
+        real.step()
+        if s_ in (1, 5, 20):
+            res[f"traj_pos{s_}"] = real.pop.positions.copy()
+    np.savez_compressed(os.path.join(OUT, "hard.npz"), **res)
+
+
 class _Replay:
     """Generator stand-in handing em_step a pre-drawn block."""
 
@@ -440,6 +477,7 @@ if __name__ == "__main__":
     reaction_cases()
     reaction_trajectories()
     tamed_cases()
+    hard_sphere_cases()
     for name in sorted(os.listdir(OUT)):
         if name.endswith(".npz"):
             print(name, os.path.getsize(os.path.join(OUT, name)))

@@ -388,9 +388,16 @@ def test_realisation_errors_map_to_reference_exceptions():
         real.step()
 
 
-def test_out_of_scope_paths_fail_loudly():
-    with pytest.raises(NotImplementedError):
-        cs.Realisation(cs.SimConfig(interaction="hard"), 0)
+def test_sorted_engine_refuses_what_it_cannot_run():
+    """Reactions, the tamed integrator and hard spheres run on the direct
+    engine; asking the sorted engine for them is a parameter error."""
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for kw in (dict(interaction="hard"), dict(integrator="tamed"), dict(r_alpha=5.0)):
+            cfg = cs.SimConfig(precision="fp32", engine="sorted", **{"r_alpha": 0.0, **kw})
+            with pytest.raises(N.NativeError, match="direct engine"):
+                cs.Realisation(cfg, 0)
 
 
 def test_default_fig1_config_runs_on_the_device():

@@ -168,3 +168,34 @@ def test_tamed_realisation_matches_reference_trajectory():
         if s in (1, 5, 20):
             np.testing.assert_allclose(real.pop.positions, g[f"traj_pos{s}"], rtol=0,
                                        atol=1e-10, err_msg=f"step {s}")
+
+
+def test_hard_sphere_sweep_bitwise_vs_reference_golden():
+    g = load_golden("hard.npz")
+    for k in range(int(g["n_cases"])):
+        size, per, eps, da, db = (float(v) for v in g[f"h{k}_meta"])
+        n = g[f"h{k}_in"].shape[0]
+        pop = cs.Population(ids=np.arange(n), positions=np.zeros((n, 2)),
+                            next_positions=g[f"h{k}_in"].copy(), species=g[f"h{k}_species"],
+                            drift=np.zeros((n, 2)), local_concentration=np.zeros(n),
+                            start_anchor=np.zeros((n, 2)))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            params = cs.MotionParams(epsilon=eps, d_alpha=da, d_beta=db, dt=1e-7,
+                                     interaction="hard")
+        cs.resolve_hard_sphere(pop, cs.Domain.square(size, periodic=bool(per)), params)
+        assert np.array_equal(pop.next_positions, g[f"h{k}_out"]), k
+
+
+def test_hard_sphere_realisation_matches_reference_trajectory():
+    g = load_golden("hard.npz")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        cfg = cs.SimConfig(n_alpha_0=30, n_beta_0=30, t_final=1.0, seed_base=9, r_alpha=0.0,
+                           interaction="hard", epsilon=0.05)
+    real = cs.Realisation(cfg, 0)
+    for s in range(1, 21):
+        real.step()
+        if s in (1, 5, 20):
+            np.testing.assert_allclose(real.pop.positions, g[f"traj_pos{s}"], rtol=0,
+                                       atol=1e-10, err_msg=f"step {s}")

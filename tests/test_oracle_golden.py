@@ -263,3 +263,13 @@ def test_tamed_restatement_matches_reference_golden():
     g = load_golden("tamed.npz")
     out = tamed_step(g["pos"], g["dcoef"], g["drift"], g["force"], g["xi"], float(g["dt"]))
     assert np.array_equal(out, g["out"])
+
+
+def test_hard_sphere_restatement_matches_reference_golden():
+    from oracle.hard import resolve_hard_sphere
+    g = load_golden("hard.npz")
+    for k in range(int(g["n_cases"])):
+        size, per, eps, da, db = g[f"h{k}_meta"]
+        out = resolve_hard_sphere(g[f"h{k}_in"], g[f"h{k}_species"], (size, size),
+                                  (bool(per), bool(per)), eps, da, db)
+        assert np.array_equal(out, g[f"h{k}_out"]), k

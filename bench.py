@@ -58,6 +58,22 @@ CONFIGS = {
                  field=True, boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=0.03,
                  gamma=0.1, secretes=(True, False), consumes=(False, True), c0="zero",
                  types="half"),
+    # cfg2's fp32 variant (BASELINE configs[2]: "fp64 and fp32 variants")
+    "cfg2f32": dict(n=100_000, n_c=512, prec="fp32", radii=(0.005, 0.01), D=(1.0, 0.5),
+                    chi=(1.0, -0.5), chi_pinned=(False, False), periodic=True, field=True,
+                    boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=0.03, gamma=0.1,
+                    secretes=(True, False), consumes=(False, True), c0="zero", types="half"),
+    # BASELINE configs[4] at one GPU (periodic, 64 seeded gaussian
+    # clusters, sigma 0.02, wrapped periodically).  Rates: cfg2's, except the
+    # consumption rate, scaled so that dt * k_beta * mean(rho_beta) equals
+    # cfg2's 0.015: with cfg2's k_beta the explicit consumption factor
+    # dt k_beta rho_beta reaches ~100 at the cluster nodes and the field step
+    # diverges (x10 per step, sign alternating), as it would in the reference
+    "cfg4": dict(n=80_000_000, n_c=8192, prec="fp32", radii=(2.1851e-5, 4.3702e-5),
+                 D=(1.0, 0.5), chi=(1.0, -0.5), chi_pinned=(False, False), periodic=True,
+                 field=True, boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=3.75e-5,
+                 gamma=0.1, secretes=(True, False), consumes=(False, True), c0="zero",
+                 types="half", init="clustered"),
 }
 DT = 1e-5
 SEED = 20241805
@@ -147,13 +163,28 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # setup
 # --------------------------------------------------------------------------
+def initial_positions(cfg: dict, rng) -> np.ndarray:
+    """Uniform in the centred unit square, or (cfg4) 64 seeded uniform centres,
+    each particle picking one uniformly, offset N(0, 0.02^2), wrapped
+    periodically into [-0.5, 0.5)."""
+    n = cfg["n"]
+    if cfg.get("init") == "clustered":
+        centres = -0.5 + rng.random((64, 2))
+        pos = centres[rng.integers(0, 64, n)]
+        pos += 0.02 * rng.standard_normal((n, 2))
+        pos = np.mod(pos + 0.5, 1.0) - 0.5
+        pos[pos >= 0.5] = -0.5
+        return pos
+    return (-0.5 + rng.random((n, 2))).astype(np.float64)
+
+
 def make_state(cfg: dict, rank: int):
     import torch
     import paper_1805_11007_b200 as cs
     n, n_c = cfg["n"], max(cfg["n_c"], 3)
     rng = np.random.default_rng(SEED + rank)
     dt_ = torch.float64 if cfg["prec"] == "fp64" else torch.float32
-    pos = (-0.5 + rng.random((n, 2))).astype(np.float64)
+    pos = initial_positions(cfg, rng)
     if cfg["types"] == "half":
         sp = (np.arange(n) >= n // 2).astype(np.uint8)
     else:
@@ -253,7 +284,7 @@ def oracle_sim(cfg: dict, pos, sp, nthreads: int):
 def run_oracle_steps(cfg, steps: int, warmup: int, budget_s: float, nthreads: int):
     rng = np.random.default_rng(SEED)
     n = cfg["n"]
-    pos = -0.5 + rng.random((n, 2))
+    pos = initial_positions(cfg, rng)
     sp = (np.arange(n) >= n // 2).astype(np.uint8) if cfg["types"] == "half" \
         else np.ones(n, np.uint8)
     if n < 100_000:

@@ -8,11 +8,12 @@
 //   k_bin_count    key[i] = f(pos[i]); counts[key]++           (atomics in L2)
 //   k_scan         starts = exclusive_scan(counts)             (single pass,
 //                  decoupled look-back; starts[nflat] = N)
-//   k_bin_scatter  slot = starts[key] + (--counts[key]); order[slot] = i
+//   k_bin_scatter  slot = starts[key] + (--counts[key]); slots[slot] = i
 //                  (the decrement leaves counts all-zero for the next step,
 //                  so no memset pass over the cell table is ever needed)
-//   k_seg_sort     restore ascending index inside each cell (cells hold a
-//                  handful of particles, insertion sort is exact and cheap)
+//   k_seg_rank     order[start + rank] = slots[t], rank = the number of the
+//                  cell's particles with a smaller index (ascending index
+//                  inside each cell, as the reference's stable sort)
 // The result is bit-identical to the reference's `order`/`starts`.
 #include "common.cuh"
 #include "scan.cuh"
@@ -36,33 +37,28 @@ __global__ void k_bin_count(const P *__restrict__ pos, long long n, BinGeom g,
 
 __global__ void k_bin_scatter(const int *__restrict__ keys, long long n,
                               const int *__restrict__ starts, int *__restrict__ counts,
-                              int *__restrict__ order, int *__restrict__ skeys) {
+                              int *__restrict__ slots) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int key = keys[i];
         const int slot = starts[key] + atomicSub(&counts[key], 1) - 1;
-        order[slot] = (int)i;
-        skeys[slot] = key;
+        slots[slot] = (int)i;
     }
 }
 
-__global__ void k_seg_sort(int *__restrict__ order, const int *__restrict__ skeys, long long n) {
+// Stable placement: the particle in slot t (cell order, arbitrary inside a
+// cell) goes to its cell start + the number of the cell's particles with a
+// smaller index (O(m) reads of the cell's L1-resident slots per particle).
+__global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict__ keys,
+                           const int *__restrict__ starts, long long n, int *__restrict__ order) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
-        const int key = skeys[t];
-        if (t > 0 && skeys[t - 1] == key) continue;
-        long long end = t + 1;
-        while (end < n && skeys[end] == key) end++;
-        if (end - t < 2) continue;
-        for (long long a = t + 1; a < end; a++) {
-            const int v = order[a];
-            long long b = a - 1;
-            while (b >= t && order[b] > v) {
-                order[b + 1] = order[b];
-                b--;
-            }
-            order[b + 1] = v;
-        }
+        const int v = slots[t];
+        const int key = keys[v];
+        const int s = starts[key], e = starts[key + 1];
+        int rank = 0;
+        for (int u = s; u < e; u++) rank += __ldg(slots + u) < v;
+        order[s + rank] = v;
     }
 }
 
@@ -114,10 +110,11 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
     }
     CS_TRY(exclusive_scan_i32(ctx, counts, starts, nflat));
     if (n > 0) {
-        k_bin_scatter<<<grid_for(n, B), B, 0, ctx->stream>>>(keys, n, starts, counts, order,
+        k_bin_scatter<<<grid_for(n, B), B, 0, ctx->stream>>>(keys, n, starts, counts,
                                                              ctx->skeys.as<int>());
         CS_LAUNCH_CHECK();
-        k_seg_sort<<<grid_for(n, B), B, 0, ctx->stream>>>(order, ctx->skeys.as<int>(), n);
+        k_seg_rank<<<grid_for(n, B), B, 0, ctx->stream>>>(ctx->skeys.as<int>(), keys, starts, n,
+                                                          order);
         CS_LAUNCH_CHECK();
     }
     ctx->launches += 3;

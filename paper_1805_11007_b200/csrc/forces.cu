@@ -14,28 +14,169 @@
 // storage is widened to binary64 on load (the fp32 variants compute on the
 // stored binary32 values exactly as the fp64 oracle would).
 //
-// One thread per sorted slot: consecutive threads handle particles of the
+// One lane per sorted slot: consecutive lanes handle particles of the
 // same/adjacent cells, so neighbour reads are shared through L1/L2.
 #include "common.cuh"
 
 namespace cs {
 
+// Direct-engine pair forces, warp-compacted.  Lane = owner particle (slot
+// t of the cell order).  The lane's ring is flattened into one candidate
+// sequence in the reference order (o1 outer, o0 inner with the periodic
+// de-duplication, ascending index in a cell) and the warp walks it with a
+// uniform trip count; an accepted pair stores (dx0, dx1, r2, pair type) in the
+// lane's shared-memory buffer.  Whenever a lane's buffer is full (and at the
+// end), the warp evaluates all buffered pairs together, one per lane (the
+// binary64 sqrt / exp / divisions run on full warps instead of on the ~20 %
+// of lanes that accept in a given step), and each owner then adds its terms
+// in buffer order = candidate order.  Same arithmetic as pair_loop: bitwise
+// equal to the reference.  The minimum image skips the division when
+// |dx| <= L/2 (then rint(dx / L) = +-0 and dx - L * (+-0) == dx).
+constexpr int DF_WARPS = 4;
+constexpr int DF_BUF = 8;
+
+struct DfBuf {
+    double dx[32 * DF_BUF], dy[32 * DF_BUF], r2[32 * DF_BUF];
+    unsigned char tt[32 * DF_BUF];
+    int base[33];
+};
+
+__device__ __forceinline__ double df_min_image(double dx, double size) {
+    if (fabs(dx) <= 0.5 * size) return dx;
+    return dsub(dx, dmul(size, rint(ddiv(dx, size))));
+}
+
+// evaluate every buffered pair of the warp, then each owner adds its terms
+__device__ __forceinline__ void df_flush(DfBuf &B, const PairTab &pt, int lane, int &pend,
+                                         double &fx, double &fy) {
+    // exclusive prefix of the lanes' counts
+    int inc = pend;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    B.base[lane] = inc - pend;
+    if (lane == 31) B.base[32] = inc;
+    __syncwarp();
+    const int total = B.base[32];
+    for (int e = lane; e < total; e += 32) {
+        int lo = 0, hi = 31;  // owner: the last lane with base <= e
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (B.base[mid] <= e) lo = mid;
+            else hi = mid - 1;
+        }
+        const int q = lo * DF_BUF + (e - B.base[lo]);
+        const double r2 = B.r2[q];
+        const double eps = pt.eps[B.tt[q]];
+        const double r = dsqrt(r2);
+        const double sc = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
+        B.dx[q] = dmul(sc, B.dx[q]);
+        B.dy[q] = dmul(sc, B.dy[q]);
+    }
+    __syncwarp();
+    for (int u = 0; u < pend; u++) {
+        fx = dadd(fx, B.dx[lane * DF_BUF + u]);
+        fy = dadd(fy, B.dy[lane * DF_BUF + u]);
+    }
+    pend = 0;
+    __syncwarp();
+}
+
 template <class P>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * DF_WARPS)
 k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,
               const int *__restrict__ order, const int *__restrict__ starts, long long n,
               BinGeom g, PairTab pt, double *__restrict__ out, const DevStatus *st) {
     if (st && st->abort) return;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int i = order[t];
+    __shared__ DfBuf bufs[DF_WARPS];
+    DfBuf &B = bufs[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const long long wstride = (long long)gridDim.x * blockDim.x;
+    for (long long base = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); base < n;
+         base += wstride) {
+        const long long t = base + lane;
+        const bool live = t < n;
+        int i = 0, ti = 0, cx = 0, cy = 0, tot = 0;
+        double xi = 0.0, yi = 0.0;
+        // the lane's valid ring cells in reference order, as (start, end)
+        int cs_[9], ce_[9], nc = 0;
+        if (live) {
+            i = order[t];
+            load2(pos, i, xi, yi);
+            cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
+            cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
+            ti = type ? (int)type[i] : 0;
+#pragma unroll
+            for (int c9 = 0; c9 < 9; c9++) {
+                const int o1 = c9 / 3 - 1, o0 = c9 % 3 - 1;
+                int g1 = cy + o1, g0 = cx + o0;
+                bool ok = true;
+                if (g.per1) {
+                    if ((g.n1 == 1 && o1 != 0) || (g.n1 == 2 && o1 == 1)) ok = false;
+                    g1 = g1 < 0 ? g1 + g.n1 : (g1 >= g.n1 ? g1 - g.n1 : g1);
+                } else if (g1 < 0 || g1 >= g.n1) {
+                    ok = false;
+                }
+                if (g.per0) {
+                    if ((g.n0 == 1 && o0 != 0) || (g.n0 == 2 && o0 == 1)) ok = false;
+                    g0 = g0 < 0 ? g0 + g.n0 : (g0 >= g.n0 ? g0 - g.n0 : g0);
+                } else if (g0 < 0 || g0 >= g.n0) {
+                    ok = false;
+                }
+                cs_[c9] = 0;
+                ce_[c9] = 0;
+                if (ok) {
+                    const int f = g1 * g.n0 + g0;
+                    cs_[c9] = starts[f];
+                    ce_[c9] = starts[f + 1];
+                    tot += ce_[c9] - cs_[c9];
+                }
+            }
+        }
+        (void)nc;
+        const int totmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
         double fx = 0.0, fy = 0.0;
-        pair_loop(pos, type, order, starts, g, pt, i,
-                  [&](int, double s, double dx0, double dx1) {
-                      fx = dadd(fx, dmul(s, dx0));
-                      fy = dadd(fy, dmul(s, dx1));
-                  });
-        reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
+        int pend = 0;
+        int c9 = 0, k = cs_[0], kend = ce_[0];
+#pragma unroll 1
+        for (int jj = 0; jj < totmax; jj++) {
+            bool acc = false;
+            if (jj < tot) {
+                while (k == kend) {  // next non-empty ring cell
+                    c9++;
+                    k = c9 == 1 ? cs_[1] : c9 == 2 ? cs_[2] : c9 == 3 ? cs_[3] : c9 == 4 ? cs_[4]
+                      : c9 == 5 ? cs_[5] : c9 == 6 ? cs_[6] : c9 == 7 ? cs_[7] : cs_[8];
+                    kend = c9 == 1 ? ce_[1] : c9 == 2 ? ce_[2] : c9 == 3 ? ce_[3] : c9 == 4 ? ce_[4]
+                         : c9 == 5 ? ce_[5] : c9 == 6 ? ce_[6] : c9 == 7 ? ce_[7] : ce_[8];
+                }
+                const int j = order[k++];
+                if (j != i) {
+                    double xj, yj;
+                    load2(pos, j, xj, yj);
+                    double dx0 = dsub(xj, xi);
+                    double dx1 = dsub(yj, yi);
+                    if (g.per0) dx0 = df_min_image(dx0, g.size0);
+                    if (g.per1) dx1 = df_min_image(dx1, g.size1);
+                    const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                    const int tt = ti * 2 + (type ? (int)type[j] : 0);
+                    if (!(r2 > pt.cut2[tt] || r2 == 0.0)) {
+                        const int q = lane * DF_BUF + pend;
+                        B.dx[q] = dx0;
+                        B.dy[q] = dx1;
+                        B.r2[q] = r2;
+                        B.tt[q] = (unsigned char)tt;
+                        pend++;
+                        acc = true;
+                    }
+                }
+            }
+            (void)acc;
+            if (__any_sync(0xffffffffu, pend == DF_BUF)) df_flush(B, pt, lane, pend, fx, fy);
+        }
+        if (__any_sync(0xffffffffu, pend > 0)) df_flush(B, pt, lane, pend, fx, fy);
+        if (live) reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
     }
 }
 
@@ -73,7 +214,7 @@ int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *ty
                        long long n, const BinGeom &g, const PairTab &pt, double *out,
                        const DevStatus *st) {
     if (n == 0) return CS_OK;
-    const int B = 256;
+    const int B = 32 * DF_WARPS;
     const int *order = ctx->order.as<int>(), *starts = ctx->starts.as<int>();
     if (prec == CS_F64)
         k_soft_forces<double><<<grid_for(n, B), B, 0, ctx->stream>>>(

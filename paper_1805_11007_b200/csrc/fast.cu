@@ -79,6 +79,8 @@ struct FastArgs {
     int *fill;          // records claimed per sub-bucket (zeroed by the bucket scan)
     long long cap;      // slots per sub-bucket region
     double2 *force;     // pair force per sorted slot (binary64)
+    int *gen;           // slots the force kernel defers to k_fast_forces_generic
+    int *gen_count;     // gen[0, *gen_count); reset by k_fast_update
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
                         // 2 skip deposits, 64 no pair terms, 128 no candidate walk, 4 store records at the slot index
                         // without claims, 8 the same plus a fire-and-forget
@@ -374,7 +376,7 @@ struct WarpQueue {
 //     and x + 0.0 == x);
 //  3. each owner adds its terms in j order = canonical order.
 // Ring cells on a periodic seam or a wall, axes with < 5 cells, and lanes
-// with > ACC_MAX hits take the generic walk (ring_forces_generic) instead.
+// with > ACC_MAX hits are deferred to k_fast_forces_generic (generic walk).
 __global__ void __launch_bounds__(128, 5)  // 96 regs: measured best (4: 560, 6: 513 us)
 k_fast_forces(const DevStatus *st) {
     const FastArgs &a = cA;
@@ -479,10 +481,10 @@ k_fast_forces(const DevStatus *st) {
         }
         if (nacc > ACC_MAX) generic = true;  // its queued terms are computed, not used
         if (generic) {
-            const double2 ff = ring_forces_generic(rec, a.starts, t, xf, yf, x, y, cx, cy, n0,
-                                                   n1, make_pair_row(ti));
-            fx = ff.x;
-            fy = ff.y;
+            // deferred to k_fast_forces_generic (seam / wall / dense owners:
+            // ~0.15 % at cfg3), so that no warp of this kernel serialises on
+            // one lane's generic walk
+            a.gen[atomicAdd(a.gen_count, 1)] = t32;
             nacc = 0;
         }
         // ---- 2. queue evaluation
@@ -515,7 +517,25 @@ k_fast_forces(const DevStatus *st) {
             }
             __syncwarp();
         }
-        if (live) a.force[t] = make_double2(fx, fy);
+        if (live && !generic) a.force[t] = make_double2(fx, fy);
+    }
+}
+
+// The owners k_fast_forces deferred: the generic per-cell ring walk
+// (reference order, exact arithmetic), one lane each.
+__global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st) {
+    const FastArgs &a = cA;
+    if (st->abort != 0) return;
+    const int cnt = *a.gen_count;
+    const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+        const int t = a.gen[q];
+        const float4 me = __ldg(rec + t);
+        const double x = (double)me.x, y = (double)me.y;
+        const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, a.g.n0);
+        const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, a.g.n1);
+        a.force[t] = ring_forces_generic(rec, a.starts, t, me.x, me.y, x, y, cx, cy, a.g.n0,
+                                         a.g.n1, make_pair_row((int)(__float_as_uint(me.z) >> 31)));
     }
 }
 
@@ -539,6 +559,7 @@ __device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, in
 __global__ void __launch_bounds__(256, CS_UPDATE_MINB)
 k_fast_update(DevStatus *st, int step) {
     const FastArgs &a = cA;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.gen_count = 0;  // k_fast_forces_generic has run
     const bool dead = st->abort != 0;
     const int m = a.gg.n * a.gg.n;
     const int n0 = a.g.n0, n1 = a.g.n1;
@@ -1071,7 +1092,7 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 constexpr int STARTS_OFF = 0;
 
 struct cs_fast {
-    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec;
+    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec, gen;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
@@ -1120,6 +1141,8 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->rec[1].ensure(nr));
     CS_TRY(f->region.ensure(sizeof(Rec) * (size_t)f->nbucket * SUBB * (size_t)f->cap));
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(f->gen.ensure(sizeof(int) * (size_t)(n + 1 > 1 ? n + 1 : 2)));  // list + counter
+    CS_CUDA(cudaMemset(f->gen.p, 0, f->gen.bytes));
     CS_TRY(f->fill.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 1)));
     CS_CUDA(cudaMemset(f->fill.p, 0, f->fill.bytes));
     CS_TRY(f->boff.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 4)));
@@ -1139,7 +1162,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
-                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec})
+                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec, &f->gen})
         b->release();
     delete f;
 }
@@ -1316,6 +1339,8 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.fill = f->fill.as<int>();
     a.cap = f->cap;
     a.force = f->force.as<double2>();
+    a.gen_count = f->gen.as<int>();
+    a.gen = f->gen.as<int>() + 1;
     {
         const char *dbg = getenv("CS_FAST_DEBUG");
         a.debug = dbg ? atoi(dbg) : 0;
@@ -1372,7 +1397,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         if (a.interact && (part & 1)) {
             k_fast_forces<<<grid, 128, 0, ctx->stream>>>(st);
             CS_LAUNCH_CHECK();
-            ctx->launches += 1;
+            k_fast_forces_generic<<<sms * 4, 128, 0, ctx->stream>>>(st);
+            CS_LAUNCH_CHECK();
+            ctx->launches += 2;
         }
         if (!(part & 2)) return CS_OK;
         // persistent grid: one contiguous processing front, so the atomics'

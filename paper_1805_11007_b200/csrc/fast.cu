@@ -521,21 +521,98 @@ k_fast_forces(const DevStatus *st) {
     }
 }
 
-// The owners k_fast_forces deferred: the generic per-cell ring walk
-// (reference order, exact arithmetic), one lane each.
+// The owners k_fast_forces deferred (seam / wall / small-grid / dense): a
+// warp per owner, lane c9 < 9 walks ring cell c9 (reference order o1 outer,
+// o0 inner, with the periodic de-duplication and wall skips of
+// motion.py:206-222).  Records inside a cell are in ascending id, so a
+// lane's accepted pairs are already in the reference order; the exact test
+// (pair_test: minimum image with rint) and the pair term are the reference's.
+// Lane 0 then adds the terms cell by cell.  A cell with more than GEN_K
+// accepted pairs sends the owner through ring_forces_generic instead.
+constexpr int GEN_K = 8;
 __global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st) {
     const FastArgs &a = cA;
     if (st->abort != 0) return;
     const int cnt = *a.gen_count;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int n0 = a.g.n0, n1 = a.g.n1;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < cnt;
+         q += (gridDim.x * blockDim.x) >> 5) {
         const int t = a.gen[q];
         const float4 me = __ldg(rec + t);
         const double x = (double)me.x, y = (double)me.y;
-        const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, a.g.n0);
-        const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, a.g.n1);
-        a.force[t] = ring_forces_generic(rec, a.starts, t, me.x, me.y, x, y, cx, cy, a.g.n0,
-                                         a.g.n1, make_pair_row((int)(__float_as_uint(me.z) >> 31)));
+        const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
+        const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
+        const PairRow pr = make_pair_row((int)(__float_as_uint(me.z) >> 31));
+        double tx[GEN_K], ty[GEN_K];
+        int nt = 0;
+        bool over = false;
+        if (lane < 9) {
+            const int o1 = lane / 3 - 1, o0 = lane % 3 - 1;
+            int g1 = cy + o1, g0 = cx + o0;
+            bool ok = true;
+            if (a.g.per1) {
+                if ((n1 == 1 && o1 != 0) || (n1 == 2 && o1 == 1)) ok = false;
+                g1 = g1 < 0 ? g1 + n1 : (g1 >= n1 ? g1 - n1 : g1);
+            } else if (g1 < 0 || g1 >= n1) {
+                ok = false;
+            }
+            if (a.g.per0) {
+                if ((n0 == 1 && o0 != 0) || (n0 == 2 && o0 == 1)) ok = false;
+                g0 = g0 < 0 ? g0 + n0 : (g0 >= n0 ? g0 - n0 : g0);
+            } else if (g0 < 0 || g0 >= n0) {
+                ok = false;
+            }
+            if (ok) {
+                const int f = g1 * n0 + g0;
+                const int kb = a.starts[f], ke = a.starts[f + 1];
+                for (int k = kb; k < ke; k++) {
+                    if (k == t) continue;
+                    const float4 r = __ldg(rec + k);
+                    const int tj = (int)(__float_as_uint(r.z) >> 31);
+                    double d0, d1;
+                    const double r2 = pair_test(r.x, r.y, me.x, me.y, x, y, pr.cf(tj),
+                                                pr.cut2(tj), d0, d1);
+                    if (r2 > 0.0) {
+                        if (nt == GEN_K) {
+                            over = true;
+                            break;
+                        }
+                        const double2 tv = pair_term(d0, d1, r2, pr.eps(tj));
+#pragma unroll
+                        for (int u = 0; u < GEN_K; u++)
+                            if (u == nt) {
+                                tx[u] = tv.x;
+                                ty[u] = tv.y;
+                            }
+                        nt++;
+                    }
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, over)) {
+            if (lane == 0)
+                a.force[t] = ring_forces_generic(rec, a.starts, t, me.x, me.y, x, y, cx, cy, n0,
+                                                 n1, pr);
+            continue;
+        }
+        double fx = 0.0, fy = 0.0;
+        const int ntmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nt);
+        for (int c9 = 0; c9 < 9; c9++) {
+            const int m = __shfl_sync(0xffffffffu, nt, c9);
+#pragma unroll
+            for (int u = 0; u < GEN_K; u++) {
+                if (u >= ntmax) break;
+                const double vx = __shfl_sync(0xffffffffu, tx[u], c9);
+                const double vy = __shfl_sync(0xffffffffu, ty[u], c9);
+                if (u < m) {
+                    fx = dadd(fx, vx);
+                    fy = dadd(fy, vy);
+                }
+            }
+        }
+        if (lane == 0) a.force[t] = make_double2(fx, fy);
     }
 }
 
@@ -1397,7 +1474,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         if (a.interact && (part & 1)) {
             k_fast_forces<<<grid, 128, 0, ctx->stream>>>(st);
             CS_LAUNCH_CHECK();
-            k_fast_forces_generic<<<sms * 4, 128, 0, ctx->stream>>>(st);
+            k_fast_forces_generic<<<sms * 16, 128, 0, ctx->stream>>>(st);
             CS_LAUNCH_CHECK();
             ctx->launches += 2;
         }

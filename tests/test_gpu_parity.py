@@ -92,6 +92,32 @@ def test_pair_sets_bit_exact_hetero(periodic):
     assert np.array_equal(f, f_or)
 
 
+@pytest.mark.parametrize("case", ["cfg2_periodic", "cfg2_walls", "dense_ring", "two_cells"])
+def test_dense_cell_forces_bitwise(case):
+    """Dense cell lists: BASELINE cfg2's density (~40 particles per cell,
+    ~360 ring candidates, ~75 accepted pairs per particle, periodic and
+    walled), ~1500-candidate rings, and 2-cell periodic axes (ring
+    de-duplication), bitwise against the oracle."""
+    rng = np.random.default_rng({"cfg2_periodic": 21, "cfg2_walls": 22, "dense_ring": 23,
+                                 "two_cells": 24}[case])
+    periodic = case != "cfg2_walls"
+    if case == "dense_ring":
+        n, radii = 24000, (0.02, 0.04)
+    elif case == "two_cells":  # 2 x 2 cells of side 0.5
+        n, radii = 600, (0.1, 0.25)
+    else:
+        n, radii = 100_000, (0.005, 0.01)
+    pos = rng.uniform(-0.5, 0.5, (n, 2))
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    params = _params(radii[0], 2 * radii[0], radius_alpha=radii[0], radius_beta=radii[1])
+    dom = cs.Domain.square(1.0, periodic=periodic)
+    f = cs.soft_forces(_pop(pos, sp), dom, params)
+    e, c, cell = params.pair_table()
+    ref = oracle.soft_forces(pos, dom.lo, dom.size, dom.periodic, e, c, cell, types=sp,
+                             nthreads=os.cpu_count() or 1)
+    assert np.array_equal(f, ref)
+
+
 def test_forces_fp32_storage_bitwise_vs_fp64_oracle_on_binary32_values():
     rng = np.random.default_rng(13)
     n = 20000

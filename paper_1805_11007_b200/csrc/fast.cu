@@ -286,11 +286,21 @@ __device__ __noinline__ Cic cic_stencil(double x, double y, GridGeom gg, ExactDi
     return c;
 }
 
-__device__ __forceinline__ void cic_deposit_q(const Cic &c, int *__restrict__ out) {
-    atomicAdd(&out[c.i00], __double2int_rn(dmul(c.w00, Q_SCALE)));
-    atomicAdd(&out[c.i10], __double2int_rn(dmul(c.w10, Q_SCALE)));
-    atomicAdd(&out[c.i01], __double2int_rn(dmul(c.w01, Q_SCALE)));
-    atomicAdd(&out[c.i11], __double2int_rn(dmul(c.w11, Q_SCALE)));
+// add of a fixed-point mass (>= 0; a non-finite coordinate, reported by the
+// update, gives INT_MIN); true when it pushes the sum past INT_MAX
+__device__ __forceinline__ bool add_overflows(int *p, int q) {
+    const int old = atomicAdd(p, q);
+    return q > 0 && old > INT_MAX - q;
+}
+
+// CIC deposit of one particle mass (int32 fixed point) with exact overflow
+// detection
+__device__ __forceinline__ bool cic_deposit_q(const Cic &c, int *__restrict__ out) {
+    bool ovf = add_overflows(&out[c.i00], __double2int_rn(dmul(c.w00, Q_SCALE)));
+    ovf |= add_overflows(&out[c.i10], __double2int_rn(dmul(c.w10, Q_SCALE)));
+    ovf |= add_overflows(&out[c.i01], __double2int_rn(dmul(c.w01, Q_SCALE)));
+    ovf |= add_overflows(&out[c.i11], __double2int_rn(dmul(c.w11, Q_SCALE)));
+    return ovf;
 }
 
 __device__ __forceinline__ PairRow make_pair_row(int ti) {
@@ -832,11 +842,13 @@ __global__ void k_fast_import(const float *__restrict__ pos, const float *__rest
     }
 }
 
-__device__ __noinline__ void deposit_record(float4 rv, GridGeom gg, ExactDiv d0, ExactDiv d1,
+__device__ __noinline__ bool deposit_record(float4 rv, GridGeom gg, ExactDiv d0, ExactDiv d1,
                                             unsigned bits, int *rho_q, int m) {
     const Cic c = cic_stencil((double)rv.x, (double)rv.y, gg, d0, d1);
-    if (bits & 1u) cic_deposit_q(c, rho_q);
-    if (bits & 2u) cic_deposit_q(c, rho_q + m);
+    bool ovf = false;
+    if (bits & 1u) ovf |= cic_deposit_q(c, rho_q);
+    if (bits & 2u) ovf |= cic_deposit_q(c, rho_q + m);
+    return ovf;
 }
 
 // Bucket sort: one block per bucket of BUCKET_CELLS consecutive cells (flat,
@@ -853,14 +865,15 @@ __device__ __noinline__ void deposit_record(float4 rv, GridGeom gg, ExactDiv d0,
 //      id-sorted inside a cell, and contiguous;
 //   4. (atomic deposit mode) CIC-deposits the bucket's records: neighbouring
 //      cells, so the integer reductions stay L2-local and deterministic.
-// A cell more populated than the int32 fixed-point deposit can sum exactly
-// stops the run with CS_DEPOSIT_OVERFLOW.
+// A deposit add that overflows the int32 fixed-point sum stops the run with
+// CS_DEPOSIT_OVERFLOW (checked on every add here; the row deposit checks its
+// adds once a cell exceeds the conservative population bound cell_max).
 __global__ void __launch_bounds__(BSORT_THREADS)
 k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long long cap,
               long long nbucket, BinGeom g, ExactDiv eff0, ExactDiv eff1, long long nflat,
               Rec *__restrict__ out, int *__restrict__ starts, GridGeom gg, ExactDiv d0,
               ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q, int deposit,
-              int cell_max, DevStatus *st, int step) {
+              int cell_max, int *__restrict__ dep_exact, DevStatus *st, int step) {
     // [SUBB cap] ids by slot, then codes (cell | arrival << 10 | part << 25) of
     // the records beyond the register-resident ones
     extern __shared__ int s_dyn[];
@@ -969,10 +982,8 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
         for (int k = 0; k < 4; k++) {
             if (cv[k] > cell_max && cfirst + k < nflat) {
                 // a grid node could collect more particle masses of 2^22 than
-                // an int32 sums exactly
-                atomicMin(&st->key, err_key(3, cfirst + k, CS_DEPOSIT_OVERFLOW));
-                st->abort = 1;
-                st->step = step;
+                // an int32 sums exactly: the row deposit checks every add
+                *dep_exact = 1;
             }
         }
     }
@@ -1019,7 +1030,12 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
         reinterpret_cast<float4 *>(out)[off + kb + rank] = r;
         if (bits_dep) {
             const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
-            if (bits) deposit_record(r, gg, d0, d1, bits, rho_q, gg.n * gg.n);
+            if (bits && deposit_record(r, gg, d0, d1, bits, rho_q, gg.n * gg.n)) {
+                atomicMin(&st->key, err_key(3, __float_as_uint(r.z) & ID_MASK,
+                                            CS_DEPOSIT_OVERFLOW));
+                st->abort = 1;
+                st->step = step;
+            }
         }
     };
 #pragma unroll
@@ -1047,8 +1063,15 @@ constexpr int DEP_ROWS = CS_DEP_ROWS;  // grid rows per block of k_fast_deposit_
 __global__ void __launch_bounds__(512)
 k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts, BinGeom g,
                     GridGeom gg, ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
-                    int *__restrict__ rho_q) {
+                    int *__restrict__ rho_q, const int *__restrict__ exact_flag,
+                    int *__restrict__ other_flag, DevStatus *st, int step) {
     extern __shared__ int acc[];  // [DEP_ROWS][2][n]
+    // exact overflow checks only when the bucket sort saw a cell populated
+    // beyond the conservative bound (returning atomics cost ~20 % here)
+    const bool exact = *exact_flag != 0;
+    __shared__ int ovf_node;
+    if (threadIdx.x == 0) ovf_node = -1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *other_flag = 0;  // the next step's flag
     const int n = gg.n, j0 = blockIdx.x * DEP_ROWS;
     const long long m = (long long)n * n;
     for (int i = threadIdx.x; i < DEP_ROWS * 2 * n; i += blockDim.x) acc[i] = 0;
@@ -1094,18 +1117,36 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
                 const int qa = __double2int_rn(dmul(dmul(g0, wy), Q_SCALE));
                 const int qb = __double2int_rn(dmul(dmul(f0, wy), Q_SCALE));
                 int *row = acc + (h ? rc : rb) * 2 * n;
-                if (bits & 1u) {
-                    atomicAdd(&row[b0], qa);
-                    atomicAdd(&row[c0], qb);
-                }
-                if (bits & 2u) {
-                    atomicAdd(&row[n + b0], qa);
-                    atomicAdd(&row[n + c0], qb);
+                if (exact) {
+                    bool ovf = false;
+                    if (bits & 1u) {
+                        ovf |= add_overflows(&row[b0], qa);
+                        ovf |= add_overflows(&row[c0], qb);
+                    }
+                    if (bits & 2u) {
+                        ovf |= add_overflows(&row[n + b0], qa);
+                        ovf |= add_overflows(&row[n + c0], qb);
+                    }
+                    if (ovf) ovf_node = (j0 + (h ? rc : rb)) * n + b0;
+                } else {
+                    if (bits & 1u) {
+                        atomicAdd(&row[b0], qa);
+                        atomicAdd(&row[c0], qb);
+                    }
+                    if (bits & 2u) {
+                        atomicAdd(&row[n + b0], qa);
+                        atomicAdd(&row[n + c0], qb);
+                    }
                 }
             }
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0 && ovf_node >= 0) {
+        atomicMin(&st->key, err_key(3, ovf_node, CS_DEPOSIT_OVERFLOW));
+        st->abort = 1;
+        st->step = step;
+    }
     for (int r = 0; r < DEP_ROWS; r++) {
         const int j = j0 + r;
         if (j >= n) break;
@@ -1169,7 +1210,7 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 constexpr int STARTS_OFF = 0;
 
 struct cs_fast {
-    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec, gen;
+    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec, gen, depflag;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
@@ -1220,6 +1261,8 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->gen.ensure(sizeof(int) * (size_t)(n + 1 > 1 ? n + 1 : 2)));  // list + counter
     CS_CUDA(cudaMemset(f->gen.p, 0, f->gen.bytes));
+    CS_TRY(f->depflag.ensure(sizeof(int) * 2));  // exact-deposit flags by step parity
+    CS_CUDA(cudaMemset(f->depflag.p, 0, f->depflag.bytes));
     CS_TRY(f->fill.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 1)));
     CS_CUDA(cudaMemset(f->fill.p, 0, f->fill.bytes));
     CS_TRY(f->boff.ensure(sizeof(int) * (size_t)(f->nbucket * SUBB + 4)));
@@ -1239,7 +1282,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
-                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec, &f->gen})
+                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec, &f->gen, &f->depflag})
         b->release();
     delete f;
 }
@@ -1291,8 +1334,8 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const Grid
         make_exact_div(f->g.eff0), make_exact_div(f->g.eff1), f->nflat, f->rec[nxt].as<Rec>(),
         cell_table(f, nxt), gg, make_exact_div(d0), make_exact_div(d1), dep ? bits[0] : 0u,
         dep ? bits[1] : 0u, f->rho_q.as<int>(), dep && !f->gather,
-        dep && (bits[0] | bits[1]) ? deposit_cell_max(gg, f) : 0, st,
-        step);
+        dep && f->gather && (bits[0] | bits[1]) ? deposit_cell_max(gg, f) : 0,
+        f->depflag.as<int>() + (step & 1), st, step);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     f->cur = nxt;
@@ -1301,7 +1344,8 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const Grid
 
 // periodic grids: the next step's deposit gathered per grid row
 static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
-                             const GridGeom &gg, const unsigned char bits[3]) {
+                             const GridGeom &gg, const unsigned char bits[3], DevStatus *st,
+                             int step) {
     const char *dbg = getenv("CS_FAST_DEBUG");
     const int debug = dbg ? atoi(dbg) : 0;
     if (p.n <= 0 || !p.field_active || (debug & 2) || !f->gather) return CS_OK;
@@ -1315,7 +1359,8 @@ static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
     }
     k_fast_deposit_rows<<<(gg.n + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
         f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
-        make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>());
+        make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>(),
+        f->depflag.as<int>() + (step & 1), f->depflag.as<int>() + ((step + 1) & 1), st, step);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;
@@ -1335,7 +1380,7 @@ int fast_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     if (p.field_active && !f->gather)
         CS_CUDA(cudaMemsetAsync(f->rho_q.p, 0, f->rho_q.bytes, ctx->stream));
     CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
-    CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits));
+    CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits, st, step));
     f->imported = true;
     return CS_OK;
 }
@@ -1501,7 +1546,7 @@ int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, co
                 const unsigned char bits[3], int part, DevStatus *st, int step) {
     (void)n;
     if (part & 1) CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
-    if (part & 2) CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits));
+    if (part & 2) CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits, st, step));
     return CS_OK;
 }
 

@@ -206,22 +206,44 @@ def test_vectorized_periodic_gradient_bitwise_equals_generic(monkeypatch):
         assert torch.equal(out["vec"][k], out["generic"][k]), k
 
 
-def test_sorted_engine_reports_fixed_point_deposit_overflow():
-    """A cell holding more particles than the int32 fixed-point deposit can
-    sum exactly (511 masses of 2^22 per grid node) stops the sorted engine with
-    CS_DEPOSIT_OVERFLOW instead of wrapping silently."""
+@pytest.mark.parametrize("mode", ["rows", "atomic"])
+def test_sorted_engine_reports_fixed_point_deposit_overflow(mode, monkeypatch):
+    """A grid node collecting more particle masses than the int32 fixed-point
+    deposit sums exactly (2^31 / 2^22 = 511 masses) stops the sorted engine
+    with CS_DEPOSIT_OVERFLOW instead of wrapping silently: 600 particles
+    sitting exactly on one node overflow it, 500 do not (the row-gathered
+    deposit of periodic grids switches to checked adds once a cell exceeds
+    the conservative bound; the atomic deposit checks every add)."""
     n, n_c = 20_000, 256
+    if mode == "atomic":
+        monkeypatch.setenv("CS_ATOMIC_DEPOSIT", "1")
+    else:
+        monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
     pos, sp, xi = _inputs(n, 4)
-    # 200 particles in one cell; here a node's CIC support spans 2 x 2 cells
-    # (grid spacing 1/256 < cell side 0.008), so the limit is 511 / 4 = 127
-    pos[:200] = np.float32(0.1)
+    sp[:] = 0  # every particle secretes into rho_alpha
+    node = np.float32(-0.5 + 154.0 / 256.0)  # a grid node, exact in binary32
+    pos[:600] = node
     a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c)
     a.step(torch.as_tensor(xi[0], device="cuda"), 1)
-    st = a.status()
-    assert st.code == cs._native.CS_DEPOSIT_OVERFLOW
-    b, sb = _sim(pos[200:], sp[200:], engine="sorted", field=True, n_c=n_c)
-    b.step(torch.as_tensor(xi[0, 200:], device="cuda"), 1)
+    assert a.status().code == cs._native.CS_DEPOSIT_OVERFLOW
+    b, sb = _sim(pos[100:], sp[100:], engine="sorted", field=True, n_c=n_c)
+    b.step(torch.as_tensor(xi[0, 100:], device="cuda"), 1)
     assert b.status().code == 0
+    monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
+
+
+def test_sorted_engine_dense_cells_below_the_node_limit_run():
+    """Cells above the conservative population bound whose nodes stay below
+    511 masses (coarse grid, fine cells: the bound is 511 / 81 = 6 per cell
+    here) run, with the checked row deposit equal to the atomic one."""
+    n, n_c = 4000, 64
+    pos, sp, xi = _inputs(n, 5)
+    pos[:40] = np.float32(0.1)  # 40 particles in one cell
+    x = torch.as_tensor(xi, device="cuda")
+    a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c, radii=(0.002, 0.002))
+    a.step(x, 3)
+    a.export_state()
+    assert a.status().code == 0
 
 
 def test_row_gather_deposit_bitwise_equals_atomic_deposit(monkeypatch):

@@ -143,3 +143,26 @@ def test_exponential_waiting_time_and_event_clock_match_reference_golden():
         assert np.array_equal(pop.species, r[f"clock_species_{until}"]), until
     assert np.array_equal(np.array(times), r["clock_times"])
     assert np.array_equal(np.array(fired), r["clock_fired"])
+
+
+def test_t4_reference_fixture_and_statistics_helper():
+    """The T4 fixture (tests/golden/make_t4.py, the reference's own
+    ensemble) holds 64 samples of every statistic, and the statistics helper
+    counts pairs / MSD / field moments as defined (small known case)."""
+    import os
+    import sys
+    import numpy as np
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from t4_stats import NAMES, compare, sample_stats
+    g = np.load(os.path.join(here, "t4_reference.npz"))
+    assert g["stats"].shape == (64, len(NAMES))
+    assert list(g["names"]) == NAMES
+    pos = np.array([[0.0, 0.0], [0.003, 0.0], [0.4999, 0.1], [-0.4999, 0.1]])
+    st = sample_stats(pos, np.zeros_like(pos), np.array([0, 0, 1, 1]), np.ones(4),
+                      np.full(4, 0.25), 1.0, 0.004)
+    assert st[NAMES.index("pairs")] == 2  # one direct pair, one across the periodic seam
+    assert st[NAMES.index("mass")] == 1.0 and abs(st[NAMES.index("l2")] - 1.0) < 1e-15
+    assert abs(st[NAMES.index("msd_alpha")] - 0.003 ** 2 / 2) < 1e-18
+    z, *_ = compare(g["stats"], g["stats"])
+    assert np.all(z == 0)

@@ -489,8 +489,47 @@ k_gemm(const double *__restrict__ A, const double *__restrict__ B, const double 
         }
 }
 
+// Small grids (n <= 256): 16x16 output tiles, one output per thread, so that
+// a 128^2 solve spreads over 64 SMs instead of 4.  Same k-ordered fma chain
+// per output as k_gemm (bitwise equal).
+template <bool TB, class O>
+__global__ void __launch_bounds__(256)
+k_gemm16(const double *__restrict__ A, const double *__restrict__ B, const double *__restrict__ E,
+         O *__restrict__ C, int n) {
+    __shared__ double As[16][17];
+    __shared__ double Bs[16][17];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int r = blockIdx.y * 16 + ty, cc = blockIdx.x * 16 + tx;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < n; k0 += 16) {
+        const int ra = blockIdx.y * 16 + ty, ka = k0 + tx;
+        As[ty][tx] = (ra < n && ka < n) ? A[(long long)ra * n + ka] : 0.0;
+        const int kb = k0 + ty, cb = blockIdx.x * 16 + tx;
+        double bv = 0.0;
+        if (kb < n && cb < n) bv = TB ? B[(long long)cb * n + kb] : B[(long long)kb * n + cb];
+        Bs[ty][tx] = bv;
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; kk++) acc = fma(As[ty][kk], Bs[kk][tx], acc);  // zero padding as k_gemm
+        __syncthreads();
+    }
+    if (r < n && cc < n) {
+        double val = acc;
+        if (E) val *= E[(long long)r * n + cc];
+        C[(long long)r * n + cc] = (O)val;
+    }
+}
+
 template <class O>
 int gemm(cs_ctx *ctx, const double *A, const double *B, bool tb, const double *E, O *C, int n) {
+    if (n <= 256) {
+        dim3 grid16((n + 15) / 16, (n + 15) / 16);
+        if (tb) k_gemm16<true, O><<<grid16, 256, 0, ctx->stream>>>(A, B, E, C, n);
+        else k_gemm16<false, O><<<grid16, 256, 0, ctx->stream>>>(A, B, E, C, n);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+        return CS_OK;
+    }
     dim3 grid((n + 63) / 64, (n + 63) / 64);
     if (tb) k_gemm<true, O><<<grid, 256, 0, ctx->stream>>>(A, B, E, C, n);
     else k_gemm<false, O><<<grid, 256, 0, ctx->stream>>>(A, B, E, C, n);

@@ -108,6 +108,33 @@ int cs_soft_force_pairs(cs_ctx *ctx, int32_t prec, const void *pos,
                         const cs_pair_params *pp, int64_t *pairs, int64_t cap,
                         int64_t *count);
 
+/* The reference's CellIndex (spatial_index.py:71-122): bucket (n, 2)
+ * positions into cells of side >= cell_side (n_cells = max(1,
+ * floor(size / cell_side)) per axis, closed upper edge).  Outputs: cell_xy
+ * (n, 2) int32, order (n) int32 (ascending id inside a cell), starts
+ * (n_cells_x * n_cells_y + 1) int32; n_cells (2) int32. */
+int cs_cell_index(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n,
+                  const cs_domain *dom, double cell_side, int32_t *cell_xy,
+                  int32_t *order, int32_t *starts, int32_t *n_cells);
+
+/* The reference's accumulate_forces (motion.py:107-161): soft pair forces
+ * over an index built with any cell side (ring reach ceil(cutoff / eff)
+ * per axis, the whole axis once 2 reach + 1 >= n on a periodic axis), single
+ * epsilon / cutoff; same summation order and arithmetic.  out (n, 2) f64. */
+int cs_index_forces(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n,
+                    const int32_t *cell_xy, const int32_t *order,
+                    const int32_t *starts, const cs_domain *dom,
+                    const int32_t *n_cells, double epsilon, double cutoff,
+                    double *out);
+
+/* The reference's deposit_gather (coupling.py:190-213): node-centric
+ * gaussian deposit, every node against every particle in index order (the
+ * cross-check of the scatter path).  pos (n, 2) of the selected species in
+ * prec; span = grid hi - lo (the periodic image span); out (n_c^2) f64. */
+int cs_deposit_gather(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n,
+                      const cs_grid *grid, double span0, double span1, double h,
+                      double cutoff, double *out);
+
 /* out = ((pos + sqrt((2 D) dt) xi) + drift dt) + force dt; pos/xi/out in
  * prec, diffusion (n) f64, drift/force (n, 2) f64 (NULL = zero). */
 int cs_em_step(cs_ctx *ctx, int32_t prec, const void *pos,

@@ -85,6 +85,12 @@ SIGNATURES = [
     ("cs_soft_force_pairs", C_i32, [C_p, C_i32, C_p, C_p, C_i64, ctypes.POINTER(Domain_t),
                                     ctypes.POINTER(PairParams_t), C_p, C_i64,
                                     ctypes.POINTER(C_i64)]),
+    ("cs_cell_index", C_i32, [C_p, C_i32, C_p, C_i64, ctypes.POINTER(Domain_t), C_f64, C_p,
+                              C_p, C_p, C_p]),
+    ("cs_index_forces", C_i32, [C_p, C_i32, C_p, C_i64, C_p, C_p, C_p,
+                                ctypes.POINTER(Domain_t), C_p, C_f64, C_f64, C_p]),
+    ("cs_deposit_gather", C_i32, [C_p, C_i32, C_p, C_i64, ctypes.POINTER(Grid_t), C_f64, C_f64,
+                                  C_f64, C_f64, C_p]),
     ("cs_em_step", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_p, C_p, C_f64, C_i64, C_p]),
     ("cs_tamed_step", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_p, C_p, C_f64, C_i64, C_p]),
     ("cs_apply_boundaries", C_i32, [C_p, C_i32, C_p, C_p, C_p, C_i64, ctypes.POINTER(Domain_t),

@@ -70,6 +70,27 @@ def deposit(pop: Population, grid: Grid, kernel: Kernel, species: Species):
     return _deposit(pop, grid, kernel, route, two=False)
 
 
+def deposit_gather(pop: Population, grid: Grid, kernel: Kernel, species: Species):
+    """Node-centric reference deposit, gaussian only (coupling.py:190-213):
+    every node against every particle of `species` in index order, on the
+    device (the cross-check of the scatter path; O(N n_c^2))."""
+    import torch
+    if kernel.kind != "gaussian":
+        raise ValueError("gather reference is defined for the gaussian kernel")
+    host = not A.on_device(pop.positions)
+    pdt = A.float_dtype_of(pop.positions)
+    pos = A.dev(pop.positions, pdt)
+    sel = A.dev(pop.species, torch.uint8) == int(species)
+    pos = pos[sel].contiguous()
+    out = A.zeros(grid.n_c * grid.n_c, torch.float64)
+    span = np.asarray(grid.hi, dtype=float) - np.asarray(grid.lo, dtype=float)
+    N.check(N.load_library().cs_deposit_gather(
+        N.context(), N.prec_code(pdt), N.ptr(pos), pos.shape[0], ctypes.byref(N.grid_struct(grid)),
+        float(span[0]), float(span[1]), float(kernel.h), float(kernel.cutoff), N.ptr(out)),
+        "cs_deposit_gather")
+    return A.back(out, host)
+
+
 def deposit_both(pop: Population, grid: Grid, kernel: Kernel):
     """(rho_alpha, rho_beta) from one particle sweep (coupling.py:165-187)."""
     return _deposit(pop, grid, kernel, pop.species, two=True)

@@ -257,6 +257,54 @@ int cs_apply_boundaries(cs_ctx *ctx, int32_t prec, void *x, void *anchor, void *
     return CS_OK;
 }
 
+int cs_cell_index(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n, const cs_domain *dom,
+                  double cell_side, int32_t *cell_xy, int32_t *order, int32_t *starts,
+                  int32_t *n_cells) {
+    CS_TRY(check_prec(prec));
+    if (!(cell_side > 0.0)) {
+        set_error("cell_side must be positive");
+        return CS_ERR_PARAM;
+    }
+    const BinGeom g = make_geom(*dom, cell_side);
+    CS_TRY(bin_particles(ctx, prec, pos, n, g));
+    const long long nflat = (long long)g.n0 * g.n1;
+    if (n > 0)
+        CS_CUDA(cudaMemcpyAsync(order, ctx->order.p, sizeof(int) * (size_t)n,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(starts, ctx->starts.p, sizeof(int) * (size_t)(nflat + 1),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    CS_TRY(launch_cell_xy(ctx, prec, pos, n, g, cell_xy));
+    n_cells[0] = g.n0;
+    n_cells[1] = g.n1;
+    return CS_OK;
+}
+
+int cs_index_forces(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n, const int32_t *cell_xy,
+                    const int32_t *order, const int32_t *starts, const cs_domain *dom,
+                    const int32_t *n_cells, double epsilon, double cutoff, double *out) {
+    CS_TRY(check_prec(prec));
+    if (!(epsilon > 0.0) || !(cutoff > 0.0) || n_cells[0] < 1 || n_cells[1] < 1) {
+        set_error("epsilon, cutoff and the cell counts must be positive");
+        return CS_ERR_PARAM;
+    }
+    const double lx = dom->hi[0] - dom->lo[0], ly = dom->hi[1] - dom->lo[1];
+    return launch_index_forces(ctx, prec, pos, n, cell_xy, order, starts, n_cells[0], n_cells[1],
+                               lx / n_cells[0], ly / n_cells[1], dom->periodic[0] != 0,
+                               dom->periodic[1] != 0, lx, ly, epsilon, cutoff, out);
+}
+
+int cs_deposit_gather(cs_ctx *ctx, int32_t prec, const void *pos, int64_t n, const cs_grid *grid,
+                      double span0, double span1, double h, double cutoff, double *out) {
+    CS_TRY(check_prec(prec));
+    if (!(h > 0) || !(cutoff > 0)) {
+        set_error("kernel bandwidth and cutoff must be positive");
+        return CS_ERR_PARAM;
+    }
+    const GridGeom gg = make_grid_geom(*grid);
+    const double inv_norm = 1.0 / ((2.0 * M_PI) * (h * h));  // coupling.py:204
+    return launch_deposit_gather(ctx, prec, pos, n, gg, span0, span1, h, cutoff, inv_norm, out);
+}
+
 int cs_deposit(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *route, int64_t n,
                const cs_grid *grid, int32_t kind, double h, double cutoff, void *rho_a,
                void *rho_b) {

@@ -310,6 +310,16 @@ int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n,
 int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,
                        long long n, const BinGeom &g, const PairTab &pt, double *out,
                        const DevStatus *st);
+int launch_cell_xy(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
+                   int *out);
+int launch_index_forces(cs_ctx *ctx, int prec, const void *pos, long long n, const int *cxy,
+                        const int *order, const int *starts, int ncx, int ncy, double effx,
+                        double effy, int perx, int pery, double lx, double ly, double eps,
+                        double cutoff, double *out);
+// field.cu
+int launch_deposit_gather(cs_ctx *ctx, int prec, const void *pos, long long np,
+                          const GridGeom &gg, double spanx, double spany, double h, double cutoff,
+                          double inv_norm, double *out);
 // motion.cu / field.cu / sim.cu
 int record_error(cs_ctx *ctx);
 int run_soft_force_pairs(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,

@@ -437,6 +437,55 @@ __global__ void k_rhs(const G *__restrict__ c, const G *__restrict__ ra, const G
     }
 }
 
+// ------------------------------------------------------------------ gather
+// deposit_gather (coupling.py:190-213): node l (x fastest, field.py:62-66)
+// against every selected particle in index order; d = node - p, minimum
+// image on a periodic grid, r2 = d0^2 + d1^2, out += inv_norm *
+// exp(-r2 / (2 h^2)) when r2 <= cutoff^2 (the reference's numpy exp is its
+// SIMD variant: 1-ulp differences from the glibc exp used here).
+template <class P>
+__global__ void k_deposit_gather(const P *__restrict__ pos, long long np, GridGeom gg,
+                                 double spanx, double spany, double h, double cutoff,
+                                 double inv_norm, double *__restrict__ out) {
+    const long long m = (long long)gg.n * gg.n;
+    const double c2 = dmul(cutoff, cutoff);
+    const double den = dmul(2.0, dmul(h, h));
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+         l += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(l % gg.n), j = (int)(l / gg.n);
+        const double nx = dadd(gg.lo0, dmul((double)i, gg.d0));
+        const double ny = dadd(gg.lo1, dmul((double)j, gg.d1));
+        double acc = 0.0;
+        for (long long p = 0; p < np; p++) {
+            double px, py;
+            load2(pos, p, px, py);
+            double d0 = dsub(nx, px), d1 = dsub(ny, py);
+            if (gg.per) {
+                d0 = dsub(d0, dmul(spanx, rint(ddiv(d0, spanx))));
+                d1 = dsub(d1, dmul(spany, rint(ddiv(d1, spany))));
+            }
+            const double r2 = dadd(dmul(d0, d0), dmul(d1, d1));
+            if (r2 <= c2) acc = dadd(acc, dmul(inv_norm, cs_exp(ddiv(-r2, den))));
+        }
+        out[l] = acc;
+    }
+}
+
+int launch_deposit_gather(cs_ctx *ctx, int prec, const void *pos, long long np,
+                          const GridGeom &gg, double spanx, double spany, double h, double cutoff,
+                          double inv_norm, double *out) {
+    const long long m = (long long)gg.n * gg.n;
+    if (prec == CS_F64)
+        k_deposit_gather<double><<<grid_for(m, 128), 128, 0, ctx->stream>>>(
+            static_cast<const double *>(pos), np, gg, spanx, spany, h, cutoff, inv_norm, out);
+    else
+        k_deposit_gather<float><<<grid_for(m, 128), 128, 0, ctx->stream>>>(
+            static_cast<const float *>(pos), np, gg, spanx, spany, h, cutoff, inv_norm, out);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
 // ------------------------------------------------------------------ GEMM
 // C = A * op(B) (row-major n x n fp64), op = transpose when TB; optional
 // element-wise scale by E; output to O.  64x64 tiles, 256 threads, 4x4 per

@@ -210,6 +210,109 @@ __global__ void k_fill_pairs(const P *__restrict__ pos, const uint8_t *__restric
     }
 }
 
+// ---------------------------------------------------------------- CellIndex
+// cell_xy of every particle (spatial_index.py:113-115: floor((p - lo) / eff),
+// clipped to the closed upper edge) -- the binning bins.cu does, exported
+template <class P>
+__global__ void k_cell_xy(const P *__restrict__ pos, long long n, BinGeom g, int *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double x, y;
+        load2(pos, i, x, y);
+        out[2 * i] = cell_axis(x, g.lo0, g.eff0, g.n0);
+        out[2 * i + 1] = cell_axis(y, g.lo1, g.eff1, g.n1);
+    }
+}
+
+// accumulate_forces / _soft_forces (motion.py:107-143): per particle, the
+// axis cells of _axis_cells (motion.py:91-104) -- reach r = ceil(cutoff /
+// eff); a periodic axis with 2 r + 1 >= n is visited once, 0 .. n-1;
+// otherwise centre - r .. centre + r, wrapped (periodic) or clipped -- y
+// outer, x inner, members in index order; reference arithmetic throughout.
+template <class P>
+__global__ void k_index_forces(const P *__restrict__ pos, long long n, const int *__restrict__ cxy,
+                               const int *__restrict__ order, const int *__restrict__ starts,
+                               int ncx, int ncy, double effx, double effy, int perx, int pery,
+                               double lx, double ly, double eps, double cutoff,
+                               double *__restrict__ out) {
+    const double cut2 = dmul(cutoff, cutoff);
+    const int rx = (int)ceil(ddiv(cutoff, effx)), ry = (int)ceil(ddiv(cutoff, effy));
+    const bool allx = perx && 2 * rx + 1 >= ncx, ally = pery && 2 * ry + 1 >= ncy;
+    const int nx_it = allx ? ncx : 2 * rx + 1, ny_it = ally ? ncy : 2 * ry + 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double xi, yi;
+        load2(pos, i, xi, yi);
+        const int cxi = cxy[2 * i], cyi = cxy[2 * i + 1];
+        double fx = 0.0, fy = 0.0;
+        for (int a = 0; a < ny_it; a++) {
+            int gy = a;
+            if (!ally) {
+                gy = cyi - ry + a;
+                if (pery) gy = (int)pymod(gy, ncy);
+                else if (gy < 0 || gy >= ncy) continue;
+            }
+            for (int b = 0; b < nx_it; b++) {
+                int gx = b;
+                if (!allx) {
+                    gx = cxi - rx + b;
+                    if (perx) gx = (int)pymod(gx, ncx);
+                    else if (gx < 0 || gx >= ncx) continue;
+                }
+                const int f = gy * ncx + gx;
+                for (int k = starts[f]; k < starts[f + 1]; k++) {
+                    const int j = order[k];
+                    if (j == i) continue;
+                    double xj, yj;
+                    load2(pos, j, xj, yj);
+                    double dx0 = dsub(xj, xi), dx1 = dsub(yj, yi);
+                    if (perx) dx0 = dsub(dx0, dmul(lx, rint(ddiv(dx0, lx))));
+                    if (pery) dx1 = dsub(dx1, dmul(ly, rint(ddiv(dx1, ly))));
+                    const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                    if (r2 > cut2 || r2 == 0.0) continue;
+                    const double r = dsqrt(r2);
+                    const double sc = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
+                    fx = dadd(fx, dmul(sc, dx0));
+                    fy = dadd(fy, dmul(sc, dx1));
+                }
+            }
+        }
+        reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
+    }
+}
+
+int launch_cell_xy(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
+                   int *out) {
+    if (n == 0) return CS_OK;
+    if (prec == CS_F64)
+        k_cell_xy<double><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+            static_cast<const double *>(pos), n, g, out);
+    else
+        k_cell_xy<float><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+            static_cast<const float *>(pos), n, g, out);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+int launch_index_forces(cs_ctx *ctx, int prec, const void *pos, long long n, const int *cxy,
+                        const int *order, const int *starts, int ncx, int ncy, double effx,
+                        double effy, int perx, int pery, double lx, double ly, double eps,
+                        double cutoff, double *out) {
+    if (n == 0) return CS_OK;
+    if (prec == CS_F64)
+        k_index_forces<double><<<grid_for(n, 128), 128, 0, ctx->stream>>>(
+            static_cast<const double *>(pos), n, cxy, order, starts, ncx, ncy, effx, effy, perx,
+            pery, lx, ly, eps, cutoff, out);
+    else
+        k_index_forces<float><<<grid_for(n, 128), 128, 0, ctx->stream>>>(
+            static_cast<const float *>(pos), n, cxy, order, starts, ncx, ncy, effx, effy, perx,
+            pery, lx, ly, eps, cutoff, out);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
 int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type,
                        long long n, const BinGeom &g, const PairTab &pt, double *out,
                        const DevStatus *st) {

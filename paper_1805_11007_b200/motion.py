@@ -139,6 +139,27 @@ def soft_forces(pop: Population, domain: Domain, params: MotionParams):
     return A.back(out, host)
 
 
+def accumulate_forces(pop: Population, index, params: MotionParams):
+    """Sum of pair_force over all neighbours within params.cutoff, per
+    particle, through a CellIndex (motion.py:146-161, _soft_forces :107-143):
+    any cell side (ring reach ceil(cutoff / eff) per axis), single epsilon and
+    cutoff, the reference's summation order and arithmetic, on the device."""
+    import torch
+    host = not A.on_device(pop.positions)
+    d = index._dev
+    pos_t = d["pos"]
+    n = pos_t.shape[0]
+    out = A.empty((n, 2), torch.float64)
+    nc = (ctypes.c_int32 * 2)(int(index.n_cells[0]), int(index.n_cells[1]))
+    dom = index.domain
+    N.check(N.load_library().cs_index_forces(
+        N.context(), N.prec_code(pos_t.dtype), N.ptr(pos_t), n, N.ptr(d["cell_xy"]),
+        N.ptr(d["order"]), N.ptr(d["starts"]),
+        ctypes.byref(N.domain_struct(dom.lo, dom.hi, dom.periodic)), nc,
+        float(params.epsilon), float(params.cutoff), N.ptr(out)), "cs_index_forces")
+    return A.back(out, host)
+
+
 def soft_force_pairs(pop: Population, domain: Domain, params: MotionParams):
     """(P, 2) int64 pairs (i, j) the force kernel accumulates, in its
     accumulation order (i ascending, ring cell, j ascending): the bit-exact

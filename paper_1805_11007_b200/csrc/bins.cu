@@ -15,6 +15,8 @@
 //                  cell's particles with a smaller index (ascending index
 //                  inside each cell, as the reference's stable sort)
 // The result is bit-identical to the reference's `order`/`starts`.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -62,6 +64,86 @@ __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict_
     }
 }
 
+// Small systems (cfg0: 10^3 particles, 10^4 cells) are launch-bound: one
+// 1024-thread block does the whole sweep in shared memory -- keys and
+// histogram, exclusive scan into `starts`, an unordered placement by
+// shared-memory claims, then the stable order: each particle goes to its
+// cell start + the number of the cell's particles with a smaller index
+// (as k_seg_rank).  Same order / starts as the multi-kernel path.
+constexpr int BIN_SMALL_THREADS = 1024;
+constexpr int BIN_SMALL_MAX_CELLS = 12 * 1024;
+constexpr long long BIN_SMALL_MAX_N = 12 * 1024;
+
+template <class P>
+__global__ void __launch_bounds__(BIN_SMALL_THREADS)
+k_bin_small(const P *__restrict__ pos, int n, BinGeom g, int *__restrict__ starts,
+            int *__restrict__ order) {
+    extern __shared__ int sm[];
+    const int nflat = g.n0 * g.n1;
+    int *cnt = sm;                 // nflat + 1: counts, then starts
+    int *fill = cnt + nflat + 1;   // nflat: claim cursors
+    int *keys = fill + nflat;      // n
+    int *slots = keys + n;         // n: particle of each slot, unordered in a cell
+    __shared__ int wsum[BIN_SMALL_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int c = tid; c <= nflat; c += BIN_SMALL_THREADS) cnt[c] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += BIN_SMALL_THREADS) {
+        double x, y;
+        load2(pos, i, x, y);
+        const int key = cell_axis(y, g.lo1, g.eff1, g.n1) * g.n0 + cell_axis(x, g.lo0, g.eff0, g.n0);
+        keys[i] = key;
+        atomicAdd(&cnt[key], 1);
+    }
+    __syncthreads();
+    // exclusive scan of cnt[0, nflat): per-thread run, block scan of the sums
+    const int per = (nflat + BIN_SMALL_THREADS - 1) / BIN_SMALL_THREADS;
+    const int c0 = tid * per, c1 = min(c0 + per, nflat);
+    int run = 0;
+    for (int c = c0; c < c1; c++) run += cnt[c];
+    int inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    int acc = inc - run + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int c = c0; c < c1; c++) {
+        const int v = cnt[c];
+        cnt[c] = acc;
+        fill[c] = acc;
+        starts[c] = acc;
+        acc += v;
+    }
+    if (tid == 0) {
+        cnt[nflat] = n;
+        starts[nflat] = n;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += BIN_SMALL_THREADS) slots[atomicAdd(&fill[keys[i]], 1)] = i;
+    __syncthreads();
+    for (int t = tid; t < n; t += BIN_SMALL_THREADS) {
+        const int v = slots[t];
+        const int key = keys[v];
+        const int s0 = cnt[key], s1 = cnt[key + 1];
+        int rank = 0;
+        for (int u = s0; u < s1; u++) rank += slots[u] < v;
+        order[s0 + rank] = v;
+    }
+}
+
 // ------------------------------------------------------------------ scan
 int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n, int *zero_in) {
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -98,6 +180,26 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
     }
     int *keys = ctx->keys.as<int>(), *counts = ctx->counts.as<int>();
     int *starts = ctx->starts.as<int>(), *order = ctx->order.as<int>();
+    if (n <= BIN_SMALL_MAX_N && nflat <= BIN_SMALL_MAX_CELLS && !getenv("CS_BIN_MULTI")) {
+        const size_t smem = sizeof(int) * (size_t)(2 * nflat + 1 + 2 * n);
+        static size_t smem_set = 0;
+        if (smem > smem_set) {
+            CS_CUDA(cudaFuncSetAttribute(k_bin_small<double>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CS_CUDA(cudaFuncSetAttribute(k_bin_small<float>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set = smem;
+        }
+        if (prec == CS_F64)
+            k_bin_small<double><<<1, BIN_SMALL_THREADS, smem, ctx->stream>>>(
+                static_cast<const double *>(pos), (int)n, g, starts, order);
+        else
+            k_bin_small<float><<<1, BIN_SMALL_THREADS, smem, ctx->stream>>>(
+                static_cast<const float *>(pos), (int)n, g, starts, order);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+        return CS_OK;
+    }
     const int B = 256;
     if (n > 0) {
         if (prec == CS_F64)

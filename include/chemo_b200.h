@@ -370,6 +370,17 @@ int cs_ens_observe(cs_ens *e, const cs_ens_state *st, int64_t *n_alpha, double *
 int cs_rng_fill(cs_ctx *ctx, uint64_t *state, int32_t n_streams, int32_t kind, int32_t k,
                 int64_t m, double *out);
 /* y = log1p(x) with the glibc-exact restatement (test seam). */
+/* One numpy Generator(PCG64) stream drawn by the whole device, bit for bit:
+ * state (host, 4 words) = {state_hi, state_lo, inc_hi, inc_lo} as numpy's
+ * bit_generator.state; kind 0 = standard_normal (the ziggurat of
+ * distributions.c), 1 = random; m values written to out (f64, or f32 when
+ * f32 != 0).  On return state[0..1] is advanced by the raws consumed, so
+ * the next draw (here or in numpy) continues the same stream.  Replaces
+ * engine.py:272-275's sequential host draws (motion.py:277, reactions.py:57)
+ * for large N. */
+int cs_rng_fill_stream(cs_ctx *ctx, uint64_t *state, int32_t kind, int64_t m, int32_t f32,
+                       void *out);
+
 int cs_log1p_batch(cs_ctx *ctx, const double *x, double *y, int64_t n);
 
 #ifdef __cplusplus

@@ -132,6 +132,7 @@ SIGNATURES = [
     ("cs_ens_status", C_i32, [C_p, C_p]),
     ("cs_ens_observe", C_i32, [C_p, ctypes.POINTER(EnsState_t), C_p, C_p]),
     ("cs_rng_fill", C_i32, [C_p, C_p, C_i32, C_i32, C_i32, C_i64, C_p]),
+    ("cs_rng_fill_stream", C_i32, [C_p, C_p, C_i32, C_i64, C_i32, C_p]),
     ("cs_log1p_batch", C_i32, [C_p, C_p, C_p, C_i64]),
 ]
 

@@ -119,6 +119,7 @@ class SimConfig:
     n_clusters: int = 64
     cluster_sigma: float = 0.02
     engine: str = "auto"            # auto | direct | sorted (fp32 only)
+    rng: str = "auto"               # auto | host | device: where the numpy streams are drawn
 
     def __post_init__(self):
         if self.experiment not in EXPERIMENTS:
@@ -167,6 +168,8 @@ class SimConfig:
             raise ValueError(f"unknown initial_positions {self.initial_positions!r}")
         if self.engine not in ("auto", "direct", "sorted"):
             raise ValueError(f"unknown engine {self.engine!r}")
+        if self.rng not in ("auto", "host", "device"):
+            raise ValueError(f"unknown rng {self.rng!r}")
         if self.engine == "sorted" and self.precision != "fp32":
             raise ValueError("the sorted engine needs precision='fp32'")
         self.motion_params()
@@ -639,11 +642,29 @@ class Realisation:
                           stacklevel=3)
             self._warned_neg = st.neg_mass_steps
 
+    # draws of at least this many values go to the device (rng="auto")
+    DEVICE_DRAW_MIN = 1 << 17
+
+    def _draw(self, k: int):
+        """The motion block (k, N, 2) and the fixed scheduler's uniforms
+        (k, N) of the next k steps, numpy's values either way: drawn on the
+        host, or on the device for large blocks (rng.draw: the same streams,
+        bit for bit, the generators advanced identically)."""
+        n = len(self._ids)
+        dev = self.config.rng == "device" or (self.config.rng == "auto" and
+                                              2 * k * n >= self.DEVICE_DRAW_MIN)
+        if dev:
+            from . import rng as R
+            xi = R.draw(self.rng_motion, "normal", (k, n, 2), self.dtype)
+            u = R.draw(self.rng_react, "uniform", (k, n)) if self._fixed else None
+            return xi, u
+        xi = self.rng_motion.standard_normal((k, n, 2))
+        u = self.rng_react.random((k, n)) if self._fixed else None
+        return xi, u
+
     def step(self) -> None:
         """Advance the whole system by dt (fixed sub-stage order)."""
-        n = len(self._ids)
-        xi = self.rng_motion.standard_normal((1, n, 2))
-        u = self.rng_react.random((1, n)) if self._fixed else None
+        xi, u = self._draw(1)
         self._advance(xi, u)
         if self.clock is not None:
             # step s reacts at now = (s + 1) dt (engine.py:387), s + 1 = step_index
@@ -667,10 +688,9 @@ class Realisation:
             k = nxt - s
             # one (N, 2) block per step, drawn as one array: bit-identical
             # to k successive draws
-            xi = self.rng_motion.standard_normal((k, n, 2))
             # one (N,) uniform block per step: rng.random((k, n)) is
             # bit-identical to k successive rng.random(n) draws
-            u = self.rng_react.random((k, n)) if self._fixed else None
+            xi, u = self._draw(k)
             self._advance(xi, u)
             self._observe(self.step_index)
         return self._observables()

@@ -210,10 +210,10 @@ __global__ void k_log1p(const double *x, double *y, long long n) {
 //                  normals of its chain from its entry offset.
 // The last normal's end is the number of raws consumed; the stream state is
 // advanced by exactly that (k_zpar_state).
-constexpr int ZC = 4096;       // raw positions per chunk
-constexpr int ZG = 64;         // chunks per group
+constexpr int ZC = 2048;       // raw positions per chunk
+constexpr int ZG = 128;        // chunks per group
 constexpr int ZE = 32;         // entry offsets tabulated per chunk
-constexpr int ZW = 2;          // warps (chunks) per block (static shared memory < 48 KB)
+constexpr int ZW = 4;          // warps (chunks) per block
 typedef unsigned __int128 u128;
 
 struct ZparState {
@@ -414,15 +414,23 @@ __global__ void __launch_bounds__(32) k_zpar_group(const unsigned *__restrict__ 
 }
 
 // groups walked from entry 0: each group's entry and first output index
-__global__ void k_zpar_top(const unsigned long long *gt, long long ngroups,
-                           long long *gentry_off) {
+// (the group tables staged in shared memory when they fit)
+constexpr int ZTOP_MAX = 160;  // groups staged: 160 * 32 * 8 B = 40 KB
+__global__ void __launch_bounds__(256) k_zpar_top(const unsigned long long *gt, long long ngroups,
+                                                  long long *gentry_off) {
+    __shared__ unsigned long long t[ZTOP_MAX * ZE];
+    const bool stage = ngroups <= ZTOP_MAX;
+    if (stage)
+        for (int i = threadIdx.x; i < ngroups * ZE; i += blockDim.x) t[i] = gt[i];
+    __syncthreads();
     if (threadIdx.x != 0) return;
+    const unsigned long long *src = stage ? t : gt;
     int e = 0;
     long long off = 0;
     for (long long g = 0; g < ngroups; g++) {
         gentry_off[2 * g] = e;
         gentry_off[2 * g + 1] = off;
-        const unsigned long long v = gt[g * ZE + e];
+        const unsigned long long v = src[g * ZE + e];
         off += (long long)(v >> 8);
         e = (int)(v & 0xff);
     }
@@ -435,15 +443,18 @@ __global__ void __launch_bounds__(32) k_zpar_resolve(const unsigned *__restrict_
                                                      long long nchunks,
                                                      const long long *gentry_off,
                                                      long long *centry_off) {
-    if (threadIdx.x != 0) return;
+    __shared__ unsigned t[ZG * ZE];
     const long long c0 = (long long)blockIdx.x * ZG;
     const int nc = (int)min((long long)ZG, nchunks - c0);
+    for (int i = threadIdx.x; i < nc * ZE; i += 32) t[i] = table[c0 * ZE + i];
+    __syncwarp();
+    if (threadIdx.x != 0) return;
     int e = (int)gentry_off[2 * blockIdx.x];
     long long off = gentry_off[2 * blockIdx.x + 1];
     for (int c = 0; c < nc; c++) {
         centry_off[2 * (c0 + c)] = e;
         centry_off[2 * (c0 + c) + 1] = off;
-        const unsigned v = table[(c0 + c) * ZE + e];
+        const unsigned v = t[c * ZE + e];
         off += v >> 8;
         e = (int)(v & 0xff);
         if (e >= ZE) e = ZE - 1;
@@ -455,7 +466,7 @@ k_zpar_emit(ZparState z, long long nchunks, const long long *centry_off, void *o
             long long *raws_used, int *bad) {
     __shared__ ZigTables zt;
     __shared__ unsigned char code_s[ZW][ZC];
-    __shared__ int oidx_s[ZW][ZC];  // output index of the value an attempt returns, or -1
+    __shared__ unsigned short oidx_s[ZW][ZC];  // output index (+1) of an attempt's value, 0: none
     zig_tables_load(zt);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -464,20 +475,20 @@ k_zpar_emit(ZparState z, long long nchunks, const long long *centry_off, void *o
     const long long base = centry_off[2 * chunk + 1];
     if (base >= z.m) return;
     unsigned char *code = code_s[warp];
-    int *oidx = oidx_s[warp];
-    for (int q = lane; q < ZC; q += 32) oidx[q] = -1;
+    unsigned short *oidx = oidx_s[warp];
+    for (int q = lane; q < ZC; q += 32) oidx[q] = 0;
     zpar_eval(z, chunk, zt, code, nullptr, bad);
     __syncwarp();
     int o = 0;  // normals of this chunk so far
     zpar_walk(
         code, (int)centry_off[2 * chunk],
         [&](int q, int f) {
-            if (lane < f) oidx[q + lane] = o + lane;
+            if (lane < f) oidx[q + lane] = (unsigned short)(o + lane + 1);
             o += f;
         },
         [&](int q) {
             if (code[q] >> 7) {
-                if (lane == 0) oidx[q] = o;
+                if (lane == 0) oidx[q] = (unsigned short)(o + 1);
                 o += 1;
             }
         });
@@ -489,7 +500,7 @@ k_zpar_emit(ZparState z, long long nchunks, const long long *centry_off, void *o
     u128 st = A * mk128(z.s_hi, z.s_lo) + C;
     lcg_jump(inc, 32, A32, C32);
     for (int q = lane; q < ZC; q += 32) {
-        const int k = oidx[q];
+        const int k = (int)oidx[q] - 1;
         if (k >= 0 && base + k < z.m) {
             double v;
             const int c = zig_attempt(st, inc, zt, v);
@@ -593,7 +604,7 @@ int cs_rng_fill_stream(cs_ctx *ctx, uint64_t *state, int32_t kind, int64_t m, in
         CS_LAUNCH_CHECK();
         k_zpar_group<<<(unsigned)ngroups, 32, 0, ctx->stream>>>(table, nchunks, gt);
         CS_LAUNCH_CHECK();
-        k_zpar_top<<<1, 32, 0, ctx->stream>>>(gt, ngroups, goff);
+        k_zpar_top<<<1, 256, 0, ctx->stream>>>(gt, ngroups, goff);
         CS_LAUNCH_CHECK();
         k_zpar_resolve<<<(unsigned)ngroups, 32, 0, ctx->stream>>>(table, nchunks, goff, coff);
         CS_LAUNCH_CHECK();

@@ -370,6 +370,18 @@ int cs_ens_observe(cs_ens *e, const cs_ens_state *st, int64_t *n_alpha, double *
 int cs_rng_fill(cs_ctx *ctx, uint64_t *state, int32_t n_streams, int32_t kind, int32_t k,
                 int64_t m, double *out);
 /* y = log1p(x) with the glibc-exact restatement (test seam). */
+/* Observables of a realisation in numpy's arithmetic (engine.py:230-235,
+ * :317-352).  cs_msd: *out (device f64) = mean over particles of
+ * (0 + dx^2) + dy^2, dx = pos - anchor in f64, numpy's pairwise reduction
+ * order.  cs_hist2d: counts (device, bins x bins u64, [y bin][x bin]) of
+ * numpy.histogram2d over the species (-1: all) with the given bin edges
+ * (device f64, bins + 1 each, numpy's linspace). */
+int cs_msd(cs_ctx *ctx, int32_t prec, const void *pos, const void *anchor, int64_t n,
+           double *out);
+int cs_hist2d(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *type, int64_t n,
+              int32_t species, const double *edges_x, const double *edges_y, int32_t bins,
+              uint64_t *counts);
+
 /* One numpy Generator(PCG64) stream drawn by the whole device, bit for bit:
  * state (host, 4 words) = {state_hi, state_lo, inc_hi, inc_lo} as numpy's
  * bit_generator.state; kind 0 = standard_normal (the ziggurat of

@@ -191,7 +191,7 @@ int cs_ctx_destroy(cs_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (Buf *b : {&ctx->keys, &ctx->skeys, &ctx->counts, &ctx->starts, &ctx->order,
                    &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->status, &ctx->pair_counts,
-                   &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar})
+                   &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar, &ctx->obs})
         b->release();
     delete ctx;
     return CS_OK;

@@ -84,7 +84,7 @@ struct cs_fast;
 struct cs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar,
+    cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar, obs,
         pair_counts, pair_offsets, host_scratch;
     cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
     int64_t launches = 0;

@@ -553,31 +553,51 @@ class Realisation:
         self._field_c = np.zeros((4, self.grid.n_c ** 2))
         self._observe(0)
 
-    def _species_hist(self, pos, species, sp) -> np.ndarray:
-        p = pos[species == sp]
-        h, _, _ = np.histogram2d(p[:, 0], p[:, 1], bins=self.config.hist_bins,
-                                 range=[[self.domain.lo[0], self.domain.hi[0]],
-                                        [self.domain.lo[1], self.domain.hi[1]]])
-        h = h.T
-        return h / p.shape[0] if p.shape[0] else h
+    def _species_hist(self, sp) -> np.ndarray:
+        """numpy.histogram2d of one species' positions over the domain
+        (engine.py:317-352), normalised by the species count, transposed --
+        binned on the device with numpy's edges (cs_hist2d)."""
+        import torch
+        s = self._state
+        b = self.config.hist_bins
+        if getattr(self, "_hist_edges", None) is None:
+            ex = np.linspace(self.domain.lo[0], self.domain.hi[0], b + 1)
+            ey = np.linspace(self.domain.lo[1], self.domain.hi[1], b + 1)
+            self._hist_edges = (torch.as_tensor(ex, device="cuda"),
+                                torch.as_tensor(ey, device="cuda"),
+                                torch.empty((b, b), dtype=torch.int64, device="cuda"))
+        ex, ey, cnt = self._hist_edges
+        N.check(N.load_library().cs_hist2d(
+            N.context(), N.prec_code(s["pos"].dtype), N.ptr(s["pos"]), N.ptr(s["species"]),
+            len(self._ids), int(sp), N.ptr(ex), N.ptr(ey), b, N.ptr(cnt)), "cs_hist2d")
+        n_sp = int((s["species"] == int(sp)).sum())
+        h = cnt.cpu().numpy().astype(np.float64)  # the b x b counts; numpy's division
+        return h / n_sp if n_sp else h
+
+    def _device_msd(self) -> float:
+        """msd (engine.py:230-235) on the device in numpy's reduction order."""
+        import torch
+        s = self._state
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        N.check(N.load_library().cs_msd(N.context(), N.prec_code(s["pos"].dtype), N.ptr(s["pos"]),
+                                        N.ptr(s["anchor"]), len(self._ids), N.ptr(out)),
+                "cs_msd")
+        return float(out.item())
 
     def _observe(self, step: int) -> None:
         snap = [k for k in range(4) if self._snapshot_steps[k] == step]
         if not (self._record_flags[step] or snap):
             return
         s = self._state
-        pos = s["pos"].double().cpu().numpy()
-        species = s["species"].cpu().numpy()
         if self._record_flags[step]:
-            anchor = s["anchor"].double().cpu().numpy()
-            n_a = int(np.count_nonzero(species == Species.ALPHA))
+            n = len(self._ids)
+            n_a = int((s["species"] == int(Species.ALPHA)).sum())
             self._times.append(step * self.dt)
-            self._counts.append((n_a, len(species) - n_a))
-            d = pos - anchor
-            self._msd.append(float((d * d).sum(axis=1).mean()))
+            self._counts.append((n_a, n - n_a))
+            self._msd.append(self._device_msd())
         for k in snap:
-            self._hist_alpha[k] = self._species_hist(pos, species, Species.ALPHA)
-            self._hist_beta[k] = self._species_hist(pos, species, Species.BETA)
+            self._hist_alpha[k] = self._species_hist(Species.ALPHA)
+            self._hist_beta[k] = self._species_hist(Species.BETA)
             self._field_c[k] = s["c"].double().cpu().numpy()
 
     # ---- stepping ----------------------------------------------------------

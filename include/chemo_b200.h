@@ -375,12 +375,13 @@ int cs_rng_fill(cs_ctx *ctx, uint64_t *state, int32_t n_streams, int32_t kind, i
  * (0 + dx^2) + dy^2, dx = pos - anchor in f64, numpy's pairwise reduction
  * order.  cs_hist2d: counts (device, bins x bins u64, [y bin][x bin]) of
  * numpy.histogram2d over the species (-1: all) with the given bin edges
- * (device f64, bins + 1 each, numpy's linspace). */
+ * (device f64, bins + 1 each, numpy's linspace); per_sample > 0: particles
+ * i / per_sample belong to consecutive samples, counts (samples, bins, bins). */
 int cs_msd(cs_ctx *ctx, int32_t prec, const void *pos, const void *anchor, int64_t n,
            double *out);
 int cs_hist2d(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *type, int64_t n,
               int32_t species, const double *edges_x, const double *edges_y, int32_t bins,
-              uint64_t *counts);
+              int64_t per_sample, uint64_t *counts);
 
 /* One numpy Generator(PCG64) stream drawn by the whole device, bit for bit:
  * state (host, 4 words) = {state_hi, state_lo, inc_hi, inc_lo} as numpy's

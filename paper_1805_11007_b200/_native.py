@@ -134,7 +134,7 @@ SIGNATURES = [
     ("cs_rng_fill", C_i32, [C_p, C_p, C_i32, C_i32, C_i32, C_i64, C_p]),
     ("cs_rng_fill_stream", C_i32, [C_p, C_p, C_i32, C_i64, C_i32, C_p]),
     ("cs_msd", C_i32, [C_p, C_i32, C_p, C_p, C_i64, C_p]),
-    ("cs_hist2d", C_i32, [C_p, C_i32, C_p, C_p, C_i64, C_i32, C_p, C_p, C_i32, C_p]),
+    ("cs_hist2d", C_i32, [C_p, C_i32, C_p, C_p, C_i64, C_i32, C_p, C_p, C_i32, C_i64, C_p]),
     ("cs_log1p_batch", C_i32, [C_p, C_p, C_p, C_i64]),
 ]
 

@@ -14,7 +14,8 @@
 //          searchsorted(edges, v, 'right') (edges = numpy's linspace, passed
 //          in), a value on the last edge moved into the last bin, outliers
 //          dropped; counts stored transposed ([y bin][x bin]) as engine.py's
-//          h.T.
+//          h.T; per_sample > 0 bins the samples of a batched ensemble (sample
+//          = index / per_sample) into consecutive b x b blocks.
 #include "common.cuh"
 
 namespace cs {
@@ -97,7 +98,7 @@ __global__ void k_msd_finish(const double *__restrict__ partial, long long n, do
 template <class P>
 __global__ void k_hist2d(const P *__restrict__ pos, const uint8_t *__restrict__ type, long long n,
                          int sp, const double *__restrict__ ex, const double *__restrict__ ey,
-                         int b, unsigned long long *__restrict__ counts) {
+                         int b, long long per, unsigned long long *__restrict__ counts) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         if (sp >= 0 && type[i] != sp) continue;
@@ -110,7 +111,8 @@ __global__ void k_hist2d(const P *__restrict__ pos, const uint8_t *__restrict__ 
         if (x == ex[b]) ix -= 1;
         if (y == ey[b]) iy -= 1;
         if (ix < 1 || ix > b || iy < 1 || iy > b) continue;
-        atomicAdd(&counts[(long long)(iy - 1) * b + (ix - 1)], 1ull);
+        const long long smp = per > 0 ? i / per : 0;  // sample of a batched ensemble
+        atomicAdd(&counts[(smp * b + (iy - 1)) * b + (ix - 1)], 1ull);
     }
 }
 
@@ -149,21 +151,23 @@ int cs_msd(cs_ctx *ctx, int32_t prec, const void *pos, const void *anchor, int64
 
 int cs_hist2d(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *type, int64_t n,
               int32_t species, const double *edges_x, const double *edges_y, int32_t bins,
-              uint64_t *counts) {
+              int64_t per_sample, uint64_t *counts) {
     using namespace cs;
-    if (bins < 1 || (species >= 0 && !type)) {
+    if (bins < 1 || (species >= 0 && !type) || per_sample < 0) {
         set_error("cs_hist2d: bins must be positive (and the species array given)");
         return CS_ERR_PARAM;
     }
-    CS_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (size_t)bins * bins, ctx->stream));
+    const long long samples = per_sample > 0 ? (n + per_sample - 1) / per_sample : 1;
+    CS_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (size_t)bins * bins * samples,
+                            ctx->stream));
     if (n == 0) return CS_OK;
     if (prec == CS_F64)
         k_hist2d<double><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-            static_cast<const double *>(pos), type, n, species, edges_x, edges_y, bins,
+            static_cast<const double *>(pos), type, n, species, edges_x, edges_y, bins, per_sample,
             reinterpret_cast<unsigned long long *>(counts));
     else
         k_hist2d<float><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-            static_cast<const float *>(pos), type, n, species, edges_x, edges_y, bins,
+            static_cast<const float *>(pos), type, n, species, edges_x, edges_y, bins, per_sample,
             reinterpret_cast<unsigned long long *>(counts));
     CS_LAUNCH_CHECK();
     ctx->launches += 1;

@@ -569,7 +569,7 @@ class Realisation:
         ex, ey, cnt = self._hist_edges
         N.check(N.load_library().cs_hist2d(
             N.context(), N.prec_code(s["pos"].dtype), N.ptr(s["pos"]), N.ptr(s["species"]),
-            len(self._ids), int(sp), N.ptr(ex), N.ptr(ey), b, N.ptr(cnt)), "cs_hist2d")
+            len(self._ids), int(sp), N.ptr(ex), N.ptr(ey), b, 0, N.ptr(cnt)), "cs_hist2d")
         n_sp = int((s["species"] == int(sp)).sum())
         h = cnt.cpu().numpy().astype(np.float64)  # the b x b counts; numpy's division
         return h / n_sp if n_sp else h

@@ -282,12 +282,10 @@ class Ensemble:
         field_c = np.zeros((S, 4, self.grid.n_c ** 2))
         lo, hi = self.domain.lo, self.domain.hi
 
-        edges = [np.linspace(lo[a], hi[a], b + 1) for a in range(2)]
-
-        def bins(v, e):  # np.histogram2d's bin index (histogramdd: right edge closed)
-            i = np.searchsorted(e, v, side="right")
-            i[v == e[-1]] -= 1
-            return i - 1
+        import torch
+        edges_d = [torch.as_tensor(np.linspace(lo[a], hi[a], b + 1), device="cuda")
+                   for a in range(2)]
+        hcnt = torch.empty((S, b, b), dtype=torch.int64, device="cuda")
 
         def observe(step):
             snap = [k for k in range(4) if snaps[k] == step]
@@ -301,21 +299,18 @@ class Ensemble:
                 counts.append(np.stack([n_a, self.n - n_a], axis=1))
                 msds.append(msd)
             if snap:
-                pos = self.state["pos"].cpu().numpy()
-                species = self.state["species"].cpu().numpy()
                 c = self.state["c"].cpu().numpy() if self.field_active or \
                     self.refresh_active else np.zeros((S, self.grid.n_c ** 2))
-                ix = bins(pos[..., 0].ravel(), edges[0]).reshape(S, -1)
-                iy = bins(pos[..., 1].ravel(), edges[1]).reshape(S, -1)
-                inside = (ix >= 0) & (ix < b) & (iy >= 0) & (iy < b)
-                sid = np.arange(S)[:, None]
+                species = self.state["species"]
                 for sp, out in ((Species.ALPHA, hist_a), (Species.BETA, hist_b)):
-                    sel = species == sp
-                    keep = sel & inside
-                    key = (sid * b * b + ix * b + iy)[keep]
-                    h = np.bincount(key, minlength=S * b * b).reshape(S, b, b)
-                    h = h.transpose(0, 2, 1).astype(np.float64)
-                    cnt = sel.sum(axis=1)
+                    # numpy.histogram2d of every sample on the device
+                    # (cs_hist2d, per_sample = n); numpy's normalisation
+                    N.check(N.load_library().cs_hist2d(
+                        N.context(), N.CS_F64, N.ptr(self.state["pos"]), N.ptr(species),
+                        S * self.n, int(sp), N.ptr(edges_d[0]), N.ptr(edges_d[1]), b, self.n,
+                        N.ptr(hcnt)), "cs_hist2d")
+                    h = hcnt.cpu().numpy().astype(np.float64)
+                    cnt = (species == int(sp)).reshape(S, -1).sum(dim=1).cpu().numpy()
                     nz = cnt > 0
                     h[nz] = h[nz] / cnt[nz][:, None, None]
                     for k in snap:

@@ -54,7 +54,7 @@ def test_hist2d_matches_numpy():
     cnt = torch.empty((b, b), dtype=torch.int64, device="cuda")
     for s in (0, 1, -1):
         N.check(N.load_library().cs_hist2d(N.context(), N.prec_code(pt.dtype), N.ptr(pt),
-                                           N.ptr(st), len(pos), s, N.ptr(ex), N.ptr(ex), b,
+                                           N.ptr(st), len(pos), s, N.ptr(ex), N.ptr(ex), b, 0,
                                            N.ptr(cnt)), "cs_hist2d")
         p = pos if s < 0 else pos[sp == s]
         h, _, _ = np.histogram2d(p[:, 0], p[:, 1], bins=b, range=[[-0.5, 0.5], [-0.5, 0.5]])

@@ -281,6 +281,19 @@ def oracle_sim(cfg: dict, pos, sp, nthreads: int):
                      field=field, fp32=cfg["prec"] == "fp32", nthreads=nthreads)
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (for the CPU baseline lines)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def run_oracle_steps(cfg, steps: int, warmup: int, budget_s: float, nthreads: int):
     rng = np.random.default_rng(SEED)
     n = cfg["n"]
@@ -321,6 +334,7 @@ def reference_arm(args, cfg, rank):
         "data": "synthetic",
         "config": {"workload": args.config, "n": cfg["n"], "grid": cfg["n_c"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{done} full step(s) of {args.config} (N={cfg['n']}) on the "
                                    f"oracle restatement (oracle/, C + numpy FFT), "
                                    f"{ncores} OpenMP threads; requested {args.steps}",
@@ -435,6 +449,7 @@ def main():
         ncores = os.cpu_count() or 1
         done, t_used, stg = run_oracle_steps(cfg, 1, 0, 30.0, ncores)
         cpu = {"value": cfg["n"] * done / t_used, "unit": UNIT, "cores": ncores, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"{done} full step of {args.config} (N={cfg['n']}, "
                          f"{cfg['n_c']}^2 grid) on the oracle restatement "
                          f"(C + numpy FFT), {ncores} OpenMP threads",

@@ -491,6 +491,7 @@ class Realisation:
         self._warned_clamp = 0
         self._warned_neg = 0
         self._dead = False
+        self._stale = False  # the sorted engine's records are newer than the state tensors
         self._init_recording()
 
     def _initial_refresh(self):
@@ -514,13 +515,23 @@ class Realisation:
         s["drift"].copy_(drift)
 
     # ---- state views ------------------------------------------------------
+    def _sync(self) -> None:
+        """Export the sorted engine's records into the (id-ordered) state
+        tensors if steps ran since the last export (a no-op for the direct
+        engine, whose state tensors are its working arrays)."""
+        if self._stale:
+            self._sim.export_state()
+            self._stale = False
+
     @property
     def device_state(self) -> dict:
+        self._sync()
         return self._state
 
     @property
     def pop(self) -> Population:
         """Host snapshot of the particle state (numpy, positions float64)."""
+        self._sync()
         s = self._state
         return Population(ids=self._ids.copy(),
                           positions=s["pos"].double().cpu().numpy(),
@@ -532,6 +543,7 @@ class Realisation:
 
     @property
     def field(self) -> Field:
+        self._sync()
         s = self._state
         return Field(c=s["c"].double().cpu().numpy(), grad=s["grad"].double().cpu().numpy(),
                      rho_alpha=s["rho_a"].double().cpu().numpy(),
@@ -588,6 +600,7 @@ class Realisation:
         snap = [k for k in range(4) if self._snapshot_steps[k] == step]
         if not (self._record_flags[step] or snap):
             return
+        self._sync()
         s = self._state
         if self._record_flags[step]:
             n = len(self._ids)
@@ -614,10 +627,11 @@ class Realisation:
         xi = torch.as_tensor(xi_host, device="cuda").to(self.dtype).contiguous()
         u = None if u_host is None else torch.as_tensor(u_host, device="cuda").contiguous()
         self._sim.step(xi, k, u=u)
-        self._sim.export_state()
+        self._stale = True  # exported lazily (state views, observables, errors)
         st = self._sim.status()
         self._report_warnings(st)
         if st.code != N.CS_OK:
+            self._sync()
             self._dead = True
             self.step_index = int(st.step)
             try:
@@ -641,6 +655,7 @@ class Realisation:
     def _react_host(self, now: float) -> None:
         """Gillespie scheduler after a device step (engine.py:389-400): the
         event clock on the host, the Beta -> Alpha trials on the device."""
+        self._sync()
         view = _SpeciesView(self._state)
         self.clock.advance(view, now, self.rng_react)
         flipped = beta_step_reactions(view, self.reaction, self.dt, self.rng_react)

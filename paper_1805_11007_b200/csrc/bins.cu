@@ -51,8 +51,11 @@ __global__ void k_bin_scatter(const int *__restrict__ keys, long long n,
 // Stable placement: the particle in slot t (cell order, arbitrary inside a
 // cell) goes to its cell start + the number of the cell's particles with a
 // smaller index (O(m) reads of the cell's L1-resident slots per particle).
+template <class P>
 __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict__ keys,
-                           const int *__restrict__ starts, long long n, int *__restrict__ order) {
+                           const int *__restrict__ starts, long long n, int *__restrict__ order,
+                           const P *__restrict__ pos, const uint8_t *__restrict__ type,
+                           P *__restrict__ spos, uint8_t *__restrict__ stype) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
         const int v = slots[t];
@@ -61,6 +64,9 @@ __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict_
         int rank = 0;
         for (int u = s; u < e; u++) rank += __ldg(slots + u) < v;
         order[s + rank] = v;
+        spos[2 * (s + rank)] = pos[2 * (long long)v];
+        spos[2 * (s + rank) + 1] = pos[2 * (long long)v + 1];
+        if (type) stype[s + rank] = type[v];
     }
 }
 
@@ -72,12 +78,13 @@ __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict_
 // (as k_seg_rank).  Same order / starts as the multi-kernel path.
 constexpr int BIN_SMALL_THREADS = 1024;
 constexpr int BIN_SMALL_MAX_CELLS = 12 * 1024;
-constexpr long long BIN_SMALL_MAX_N = 12 * 1024;
+constexpr long long BIN_SMALL_MAX_N = 4 * 1024;
 
 template <class P>
 __global__ void __launch_bounds__(BIN_SMALL_THREADS)
 k_bin_small(const P *__restrict__ pos, int n, BinGeom g, int *__restrict__ starts,
-            int *__restrict__ order) {
+            int *__restrict__ order, const uint8_t *__restrict__ type, P *__restrict__ spos,
+            uint8_t *__restrict__ stype) {
     extern __shared__ int sm[];
     const int nflat = g.n0 * g.n1;
     int *cnt = sm;                 // nflat + 1: counts, then starts
@@ -142,6 +149,13 @@ k_bin_small(const P *__restrict__ pos, int n, BinGeom g, int *__restrict__ start
         for (int u = s0; u < s1; u++) rank += slots[u] < v;
         order[s0 + rank] = v;
     }
+    __syncthreads();  // the block's order writes are visible to the block
+    for (int k = tid; k < n; k += BIN_SMALL_THREADS) {  // coalesced stores of the copies
+        const int v = order[k];
+        spos[2 * k] = pos[2 * (long long)v];
+        spos[2 * k + 1] = pos[2 * (long long)v + 1];
+        if (type) stype[k] = type[v];
+    }
 }
 
 // ------------------------------------------------------------------ scan
@@ -162,7 +176,8 @@ int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n, int *z
 }
 
 // ------------------------------------------------------------------ driver
-int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g) {
+int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
+                  const uint8_t *type) {
     const long long nflat = (long long)g.n0 * g.n1;
     if (nflat >= (1LL << 31) - 1) {
         set_error("cell table too large (%lld cells)", nflat);
@@ -180,6 +195,9 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
     }
     int *keys = ctx->keys.as<int>(), *counts = ctx->counts.as<int>();
     int *starts = ctx->starts.as<int>(), *order = ctx->order.as<int>();
+    CS_TRY(ctx->spos.ensure((prec == CS_F64 ? 16 : 8) * (size_t)(n > 0 ? n : 1)));
+    CS_TRY(ctx->stype.ensure((size_t)(n > 0 ? n : 1)));
+    uint8_t *stype = ctx->stype.as<uint8_t>();
     if (n <= BIN_SMALL_MAX_N && nflat <= BIN_SMALL_MAX_CELLS && !getenv("CS_BIN_MULTI")) {
         const size_t smem = sizeof(int) * (size_t)(2 * nflat + 1 + 2 * n);
         static size_t smem_set = 0;
@@ -192,10 +210,12 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
         }
         if (prec == CS_F64)
             k_bin_small<double><<<1, BIN_SMALL_THREADS, smem, ctx->stream>>>(
-                static_cast<const double *>(pos), (int)n, g, starts, order);
+                static_cast<const double *>(pos), (int)n, g, starts, order, type,
+                ctx->spos.as<double>(), stype);
         else
             k_bin_small<float><<<1, BIN_SMALL_THREADS, smem, ctx->stream>>>(
-                static_cast<const float *>(pos), (int)n, g, starts, order);
+                static_cast<const float *>(pos), (int)n, g, starts, order, type,
+                ctx->spos.as<float>(), stype);
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
         return CS_OK;
@@ -215,8 +235,14 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
         k_bin_scatter<<<grid_for(n, B), B, 0, ctx->stream>>>(keys, n, starts, counts,
                                                              ctx->skeys.as<int>());
         CS_LAUNCH_CHECK();
-        k_seg_rank<<<grid_for(n, B), B, 0, ctx->stream>>>(ctx->skeys.as<int>(), keys, starts, n,
-                                                          order);
+        if (prec == CS_F64)
+            k_seg_rank<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
+                ctx->skeys.as<int>(), keys, starts, n, order, static_cast<const double *>(pos),
+                type, ctx->spos.as<double>(), stype);
+        else
+            k_seg_rank<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
+                ctx->skeys.as<int>(), keys, starts, n, order, static_cast<const float *>(pos),
+                type, ctx->spos.as<float>(), stype);
         CS_LAUNCH_CHECK();
     }
     ctx->launches += 3;

@@ -191,7 +191,8 @@ int cs_ctx_destroy(cs_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (Buf *b : {&ctx->keys, &ctx->skeys, &ctx->counts, &ctx->starts, &ctx->order,
                    &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->status, &ctx->pair_counts,
-                   &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar, &ctx->obs})
+                   &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar, &ctx->obs, &ctx->spos,
+                   &ctx->stype})
         b->release();
     delete ctx;
     return CS_OK;
@@ -202,7 +203,7 @@ int cs_soft_forces(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *ty
     CS_TRY(check_prec(prec));
     CS_TRY(check_pairs(pp));
     const BinGeom g = make_geom(*dom, pp->cell_cutoff);
-    CS_TRY(bin_particles(ctx, prec, pos, n, g));
+    CS_TRY(bin_particles(ctx, prec, pos, n, g, type));
     CS_TRY(launch_soft_forces(ctx, prec, pos, type, n, g, make_pairtab(*pp), out, nullptr));
     return CS_OK;
 }

@@ -84,7 +84,8 @@ struct cs_fast;
 struct cs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar, obs,
+    cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar, obs, spos,
+        stype,
         pair_counts, pair_offsets, host_scratch;
     cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
     int64_t launches = 0;
@@ -303,7 +304,10 @@ inline int grid_for(long long n, int block, int max_blocks = 148 * 64) {
 
 // ---------------------------------------------------------------- launchers
 // bins.cu
-int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g);
+// order / starts of the reference's cell list, and positions (and types, if
+// given) copied into that order in ctx->spos / ctx->stype for the force walk
+int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
+                  const uint8_t *type = nullptr);
 int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n,
                        int *zero_in = nullptr);
 // forces.cu

@@ -88,7 +88,8 @@ template <class P>
 __global__ void __launch_bounds__(32 * DF_WARPS)
 k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,
               const int *__restrict__ order, const int *__restrict__ starts, long long n,
-              BinGeom g, PairTab pt, double *__restrict__ out, const DevStatus *st) {
+              BinGeom g, PairTab pt, double *__restrict__ out, const DevStatus *st,
+              const P *__restrict__ spos, const uint8_t *__restrict__ stype) {
     if (st && st->abort) return;
     __shared__ DfBuf bufs[DF_WARPS];
     DfBuf &B = bufs[threadIdx.x >> 5];
@@ -151,16 +152,16 @@ k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,
                     kend = c9 == 1 ? ce_[1] : c9 == 2 ? ce_[2] : c9 == 3 ? ce_[3] : c9 == 4 ? ce_[4]
                          : c9 == 5 ? ce_[5] : c9 == 6 ? ce_[6] : c9 == 7 ? ce_[7] : ce_[8];
                 }
-                const int j = order[k++];
-                if (j != i) {
+                const int kk = k++;  // slot of the candidate (cell order, ascending id in a cell)
+                if (kk != (int)t) {
                     double xj, yj;
-                    load2(pos, j, xj, yj);
+                    load2(spos, kk, xj, yj);  // positions copied into slot order
                     double dx0 = dsub(xj, xi);
                     double dx1 = dsub(yj, yi);
                     if (g.per0) dx0 = df_min_image(dx0, g.size0);
                     if (g.per1) dx1 = df_min_image(dx1, g.size1);
                     const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
-                    const int tt = ti * 2 + (type ? (int)type[j] : 0);
+                    const int tt = ti * 2 + (stype ? (int)stype[kk] : 0);
                     if (!(r2 > pt.cut2[tt] || r2 == 0.0)) {
                         const int q = lane * DF_BUF + pend;
                         B.dx[q] = dx0;
@@ -319,12 +320,16 @@ int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *ty
     if (n == 0) return CS_OK;
     const int B = 32 * DF_WARPS;
     const int *order = ctx->order.as<int>(), *starts = ctx->starts.as<int>();
+    // bin_particles left the positions (and types) in cell order in ctx->spos / stype
+    uint8_t *stype = type ? ctx->stype.as<uint8_t>() : nullptr;
     if (prec == CS_F64)
         k_soft_forces<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
-            static_cast<const double *>(pos), type, order, starts, n, g, pt, out, st);
+            static_cast<const double *>(pos), type, order, starts, n, g, pt, out, st,
+            ctx->spos.as<double>(), stype);
     else
         k_soft_forces<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
-            static_cast<const float *>(pos), type, order, starts, n, g, pt, out, st);
+            static_cast<const float *>(pos), type, order, starts, n, g, pt, out, st,
+            ctx->spos.as<float>(), stype);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;

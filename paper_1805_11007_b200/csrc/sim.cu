@@ -475,7 +475,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         if (p.interaction == 1) {
             {
                 StageMark m(sim, CS_STAGE_BIN);
-                CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom));
+                CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom, s->type));
             }
             StageMark m(sim, CS_STAGE_FORCE);
             CS_TRY(launch_soft_forces(ctx, p.prec, s->pos, s->type, n, sim->geom, sim->pt,

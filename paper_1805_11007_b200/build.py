@@ -62,15 +62,26 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
               *ARCH, "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include"),
               *(extra or [])]
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
-        cmd = [nv, "-c", src, "-o", obj, *common]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        hdr_t = max(os.path.getmtime(f) for f in headers())
+        if (not force and os.path.exists(obj) and out is None
+                and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)):
+            return obj, None
+        r = subprocess.run([nv, "-c", src, "-o", obj, *common], capture_output=True, text=True)
         if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+            return None, r.stdout + r.stderr
+        return obj, (r.stderr if verbose else None)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        results = list(pool.map(compile_one, sources()))
+    for src, (obj, msg) in zip(sources(), results):
+        if obj is None:
+            sys.stderr.write(msg)
             raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
+        if msg:
+            sys.stderr.write(msg)
         objs.append(obj)
     tmp = so + ".tmp"
     cmd = [nv, "-shared", *ARCH, "-o", tmp, *objs, "-L", cuda_lib, "-lcufft",

@@ -94,8 +94,7 @@ int launch_boundaries(cs_ctx *ctx, int prec, void *x, void *anchor, long long n,
                       const cs_domain &d, DevStatus *st);
 int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
                    const GridGeom &gg, int kind, double h, double cutoff,
-                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
-                   bool zero_first);
+                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st);
 bool gauss_too_wide(const GridGeom &gg, double cutoff);
 int launch_bilinear(cs_ctx *ctx, int prec, const void *pts, long long np, const void *vals, int m,
                     const GridGeom &gg, void *out, unsigned long long *clamped);
@@ -192,7 +191,8 @@ int cs_ctx_destroy(cs_ctx *ctx) {
     for (Buf *b : {&ctx->keys, &ctx->skeys, &ctx->counts, &ctx->starts, &ctx->order,
                    &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->status, &ctx->pair_counts,
                    &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar, &ctx->obs, &ctx->spos,
-                   &ctx->stype})
+                   &ctx->stype, &ctx->dep_keys, &ctx->dep_counts, &ctx->dep_starts,
+                   &ctx->dep_slots, &ctx->dep_pos, &ctx->dep_meta})
         b->release();
     delete ctx;
     return CS_OK;
@@ -329,8 +329,7 @@ int cs_deposit(cs_ctx *ctx, int32_t prec, const void *pos, const uint8_t *route,
         CS_TRY(tmp->ensure((size_t)grid->n_c * grid->n_c * (prec == CS_F64 ? 8 : 4)));
         rb = tmp->p;
     }
-    return launch_deposit(ctx, prec, pos, route, n, gg, kind, h, cutoff, bits, rho_a, rb, nullptr,
-                          true);
+    return launch_deposit(ctx, prec, pos, route, n, gg, kind, h, cutoff, bits, rho_a, rb, nullptr);
 }
 
 int cs_bilinear(cs_ctx *ctx, int32_t prec, const void *points, int64_t np, const void *values,

@@ -86,7 +86,9 @@ struct cs_ctx {
     cudaStream_t stream = nullptr;
     cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar, obs, spos,
         stype,
-        pair_counts, pair_offsets, host_scratch;
+        pair_counts, pair_offsets, host_scratch,
+        // ordered deposit (deposit.cu): bin keys / counts / starts, slots, sorted copies
+        dep_keys, dep_counts, dep_starts, dep_slots, dep_pos, dep_meta;
     cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
     int64_t launches = 0;
 };

@@ -17,14 +17,14 @@
 //   fixed-step reactions (reactions.py:43-81).
 // The Brownian increments and reaction uniforms of every realisation come
 // from its own generator streams on the host (the reference's RNG
-// contract), K steps at a time.  Deposits accumulate with shared-memory
-// fp64 atomics (the summation order of concurrent stamps differs from the
-// reference's particle order; tolerance as for the direct engine).
+// contract), K steps at a time.  Deposits are node gathers in the
+// reference's particle order (bit-identical; see ens_deposit).
 #include <string.h>
 
 #include <vector>
 
 #include "common.cuh"
+#include "deposit.cuh"
 
 namespace cs {
 
@@ -128,6 +128,165 @@ __device__ __forceinline__ void set_status(DevStatus *st, int *s_abort, unsigned
 }
 
 constexpr int ENS_THREADS = 256;
+constexpr int ENS_MERGE_ROWS = 16;  // gaussian stamps up to 16 rows tall: merged row by row
+
+// deposit_both inside the CTA in the reference's summation order (the
+// algorithm of deposit.cu, with rows as bins: the grid is neumann, nc <= 64).
+// key[p] = deposit row * nc + deposit column (-1: not depositing), order =
+// depositing particles by row, ascending index inside a row.
+__device__ __noinline__ void ens_deposit(const EnsArgs &a, const double *pos, const uint8_t *type,
+                                         int *key, int *order, int *dstart, double *ra,
+                                         double *rb, int tid, int lane, int warp) {
+    const GridGeom &gg = a.gg;
+    const int nc = gg.n, m = nc * nc, n = a.n;
+    const int kind = a.deposit_kind;
+    int *dcur = dstart + nc + 1;
+    for (int r = tid; r <= nc; r += ENS_THREADS) dstart[r] = 0;
+    __syncthreads();
+    for (int p = tid; p < n; p += ENS_THREADS) {
+        int k = -1;
+        if (route_bits(type, p, a.route)) {
+            const double u0 = ddiv(dsub(pos[2 * p], gg.lo0), gg.d0);
+            const double u1 = ddiv(dsub(pos[2 * p + 1], gg.lo1), gg.d1);
+            if (fabs(u0) < 0x1p52 && fabs(u1) < 0x1p52) {
+                const int r = dep_bin_axis(u1, kind, nc, 0);
+                k = r * nc + dep_bin_axis(u0, kind, nc, 0);
+                atomicAdd(&dstart[r + 1], 1);
+            }
+        }
+        key[p] = k;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int carry = 0;
+        for (int r0 = 1; r0 <= nc; r0 += 32) {
+            const int r = r0 + lane;
+            int v = r <= nc ? dstart[r] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, d);
+                if (lane >= d) v += y;
+            }
+            if (r <= nc) dstart[r] = v + carry;
+            carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+        __syncwarp();
+        for (int r = lane; r < nc; r += 32) dcur[r] = dstart[r];
+        __syncwarp();
+        for (int p0 = 0; p0 < n; p0 += 32) {  // stable placement, 32 at a time
+            const int p = p0 + lane;
+            const int k = p < n ? key[p] : -1;
+            const int r = k >= 0 ? k / nc : -1 - lane;
+            const unsigned same = __match_any_sync(0xffffffffu, r);
+            const int rank = __popc(same & ((1u << lane) - 1u));
+            int base = 0;
+            if (k >= 0) base = dcur[r];
+            __syncwarp();
+            if (k >= 0) {
+                order[base + rank] = p;
+                if (rank == __popc(same) - 1) dcur[r] = base + rank + 1;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (kind == CS_CIC) {
+        const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
+        for (int l = tid; l < m; l += ENS_THREADS) {
+            const int j = l / nc, i = l - j * nc;
+            double sa = 0.0, sb = 0.0;
+            for (int q = 0; q < 4; q++) {
+                const int bx = i - (q & 1), by = j - (q >> 1);
+                if (bx < 0 || by < 0 || bx > nc - 2 || by > nc - 2) continue;
+                const int want = by * nc + bx;
+                double ca = 0.0, cb = 0.0;
+                for (int t = dstart[by]; t < dstart[by + 1]; t++) {
+                    const int p = order[t];
+                    if (key[p] != want) continue;
+                    const double w = cic_weight(pos[2 * p], pos[2 * p + 1], gg, unit, q);
+                    const unsigned bits = route_bits(type, p, a.route);
+                    if (bits & 1u) ca = dadd(ca, w);
+                    if (bits & 2u) cb = dadd(cb, w);
+                }
+                sa = dadd(sa, ca);
+                sb = dadd(sb, cb);
+            }
+            ra[l] = sa;
+            rb[l] = sb;
+        }
+        return;
+    }
+    const GaussParams &gp = a.gp;
+    for (int l = tid; l < m; l += ENS_THREADS) {
+        const int j = l / nc, i = l - j * nc;
+        const int r0 = max(j - gp.w1, 0), r1 = min(j + gp.w1, nc - 1);
+        const int c0 = i - gp.w0, c1 = i + gp.w0;
+        // merge of the window rows (each ascending in index): per row the
+        // next stamp on this node and its value
+        int hd[ENS_MERGE_ROWS], he[ENS_MERGE_ROWS];
+        double hv[ENS_MERGE_ROWS];
+        const int nr = r1 - r0 + 1;
+        auto advance = [&](int q, int t) {
+            for (; t < he[q]; t++) {
+                const int p = order[t];
+                const int col = key[p] - (key[p] / nc) * nc;
+                if (col < c0 || col > c1) continue;
+                double v;
+                if (gauss_term(pos[2 * p], pos[2 * p + 1], i, j, gg, gp, v)) {
+                    hv[q] = v;
+                    break;
+                }
+            }
+            hd[q] = t;
+        };
+        double sa = 0.0, sb = 0.0;
+        if (nr <= ENS_MERGE_ROWS) {
+            for (int q = 0; q < nr; q++) {
+                he[q] = dstart[r0 + q + 1];
+                advance(q, dstart[r0 + q]);
+            }
+            for (;;) {
+                int best = -1, bp = 0x7fffffff;
+                for (int q = 0; q < nr; q++) {
+                    if (hd[q] < he[q] && order[hd[q]] < bp) {
+                        bp = order[hd[q]];
+                        best = q;
+                    }
+                }
+                if (best < 0) break;
+                const unsigned bits = route_bits(type, bp, a.route);
+                if (bits & 1u) sa = dadd(sa, hv[best]);
+                if (bits & 2u) sb = dadd(sb, hv[best]);
+                advance(best, hd[best] + 1);
+            }
+        } else {  // a very tall stamp: repeated selection of the next index
+            int last = -1;
+            for (;;) {
+                int bp = 0x7fffffff;
+                double bv = 0.0;
+                for (int t = dstart[r0]; t < dstart[r1 + 1]; t++) {
+                    const int p = order[t];
+                    if (p <= last || p >= bp) continue;
+                    const int col = key[p] - (key[p] / nc) * nc;
+                    if (col < c0 || col > c1) continue;
+                    double v;
+                    if (gauss_term(pos[2 * p], pos[2 * p + 1], i, j, gg, gp, v)) {
+                        bp = p;
+                        bv = v;
+                    }
+                }
+                if (bp == 0x7fffffff) break;
+                const unsigned bits = route_bits(type, bp, a.route);
+                if (bits & 1u) sa = dadd(sa, bv);
+                if (bits & 2u) sb = dadd(sb, bv);
+                last = bp;
+            }
+        }
+        ra[l] = sa;
+        rb[l] = sb;
+    }
+}
+
 
 __global__ void __launch_bounds__(ENS_THREADS)
 k_ensemble(const __grid_constant__ EnsArgs a) {
@@ -142,7 +301,8 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
     double *lc = frc + 2 * n, *c = lc + n, *ra = c + m, *rb = ra + m;
     int *order = reinterpret_cast<int *>(ra + 8 * a.qper);
     int *starts = order + n, *cur = starts + a.ncell + 1, *key = cur + a.ncell;
-    uint8_t *type = reinterpret_cast<uint8_t *>(key + n);
+    int *dstart = key + n;  // deposit rows: starts (nc + 1), cursors (nc)
+    uint8_t *type = reinterpret_cast<uint8_t *>(dstart + 2 * a.nc + 1);
     DevStatus *st = a.st + s;
     for (int i = tid; i < 2 * n; i += ENS_THREADS) {
         pos[i] = a.pos[2 * n * s + i];
@@ -166,58 +326,11 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         const GridGeom &gg = a.gg;
         const int nc = gg.n;
         if (a.field) {
-            // ---- deposit_both (coupling.py:77-110, 113-138)
-            for (int l = tid; l < m; l += ENS_THREADS) {
-                ra[l] = 0.0;
-                rb[l] = 0.0;
-            }
-            __syncthreads();
-            for (int p = tid; p < n; p += ENS_THREADS) {
-                const unsigned bits = route_bits(type, p, a.route);
-                if (!bits) continue;
-                const double x = pos[2 * p], y = pos[2 * p + 1];
-                const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
-                const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
-                if (a.deposit_kind == CS_GAUSSIAN) {
-                    const long long b0 = (long long)floor(dadd(u0, 0.5));
-                    const long long b1 = (long long)floor(dadd(u1, 0.5));
-                    for (int o1 = -a.gp.w1; o1 <= a.gp.w1; o1++) {
-                        const long long j = b1 + o1;
-                        if (j < 0 || j >= nc) continue;
-                        const double dy = dmul(dsub(u1, (double)(b1 + o1)), gg.d1);
-                        const double dy2 = dmul(dy, dy);
-                        for (int o0 = -a.gp.w0; o0 <= a.gp.w0; o0++) {
-                            const long long i = b0 + o0;
-                            if (i < 0 || i >= nc) continue;
-                            const double dxp = dmul(dsub(u0, (double)(b0 + o0)), gg.d0);
-                            const double r2 = dadd(dmul(dxp, dxp), dy2);
-                            if (r2 <= a.gp.cut2) {
-                                const double v =
-                                    dmul(a.gp.inv_norm, cs_exp(-ddiv(r2, a.gp.two_h2)));
-                                if (bits & 1u) atomicAdd(&ra[j * nc + i], v);
-                                if (bits & 2u) atomicAdd(&rb[j * nc + i], v);
-                            }
-                        }
-                    }
-                } else {
-                    long long b0 = (long long)floor(u0), b1 = (long long)floor(u1);
-                    b0 = b0 < 0 ? 0 : (b0 > nc - 2 ? nc - 2 : b0);
-                    b1 = b1 < 0 ? 0 : (b1 > nc - 2 ? nc - 2 : b1);
-                    const double f0 = dsub(u0, (double)b0), f1 = dsub(u1, (double)b1);
-                    const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
-                    const double w[4] = {dmul(dmul(dsub(1.0, f0), dsub(1.0, f1)), unit),
-                                         dmul(dmul(f0, dsub(1.0, f1)), unit),
-                                         dmul(dmul(dsub(1.0, f0), f1), unit),
-                                         dmul(dmul(f0, f1), unit)};
-                    const long long at[4] = {b1 * nc + b0, b1 * nc + b0 + 1, (b1 + 1) * nc + b0,
-                                             (b1 + 1) * nc + b0 + 1};
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        if (bits & 1u) atomicAdd(&ra[at[q]], w[q]);
-                        if (bits & 2u) atomicAdd(&rb[at[q]], w[q]);
-                    }
-                }
-            }
+            // ---- deposit_both (coupling.py:77-110, 113-138), every node summed
+            // in the reference's particle order (see deposit.cu): depositing
+            // particles binned by deposit row (CIC: base row, gaussian: nearest
+            // row), ascending index inside a row; then one thread per node
+            ens_deposit(a, pos, type, key, order, dstart, ra, rb, tid, lane, warp);
             __syncthreads();
             // ---- rhs (field.py:224-229), in place into ra
             for (int l = tid; l < m; l += ENS_THREADS) {
@@ -638,7 +751,8 @@ static size_t ens_scratch(int nc) {
 static size_t ens_smem(int n, int nc, int ncell) {
     const size_t m = (size_t)nc * nc;
     return sizeof(double) * (9 * (size_t)n + m + ens_scratch(nc)) +
-           sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1) + (size_t)n + 16;
+           sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1 + 2 * (size_t)nc + 1) +
+           (size_t)n + 16;
 }
 
 int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {

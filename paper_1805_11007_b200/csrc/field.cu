@@ -3,7 +3,6 @@
 // step, the gradient stencil and bilinear sampling.
 //
 // References (chemosim/):
-//   deposits       coupling.py:45-187  (_gauss_scatter_pair, _cic_scatter)
 //   rhs            field.py:220-227    c(1 - dt g) + (dt ka) ra - (rb c)(dt kb)
 //   solve          field.py:162-201    (I - dt d_c L) c' = rhs
 //                  neumann: DCT-I modal solve, 4 dense GEMMs through the
@@ -16,9 +15,7 @@
 //                  negative weighted mass < -1e-12 -> warning
 //   gradient       field.py:128-137, 242-245  CSR rows in column order
 //   bilinear       coupling.py:216-262
-// Deposits accumulate with native f64 (or f32) atomics in L2; the stamp
-// arithmetic is the reference's, only the summation order of concurrent
-// contributions differs (T1 tolerance 1e-12).
+// Deposits: deposit.cu (node gathers in the reference's summation order).
 #include <cufft.h>
 #include <math.h>
 
@@ -27,159 +24,6 @@
 #include "common.cuh"
 
 namespace cs {
-
-// ------------------------------------------------------------------ deposit
-template <class G>
-__device__ __forceinline__ void atomic_add_g(G *a, double v);
-template <>
-__device__ __forceinline__ void atomic_add_g<double>(double *a, double v) {
-    atomicAdd(a, v);
-}
-template <>
-__device__ __forceinline__ void atomic_add_g<float>(float *a, double v) {
-    atomicAdd(a, (float)v);
-}
-
-template <class P, class G>
-__global__ void k_deposit_cic(const P *__restrict__ pos, const uint8_t *__restrict__ type,
-                              long long n, GridGeom gg, Route route, G *__restrict__ ra,
-                              G *__restrict__ rb, const DevStatus *st) {
-    if (st && st->abort) return;
-    const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
-    const int nc = gg.n;
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x) {
-        const unsigned bits = route_bits(type, p, route);
-        if (!bits) continue;
-        double x, y;
-        load2(pos, p, x, y);
-        const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
-        const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
-        long long b0, b1, c0, c1;
-        double f0, f1;
-        if (gg.per) {
-            const double base0 = floor(u0), base1 = floor(u1);
-            f0 = dsub(u0, base0);
-            f1 = dsub(u1, base1);
-            b0 = pymod((long long)base0, nc);
-            b1 = pymod((long long)base1, nc);
-            c0 = (b0 + 1) % nc;
-            c1 = (b1 + 1) % nc;
-        } else {
-            b0 = (long long)floor(u0);
-            b1 = (long long)floor(u1);
-            b0 = b0 < 0 ? 0 : (b0 > nc - 2 ? nc - 2 : b0);
-            b1 = b1 < 0 ? 0 : (b1 > nc - 2 ? nc - 2 : b1);
-            f0 = dsub(u0, (double)b0);
-            f1 = dsub(u1, (double)b1);
-            c0 = b0 + 1;
-            c1 = b1 + 1;
-        }
-        const double w00 = dmul(dmul(dsub(1.0, f0), dsub(1.0, f1)), unit);
-        const double w10 = dmul(dmul(f0, dsub(1.0, f1)), unit);
-        const double w01 = dmul(dmul(dsub(1.0, f0), f1), unit);
-        const double w11 = dmul(dmul(f0, f1), unit);
-        for (int which = 0; which < 2; which++) {
-            if (!(bits & (1u << which))) continue;
-            G *out = which == 0 ? ra : rb;
-            atomic_add_g(&out[b1 * nc + b0], w00);
-            atomic_add_g(&out[b1 * nc + c0], w10);
-            atomic_add_g(&out[c1 * nc + b0], w01);
-            atomic_add_g(&out[c1 * nc + c0], w11);
-        }
-    }
-}
-
-template <class P, class G>
-__global__ void k_deposit_gauss(const P *__restrict__ pos, const uint8_t *__restrict__ type,
-                                long long n, GridGeom gg, Route route, GaussParams gp,
-                                G *__restrict__ ra, G *__restrict__ rb, const DevStatus *st) {
-    if (st && st->abort) return;
-    const int nc = gg.n;
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x) {
-        const unsigned bits = route_bits(type, p, route);
-        if (!bits) continue;
-        double x, y;
-        load2(pos, p, x, y);
-        const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
-        const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
-        const long long b0 = (long long)floor(dadd(u0, 0.5));
-        const long long b1 = (long long)floor(dadd(u1, 0.5));
-        for (int o1 = -gp.w1; o1 <= gp.w1; o1++) {
-            long long j = b1 + o1;
-            if (gg.per) j = pymod(j, nc);
-            else if (j < 0 || j >= nc) continue;
-            const double dy = dmul(dsub(u1, (double)(b1 + o1)), gg.d1);
-            const double dy2 = dmul(dy, dy);
-            for (int o0 = -gp.w0; o0 <= gp.w0; o0++) {
-                long long i = b0 + o0;
-                if (gg.per) i = pymod(i, nc);
-                else if (i < 0 || i >= nc) continue;
-                const double dxp = dmul(dsub(u0, (double)(b0 + o0)), gg.d0);
-                const double r2 = dadd(dmul(dxp, dxp), dy2);
-                if (r2 <= gp.cut2) {
-                    const double v = dmul(gp.inv_norm, cs_exp(-ddiv(r2, gp.two_h2)));
-                    if (bits & 1u) atomic_add_g(&ra[j * nc + i], v);
-                    if (bits & 2u) atomic_add_g(&rb[j * nc + i], v);
-                }
-            }
-        }
-    }
-}
-
-GaussParams make_gauss(const GridGeom &gg, double h, double cutoff) {
-    GaussParams gp;
-    gp.inv_norm = 1.0 / (2.0 * M_PI * h * h);
-    gp.two_h2 = 2.0 * h * h;
-    gp.cut2 = cutoff * cutoff;
-    gp.w0 = (int)floor(cutoff / gg.d0 + 0.5);
-    gp.w1 = (int)floor(cutoff / gg.d1 + 0.5);
-    return gp;
-}
-
-int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
-                   const GridGeom &gg, int kind, double h, double cutoff,
-                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
-                   bool zero_first) {
-    const size_t m = (size_t)gg.n * gg.n;
-    const size_t es = prec == CS_F64 ? 8 : 4;
-    if (zero_first) {
-        CS_CUDA(cudaMemsetAsync(ra, 0, m * es, ctx->stream));
-        CS_CUDA(cudaMemsetAsync(rb, 0, m * es, ctx->stream));
-    }
-    if (n == 0) return CS_OK;
-    Route r;
-    r.bits[0] = bits[0];
-    r.bits[1] = bits[1];
-    r.bits[2] = bits[2];
-    const int B = 256;
-    const int G = grid_for(n, B);
-    if (kind == CS_CIC) {
-        if (prec == CS_F64)
-            k_deposit_cic<double, double><<<G, B, 0, ctx->stream>>>(
-                (const double *)pos, type, n, gg, r, (double *)ra, (double *)rb, st);
-        else
-            k_deposit_cic<float, float><<<G, B, 0, ctx->stream>>>(
-                (const float *)pos, type, n, gg, r, (float *)ra, (float *)rb, st);
-    } else {
-        const GaussParams gp = make_gauss(gg, h, cutoff);
-        if (prec == CS_F64)
-            k_deposit_gauss<double, double><<<G, B, 0, ctx->stream>>>(
-                (const double *)pos, type, n, gg, r, gp, (double *)ra, (double *)rb, st);
-        else
-            k_deposit_gauss<float, float><<<G, B, 0, ctx->stream>>>(
-                (const float *)pos, type, n, gg, r, gp, (float *)ra, (float *)rb, st);
-    }
-    CS_LAUNCH_CHECK();
-    ctx->launches += 1;
-    return CS_OK;
-}
-
-bool gauss_too_wide(const GridGeom &gg, double cutoff) {
-    const double dmin = gg.d0 < gg.d1 ? gg.d0 : gg.d1;
-    return gg.per && ((int)floor(cutoff / dmin + 0.5)) * 2 + 1 > gg.n;
-}
 
 // ------------------------------------------------------------------ bilinear
 template <class P, class G>

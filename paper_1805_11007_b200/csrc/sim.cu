@@ -23,8 +23,7 @@ namespace cs {
 
 int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,
                    const GridGeom &gg, int kind, double h, double cutoff,
-                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st,
-                   bool zero_first);
+                   const unsigned char bits[3], void *ra, void *rb, const DevStatus *st);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
                     DevStatus *st, int step, int *zero_q = nullptr);
 int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double dt,
@@ -458,7 +457,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 StageMark m(sim, CS_STAGE_DEPOSIT);
                 CS_TRY(launch_deposit(ctx, p.prec, s->pos, s->type, n, sim->gg, p.deposit_kind,
                                       p.kernel_h, p.kernel_cutoff, sim->bits, s->rho_a, s->rho_b,
-                                      st, true));
+                                      st));
             }
             {
                 StageMark m(sim, CS_STAGE_SOLVE);

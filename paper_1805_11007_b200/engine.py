@@ -333,7 +333,13 @@ class DeviceSim:
         self.n = int(params.n)
         self.prec = int(params.prec)
         h = N.C_p()
-        N.check(N.load_library().cs_sim_create(N.context(), ctypes.byref(params),
+        self._ctx = N.context()
+        # the stream this simulation was created on: every call rebinds the
+        # (process-wide) library context to it, so a later N.context() under
+        # another torch stream cannot move the simulation off it
+        import torch
+        self._stream = N.C_p(torch.cuda.current_stream().cuda_stream)
+        N.check(N.load_library().cs_sim_create(self._ctx, ctypes.byref(params),
                                                ctypes.byref(h)), "cs_sim_create")
         self._h = h
         self._st = N.SimState_t()
@@ -349,7 +355,7 @@ class DeviceSim:
         (u: k (N,) f64 blocks of reaction uniforms when params.react)."""
         if stride is None:
             stride = 2 * self.n
-        lib = N.load_library()
+        lib = self._bind()
         if u is None:
             N.check(lib.cs_sim_step(self._h, ctypes.byref(self._st), N.ptr(xi), int(stride),
                                     int(k)), "cs_sim_step")
@@ -358,9 +364,14 @@ class DeviceSim:
                                           int(stride), N.ptr(u), self.n, int(k)),
                     "cs_sim_step_react")
 
+    def _bind(self):
+        lib = N.load_library()
+        lib.cs_ctx_set_stream(self._ctx, self._stream)
+        return lib
+
     def status(self) -> N.Status_t:
         st = N.Status_t()
-        N.check(N.load_library().cs_sim_status(self._h, ctypes.byref(st)), "cs_sim_status")
+        N.check(self._bind().cs_sim_status(self._h, ctypes.byref(st)), "cs_sim_status")
         return st
 
     @property
@@ -370,12 +381,12 @@ class DeviceSim:
 
     def import_state(self) -> None:
         """Reload the engine's internal state from the state tensors."""
-        N.check(N.load_library().cs_sim_import(self._h, ctypes.byref(self._st)), "cs_sim_import")
+        N.check(self._bind().cs_sim_import(self._h, ctypes.byref(self._st)), "cs_sim_import")
 
     def export_state(self) -> None:
         """Write the engine's internal state back into the state tensors
         (sorted engine; a no-op for the direct engine)."""
-        N.check(N.load_library().cs_sim_export(self._h, ctypes.byref(self._st)), "cs_sim_export")
+        N.check(self._bind().cs_sim_export(self._h, ctypes.byref(self._st)), "cs_sim_export")
 
     def launches(self) -> int:
         return int(N.load_library().cs_sim_launches(self._h))
@@ -794,8 +805,16 @@ def run_ensemble(config: SimConfig) -> EnsembleResult:
     are reduced in sample order either way; ``threads`` sizes the host pool
     that draws the samples' random blocks."""
     from . import ensemble as E
+    ens = None
     if E.supported(config) is None and os.environ.get("CS_ENSEMBLE") != "sequential":
-        ens = E.Ensemble(config, threads=config.threads if config.threads > 1 else None)
+        try:
+            ens = E.Ensemble(config, threads=config.threads if config.threads > 1 else None)
+        except N.NativeError as exc:
+            # a realisation too large for one CTA's shared memory (cs_ens_create
+            # reports it): run the samples one by one instead
+            if "shared memory" not in str(exc):
+                raise
+    if ens is not None:
         try:
             all_obs = ens.run()
         finally:

@@ -207,12 +207,14 @@ class Ensemble:
             self._obs = (torch.empty(self.S, dtype=torch.int64, device="cuda"),
                          torch.empty(self.S, dtype=torch.float64, device="cuda"))
         na, msd = self._obs
+        N.context()  # on the current stream: ordered after the step kernels queued on it
         N.check(N.load_library().cs_ens_observe(self._h, ctypes.byref(self._st), N.ptr(na),
                                                 N.ptr(msd)), "cs_ens_observe")
         return na.cpu().numpy(), msd.cpu().numpy()
 
     def status(self):
         out = (N.Status_t * self.S)()
+        N.context()  # the status copy follows the step kernels on the current stream
         N.check(N.load_library().cs_ens_status(self._h, out), "cs_ens_status")
         return out
 
@@ -346,6 +348,7 @@ class Ensemble:
                         side.wait_event(done[i])
                     drawn_i = self._draw_device(k, into=bufs[i])
                     ready[i].record(side)
+                N.context()  # rebind the library to the main stream
                 return drawn_i
             done_used = [False, False]
             side.wait_stream(main)

@@ -1,13 +1,13 @@
 """Batched ensembles (csrc/ensemble.cu) against the
 sample-by-sample Realisation path and the reference's own trajectories.
 
-Without a deposit the batched engine performs the direct engine's
-arithmetic in the same order, so field-free ensembles (the counts and msd
-presets) must equal the sequential run bit for bit.  With the field on the
-shared-memory deposit sums concurrent stamps in a different order (1e-16),
-so single-step states agree to 1e-12 and the reference's own fig1-like
-trajectory (tests/golden/reaction_traj.npz) to the composed-trajectory
-tolerance 1e-10 over 30 steps, species exactly."""
+The batched engine performs the direct engine's arithmetic in the same
+order -- the deposit included: both gather every node's stamps in the
+reference's particle order -- so ensembles equal the sequential run bit for
+bit, with and without the field.  Against the reference's own fig1-like
+trajectory (tests/golden/reaction_traj.npz) the composed-trajectory
+tolerance 1e-10 over 30 steps applies (the DCT solve's GEMM accumulation
+order is not OpenBLAS's), species exactly."""
 
 import os
 import warnings
@@ -55,10 +55,10 @@ def test_field_free_ensembles_equal_sequential_bitwise(preset, kw, monkeypatch):
     assert seq.seeds == bat.seeds and bat.samples == 5
 
 
-def test_fig1_ensemble_states_track_sequential_realisations():
+def test_fig1_ensemble_states_equal_sequential_realisations():
     """fig1 (soft forces, gaussian deposit on the neumann 52^2 grid,
-    fixed-step reactions): after 25 steps every sample's state is within
-    1e-10 of its own Realisation, species identical."""
+    fixed-step reactions): after 25 steps every sample's state is bit for
+    bit its own Realisation's (both engines deposit in particle order)."""
     cfg = _quiet(samples=6, seed_base=3, r_alpha=4000.0, r_beta=2000.0)
     cfg = _quiet(**{**cfg.as_dict(), "t_final": 25 * cfg.dt})
     ens = Ensemble(cfg)
@@ -75,6 +75,8 @@ def test_fig1_ensemble_states_track_sequential_realisations():
         np.testing.assert_allclose(pos[s], r.pop.positions, rtol=0, atol=1e-10)
         assert np.array_equal(sp[s], r.pop.species)
         np.testing.assert_allclose(c[s], r.field.c, rtol=1e-9, atol=1e-9)
+        assert np.array_equal(c[s], r.field.c), s
+        assert np.array_equal(pos[s], r.pop.positions), s
     ens.close()
 
 
@@ -120,11 +122,72 @@ def test_device_rng_ensemble_equals_host_rng_ensemble():
     for k in (7, 13):
         a.advance(k)
         b.advance(k)
-    for key in ("pos", "species", "anchor"):
-        assert torch.equal(a.state[key], b.state[key]) or key != "pos" or \
-            torch.allclose(a.state[key], b.state[key], rtol=0, atol=1e-12), key
+    for key in ("pos", "species", "anchor", "c"):
+        assert torch.equal(a.state[key], b.state[key]), key
     a.close()
     b.close()
+
+
+def test_long_blocks_many_samples_device_rng_run_equals_host_rng_run():
+    """Ensemble.run with the device RNG drawing the next block on a side
+    stream: the status and observables of each block must be read after the
+    block's step kernel (same stream), so many samples x long blocks give
+    the host-RNG run's observables bit for bit."""
+    cfg = _quiet(samples=96, seed_base=21, r_alpha=2000.0, r_beta=800.0, output_every=150)
+    cfg = _quiet(**{**cfg.as_dict(), "t_final": 600 * cfg.dt})
+    runs = []
+    for rng in ("device", "host"):
+        e = Ensemble(cfg, rng=rng)
+        runs.append(e.run())
+        e.close()
+    for oa, ob in zip(*runs):
+        for name in ("times", "counts", "msd", "hist_alpha", "hist_beta", "field_c"):
+            assert np.array_equal(getattr(oa, name), getattr(ob, name)), name
+
+
+def test_fig1_cli_reruns_byte_identical(tmp_path):
+    """Acceptance criterion 10 of the reference
+    (pkg/tests/test_acceptance.py:341-355): two `--experiment fig1
+    --samples 2` runs write byte-identical CSV files -- on the batched
+    engine and on the sample-by-sample Realisation path (direct engine)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("batched", "sequential"):
+        for tag in ("a", "b"):
+            env = dict(os.environ, PYTHONPATH=root)
+            if mode == "sequential":
+                env["CS_ENSEMBLE"] = "sequential"
+            out = tmp_path / f"{mode}_{tag}"
+            proc = subprocess.run([sys.executable, "-m", "paper_1805_11007_b200", "--experiment",
+                                   "fig1", "--samples", "2", "--output-dir", str(out)],
+                                  capture_output=True, text=True, env=env, cwd=root)
+            assert proc.returncode == 0, proc.stderr
+            outs[(mode, tag)] = out
+    for mode in ("batched", "sequential"):
+        a, b = outs[(mode, "a")], outs[(mode, "b")]
+        names = sorted(p.name for p in a.glob("*.csv"))
+        assert names
+        for name in names:
+            assert (a / name).read_bytes() == (b / name).read_bytes(), (mode, name)
+    # and the two engines agree with each other byte for byte
+    for name in sorted(p.name for p in outs[("batched", "a")].glob("*.csv")):
+        assert (outs[("batched", "a")] / name).read_bytes() == \
+            (outs[("sequential", "a")] / name).read_bytes(), name
+
+
+def test_run_ensemble_beyond_one_cta_falls_back(monkeypatch):
+    """A realisation whose state exceeds one CTA's shared memory (here 3000
+    particles on a 52^2 grid) runs sample by sample instead of failing."""
+    cfg = _quiet(n_alpha_0=1500, n_beta_0=1500, samples=2, r_alpha=0.0,
+                 t_final=0.0)
+    cfg = _quiet(**{**cfg.as_dict(), "t_final": 3 * cfg.dt})
+    res = cs.run_ensemble(cfg)
+    monkeypatch.setenv("CS_ENSEMBLE", "sequential")
+    seq = cs.run_ensemble(cfg)
+    assert np.array_equal(res.msd_mean, seq.msd_mean)
+    assert np.array_equal(res.counts_mean, seq.counts_mean)
 
 
 def test_tamed_ensemble_tracks_realisations():

@@ -2,7 +2,7 @@
 reference's own golden outputs.  Tier T1/T2 of SURVEY 8c:
 
   pair sets, forces, EM, boundaries, gradient, bilinear : bit-exact (fp64)
-  deposits (atomic accumulation order)                  : 1e-12 relative
+  deposits (node gathers in the reference's particle order): bit-exact
   implicit solve (GEMM / FFT vs OpenBLAS / SuperLU)      : rtol 1e-11, atol 1e-13
   multi-step trajectories with the field on             : 1e-10 absolute
   fp32 storage                                          : bit-exact vs the fp64
@@ -238,8 +238,7 @@ def test_coupling_golden():
         pop = _pop(g[f"k{k}_pos"], g[f"k{k}_species"])
         ra, rb = cs.deposit_both(pop, grid, kern)
         for got, ref in ((ra, g[f"k{k}_ra"]), (rb, g[f"k{k}_rb"])):
-            scale = max(np.abs(ref).max(), 1.0)
-            assert np.max(np.abs(got - ref)) <= 1e-12 * scale, k
+            assert np.array_equal(got, ref), k
         f = cs.Field(c=g[f"k{k}_c"], grad=g[f"k{k}_grad"], rho_alpha=ra, rho_beta=rb)
         import warnings
         with warnings.catch_warnings():
@@ -247,6 +246,42 @@ def test_coupling_golden():
             cs.refresh_particle_fields(pop, f, grid, chi)
         assert np.array_equal(pop.local_concentration, g[f"k{k}_conc"]), k
         assert np.array_equal(pop.drift, g[f"k{k}_drift"]), k
+
+
+@pytest.mark.parametrize("kind,per,n,n_c,clustered", [
+    ("cic", False, 10_000, 128, False),     # cfg1-like
+    ("cic", True, 100_000, 512, False),     # cfg2-like
+    ("cic", True, 50_000, 64, True),        # dense cells
+    ("gaussian", False, 1_000, 52, True),   # fig1-like clusters: > 48 stamps per node
+    ("gaussian", True, 20_000, 128, False),
+])
+def test_deposit_bitwise_vs_oracle_and_rerun(kind, per, n, n_c, clustered):
+    """deposit_both at sizes beyond the goldens: bit for bit the oracle's
+    particle-order sums (pinned to the reference), and identical on a rerun
+    (no atomics in the summation order)."""
+    rng = np.random.default_rng(n + n_c)
+    if clustered:
+        centres = rng.uniform(-0.3, 0.3, (4, 2))
+        pos = centres[rng.integers(0, 4, n)] + rng.normal(0, 0.03, (n, 2))
+        pos = np.clip(pos, -0.5, 0.4999)
+    else:
+        pos = rng.uniform(-0.5, 0.5, (n, 2))
+    sp = rng.integers(0, 2, n).astype(np.uint8)
+    grid = cs.Grid.square(n_c, 1.0, "periodic" if per else "neumann")
+    h = 0.02 if kind == "gaussian" else 0.0
+    kern = cs.Kernel(kind="cic") if kind == "cic" else cs.Kernel("gaussian", h, 3 * h)
+    pop = _pop(pos, sp)
+    ra, rb = cs.deposit_both(pop, grid, kern)
+    ra2, rb2 = cs.deposit_both(pop, grid, kern)
+    assert np.array_equal(ra, ra2) and np.array_equal(rb, rb2)
+    lo = list(grid.lo)
+    if kind == "cic":
+        ea = oracle.cic_deposit(pos, sp == 0, n_c, lo, grid.spacing, per)
+        eb = oracle.cic_deposit(pos, sp == 1, n_c, lo, grid.spacing, per)
+    else:
+        ea, eb = oracle.gauss_deposit(pos, sp, n_c, lo, grid.spacing, per, h, 3 * h)
+    assert np.array_equal(ra, ea)
+    assert np.array_equal(rb, eb)
 
 
 def test_gaussian_cutoff_wider_than_periodic_grid_rejected():

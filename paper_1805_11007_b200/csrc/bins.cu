@@ -18,13 +18,18 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "deposit.cuh"
 #include "scan.cuh"
 
 namespace cs {
 
-template <class P>
+// keys[i] = cell of particle i; with a DepBin also keys[n + i] = nflat +
+// its deposit bin (-1: not depositing) -- one count array for both
+template <class P, bool DEP>
 __global__ void k_bin_count(const P *__restrict__ pos, long long n, BinGeom g,
-                            int *__restrict__ keys, int *__restrict__ counts) {
+                            int *__restrict__ keys, int *__restrict__ counts,
+                            const uint8_t *__restrict__ type, DepBin dep) {
+    const int nflat = g.n0 * g.n1;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double x, y;
@@ -34,35 +39,66 @@ __global__ void k_bin_count(const P *__restrict__ pos, long long n, BinGeom g,
         const int key = c1 * g.n0 + c0;
         keys[i] = key;
         atomicAdd(&counts[key], 1);
+        if (DEP) {
+            int dk = -1;
+            if (route_bits(type, i, dep.route)) {
+                const GridGeom &gg = dep.gg;
+                const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
+                const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+                if (fabs(u0) < 0x1p52 && fabs(u1) < 0x1p52) {
+                    dk = nflat + dep_bin_axis(u1, dep.kind, gg.n, gg.per) * gg.n +
+                         dep_bin_axis(u0, dep.kind, gg.n, gg.per);
+                    atomicAdd(&counts[dk], 1);
+                }
+            }
+            keys[n + i] = dk;
+        }
     }
 }
 
+template <bool DEP>
 __global__ void k_bin_scatter(const int *__restrict__ keys, long long n,
                               const int *__restrict__ starts, int *__restrict__ counts,
                               int *__restrict__ slots) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int key = keys[i];
-        const int slot = starts[key] + atomicSub(&counts[key], 1) - 1;
-        slots[slot] = (int)i;
+        slots[starts[key] + atomicSub(&counts[key], 1) - 1] = (int)i;
+        if (DEP) {
+            const int dk = keys[n + i];
+            if (dk >= 0) slots[starts[dk] + atomicSub(&counts[dk], 1) - 1] = (int)i;
+        }
     }
 }
 
 // Stable placement: the particle in slot t (cell order, arbitrary inside a
 // cell) goes to its cell start + the number of the cell's particles with a
 // smaller index (O(m) reads of the cell's L1-resident slots per particle).
-template <class P>
+// Deposit slots (t >= n, with a DepBin) are ranked the same way inside
+// their bin; the particle's position and (index, route) word are copied to
+// dpos / dmeta at t - n.
+template <class P, bool DEP>
 __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict__ keys,
                            const int *__restrict__ starts, long long n, int *__restrict__ order,
                            const P *__restrict__ pos, const uint8_t *__restrict__ type,
-                           P *__restrict__ spos, uint8_t *__restrict__ stype) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+                           P *__restrict__ spos, uint8_t *__restrict__ stype, int nall,
+                           P *__restrict__ dpos, unsigned *__restrict__ dmeta, Route route) {
+    const long long total = DEP ? (long long)starts[nall] : n;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const int v = slots[t];
-        const int key = keys[v];
+        const bool dep = DEP && t >= n;
+        const int key = dep ? keys[n + v] : keys[v];
         const int s = starts[key], e = starts[key + 1];
         int rank = 0;
         for (int u = s; u < e; u++) rank += __ldg(slots + u) < v;
+        if (dep) {
+            const long long d = s + rank - n;
+            reinterpret_cast<typename Vec2<P>::T *>(dpos)[d] =
+                reinterpret_cast<const typename Vec2<P>::T *>(pos)[v];
+            dmeta[d] = (unsigned)v | (route_bits(type, v, route) << 30);
+            continue;
+        }
         order[s + rank] = v;
         spos[2 * (s + rank)] = pos[2 * (long long)v];
         spos[2 * (s + rank) + 1] = pos[2 * (long long)v + 1];
@@ -176,29 +212,43 @@ int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n, int *z
 }
 
 // ------------------------------------------------------------------ driver
+template <class P, bool DEP>
+static void bin_launch(cs_ctx *ctx, const P *pos, long long n, const BinGeom &g,
+                       const uint8_t *type, const DepBin &dep, int nall, int phase) {
+    const int B = 256;
+    int *keys = ctx->keys.as<int>(), *counts = ctx->counts.as<int>();
+    int *starts = ctx->starts.as<int>();
+    if (phase == 0)
+        k_bin_count<P, DEP><<<grid_for(n, B), B, 0, ctx->stream>>>(pos, n, g, keys, counts, type,
+                                                                    dep);
+    else if (phase == 1)
+        k_bin_scatter<DEP><<<grid_for(n, B), B, 0, ctx->stream>>>(keys, n, starts, counts,
+                                                                  ctx->skeys.as<int>());
+    else
+        k_seg_rank<P, DEP><<<grid_for(DEP ? 2 * n : n, B), B, 0, ctx->stream>>>(
+            ctx->skeys.as<int>(), keys, starts, n, ctx->order.as<int>(), pos, type,
+            ctx->spos.as<P>(), ctx->stype.as<uint8_t>(), nall, ctx->dep_pos.as<P>(),
+            ctx->dep_meta.as<unsigned>(), dep.route);
+}
+
 int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
-                  const uint8_t *type) {
+                  const uint8_t *type, const DepBin *dep, bool *dep_done) {
+    if (dep_done) *dep_done = false;
     const long long nflat = (long long)g.n0 * g.n1;
-    if (nflat >= (1LL << 31) - 1) {
-        set_error("cell table too large (%lld cells)", nflat);
+    const long long nb = dep ? (long long)dep->gg.n * dep->gg.n : 0;
+    const long long nall = nflat + nb;
+    if (nall >= (1LL << 31) - 1 || (dep && 2 * n >= (1LL << 31) - 1)) {
+        set_error("cell table too large (%lld cells)", nall);
         return CS_ERR_PARAM;
     }
-    const size_t nb = sizeof(int) * (size_t)(n > 0 ? n : 1);
-    CS_TRY(ctx->keys.ensure(nb));
-    CS_TRY(ctx->skeys.ensure(nb));
-    CS_TRY(ctx->order.ensure(nb));
-    CS_TRY(ctx->starts.ensure(sizeof(int) * (size_t)(nflat + 1)));
-    const size_t cb = sizeof(int) * (size_t)nflat;
-    if (ctx->counts.bytes < cb) {
-        CS_TRY(ctx->counts.ensure(cb));
-        CS_CUDA(cudaMemsetAsync(ctx->counts.p, 0, ctx->counts.bytes, ctx->stream));
-    }
-    int *keys = ctx->keys.as<int>(), *counts = ctx->counts.as<int>();
-    int *starts = ctx->starts.as<int>(), *order = ctx->order.as<int>();
-    CS_TRY(ctx->spos.ensure((prec == CS_F64 ? 16 : 8) * (size_t)(n > 0 ? n : 1)));
-    CS_TRY(ctx->stype.ensure((size_t)(n > 0 ? n : 1)));
+    const size_t np = (size_t)(n > 0 ? n : 1);
+    CS_TRY(ctx->order.ensure(sizeof(int) * np));
+    CS_TRY(ctx->spos.ensure((prec == CS_F64 ? 16 : 8) * np));
+    CS_TRY(ctx->stype.ensure(np));
     uint8_t *stype = ctx->stype.as<uint8_t>();
     if (n <= BIN_SMALL_MAX_N && nflat <= BIN_SMALL_MAX_CELLS && !getenv("CS_BIN_MULTI")) {
+        CS_TRY(ctx->starts.ensure(sizeof(int) * (size_t)(nflat + 1)));
+        int *starts = ctx->starts.as<int>(), *order = ctx->order.as<int>();
         const size_t smem = sizeof(int) * (size_t)(2 * nflat + 1 + 2 * n);
         static size_t smem_set = 0;
         if (smem > smem_set) {
@@ -220,32 +270,40 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
         ctx->launches += 1;
         return CS_OK;
     }
-    const int B = 256;
-    if (n > 0) {
-        if (prec == CS_F64)
-            k_bin_count<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
-                static_cast<const double *>(pos), n, g, keys, counts);
-        else
-            k_bin_count<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
-                static_cast<const float *>(pos), n, g, keys, counts);
-        CS_LAUNCH_CHECK();
+    const size_t nk = dep ? 2 * np : np;
+    CS_TRY(ctx->keys.ensure(sizeof(int) * nk));
+    CS_TRY(ctx->skeys.ensure(sizeof(int) * nk));
+    CS_TRY(ctx->starts.ensure(sizeof(int) * (size_t)(nall + 1)));
+    if (dep) {
+        CS_TRY(ctx->dep_pos.ensure((prec == CS_F64 ? 16 : 8) * np));
+        CS_TRY(ctx->dep_meta.ensure(sizeof(unsigned) * np));
     }
-    CS_TRY(exclusive_scan_i32(ctx, counts, starts, nflat));
-    if (n > 0) {
-        k_bin_scatter<<<grid_for(n, B), B, 0, ctx->stream>>>(keys, n, starts, counts,
-                                                             ctx->skeys.as<int>());
-        CS_LAUNCH_CHECK();
-        if (prec == CS_F64)
-            k_seg_rank<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
-                ctx->skeys.as<int>(), keys, starts, n, order, static_cast<const double *>(pos),
-                type, ctx->spos.as<double>(), stype);
-        else
-            k_seg_rank<float><<<grid_for(n, B), B, 0, ctx->stream>>>(
-                ctx->skeys.as<int>(), keys, starts, n, order, static_cast<const float *>(pos),
-                type, ctx->spos.as<float>(), stype);
-        CS_LAUNCH_CHECK();
+    const size_t cb = sizeof(int) * (size_t)nall;
+    if (ctx->counts.bytes < cb) {  // kept all-zero between calls (the scatter counts down)
+        CS_TRY(ctx->counts.ensure(cb));
+        CS_CUDA(cudaMemsetAsync(ctx->counts.p, 0, ctx->counts.bytes, ctx->stream));
     }
-    ctx->launches += 3;
+    const DepBin none{};
+    const DepBin &d = dep ? *dep : none;
+    for (int phase = 0; phase < 3; phase++) {
+        if (phase == 1) CS_TRY(exclusive_scan_i32(ctx, ctx->counts.as<int>(),
+                                                  ctx->starts.as<int>(), nall));
+        if (n == 0) continue;
+        if (prec == CS_F64) {
+            if (dep) bin_launch<double, true>(ctx, static_cast<const double *>(pos), n, g, type, d,
+                                              (int)nall, phase);
+            else bin_launch<double, false>(ctx, static_cast<const double *>(pos), n, g, type, d,
+                                           (int)nall, phase);
+        } else {
+            if (dep) bin_launch<float, true>(ctx, static_cast<const float *>(pos), n, g, type, d,
+                                             (int)nall, phase);
+            else bin_launch<float, false>(ctx, static_cast<const float *>(pos), n, g, type, d,
+                                          (int)nall, phase);
+        }
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    if (dep_done) *dep_done = dep != nullptr;
     return CS_OK;
 }
 

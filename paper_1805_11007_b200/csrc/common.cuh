@@ -308,8 +308,18 @@ inline int grid_for(long long n, int block, int max_blocks = 148 * 64) {
 // bins.cu
 // order / starts of the reference's cell list, and positions (and types, if
 // given) copied into that order in ctx->spos / ctx->stype for the force walk
+struct DepBin;
+// With `dep`, the same pass also bins the depositing particles for the
+// ordered deposit (deposit.cu): their bins follow the cells in ctx->counts /
+// ctx->starts (starts[nflat + b], slots numbered from n), the positions and
+// (index, route) words in bin order go to ctx->dep_pos / ctx->dep_meta.
+// *dep_done tells whether it did (the single-block small path does not).
 int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
-                  const uint8_t *type = nullptr);
+                  const uint8_t *type = nullptr, const DepBin *dep = nullptr,
+                  bool *dep_done = nullptr);
+int launch_deposit_binned(cs_ctx *ctx, int prec, const GridGeom &gg, int kind, double h,
+                          double cutoff, const int *starts, int off, void *ra, void *rb,
+                          const DevStatus *st);
 int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n,
                        int *zero_in = nullptr);
 // forces.cu
@@ -346,6 +356,13 @@ __device__ __forceinline__ unsigned route_bits(const uint8_t *type, long long p,
 struct GaussParams {
     double inv_norm, two_h2, cut2;
     int w0, w1;
+};
+
+// Deposit bins built together with the cell list (bins.cu / deposit.cu).
+struct DepBin {
+    GridGeom gg;
+    int kind;  // CS_CIC / CS_GAUSSIAN
+    Route route;
 };
 
 GaussParams make_gauss(const GridGeom &gg, double h, double cutoff);

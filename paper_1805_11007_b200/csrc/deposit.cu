@@ -90,7 +90,7 @@ __global__ void k_dep_rank(const int *__restrict__ slots, const int *__restrict_
 
 template <class P, class G>
 __global__ void __launch_bounds__(256)
-k_dep_gather_cic(const int *__restrict__ starts, const P *__restrict__ spos,
+k_dep_gather_cic(const int *__restrict__ starts, int off, const P *__restrict__ spos,
                  const unsigned *__restrict__ meta, GridGeom gg, G *__restrict__ ra,
                  G *__restrict__ rb, const DevStatus *st) {
     if (st && st->abort) return;
@@ -112,8 +112,8 @@ k_dep_gather_cic(const int *__restrict__ starts, const P *__restrict__ spos,
             }
             const int key = by * n + bx;
             double ca = 0.0, cb = 0.0;
-            const int e = starts[key + 1];
-            for (int t = starts[key]; t < e; t++) {
+            const int e = starts[key + 1] - off;
+            for (int t = starts[key] - off; t < e; t++) {
                 double x, y;
                 load2(spos, t, x, y);
                 const double w = cic_weight(x, y, gg, unit, q);
@@ -134,7 +134,8 @@ k_dep_gather_cic(const int *__restrict__ starts, const P *__restrict__ spos,
 template <class Visit>
 __device__ __forceinline__ void gauss_window(int i, int j, const GridGeom &gg,
                                              const GaussParams &gp,
-                                             const int *__restrict__ starts, Visit visit) {
+                                             const int *__restrict__ starts, int off,
+                                             Visit visit) {
     const int n = gg.n;
     for (int o1 = -gp.w1; o1 <= gp.w1; o1++) {
         int jj = j + o1;
@@ -158,7 +159,8 @@ __device__ __forceinline__ void gauss_window(int i, int j, const GridGeom &gg,
             ns = seg[0][0] <= seg[0][1] ? 1 : 0;
         }
         for (int k = 0; k < ns; k++) {
-            const int t0 = starts[jj * n + seg[k][0]], t1 = starts[jj * n + seg[k][1] + 1];
+            const int t0 = starts[jj * n + seg[k][0]] - off;
+            const int t1 = starts[jj * n + seg[k][1] + 1] - off;
             for (int t = t0; t < t1; t++) visit(t);
         }
     }
@@ -168,7 +170,7 @@ constexpr int DEP_BUF = 48;
 
 template <class P, class G>
 __global__ void __launch_bounds__(128)
-k_dep_gather_gauss(const int *__restrict__ starts, const P *__restrict__ spos,
+k_dep_gather_gauss(const int *__restrict__ starts, int off, const P *__restrict__ spos,
                    const unsigned *__restrict__ meta, GridGeom gg, GaussParams gp,
                    G *__restrict__ ra, G *__restrict__ rb, const DevStatus *st) {
     if (st && st->abort) return;
@@ -187,7 +189,7 @@ k_dep_gather_gauss(const int *__restrict__ starts, const P *__restrict__ spos,
         while (more) {
             int cnt = 0;
             more = false;
-            gauss_window(i, j, gg, gp, starts, [&](int t) {
+            gauss_window(i, j, gg, gp, starts, off, [&](int t) {
                 const unsigned mk = meta[t];
                 const unsigned id = mk & DEP_ID_MASK;
                 if ((long long)id <= last) return;
@@ -241,10 +243,50 @@ bool gauss_too_wide(const GridGeom &gg, double cutoff) {
 }
 
 template <class P, class G>
+static int dep_gather_t(cs_ctx *ctx, const int *starts, int off, const P *spos,
+                        const unsigned *meta, const GridGeom &gg, int kind, double h,
+                        double cutoff, G *ra, G *rb, const DevStatus *st) {
+    const long long nb = (long long)gg.n * gg.n;
+    if (kind == CS_CIC) {
+        k_dep_gather_cic<P, G><<<grid_for(nb, 256), 256, 0, ctx->stream>>>(starts, off, spos,
+                                                                            meta, gg, ra, rb, st);
+    } else {
+        const GaussParams gp = make_gauss(gg, h, cutoff);
+        k_dep_gather_gauss<P, G><<<grid_for(nb, 128), 128, 0, ctx->stream>>>(
+            starts, off, spos, meta, gg, gp, ra, rb, st);
+    }
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+// The gather alone, over bins built by bin_particles(..., DepBin) together
+// with the cell list: the deposit bins' starts are starts[nflat ..] and
+// their slots are numbered from n (off = n).
+int launch_deposit_binned(cs_ctx *ctx, int prec, const GridGeom &gg, int kind, double h,
+                          double cutoff, const int *starts, int off, void *ra, void *rb,
+                          const DevStatus *st) {
+    if (prec == CS_F64)
+        return dep_gather_t<double, double>(ctx, starts, off, ctx->dep_pos.as<double>(),
+                                            ctx->dep_meta.as<unsigned>(), gg, kind, h, cutoff,
+                                            (double *)ra, (double *)rb, st);
+    return dep_gather_t<float, float>(ctx, starts, off, ctx->dep_pos.as<float>(),
+                                      ctx->dep_meta.as<unsigned>(), gg, kind, h, cutoff,
+                                      (float *)ra, (float *)rb, st);
+}
+
+template <class P, class G>
 static int deposit_t(cs_ctx *ctx, const P *pos, const uint8_t *type, long long n,
                      const GridGeom &gg, int kind, double h, double cutoff, const Route &r,
                      G *ra, G *rb, const DevStatus *st) {
     const long long nb = (long long)gg.n * gg.n;
+    if (kind == CS_GAUSSIAN) {
+        const GaussParams gp = make_gauss(gg, h, cutoff);
+        if (gp.w0 > 64 || gp.w1 > 64) {
+            set_error("deposit: gaussian stamp wider than 129 nodes");
+            return CS_ERR_PARAM;
+        }
+    }
     if (nb >= (1LL << 31) - 1 || n > (long long)DEP_ID_MASK) {
         set_error("deposit: grid or particle count too large");
         return CS_ERR_PARAM;
@@ -278,21 +320,7 @@ static int deposit_t(cs_ctx *ctx, const P *pos, const uint8_t *type, long long n
         CS_LAUNCH_CHECK();
         ctx->launches += 3;
     }
-    if (kind == CS_CIC) {
-        k_dep_gather_cic<P, G><<<grid_for(nb, 256), 256, 0, ctx->stream>>>(starts, spos, meta, gg,
-                                                                            ra, rb, st);
-    } else {
-        const GaussParams gp = make_gauss(gg, h, cutoff);
-        if (gp.w0 > 64 || gp.w1 > 64) {
-            set_error("deposit: gaussian stamp wider than 129 nodes");
-            return CS_ERR_PARAM;
-        }
-        k_dep_gather_gauss<P, G><<<grid_for(nb, 128), 128, 0, ctx->stream>>>(
-            starts, spos, meta, gg, gp, ra, rb, st);
-    }
-    CS_LAUNCH_CHECK();
-    ctx->launches += 1;
-    return CS_OK;
+    return dep_gather_t<P, G>(ctx, starts, 0, spos, meta, gg, kind, h, cutoff, ra, rb, st);
 }
 
 int launch_deposit(cs_ctx *ctx, int prec, const void *pos, const uint8_t *type, long long n,

@@ -452,12 +452,31 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
     for (int kk = 0; kk < k; kk++) {
         const int step = sim->steps_done + kk;
         const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
+        // the cell list and the deposit bins come from the same start-of-step
+        // positions: one binning pass builds both (the deposit is a gather
+        // over its bins, deposit.cu)
+        bool binned = false, dep_binned = false;
+        if (p.field_active && p.interaction == 1) {
+            StageMark m(sim, CS_STAGE_BIN);
+            DepBin db;
+            db.gg = sim->gg;
+            db.kind = p.deposit_kind;
+            for (int t = 0; t < 3; t++) db.route.bits[t] = sim->bits[t];
+            CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom, s->type, &db, &dep_binned));
+            binned = true;
+        }
         if (p.field_active) {
             {
                 StageMark m(sim, CS_STAGE_DEPOSIT);
-                CS_TRY(launch_deposit(ctx, p.prec, s->pos, s->type, n, sim->gg, p.deposit_kind,
-                                      p.kernel_h, p.kernel_cutoff, sim->bits, s->rho_a, s->rho_b,
-                                      st));
+                if (dep_binned)
+                    CS_TRY(launch_deposit_binned(
+                        ctx, p.prec, sim->gg, p.deposit_kind, p.kernel_h, p.kernel_cutoff,
+                        ctx->starts.as<int>() + (size_t)sim->geom.n0 * sim->geom.n1, (int)n,
+                        s->rho_a, s->rho_b, st));
+                else
+                    CS_TRY(launch_deposit(ctx, p.prec, s->pos, s->type, n, sim->gg,
+                                          p.deposit_kind, p.kernel_h, p.kernel_cutoff, sim->bits,
+                                          s->rho_a, s->rho_b, st));
             }
             {
                 StageMark m(sim, CS_STAGE_SOLVE);
@@ -472,7 +491,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         }
         const double *force = nullptr;
         if (p.interaction == 1) {
-            {
+            if (!binned) {
                 StageMark m(sim, CS_STAGE_BIN);
                 CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom, s->type));
             }

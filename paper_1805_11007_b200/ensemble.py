@@ -188,7 +188,7 @@ class Ensemble:
         import torch
         if self.rng == "device" and drawn is None:
             xd, ud = self._draw_device(k)
-        elif isinstance(drawn, tuple) and hasattr(drawn[0], "device"):  # device blocks
+        elif isinstance(drawn, tuple) and torch.is_tensor(drawn[0]):  # device blocks
             xd, ud = drawn
         else:
             xi, u = drawn if drawn is not None else self._draw(k)

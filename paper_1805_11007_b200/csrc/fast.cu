@@ -149,15 +149,20 @@ struct PairRow {  // table row of this particle's type: index = partner type
 
 // Exact reference pair test (motion.py:231-239).  Returns r2 > 0 when
 // accepted (displacement in dx0/dx1), 0 otherwise.  A binary32 prefilter
-// runs first: it never rejects an accepted pair (every binary32 op has
-// relative error <= 2^-24, far inside the 1e-5 margin of cf).
+// runs first when neither axis wraps: then fx = xj - xf is one rounded
+// binary32 op (exact under Sterbenz for nearby coordinates) and the
+// squared distance carries a relative error ~2^-23, far inside the 1e-5
+// margin of cf, so it never rejects an accepted pair.  A pair across a
+// periodic seam skips it: (xj - x) - L cancels to ~cutoff from a binary32
+// difference rounded at ~L, a relative error of ~1e-4 that would reject
+// pairs at the cutoff edge (found at N = 10^7 by
+// test_gpu_cfg3_pin.py::test_cfg3_field_off_sorted_equals_direct_bitwise_5_steps).
 __device__ __forceinline__ double pair_test(float xjf, float yjf, float xf, float yf, double x,
                                             double y, float cf, double cut2, double &dx0,
                                             double &dx1) {
-    float fx = xjf - xf, fy = yjf - yf;
-    if (cA.g.per0 && fabsf(fx) > cA.halff0) fx -= copysignf(cA.sizef0, fx);
-    if (cA.g.per1 && fabsf(fy) > cA.halff1) fy -= copysignf(cA.sizef1, fy);
-    if (fmaf(fx, fx, fy * fy) > cf) return 0.0;
+    const float fx = xjf - xf, fy = yjf - yf;
+    const bool wraps = (cA.g.per0 && fabsf(fx) > cA.halff0) || (cA.g.per1 && fabsf(fy) > cA.halff1);
+    if (!wraps && fmaf(fx, fx, fy * fy) > cf) return 0.0;
     dx0 = dsub((double)xjf, x);
     dx1 = dsub((double)yjf, y);
     if (cA.g.per0) dx0 = min_image(dx0, cA.g.size0, cA.half0);

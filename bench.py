@@ -43,16 +43,17 @@ CONFIGS = {
     # name: BASELINE.json configs[i] mapped per SURVEY 8d
     "cfg0": dict(n=1000, n_c=0, prec="fp64", radii=None, eps=0.005, D=(1.0, 1.0),
                  chi=(0.0, 0.0), chi_pinned=(True, True), periodic=False, field=False,
-                 types="beta"),
+                 types="beta", bound="launch"),
     "cfg1": dict(n=10_000, n_c=128, prec="fp64", radii=None, eps=0.005, D=(1.0, 1.0),
                  chi=(0.0, 1.0), chi_pinned=(True, False), periodic=False, field=True,
                  boundary="neumann", d_c=1.0, k_alpha=0.1, k_beta=0.0, gamma=0.1,
                  secretes=(False, True), consumes=(False, False), c0="linear_x",
-                 types="beta"),
+                 types="beta", bound="launch"),
     "cfg2": dict(n=100_000, n_c=512, prec="fp64", radii=(0.005, 0.01), D=(1.0, 0.5),
                  chi=(1.0, -0.5), chi_pinned=(False, False), periodic=True, field=True,
                  boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=0.03, gamma=0.1,
-                 secretes=(True, False), consumes=(False, True), c0="zero", types="half"),
+                 secretes=(True, False), consumes=(False, True), c0="zero", types="half",
+                 bound="fp64"),
     "cfg3": dict(n=10_000_000, n_c=4096, prec="fp32", radii=(6.1804e-5, 1.2361e-4),
                  D=(1.0, 0.5), chi=(1.0, -0.5), chi_pinned=(False, False), periodic=True,
                  field=True, boundary="periodic", d_c=1.0, k_alpha=0.1, k_beta=0.03,
@@ -281,6 +282,62 @@ def oracle_sim(cfg: dict, pos, sp, nthreads: int):
                      field=field, fp32=cfg["prec"] == "fp32", nthreads=nthreads)
 
 
+def config_dict(name: str, cfg: dict, world: int) -> dict:
+    """The workload description both arms print (same keys and values)."""
+    return {"workload": f"{name}: N={cfg['n']}, {cfg['n_c']}^2 "
+                        f"{cfg.get('boundary', '-')} grid, {cfg['prec']} storage",
+            "parallelism": "single" if world == 1 else f"replicas{world}",
+            "l2": "per-step working set > 126 MB L2 (no flush needed)"
+            if cfg["n"] >= 1_000_000 else
+            "working set L2-resident (launch/latency-bound config; absolute numbers)"}
+
+
+def reference_numba(name: str):
+    """The reference's own functions timed on one core (tools/time_reference.py,
+    build container: the reference does not travel to the GPU box)."""
+    path = os.path.join(ROOT, "profiles", "r02", f"reference_numba_{name}.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return {k: d[k] for k in ("value_1core", "value_replicas", "unit", "cpu_model", "cores",
+                                  "stage_s_per_step", "pde", "note") if k in d}
+    except Exception:
+        return None
+
+
+def roofline_entry(name, cfg, fu_gbs, peak, peak_src, traffic, ab, t_fu, stages):
+    """The F+U stage against the roof that bounds it: HBM for the binary32
+    configs (cfg2f32, cfg3, cfg4); the FP64 pipe for cfg2 (binary64 pair
+    terms: FLOPs per step counted by ncu, profiles/r02/fp64_<cfg>.json, over
+    the measured DFMA peak); cfg0 / cfg1 are launch/latency-bound (L2-resident
+    working sets of <= 2 MB): their HBM fraction is shown for completeness."""
+    bound = cfg.get("bound", "hbm")
+    e = {"bound": bound, "kernel": "force+update stage (bin, forces, update)",
+         "achieved": fu_gbs, "peak": peak, "unit": "GB/s",
+         "frac": (fu_gbs / peak) if fu_gbs else None,
+         "traffic": traffic.get("fu_bytes_per_step") if traffic else None,
+         "algorithmic_bytes_per_step": ab["fu"], "t_ms": t_fu, "peak_source": peak_src}
+    if bound == "launch":
+        e["note"] = ("launch/latency-bound: the per-step working set is L2-resident; "
+                     "ms_per_step is the number that matters, the HBM fraction is not a roof")
+    if bound == "fp64":
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02", f"fp64_{name}.json")) as fh:
+                f = json.load(fh)
+            t = stages["force"]
+            ach = f["force_fp64_flop_per_step"] / (t / 1e3) / 1e12
+            e.update({"hbm": {"achieved": fu_gbs, "peak": peak, "unit": "GB/s",
+                              "frac": (fu_gbs / peak) if fu_gbs else None},
+                      "kernel": "pair forces (binary64 pair terms)",
+                      "achieved": ach, "peak": f["fp64_fma_tflops"], "unit": "TFLOP/s",
+                      "frac": ach / f["fp64_fma_tflops"], "t_ms": t,
+                      "peak_source": f.get("peak_source", "measured DFMA microbenchmark"),
+                      "flop_source": f.get("flop_source", "ncu")})
+        except Exception:
+            e["note"] = "FP64-bound; FLOP count not measured yet (profiles/r02/fp64_*.json)"
+    return e
+
+
 def cpu_model() -> str:
     """The host CPU's model name (for the CPU baseline lines)."""
     try:
@@ -332,7 +389,7 @@ def reference_arm(args, cfg, rank):
         "ms_per_step": 1e3 * t_used / done, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 (fp32 storage)" if cfg["prec"] == "fp32" else "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "n": cfg["n"], "grid": cfg["n_c"]},
+        "config": config_dict(args.config, cfg, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
                          "cpu_model": cpu_model(),
                          "sample": f"{done} full step(s) of {args.config} (N={cfg['n']}) on the "
@@ -340,6 +397,7 @@ def reference_arm(args, cfg, rank):
                                    f"{ncores} OpenMP threads; requested {args.steps}",
                          "stage_s": stages},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_numba": reference_numba(args.config),
     }
     print(json.dumps(line), flush=True)
 
@@ -462,16 +520,9 @@ def main():
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if cfg["prec"] == "fp64" else "f64 (fp32 storage)",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: N={n}, {cfg['n_c']}^2 "
-                                   f"{cfg.get('boundary', '-')} grid, {cfg['prec']} storage",
-                       "parallelism": "single" if world == 1 else f"replicas{world}",
-                       "l2": "per-step working set > 126 MB L2 (no flush needed)"},
-            "roofline": {"bound": "hbm", "kernel": "force+update stage (bin, forces, update)",
-                         "achieved": fu_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": (fu_gbs / peak) if fu_gbs else None,
-                         "traffic": traffic.get("fu_bytes_per_step") if traffic else None,
-                         "algorithmic_bytes_per_step": ab["fu"], "t_ms": t_fu,
-                         "peak_source": peak_src},
+            "config": config_dict(args.config, cfg, world),
+            "roofline": roofline_entry(args.config, cfg, fu_gbs, peak, peak_src, traffic, ab,
+                                       t_fu, stages),
             "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s",
                               "frac": step_gbs / peak, "algorithmic_bytes_per_step": ab["total"]},
             "stage_ms": {k: round(v, 4) for k, v in stages.items()},
@@ -480,6 +531,7 @@ def main():
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "reference_numba": reference_numba(args.config),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -4,6 +4,7 @@
 #include <cufft.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -463,8 +464,23 @@ struct cs_field_ops {
     double *F = nullptr, *Inv = nullptr, *E = nullptr, *T1 = nullptr, *T2 = nullptr;
     double *lx = nullptr, *ly = nullptr;
     void *rhs = nullptr;   // G (fft / identity) or double (dct)
-    void *spec = nullptr;  // complex n x (n/2+1)
+    void *spec = nullptr;  // complex n x (n/2+1) (cuFFT path)
     cufftHandle pf = 0, pi = 0;
     bool have_plans = false;
+    void *specT = nullptr, *tw = nullptr;  // spectral.cu: transposed half spectrum, twiddles
 };
+
+namespace cs {
+// spectral.cu: the periodic solve as three fused passes (n = 2^k, 16..8192);
+// CS_CUFFT=1 selects the cuFFT path instead (comparisons)
+int spectral_supported(int n);
+inline bool spectral_on(const cs_field_ops *ops) {
+    return ops->kind == 2 && spectral_supported(ops->gg.n) && !getenv("CS_CUFFT");
+}
+int spectral_step_q(cs_field_ops *ops, float *c, const int *q, double gamma, double ka,
+                    double kb, double scale, const DevStatus *st);
+int spectral_step_g(cs_field_ops *ops, void *c, const void *ra, const void *rb, double gamma,
+                    double ka, double kb, const DevStatus *st);
+int spectral_solve(cs_field_ops *ops, const void *rhs, void *out);
+}  // namespace cs
 

@@ -1215,7 +1215,7 @@ k_fast_rhs(const float *__restrict__ c, const int *__restrict__ q, long long m, 
 constexpr int STARTS_OFF = 0;
 
 struct cs_fast {
-    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, spec, gen, depflag;
+    cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, gen, depflag;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
@@ -1229,11 +1229,6 @@ struct cs_fast {
 namespace cs {
 
 int field_solve_rhs(cs_field_ops *ops, void *out);
-int spectral_supported(int n);
-size_t spectral_spec_bytes();
-int spectral_step(cs_ctx *ctx, float *c, const int *q, double one_m_dtg, double dka, double dkb,
-                  int has_g, int has_a, int has_b, double scale, const double *lx,
-                  const double *ly, double dtdc, float2 *spec, const DevStatus *st);
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,
                     DevStatus *st, int step, int *zero_q = nullptr);
 
@@ -1287,7 +1282,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
-                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->spec, &f->gen, &f->depflag})
+                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->gen, &f->depflag})
         b->release();
     delete f;
 }
@@ -1426,18 +1421,9 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
     const long long m = (long long)c.gg.n * c.gg.n;
     const double dt = p.dt;
     const double scale = (1.0 / Q_SCALE) * (1.0 / (c.gg.d0 * c.gg.d1));
-    if (c.ops->kind == 2 && c.ops->prec != CS_F64 && spectral_supported(c.gg.n) &&
-        !getenv("CS_CUFFT")) {
-        // periodic binary32 grid: the fused three-pass solve (spectral.cu)
-        if (!f->spec.p) {
-            CS_TRY(f->spec.ensure(spectral_spec_bytes()));
-            CS_CUDA(cudaMemset(f->spec.p, 0, f->spec.bytes));  // padding columns stay 0
-        }
-        return spectral_step(ctx, (float *)s->c, f->rho_q.as<int>(), 1.0 - dt * p.gamma,
-                             dt * p.k_alpha, dt * p.k_beta, p.gamma != 0.0, p.k_alpha != 0.0,
-                             p.k_beta != 0.0, scale, c.ops->lx, c.ops->ly,
-                             c.ops->dt * c.ops->d_c, f->spec.as<float2>(), st);
-    }
+    if (spectral_on(c.ops) && c.ops->prec == CS_F32)  // periodic: the fused three-pass solve
+        return spectral_step_q(c.ops, (float *)s->c, f->rho_q.as<int>(), p.gamma, p.k_alpha,
+                               p.k_beta, scale, st);
     if (c.ops->kind == 1)  // neumann DCT path solves in binary64
         k_fast_rhs<double><<<grid_for(m, 256, 148 * 16), 256, 0, ctx->stream>>>(
             (const float *)s->c, f->rho_q.as<int>(), m, 1.0 - dt * p.gamma, dt * p.k_alpha,

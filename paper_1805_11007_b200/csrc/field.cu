@@ -546,8 +546,9 @@ int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double
     CS_CUDA(cudaMalloc(&ops->ly, n * 8));
     CS_CUDA(cudaMemcpy(ops->lx, lx.data(), n * 8, cudaMemcpyHostToDevice));
     CS_CUDA(cudaMemcpy(ops->ly, ly.data(), n * 8, cudaMemcpyHostToDevice));
-    const size_t nh = (size_t)n / 2 + 1;
     CS_CUDA(cudaMalloc(&ops->rhs, m * es));
+    if (spectral_on(ops)) return CS_OK;  // spectral.cu allocates its own buffers
+    const size_t nh = (size_t)n / 2 + 1;
     CS_CUDA(cudaMalloc(&ops->spec, (size_t)n * nh * 2 * es));
     CS_TRY(cufft_check(cufftPlan2d(&ops->pf, n, n, prec == CS_F64 ? CUFFT_D2Z : CUFFT_R2C),
                        "plan fwd"));
@@ -564,7 +565,8 @@ void field_ops_destroy(cs_field_ops *ops) {
         cufftDestroy(ops->pi);
     }
     for (void *p : {(void *)ops->F, (void *)ops->Inv, (void *)ops->E, (void *)ops->T1,
-                    (void *)ops->T2, (void *)ops->lx, (void *)ops->ly, ops->rhs, ops->spec})
+                    (void *)ops->T2, (void *)ops->lx, (void *)ops->ly, ops->rhs, ops->spec,
+                    ops->specT, ops->tw})
         if (p) cudaFree(p);
     delete ops;
 }
@@ -591,6 +593,11 @@ int field_solve_rhs(cs_field_ops *ops, void *out) {
         else
             CS_TRY(gemm<float>(ctx, ops->T1, ops->Inv, true, nullptr, (float *)out, n));
         return CS_OK;
+    }
+    if (spectral_on(ops)) return spectral_solve(ops, ops->rhs, out);
+    if (!ops->have_plans) {
+        set_error("periodic solve: no cuFFT plans (CS_CUFFT set after the operator was built)");
+        return CS_ERR_PARAM;
     }
     CS_TRY(cufft_check(cufftSetStream(ops->pf, ctx->stream), "stream"));
     CS_TRY(cufft_check(cufftSetStream(ops->pi, ctx->stream), "stream"));

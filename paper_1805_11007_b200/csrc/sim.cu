@@ -480,9 +480,14 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
             }
             {
                 StageMark m(sim, CS_STAGE_SOLVE);
-                CS_TRY(field_rhs(sim->ops, s->c, s->rho_a, s->rho_b, p.k_alpha, p.k_beta,
-                                 p.gamma, st));
-                CS_TRY(field_solve_rhs(sim->ops, s->c));
+                if (spectral_on(sim->ops)) {  // rhs fused into the spectral passes
+                    CS_TRY(spectral_step_g(sim->ops, s->c, s->rho_a, s->rho_b, p.gamma,
+                                           p.k_alpha, p.k_beta, st));
+                } else {
+                                    CS_TRY(field_rhs(sim->ops, s->c, s->rho_a, s->rho_b, p.k_alpha, p.k_beta,
+                                     p.gamma, st));
+                    CS_TRY(field_solve_rhs(sim->ops, s->c));
+                }
             }
             {
                 StageMark m(sim, CS_STAGE_GRADIENT);

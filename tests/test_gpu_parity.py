@@ -229,6 +229,52 @@ def test_periodic_fft_solve_large_matches_oracle():
     assert np.allclose(got, ref, rtol=1e-11, atol=1e-12)
 
 
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048])
+def test_spectral_periodic_solve_vs_oracle_and_cufft(n, monkeypatch):
+    """The own three-pass spectral solve (csrc/spectral.cu) for every
+    power-of-two periodic grid: binary64 against the oracle's solve (SuperLU
+    up to 64^2, FFT diagonalisation above) at the T1 solve tolerance, and
+    binary64 / binary32 against the cuFFT path (CS_CUFFT=1)."""
+    grid = cs.Grid.square(n, 1.0, "periodic")
+    fp = cs.FieldParams(d_c=1.0)
+    dt = 1e-5 if n >= 512 else 1e-3
+    rhs = np.random.default_rng(n).standard_normal(n * n)
+    got = cs.build_operators(grid, fp, dt).solve(rhs)
+    ref = oracle.build_operators(n, grid.spacing, True, 1.0, dt,
+                                 splu_max=64).solve(rhs)
+    assert np.allclose(got, ref, rtol=1e-11, atol=1e-12)
+    r32 = torch.as_tensor(rhs, device="cuda").float()
+    got32 = cs.build_operators(grid, fp, dt).solve(r32).double().cpu().numpy()
+    monkeypatch.setenv("CS_CUFFT", "1")
+    lib64 = cs.build_operators(grid, fp, dt).solve(rhs)
+    lib32 = cs.build_operators(grid, fp, dt).solve(r32).double().cpu().numpy()
+    monkeypatch.delenv("CS_CUFFT")
+    assert np.max(np.abs(got - lib64)) <= 1e-13 * np.abs(lib64).max()
+    assert np.max(np.abs(got32 - lib32)) <= 2e-6 * np.abs(lib32).max()
+    assert np.max(np.abs(got32 - ref)) <= 2e-6 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_spectral_binary32_as_accurate_as_cufft(n, monkeypatch):
+    """At the cfg3 / cfg4 grid sizes: the own binary32 solve's error against
+    the binary64 solve (itself within 1e-13 of cuFFT's D2Z/Z2D) is at most
+    1.5x cuFFT's binary32 R2C/C2R error, in max and in rms."""
+    grid = cs.Grid.square(n, 1.0, "periodic")
+    fp = cs.FieldParams(d_c=1.0)
+    rhs = torch.as_tensor(0.5 + 0.1 * np.random.default_rng(n).standard_normal(n * n),
+                          device="cuda")
+    ref = cs.build_operators(grid, fp, 1e-5).solve(rhs)
+    own = cs.build_operators(grid, fp, 1e-5).solve(rhs.float()).double()
+    monkeypatch.setenv("CS_CUFFT", "1")
+    lib = cs.build_operators(grid, fp, 1e-5).solve(rhs.float()).double()
+    lib64 = cs.build_operators(grid, fp, 1e-5).solve(rhs)
+    monkeypatch.delenv("CS_CUFFT")
+    assert float((ref - lib64).abs().max()) <= 1e-13 * float(ref.abs().max())
+    e_own, e_lib = (own - ref).abs(), (lib - ref).abs()
+    assert float(e_own.max()) <= 1.5 * float(e_lib.max())
+    assert float(e_own.square().mean().sqrt()) <= 1.5 * float(e_lib.square().mean().sqrt())
+
+
 def test_coupling_golden():
     g = load_golden("coupling.npz")
     for k in range(int(g["n_cases"])):

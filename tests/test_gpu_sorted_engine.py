@@ -319,3 +319,29 @@ def test_sorted_engine_reports_bucket_overflow(monkeypatch):
     b.export_state()
     assert b.status().code == 0 and c.status().code == 0
     assert torch.equal(sb["pos"], sc["pos"])
+
+
+@pytest.mark.parametrize("n_c,n", [(512, 100_000), (8192, 400_000)])
+def test_spectral_solve_sorted_engine_vs_cufft(n_c, n, monkeypatch):
+    """cfg2f32's 512^2 and cfg4's 8192^2 periodic binary32 grids on the own
+    spectral solve: one field-on step from a non-zero field against the same
+    engine on cuFFT (c within binary32 FFT rounding: 3e-5 of max|c| at the
+    largest of 67 M nodes; the accuracy of both transforms against binary64
+    is compared in test_gpu_parity.py)."""
+    pos, sp, xi = _inputs(n, 11)
+    rng = np.random.default_rng(12)
+    c0 = (0.5 + 0.1 * rng.standard_normal(n_c * n_c)).astype(np.float32).astype(np.float64)
+    x = torch.as_tensor(xi, device="cuda")
+    res = {}
+    for mode in ("own", "cufft"):
+        if mode == "cufft":
+            monkeypatch.setenv("CS_CUFFT", "1")
+        a, sa = _sim(pos, sp, engine="sorted", field=True, n_c=n_c, c0=c0,
+                     radii=(2e-4, 4e-4))
+        a.step(x[:2], 2)
+        a.export_state()
+        assert a.status().code == 0
+        res[mode] = {k: sa[k].double().cpu().numpy() for k in ("pos", "c")}
+    monkeypatch.delenv("CS_CUFFT", raising=False)
+    cmax = np.abs(res["cufft"]["c"]).max()
+    assert np.max(np.abs(res["own"]["c"] - res["cufft"]["c"])) <= 3e-5 * cmax

@@ -258,7 +258,14 @@ typedef struct {
  * cs_sim_export; drift/local_c/next_pos are not stored per step.  AUTO picks
  * SORTED for fp32 runs that need none of the per-step stores and whose cell
  * occupancy is low (<= 4 per cell), DIRECT otherwise. */
-enum cs_engine { CS_ENGINE_AUTO = 0, CS_ENGINE_DIRECT = 1, CS_ENGINE_SORTED = 2 };
+enum cs_engine { CS_ENGINE_AUTO = 0, CS_ENGINE_DIRECT = 1, CS_ENGINE_SORTED = 2,
+                 CS_ENGINE_CTA = 3 };
+/* CTA: a small binary64 system (n <= 4096, no grid or a neumann grid of
+ * n_c <= 64, soft or no interaction, no next_pos store) held in ONE CTA's
+ * shared memory for all k steps of a call -- the ensemble engine (cs_ens_*)
+ * with one realisation: one launch per call instead of ~15 per step.  AUTO
+ * picks it when the system fits (cs_ens_create succeeds), the DIRECT
+ * engine otherwise; the results are the DIRECT engine's bit for bit. */
 
 typedef struct {
     void *pos;               /* (n, 2) prec, in/out */

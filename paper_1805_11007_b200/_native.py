@@ -24,7 +24,7 @@ CS_DEPOSIT_OVERFLOW = 5
 CS_SORT_OVERFLOW = 6
 CS_F64, CS_F32 = 0, 1
 CS_GAUSSIAN, CS_CIC = 0, 1
-CS_ENGINE_AUTO, CS_ENGINE_DIRECT, CS_ENGINE_SORTED = 0, 1, 2
+CS_ENGINE_AUTO, CS_ENGINE_DIRECT, CS_ENGINE_SORTED, CS_ENGINE_CTA = 0, 1, 2, 3
 
 C_i32, C_i64, C_f64, C_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 

@@ -43,10 +43,9 @@ __device__ __forceinline__ double cic_weight(double x, double y, const GridGeom 
 
 // The stamp value particle (x, y) leaves on node (i, j) (coupling.py:95-110):
 // false if the node is outside its stamp or beyond the cutoff.
-__device__ __forceinline__ bool gauss_term(double x, double y, int i, int j, const GridGeom &gg,
-                                           const GaussParams &gp, double &v) {
-    const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
-    const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+__device__ __forceinline__ bool gauss_term_u(double u0, double u1, int i, int j,
+                                             const GridGeom &gg, const GaussParams &gp,
+                                             double &v) {
     const long long b0 = (long long)floor(dadd(u0, 0.5));
     const long long b1 = (long long)floor(dadd(u1, 0.5));
     long long o0 = (long long)i - b0, o1 = (long long)j - b1;
@@ -64,6 +63,11 @@ __device__ __forceinline__ bool gauss_term(double x, double y, int i, int j, con
     if (!(r2 <= gp.cut2)) return false;
     v = dmul(gp.inv_norm, cs_exp(-ddiv(r2, gp.two_h2)));
     return true;
+}
+__device__ __forceinline__ bool gauss_term(double x, double y, int i, int j, const GridGeom &gg,
+                                           const GaussParams &gp, double &v) {
+    return gauss_term_u(ddiv(dsub(x, gg.lo0), gg.d0), ddiv(dsub(y, gg.lo1), gg.d1), i, j, gg,
+                        gp, v);
 }
 
 }  // namespace cs

@@ -19,6 +19,7 @@
 // from its own generator streams on the host (the reference's RNG
 // contract), K steps at a time.  Deposits are node gathers in the
 // reference's particle order (bit-identical; see ens_deposit).
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -56,6 +57,9 @@ struct EnsArgs {
     double p_ab, r_beta;
     int qper;  // doubles of pair queue per warp (in the grid scratch ra/rb)
     int tamed;
+    int thread_forces;  // a thread per particle instead of a warp (sparse systems)
+    int scratch;        // doubles of grid scratch (ra, rb / pair queues) after c
+    int pbits_words;    // u64 words of the gaussian deposit's particle bitsets (0: binned path)
 };
 
 // C = A op(B) (E *) for n <= 64 inside one CTA: T = ceil(n / 4) and thread
@@ -128,81 +132,157 @@ __device__ __forceinline__ void set_status(DevStatus *st, int *s_abort, unsigned
 }
 
 constexpr int ENS_THREADS = 256;
-constexpr int ENS_MERGE_ROWS = 16;  // gaussian stamps up to 16 rows tall: merged row by row
+
+constexpr int ENS_DEP_BUF = 16;
+constexpr int ENS_PBITS_MAX = 1024;  // particles per realisation for the bitset deposit  // stamps per node sorted in a thread's buffer (more: selection)
 
 // deposit_both inside the CTA in the reference's summation order (the
-// algorithm of deposit.cu, with rows as bins: the grid is neumann, nc <= 64).
-// key[p] = deposit row * nc + deposit column (-1: not depositing), order =
-// depositing particles by row, ascending index inside a row.
+// algorithm of deposit.cu, in shared memory; the grid is neumann, nc <= 64):
+// depositing particles binned by their deposit bin (CIC: base cell,
+// gaussian: nearest node), ascending index inside a bin; then one thread per
+// node sums its stamps in particle order.  key[p] = the bin (-1: not
+// depositing); bend[k] = the end of bin k's range in order[] (its start is
+// bend[k - 1]); uu (the force scratch, free until the pair forces) keeps
+// each particle's grid coordinates u = (x - lo) / d; slots (the local
+// concentration rows, rewritten by the refresh) the unordered claims; a
+// 64-bit mask per row marks the occupied bins, so that a node visits only
+// the non-empty bins of its stamp window.  Gaussian stamps of up to
+// ENS_PBITS_MAX particles skip the bins: per grid row and per grid column a
+// bitset over the particle indices (pbits) marks the particles binned
+// there, and a node's candidates are (OR of its window rows) AND (OR of its
+// window columns) -- visited in ascending index with no sorting.
 __device__ __noinline__ void ens_deposit(const EnsArgs &a, const double *pos, const uint8_t *type,
-                                         int *key, int *order, int *dstart, double *ra,
-                                         double *rb, int tid, int lane, int warp) {
+                                         int *key, int *order, int *bend, int *slots,
+                                         double *uu, unsigned long long *pbits, double *ra,
+                                         double *rb, int tid) {
+    __shared__ unsigned long long s_rowmask[64];
+    __shared__ int s_wsum[32];
+    const int NTH = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const GridGeom &gg = a.gg;
     const int nc = gg.n, m = nc * nc, n = a.n;
     const int kind = a.deposit_kind;
-    int *dcur = dstart + nc + 1;
-    for (int r = tid; r <= nc; r += ENS_THREADS) dstart[r] = 0;
+    const int W = (n + 63) >> 6;  // bitset words per grid row / column
+    const bool use_bits = kind == CS_GAUSSIAN && pbits != nullptr;
+    for (int k = tid; k < m; k += NTH) bend[k] = 0;
+    for (int r = tid; r < 64; r += NTH) s_rowmask[r] = 0ULL;
+    if (use_bits)
+        for (int w = tid; w < 2 * nc * W; w += NTH) pbits[w] = 0ULL;
     __syncthreads();
-    for (int p = tid; p < n; p += ENS_THREADS) {
+    for (int p = tid; p < n; p += NTH) {
         int k = -1;
         if (route_bits(type, p, a.route)) {
             const double u0 = ddiv(dsub(pos[2 * p], gg.lo0), gg.d0);
             const double u1 = ddiv(dsub(pos[2 * p + 1], gg.lo1), gg.d1);
+            uu[2 * p] = u0;
+            uu[2 * p + 1] = u1;
             if (fabs(u0) < 0x1p52 && fabs(u1) < 0x1p52) {
-                const int r = dep_bin_axis(u1, kind, nc, 0);
-                k = r * nc + dep_bin_axis(u0, kind, nc, 0);
-                atomicAdd(&dstart[r + 1], 1);
+                const int r = dep_bin_axis(u1, kind, nc, 0), c = dep_bin_axis(u0, kind, nc, 0);
+                k = r * nc + c;
+                atomicOr(&s_rowmask[r], 1ULL << c);
+                if (use_bits) {
+                    atomicOr(&pbits[r * W + (p >> 6)], 1ULL << (p & 63));
+                    atomicOr(&pbits[(nc + c) * W + (p >> 6)], 1ULL << (p & 63));
+                } else {
+                    atomicAdd(&bend[k], 1);
+                }
             }
         }
         key[p] = k;
     }
     __syncthreads();
-    if (warp == 0) {
-        int carry = 0;
-        for (int r0 = 1; r0 <= nc; r0 += 32) {
-            const int r = r0 + lane;
-            int v = r <= nc ? dstart[r] : 0;
+    if (use_bits) {
+        const GaussParams &gp = a.gp;
+        for (int l = tid; l < m; l += NTH) {
+            const int j = l / nc, i = l - j * nc;
+            const int r0 = max(j - gp.w1, 0), r1 = min(j + gp.w1, nc - 1);
+            const int cl = max(i - gp.w0, 0), ch = min(i + gp.w0, nc - 1);
+            const unsigned long long cmask =
+                ch - cl >= 63 ? ~0ULL : (((1ULL << (ch - cl + 1)) - 1ULL) << cl);
+            unsigned long long any = 0ULL;
+            for (int r = r0; r <= r1; r++) any |= s_rowmask[r];
+            double sa = 0.0, sb = 0.0;
+            if (any & cmask) {
+                for (int w = 0; w < W; w++) {
+                    unsigned long long mr = 0ULL, mc = 0ULL;
+                    for (int r = r0; r <= r1; r++) mr |= pbits[r * W + w];
+                    if (!mr) continue;
+                    for (int c = cl; c <= ch; c++) mc |= pbits[(nc + c) * W + w];
+                    unsigned long long mm = mr & mc;
+                    while (mm) {
+                        const int p = (w << 6) + __ffsll((long long)mm) - 1;
+                        mm &= mm - 1ULL;
+                        double v;
+                        if (!gauss_term_u(uu[2 * p], uu[2 * p + 1], i, j, gg, gp, v)) continue;
+                        const unsigned bits = route_bits(type, p, a.route);
+                        if (bits & 1u) sa = dadd(sa, v);
+                        if (bits & 2u) sb = dadd(sb, v);
+                    }
+                }
+            }
+            ra[l] = sa;
+            rb[l] = sb;
+        }
+        return;
+    }
+    {  // exclusive scan of the counts in place: a run of bins per thread
+        const int per = (m + NTH - 1) / NTH;
+        const int k0 = tid * per, k1 = min(k0 + per, m);
+        int run = 0;
+        for (int k = k0; k < k1; k++) run += bend[k];
+        int inc = run;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < NTH / 32 ? s_wsum[lane] : 0;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, v, d);
-                if (lane >= d) v += y;
+                const int y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
             }
-            if (r <= nc) dstart[r] = v + carry;
-            carry += __shfl_sync(0xffffffffu, v, 31);
+            if (lane < NTH / 32) s_wsum[lane] = w;
         }
-        __syncwarp();
-        for (int r = lane; r < nc; r += 32) dcur[r] = dstart[r];
-        __syncwarp();
-        for (int p0 = 0; p0 < n; p0 += 32) {  // stable placement, 32 at a time
-            const int p = p0 + lane;
-            const int k = p < n ? key[p] : -1;
-            const int r = k >= 0 ? k / nc : -1 - lane;
-            const unsigned same = __match_any_sync(0xffffffffu, r);
-            const int rank = __popc(same & ((1u << lane) - 1u));
-            int base = 0;
-            if (k >= 0) base = dcur[r];
-            __syncwarp();
-            if (k >= 0) {
-                order[base + rank] = p;
-                if (rank == __popc(same) - 1) dcur[r] = base + rank + 1;
-            }
-            __syncwarp();
+        __syncthreads();
+        int acc = inc - run + (warp > 0 ? s_wsum[warp - 1] : 0);
+        for (int k = k0; k < k1; k++) {
+            const int v = bend[k];
+            bend[k] = acc;
+            acc += v;
         }
+    }
+    __syncthreads();
+    // unordered claims (bend[k]: start -> end of bin k), then every particle
+    // at its bin start + the number of the bin's particles with a smaller index
+    for (int p = tid; p < n; p += NTH)
+        if (key[p] >= 0) slots[atomicAdd(&bend[key[p]], 1)] = p;
+    __syncthreads();
+    const int total = bend[m - 1];
+    for (int t = tid; t < total; t += NTH) {
+        const int v = slots[t];
+        const int k = key[v];
+        const int s0 = k ? bend[k - 1] : 0, s1 = bend[k];
+        int rank = 0;
+        for (int u = s0; u < s1; u++) rank += slots[u] < v;
+        order[s0 + rank] = v;
     }
     __syncthreads();
     if (kind == CS_CIC) {
         const double unit = ddiv(1.0, dmul(gg.d0, gg.d1));
-        for (int l = tid; l < m; l += ENS_THREADS) {
+        for (int l = tid; l < m; l += NTH) {
             const int j = l / nc, i = l - j * nc;
             double sa = 0.0, sb = 0.0;
             for (int q = 0; q < 4; q++) {
                 const int bx = i - (q & 1), by = j - (q >> 1);
                 if (bx < 0 || by < 0 || bx > nc - 2 || by > nc - 2) continue;
-                const int want = by * nc + bx;
+                if (!((s_rowmask[by] >> bx) & 1ULL)) continue;  // an empty base cell
+                const int k = by * nc + bx;
                 double ca = 0.0, cb = 0.0;
-                for (int t = dstart[by]; t < dstart[by + 1]; t++) {
+                for (int t = k ? bend[k - 1] : 0; t < bend[k]; t++) {
                     const int p = order[t];
-                    if (key[p] != want) continue;
                     const double w = cic_weight(pos[2 * p], pos[2 * p + 1], gg, unit, q);
                     const unsigned bits = route_bits(type, p, a.route);
                     if (bits & 1u) ca = dadd(ca, w);
@@ -217,104 +297,96 @@ __device__ __noinline__ void ens_deposit(const EnsArgs &a, const double *pos, co
         return;
     }
     const GaussParams &gp = a.gp;
-    for (int l = tid; l < m; l += ENS_THREADS) {
+    for (int l = tid; l < m; l += NTH) {
         const int j = l / nc, i = l - j * nc;
         const int r0 = max(j - gp.w1, 0), r1 = min(j + gp.w1, nc - 1);
-        const int c0 = i - gp.w0, c1 = i + gp.w0;
-        // merge of the window rows (each ascending in index): per row the
-        // next stamp on this node and its value
-        int hd[ENS_MERGE_ROWS], he[ENS_MERGE_ROWS];
-        double hv[ENS_MERGE_ROWS];
-        const int nr = r1 - r0 + 1;
-        auto advance = [&](int q, int t) {
-            for (; t < he[q]; t++) {
-                const int p = order[t];
-                const int col = key[p] - (key[p] / nc) * nc;
-                if (col < c0 || col > c1) continue;
-                double v;
-                if (gauss_term(pos[2 * p], pos[2 * p + 1], i, j, gg, gp, v)) {
-                    hv[q] = v;
-                    break;
-                }
-            }
-            hd[q] = t;
-        };
+        const int cl = max(i - gp.w0, 0), ch = min(i + gp.w0, nc - 1);
+        const unsigned long long cmask =
+            ch - cl >= 63 ? ~0ULL : (((1ULL << (ch - cl + 1)) - 1ULL) << cl);
+        // the stamps on this node in batches of the ENS_DEP_BUF smallest
+        // particle indices above the previous batch's, each sorted and summed
+        unsigned idb[ENS_DEP_BUF];
+        double vb[ENS_DEP_BUF];
         double sa = 0.0, sb = 0.0;
-        if (nr <= ENS_MERGE_ROWS) {
-            for (int q = 0; q < nr; q++) {
-                he[q] = dstart[r0 + q + 1];
-                advance(q, dstart[r0 + q]);
-            }
-            for (;;) {
-                int best = -1, bp = 0x7fffffff;
-                for (int q = 0; q < nr; q++) {
-                    if (hd[q] < he[q] && order[hd[q]] < bp) {
-                        bp = order[hd[q]];
-                        best = q;
+        int last = -1;
+        bool more = true;
+        while (more) {
+            int cnt = 0;
+            more = false;
+            for (int r = r0; r <= r1; r++) {
+                unsigned long long bits = s_rowmask[r] & cmask;
+                while (bits) {
+                    const int c = __ffsll((long long)bits) - 1;
+                    bits &= bits - 1ULL;
+                    const int k = r * nc + c;
+                    for (int t = k ? bend[k - 1] : 0; t < bend[k]; t++) {
+                        const int p = order[t];
+                        if (p <= last) continue;
+                        if (cnt == ENS_DEP_BUF && p > (int)idb[ENS_DEP_BUF - 1]) {
+                            more = true;
+                            break;  // the rest of this bin is larger still
+                        }
+                        double v;
+                        if (!gauss_term_u(uu[2 * p], uu[2 * p + 1], i, j, gg, gp, v)) continue;
+                        int q = cnt;
+                        if (cnt == ENS_DEP_BUF) {
+                            more = true;
+                            q = ENS_DEP_BUF - 1;
+                        } else {
+                            cnt++;
+                        }
+                        while (q > 0 && (int)idb[q - 1] > p) {
+                            idb[q] = idb[q - 1];
+                            vb[q] = vb[q - 1];
+                            q--;
+                        }
+                        idb[q] = (unsigned)p;
+                        vb[q] = v;
                     }
                 }
-                if (best < 0) break;
-                const unsigned bits = route_bits(type, bp, a.route);
-                if (bits & 1u) sa = dadd(sa, hv[best]);
-                if (bits & 2u) sb = dadd(sb, hv[best]);
-                advance(best, hd[best] + 1);
             }
-        } else {  // a very tall stamp: repeated selection of the next index
-            int last = -1;
-            for (;;) {
-                int bp = 0x7fffffff;
-                double bv = 0.0;
-                for (int t = dstart[r0]; t < dstart[r1 + 1]; t++) {
-                    const int p = order[t];
-                    if (p <= last || p >= bp) continue;
-                    const int col = key[p] - (key[p] / nc) * nc;
-                    if (col < c0 || col > c1) continue;
-                    double v;
-                    if (gauss_term(pos[2 * p], pos[2 * p + 1], i, j, gg, gp, v)) {
-                        bp = p;
-                        bv = v;
-                    }
-                }
-                if (bp == 0x7fffffff) break;
-                const unsigned bits = route_bits(type, bp, a.route);
-                if (bits & 1u) sa = dadd(sa, bv);
-                if (bits & 2u) sb = dadd(sb, bv);
-                last = bp;
+            for (int q = 0; q < cnt; q++) {
+                const unsigned bits = route_bits(type, (int)idb[q], a.route);
+                if (bits & 1u) sa = dadd(sa, vb[q]);
+                if (bits & 2u) sb = dadd(sb, vb[q]);
             }
+            if (cnt) last = (int)idb[cnt - 1];
         }
         ra[l] = sa;
         rb[l] = sb;
     }
 }
 
-
-__global__ void __launch_bounds__(ENS_THREADS)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 k_ensemble(const __grid_constant__ EnsArgs a) {
     extern __shared__ double sm[];
     __shared__ int s_abort;
-    __shared__ double s_red[ENS_THREADS / 32];
-    __shared__ int s_flag[ENS_THREADS / 32];
+    __shared__ double s_red[NT / 32];
+    __shared__ int s_flag[NT / 32];
     const int n = a.n, m = a.nc * a.nc, tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const long long s = blockIdx.x;
     double *pos = sm, *anc = pos + 2 * n, *drift = anc + 2 * n, *frc = drift + 2 * n;
     double *lc = frc + 2 * n, *c = lc + n, *ra = c + m, *rb = ra + m;
-    int *order = reinterpret_cast<int *>(ra + 8 * a.qper);
+    int *order = reinterpret_cast<int *>(ra + a.scratch);
     int *starts = order + n, *cur = starts + a.ncell + 1, *key = cur + a.ncell;
-    int *dstart = key + n;  // deposit rows: starts (nc + 1), cursors (nc)
-    uint8_t *type = reinterpret_cast<uint8_t *>(dstart + 2 * a.nc + 1);
+    int *dbend = key + n;  // deposit bins: the end of each bin's range (nc^2)
+    unsigned long long *pbits =  // per grid row / column particle bitsets (gaussian deposit)
+        reinterpret_cast<unsigned long long *>(ra + a.scratch - a.pbits_words);
+    uint8_t *type = reinterpret_cast<uint8_t *>(dbend + a.nc * a.nc);
     DevStatus *st = a.st + s;
-    for (int i = tid; i < 2 * n; i += ENS_THREADS) {
+    for (int i = tid; i < 2 * n; i += NT) {
         pos[i] = a.pos[2 * n * s + i];
         anc[i] = a.anchor[2 * n * s + i];
         drift[i] = a.drift[2 * n * s + i];
     }
-    for (int i = tid; i < n; i += ENS_THREADS) {
+    for (int i = tid; i < n; i += NT) {
         lc[i] = a.local_c[n * s + i];
         type[i] = a.type[n * s + i];
     }
     if (a.field || a.refresh)
-        for (int l = tid; l < m; l += ENS_THREADS) c[l] = a.c[(long long)m * s + l];
+        for (int l = tid; l < m; l += NT) c[l] = a.c[(long long)m * s + l];
     if (tid == 0) s_abort = st->abort;
     long long clamped = 0;
     unsigned long long high_n = 0;
@@ -330,10 +402,11 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             // in the reference's particle order (see deposit.cu): depositing
             // particles binned by deposit row (CIC: base row, gaussian: nearest
             // row), ascending index inside a row; then one thread per node
-            ens_deposit(a, pos, type, key, order, dstart, ra, rb, tid, lane, warp);
+            ens_deposit(a, pos, type, key, order, dbend, reinterpret_cast<int *>(lc), frc,
+                        a.pbits_words ? pbits : nullptr, ra, rb, tid);
             __syncthreads();
             // ---- rhs (field.py:224-229), in place into ra
-            for (int l = tid; l < m; l += ENS_THREADS) {
+            for (int l = tid; l < m; l += NT) {
                 const double cv = c[l];
                 double r = a.has_g ? dmul(cv, a.one_m_dtg) : cv;
                 if (a.has_a) r = dadd(r, dmul(a.dka, ra[l]));
@@ -351,13 +424,13 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 __syncthreads();
                 cta_gemm<true>(rb, a.Inv, nullptr, c, nc);    // c = U Inv^T
             } else {
-                for (int l = tid; l < m; l += ENS_THREADS) c[l] = ra[l];
+                for (int l = tid; l < m; l += NT) c[l] = ra[l];
             }
             __syncthreads();
             // ---- post-checks (field.py:229-238): non-finite, negative mass
             double neg = 0.0;
             int flags = 0;
-            for (int l = tid; l < m; l += ENS_THREADS) {
+            for (int l = tid; l < m; l += NT) {
                 const double v = c[l];
                 if (!isfinite(v)) flags |= 1;
                 if (v < 0.0) {
@@ -380,7 +453,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             if (tid == 0) {
                 double t = 0.0;
                 int f = 0;
-                for (int w = 0; w < ENS_THREADS / 32; w++) {
+                for (int w = 0; w < NT / 32; w++) {
                     t += s_red[w];
                     f |= s_flag[w];
                 }
@@ -395,7 +468,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         }
         // ---- refresh (coupling.py:302-325)
         if (a.refresh) {
-            for (int p = tid; p < n; p += ENS_THREADS) {
+            for (int p = tid; p < n; p += NT) {
                 Bilin b;
                 clamped += 2 * bilinear_stencil(pos[2 * p], pos[2 * p + 1], gg, b);
                 lc[p] = bilinear_apply(b, c, 1, 0);
@@ -415,49 +488,82 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         }
         // ---- cell list + pair forces (motion.py:170-245)
         if (a.interact) {
-            for (int f = tid; f <= a.ncell; f += ENS_THREADS) starts[f] = 0;
+            for (int f = tid; f <= a.ncell; f += NT) starts[f] = 0;
             __syncthreads();
-            for (int p = tid; p < n; p += ENS_THREADS) {
+            for (int p = tid; p < n; p += NT) {
                 const int k = cell_axis(pos[2 * p + 1], a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
                               cell_axis(pos[2 * p], a.g.lo0, a.g.eff0, a.g.n0);
                 key[p] = k;
                 atomicAdd(&starts[k + 1], 1);
             }
             __syncthreads();
-            if (warp == 0) {  // inclusive scan of starts[1..ncell] (counts) by one warp
-                int carry = 0;
-                for (int f0 = 1; f0 <= a.ncell; f0 += 32) {
-                    const int f = f0 + lane;
-                    int v = f <= a.ncell ? starts[f] : 0;
+            {  // inclusive scan of starts[1..ncell] (the counts): a run of cells
+               // per thread, then the block's run totals
+                const int per = (a.ncell + NT - 1) / NT;
+                const int f0 = 1 + tid * per, f1 = min(f0 + per, a.ncell + 1);
+                int run = 0;
+                for (int f = f0; f < f1; f++) run += starts[f];
+                int inc = run;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += y;
+                }
+                if (lane == 31) s_flag[warp] = inc;
+                __syncthreads();
+                if (warp == 0) {
+                    int w = lane < NT / 32 ? s_flag[lane] : 0;
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, v, d);
-                        if (lane >= d) v += y;
+                        const int y = __shfl_up_sync(0xffffffffu, w, d);
+                        if (lane >= d) w += y;
                     }
-                    if (f <= a.ncell) starts[f] = v + carry;
-                    carry += __shfl_sync(0xffffffffu, v, 31);
+                    if (lane < NT / 32) s_flag[lane] = w;
                 }
-                __syncwarp();
-                for (int f = lane; f < a.ncell; f += 32) cur[f] = starts[f];
-                __syncwarp();
+                __syncthreads();
+                int acc = inc - run + (warp > 0 ? s_flag[warp - 1] : 0);
+                for (int f = f0; f < f1; f++) {
+                    acc += starts[f];
+                    starts[f] = acc;
+                }
+                __syncthreads();
+                for (int f = tid; f < a.ncell; f += NT) cur[f] = starts[f];
+                __syncthreads();
+            }
+            {
                 // stable placement (ascending index inside a cell,
-                // motion.py:195-199), 32 particles at a time in index order
-                for (int p0 = 0; p0 < n; p0 += 32) {
-                    const int p = p0 + lane;
-                    const int k = p < n ? key[p] : -1 - lane;
-                    const unsigned same = __match_any_sync(0xffffffffu, k);
-                    const int rank = __popc(same & ((1u << lane) - 1u));
-                    int base = 0;
-                    if (p < n) base = cur[k];
-                    __syncwarp();
-                    if (p < n) {
-                        order[base + rank] = p;
-                        if (rank == __popc(same) - 1) cur[k] = base + rank + 1;
-                    }
-                    __syncwarp();
+                // motion.py:195-199): unordered claims into the cell ranges
+                // (the force scratch holds the slots), then every particle at
+                // its cell start + the number of the cell's particles with a
+                // smaller index
+                int *slots = reinterpret_cast<int *>(frc);
+                for (int p = tid; p < n; p += NT) slots[atomicAdd(&cur[key[p]], 1)] = p;
+                __syncthreads();
+                for (int t = tid; t < n; t += NT) {
+                    const int v = slots[t];
+                    const int k = key[v];
+                    const int s0 = starts[k], s1 = starts[k + 1];
+                    int rank = 0;
+                    for (int u = s0; u < s1; u++) rank += slots[u] < v;
+                    order[s0 + rank] = v;
                 }
             }
             __syncthreads();
+            if (a.thread_forces) {
+                // sparse systems (<= 2 particles per cell; the single-
+                // realisation CTA engine): one thread per particle walks its
+                // ring in the reference order (common.cuh pair_loop)
+                for (int i = tid; i < n; i += NT) {
+                    double fx = 0.0, fy = 0.0;
+                    pair_loop(pos, type, order, starts, a.g, a.pt, i,
+                              [&](int, double sc, double dx0, double dx1) {
+                                  fx = dadd(fx, dmul(sc, dx0));
+                                  fy = dadd(fy, dmul(sc, dx1));
+                              });
+                    frc[2 * i] = fx;
+                    frc[2 * i + 1] = fy;
+                }
+            } else {
             // one warp per particle: the lanes test its ring candidates 32 at
             // a time in ring order (cells o1-major, ascending index inside a
             // cell) and evaluate the accepted pair terms in parallel; the
@@ -465,7 +571,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             const BinGeom &g = a.g;
             double *wq = ra + (long long)warp * a.qper;  // this warp's pair queue
             const int qcap = a.qper / 4;
-            for (int i = warp; i < n; i += ENS_THREADS / 32) {
+            for (int i = warp; i < n; i += NT / 32) {
                 const double xi = pos[2 * i], yi = pos[2 * i + 1];
                 const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
                 const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
@@ -569,11 +675,12 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                     frc[2 * i + 1] = fy;
                 }
             }
+            }
         }
         __syncthreads();
         // ---- Euler-Maruyama + boundaries (motion.py:268-282, 355-430)
         const double *xk = a.xi + (long long)kk * a.xs + 2LL * n * s;
-        for (int p = tid; p < n; p += ENS_THREADS) {
+        for (int p = tid; p < n; p += NT) {
             const int t = type[p] ? 1 : 0;
             const double amp = a.amp[t];
             const double f0 = a.interact ? frc[2 * p] : 0.0, f1 = a.interact ? frc[2 * p + 1] : 0.0;
@@ -612,7 +719,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         // ---- fixed-step reactions (reactions.py:43-81)
         if (a.react) {
             const double *uk = a.u + (long long)kk * a.us + (long long)n * s;
-            for (int p = tid; p < n; p += ENS_THREADS) {
+            for (int p = tid; p < n; p += NT) {
                 const double ui = uk[p];
                 if (type[p] == 0) {
                     if (a.p_ab > 1.0) {
@@ -639,17 +746,17 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         }
     }
     __syncthreads();
-    for (int i = tid; i < 2 * n; i += ENS_THREADS) {
+    for (int i = tid; i < 2 * n; i += NT) {
         a.pos[2 * n * s + i] = pos[i];
         a.anchor[2 * n * s + i] = anc[i];
         a.drift[2 * n * s + i] = drift[i];
     }
-    for (int i = tid; i < n; i += ENS_THREADS) {
+    for (int i = tid; i < n; i += NT) {
         a.local_c[n * s + i] = lc[i];
         a.type[n * s + i] = type[i];
     }
     if (a.field)
-        for (int l = tid; l < m; l += ENS_THREADS) a.c[(long long)m * s + l] = c[l];
+        for (int l = tid; l < m; l += NT) a.c[(long long)m * s + l] = c[l];
     if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
     if (high_n) {
         atomicAdd(&st->react_high_n, high_n);
@@ -736,23 +843,30 @@ struct cs_ens {
     cs_field_ops *ops = nullptr;
     cs::Buf status;  // DevStatus[n_real]
     size_t smem = 0;
+    int threads = 256;
 };
 
 namespace cs {
 
 // scratch doubles after c: ra and rb of the field stage, reused as the warps'
 // pair queues by the force stage (at least 64 entries of 4 doubles per warp)
-static size_t ens_scratch(int nc) {
+// pbits: u64 words of the gaussian deposit's bitsets (2 nc ceil(n/64)),
+// after ra and rb (the pair queues reuse the whole region later)
+static size_t ens_scratch(int nc, int warps, size_t pbits = 0) {
     const size_t m = (size_t)nc * nc;
-    const size_t q = (ENS_THREADS / 32) * 4 * 64;
-    return 2 * m > q ? 2 * m : q;
+    const size_t q = (size_t)warps * 4 * 64;
+    return 2 * m + pbits > q ? 2 * m + pbits : q;
 }
 
-static size_t ens_smem(int n, int nc, int ncell) {
+static size_t ens_pbits_words(const cs_sim_params *p, int nc) {
+    if (!p->field_active || p->deposit_kind != CS_GAUSSIAN || p->n > ENS_PBITS_MAX) return 0;
+    return 2 * (size_t)nc * (size_t)((p->n + 63) / 64);
+}
+
+static size_t ens_smem(int n, int nc, int ncell, int warps, size_t pbits) {
     const size_t m = (size_t)nc * nc;
-    return sizeof(double) * (9 * (size_t)n + m + ens_scratch(nc)) +
-           sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1 + 2 * (size_t)nc + 1) +
-           (size_t)n + 16;
+    return sizeof(double) * (9 * (size_t)n + m + ens_scratch(nc, warps, pbits)) +
+           sizeof(int) * (2 * (size_t)n + 2 * (size_t)ncell + 1 + m) + (size_t)n + 16;
 }
 
 int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
@@ -822,8 +936,16 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
     a.react = p->react;
     a.p_ab = p->react_p_ab;
     a.r_beta = p->react_r_beta;
-    a.qper = (int)(ens_scratch(a.nc) / (ENS_THREADS / 32));
-    e->smem = ens_smem(a.n, a.nc, a.ncell);
+    // one realisation (the CTA engine of cs_sim): 1024 threads, and a thread
+    // per particle for the pair forces when the system is sparse
+    e->threads = n_real == 1 ? (getenv("CS_CTA_THREADS") ? atoi(getenv("CS_CTA_THREADS")) : 512)
+                             : ENS_THREADS;
+    a.thread_forces = n_real == 1 && a.interact && (double)a.n <= 2.0 * (double)a.ncell;
+    const size_t pw = ens_pbits_words(p, a.nc);
+    a.pbits_words = (int)pw;
+    a.scratch = (int)ens_scratch(a.nc, e->threads / 32, pw);
+    a.qper = a.scratch / (e->threads / 32);
+    e->smem = ens_smem(a.n, a.nc, a.ncell, e->threads / 32, pw);
     int dev_max = 0;
     CS_CUDA(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                    ctx->device));
@@ -832,7 +954,11 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
                   dev_max);
         return CS_ERR_PARAM;
     }
-    CS_CUDA(cudaFuncSetAttribute(k_ensemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble<ENS_THREADS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem));
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)e->smem));
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)e->smem));
     CS_TRY(e->status.ensure(sizeof(DevStatus) * (size_t)n_real));
     std::vector<DevStatus> init((size_t)n_real);
@@ -878,10 +1004,29 @@ int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u
     a.st = e->status.as<DevStatus>();
     a.k_steps = k;
     a.step0 = e->steps_done;
-    k_ensemble<<<e->n_real, ENS_THREADS, e->smem, e->ctx->stream>>>(a);
+    if (e->threads == 1024)
+        k_ensemble<1024><<<e->n_real, 1024, e->smem, e->ctx->stream>>>(a);
+    else if (e->threads == 512)
+        k_ensemble<512><<<e->n_real, 512, e->smem, e->ctx->stream>>>(a);
+    else
+        k_ensemble<ENS_THREADS><<<e->n_real, ENS_THREADS, e->smem, e->ctx->stream>>>(a);
     CS_LAUNCH_CHECK();
     e->ctx->launches += 1;
     e->steps_done += k;
+    return CS_OK;
+}
+
+int ens_reset_status(cs_ens *e) {
+    std::vector<DevStatus> init((size_t)e->n_real);
+    for (auto &d : init) {
+        d = DevStatus{};
+        d.key = ~0ULL;
+        d.step = -1;
+    }
+    CS_CUDA(cudaMemcpyAsync(e->status.p, init.data(), sizeof(DevStatus) * init.size(),
+                            cudaMemcpyHostToDevice, e->ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+    e->steps_done = 0;
     return CS_OK;
 }
 

@@ -38,6 +38,12 @@ int launch_react(cs_ctx *ctx, uint8_t *type, const double *local_c, double *drif
                  const double *u, long long n, double p_ab, double r_beta, double dt,
                  DevStatus *st);
 
+int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out);
+void ens_destroy(cs_ens *e);
+int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u, int k);
+int ens_status(cs_ens *e, cs_status *out);
+int ens_reset_status(cs_ens *e);
+
 struct FastStepCfg {
     const cs_sim_params *p;
     BinGeom g;
@@ -212,6 +218,8 @@ struct cs_sim {
     unsigned char bits[3] = {0, 0, 0};
     int engine = CS_ENGINE_DIRECT;
     cs_fast *fast = nullptr;
+    cs_ens *ens = nullptr;              // CTA engine: one realisation of the ensemble engine
+    cs::Buf cta_drift, cta_lc, cta_type;  // its state rows the caller did not provide
     cs::Buf status;  // this simulation's DevStatus
     cs::DevStatus *dstat() { return status.as<cs::DevStatus>(); }
     // optional per-stage device timing (CUDA events on the step stream)
@@ -286,6 +294,22 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
             set_error("the sorted engine stores binary32 records (prec must be CS_F32)");
             return CS_ERR_PARAM;
         }
+        const bool grid = p->field_active || p->refresh_active;
+        const bool want_cta =
+            p->engine == CS_ENGINE_CTA ||
+            (p->engine == CS_ENGINE_AUTO && p->prec == CS_F64 && p->n >= 1 && p->n <= 4096 &&
+             (p->interaction == 0 || p->interaction == 1) && !p->store_next &&
+             (!grid || (!p->grid.periodic && p->grid.n_c <= 64)) && !getenv("CS_NO_CTA"));
+        if (want_cta) {
+            const int rc = ens_create(ctx, p, 1, &sim->ens);
+            if (rc == CS_OK) {
+                sim->engine = CS_ENGINE_CTA;
+            } else {
+                ens_destroy(sim->ens);
+                sim->ens = nullptr;
+                if (p->engine == CS_ENGINE_CTA) return rc;  // asked for explicitly
+            }
+        }
         if (want_sorted) {
             sim->engine = CS_ENGINE_SORTED;
             sim->geom = g;
@@ -306,6 +330,10 @@ void sim_destroy(cs_sim *sim) {
     if (!sim) return;
     field_ops_destroy(sim->ops);
     fast_destroy(sim->fast);
+    ens_destroy(sim->ens);
+    sim->cta_drift.release();
+    sim->cta_lc.release();
+    sim->cta_type.release();
     sim->status.release();
     if (sim->side) {
         cudaStreamSynchronize(sim->side);
@@ -318,6 +346,7 @@ void sim_destroy(cs_sim *sim) {
 }
 
 int sim_reset_status(cs_sim *sim) {
+    if (sim->ens) CS_TRY(ens_reset_status(sim->ens));
     DevStatus init{};
     init.key = ~0ULL;
     init.step = -1;
@@ -382,6 +411,51 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
     const size_t es = p.prec == CS_F64 ? 8 : 4;
     const long long n = p.n;
     const int64_t l0 = ctx->launches;
+    if (sim->engine == CS_ENGINE_CTA) {
+        // one launch runs all k steps in shared memory (ensemble.cu, S = 1);
+        // its xi / u layouts are (k, 1, n, 2) / (k, 1, n): caller strides of
+        // 2n / n run as one call, others one call per step
+        cs_ens_state es{};
+        const size_t nn = (size_t)n;
+        es.pos = (double *)s->pos;
+        es.anchor = (double *)s->anchor;
+        es.c = (double *)s->c;
+        if (s->drift) {
+            es.drift = s->drift;
+        } else {
+            if (!sim->cta_drift.p) {
+                CS_TRY(sim->cta_drift.ensure(16 * nn));
+                CS_CUDA(cudaMemsetAsync(sim->cta_drift.p, 0, 16 * nn, ctx->stream));
+            }
+            es.drift = sim->cta_drift.as<double>();
+        }
+        if (s->local_c) {
+            es.local_c = s->local_c;
+        } else {
+            CS_TRY(sim->cta_lc.ensure(8 * nn));
+            es.local_c = sim->cta_lc.as<double>();
+        }
+        if (s->type) {
+            es.type = s->type;
+        } else {
+            if (!sim->cta_type.p) {
+                CS_TRY(sim->cta_type.ensure(nn));
+                CS_CUDA(cudaMemsetAsync(sim->cta_type.p, 0, nn, ctx->stream));
+            }
+            es.type = sim->cta_type.as<uint8_t>();
+        }
+        StageMark m(sim, CS_STAGE_FORCE);  // the whole fused step
+        if (stride == 2 * n && (!u || u_stride == n)) {
+            CS_TRY(ens_step(sim->ens, &es, (const double *)xi, u, k));
+        } else {
+            for (int kk = 0; kk < k; kk++)
+                CS_TRY(ens_step(sim->ens, &es, (const double *)xi + (size_t)kk * stride,
+                                u ? u + (size_t)kk * u_stride : nullptr, 1));
+        }
+        sim->steps_done += k;
+        sim->last_launches = ctx->launches - l0;
+        return CS_OK;
+    }
     if (sim->engine == CS_ENGINE_SORTED) {
         FastStepCfg c;
         c.p = &p;
@@ -574,6 +648,11 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
 
 int sim_status(cs_sim *sim, cs_status *out) {
     cs_ctx *ctx = sim->ctx;
+    if (sim->ens) {
+        CS_TRY(ens_status(sim->ens, out));
+        out->steps_done = sim->steps_done;
+        return CS_OK;
+    }
     DevStatus d;
     CS_CUDA(cudaMemcpyAsync(&d, sim->status.p, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
     CS_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -308,7 +308,7 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
     p.store_samples = int(bool(store_samples))
     p.store_next = int(bool(store_next))
     p.engine = {"auto": N.CS_ENGINE_AUTO, "direct": N.CS_ENGINE_DIRECT,
-                "sorted": N.CS_ENGINE_SORTED}[engine]
+                "sorted": N.CS_ENGINE_SORTED, "cta": N.CS_ENGINE_CTA}[engine]
     if reaction is not None and reaction.scheduler == "fixed" and (
             reaction.r_alpha > 0 or reaction.r_beta > 0):
         p.react = 1
@@ -377,7 +377,7 @@ class DeviceSim:
     @property
     def engine(self) -> str:
         e = int(N.load_library().cs_sim_engine(self._h))
-        return "sorted" if e == N.CS_ENGINE_SORTED else "direct"
+        return {N.CS_ENGINE_SORTED: "sorted", N.CS_ENGINE_CTA: "cta"}.get(e, "direct")
 
     def import_state(self) -> None:
         """Reload the engine's internal state from the state tensors."""

@@ -179,7 +179,7 @@ def initial_positions(cfg: dict, rng) -> np.ndarray:
     return (-0.5 + rng.random((n, 2))).astype(np.float64)
 
 
-def make_state(cfg: dict, rank: int):
+def make_state(cfg: dict, rank: int, xi_by_slot: bool = False):
     import torch
     import paper_1805_11007_b200 as cs
     n, n_c = cfg["n"], max(cfg["n_c"], 3)
@@ -226,7 +226,8 @@ def make_state(cfg: dict, rank: int):
         field_active=cfg["field"], refresh_active=cfg["field"] or cfg.get("c0") == "linear_x",
         grid=grid, fparams=fp, kernel=cs.Kernel(kind="cic"),
         secretes=cfg.get("secretes", (False, False)), consumes=cfg.get("consumes", (False, False)),
-        chi=cfg["chi"], chi_pinned=cfg["chi_pinned"], store_samples=False, store_next=False)
+        chi=cfg["chi"], chi_pinned=cfg["chi_pinned"], store_samples=False, store_next=False,
+        xi_by_slot=xi_by_slot)
     if cfg["field"] or cfg.get("c0") == "linear_x":
         f = cs.Field(c=st["c"], grad=st["grad"], rho_alpha=st["rho_a"], rho_beta=st["rho_b"])
         cs.gradient(f, cs.build_operators(grid, fp, DT))
@@ -414,6 +415,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-perf-mode", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -505,6 +507,52 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(sim, n, dt_, K, W, barrier, world)
 
+    # ---- performance mode (SURVEY 7 hard part 6): the sorted engine reading
+    # the increments by storage slot (coalesced) instead of by particle id;
+    # same distribution (parity tier T4), not the same trajectory
+    perf = None
+    engine_name = sim.engine
+    if engine_name == "sorted" and not args.no_perf_mode:
+        del sim
+        torch.cuda.empty_cache()
+        sim2, _, _, _ = make_state(cfg, rank, xi_by_slot=True)
+        for w in range(W):
+            sim2.step(xi[w % blocks], 1)
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if W + K <= blocks:
+            sim2.step(xi[W:W + K], K)
+        else:
+            for k in range(K):
+                sim2.step(xi[(W + k) % blocks], 1)
+        sim2.export_state()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        if sim2.status().code != 0:
+            raise RuntimeError("performance-mode run failed")
+        pms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([pms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pms = float(t.item())
+        sim2.set_profiling(True)
+        for k in range(KP):
+            sim2.step(xi[(W + k) % blocks], 1)
+        pst = {k: v / KP for k, v in sim2.stage_times().items()}
+        sim2.set_profiling(False)
+        p_fu = pst["bin"] + pst["force"] + pst["update"]
+        perf = {"value": n * world * K / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / K,
+                "stage_ms": {k: round(v, 4) for k, v in pst.items()},
+                "roofline_frac": (ab["fu"] / (p_fu / 1e3) / 1e9) / peak,
+                "xi_order": "slot",
+                "note": "performance mode: increments consumed in storage-slot order "
+                        "(cs_sim_params.xi_by_slot); i.i.d. N(0,1), so the same dynamics in "
+                        "distribution (tests/test_gpu_t4.py), not the reference's trajectory"}
+        del sim2
+
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -530,12 +578,13 @@ def main():
             "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s",
                               "frac": step_gbs / peak, "algorithmic_bytes_per_step": ab["total"]},
             "stage_ms": {k: round(v, 4) for k, v in stages.items()},
-            "engine": sim.engine,
+            "engine": engine_name,
             "clocks": clocks.summary(),
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "reference_numba": reference_numba(args.config),
+            "perf_mode": perf,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

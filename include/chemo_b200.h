@@ -249,6 +249,13 @@ typedef struct {
      * DIRECT engine, n <= 65536 (O(n^2) scan), next_pos required. */
     double hard_eps;         /* the sphere diameter epsilon */
     double diffusion[2];     /* D per type (the sweep's split) */
+    /* Performance mode (hard part 6), SORTED engine only: the step's
+     * increments are consumed in the engine's storage-slot order (cell-sorted
+     * records) instead of by particle id -- coalesced reads instead of a
+     * random gather.  The increments are i.i.d. N(0,1), so the dynamics are
+     * the same in distribution (parity tier T4), not trajectory for
+     * trajectory.  0 = by id (the reference's layout). */
+    int32_t xi_by_slot;
 } cs_sim_params;
 
 /* Engines.  DIRECT keeps the reference layout (rows in id order) and

@@ -51,7 +51,7 @@ class SimParams_t(ctypes.Structure):
                 ("chi", C_f64 * 2), ("chi_pinned", C_i32 * 2), ("store_samples", C_i32),
                 ("store_next", C_i32), ("engine", C_i32), ("react", C_i32),
                 ("react_p_ab", C_f64), ("react_r_beta", C_f64), ("integrator", C_i32),
-                ("hard_eps", C_f64), ("diffusion", C_f64 * 2)]
+                ("hard_eps", C_f64), ("diffusion", C_f64 * 2), ("xi_by_slot", C_i32)]
 
 
 class SimState_t(ctypes.Structure):

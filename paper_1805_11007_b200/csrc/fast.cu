@@ -85,8 +85,8 @@ struct FastArgs {
                         // 2 skip deposits, 64 no pair terms, 128 no candidate walk, 4 store records at the slot index
                         // without claims, 8 the same plus a fire-and-forget
                         // claim (4/8/32: timing only, wrong results)
-                        // 32 xi read at the slot index (timing only: wrong results)
-    const float *xi;    // this step's (N, 2) increments, indexed by id
+    const float *xi;    // this step's (N, 2) increments, indexed by id (or slot: xi_slot)
+    int xi_slot;        // performance mode: increments by storage slot (cs_sim_params.xi_by_slot)
     const float *grad;  // (n_c^2, 2)
     int *rho_q;         // 2 * m fixed-point deposits (a | b)
     long long n;
@@ -689,9 +689,16 @@ k_fast_update(DevStatus *st, int step) {
         const double x = (double)xf, y = (double)yf;
         const int ti = (int)(meta >> 31);
         const unsigned id = meta & ID_MASK;
-        const unsigned zi = (a.debug & 32) ? (unsigned)t : id;  // 32: diagnostic only
-        const float2 z = (a.debug & 1) ? __ldg(reinterpret_cast<const float2 *>(a.xi) + zi)
-                                       : ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + zi);
+        // the particle's increment: xi[id] (the reference's layout: a random
+        // gather, kept in L2 by evict_last), or xi[slot] in performance mode
+        // (xi_by_slot: a coalesced stream)
+        float2 z;
+        if (a.xi_slot)
+            z = __ldcs(reinterpret_cast<const float2 *>(a.xi) + t);
+        else if (a.debug & 1)
+            z = __ldg(reinterpret_cast<const float2 *>(a.xi) + id);
+        else
+            z = ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
         const double fx = f.x, fy = f.y;  // zero without interactions
 #if CS_CLAIM_AGG
         if (p_have) {
@@ -1459,6 +1466,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         a.debug = dbg ? atoi(dbg) : 0;
     }
     a.xi = (const float *)xi;
+    a.xi_slot = p.xi_by_slot ? 1 : 0;
     a.grad = (const float *)s->grad;
     a.rho_q = f->rho_q.as<int>();
     a.n = n;

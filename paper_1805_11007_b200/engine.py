@@ -120,6 +120,8 @@ class SimConfig:
     cluster_sigma: float = 0.02
     engine: str = "auto"            # auto | direct | sorted (fp32 only)
     rng: str = "auto"               # auto | host | device: where the numpy streams are drawn
+    xi_order: str = "id"            # id | slot: performance mode of the sorted engine
+                                    # (increments by storage slot; same distribution, T4)
 
     def __post_init__(self):
         if self.experiment not in EXPERIMENTS:
@@ -172,6 +174,10 @@ class SimConfig:
             raise ValueError(f"unknown rng {self.rng!r}")
         if self.engine == "sorted" and self.precision != "fp32":
             raise ValueError("the sorted engine needs precision='fp32'")
+        if self.xi_order not in ("id", "slot"):
+            raise ValueError(f"unknown xi_order {self.xi_order!r}")
+        if self.xi_order == "slot" and self.precision != "fp32":
+            raise ValueError("xi_order='slot' is the sorted engine's mode (precision='fp32')")
         self.motion_params()
         self.field_params()
         self.kernel()
@@ -248,6 +254,24 @@ class SimConfig:
     def as_dict(self) -> dict:
         return asdict(self)
 
+    def reference_dict(self) -> dict:
+        """The reference's SimConfig fields (engine.py:56-108), plus the
+        extension fields (below '# ---- extensions') whose values differ from
+        their defaults: the manifest stays the reference's file contract for
+        runs that use no extension."""
+        d = asdict(self)
+        defaults = SimConfig.__dataclass_fields__
+        for name in EXTENSION_FIELDS:
+            if d[name] == defaults[name].default:
+                del d[name]
+        return d
+
+
+EXTENSION_FIELDS = ("precision", "radius_alpha", "radius_beta", "chi_alpha", "secrete_alpha",
+                    "secrete_beta", "consume_alpha", "consume_beta", "alpha_init",
+                    "initial_positions", "n_clusters", "cluster_sigma", "engine", "rng",
+                    "xi_order")
+
 
 def msd(pop: Population) -> float:
     """Mean over particles of squared displacement from the start anchor."""
@@ -272,7 +296,8 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
                       refresh_active, grid: Grid | None, fparams: FieldParams | None,
                       kernel: Kernel | None, secretes, consumes, chi, chi_pinned,
                       store_samples, store_next, engine: str = "auto",
-                      reaction: ReactionParams | None = None) -> N.SimParams_t:
+                      reaction: ReactionParams | None = None,
+                      xi_by_slot: bool = False) -> N.SimParams_t:
     p = N.SimParams_t()
     p.n = int(n)
     p.prec = prec
@@ -281,6 +306,7 @@ def sim_params_struct(*, n, prec, domain: Domain, motion: MotionParams, dt, fiel
     p.interaction = {"soft": 1, "hard": 2}.get(motion.interaction, 0)
     p.hard_eps = float(motion.epsilon)
     p.diffusion[0], p.diffusion[1] = float(motion.d_alpha), float(motion.d_beta)
+    p.xi_by_slot = 1 if xi_by_slot else 0
     p.integrator = 1 if getattr(motion, "integrator", "em") == "tamed" else 0
     if p.interaction:
         eps, cut, cell = motion.pair_table()
@@ -491,7 +517,8 @@ class Realisation:
             secretes=(config.secrete_alpha, config.secrete_beta),
             consumes=(config.consume_alpha, config.consume_beta), chi=self._chi,
             chi_pinned=self._chi_pinned, store_samples=self._stores,
-            store_next=self._stores, engine=config.engine, reaction=self.reaction)
+            store_next=self._stores, engine=config.engine, reaction=self.reaction,
+            xi_by_slot=config.xi_order == "slot")
         self._sim = DeviceSim(params, self._state)
         self._fixed = self.reactions_active and self.reaction.scheduler == "fixed"
         self.clock = None

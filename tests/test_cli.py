@@ -182,6 +182,7 @@ def test_counts_run_byte_identical_to_reference(tmp_path):
     assert set(manifest) == set(ref) | {"wall_clock_seconds", "created"}
     for key in ("version", "experiment", "samples", "seeds", "outputs"):
         assert manifest[key] == ref[key], key
+    assert set(manifest["config"]) == set(ref["config"])  # the reference's key set
     for key, value in ref["config"].items():
         assert manifest["config"][key] == value, key
 

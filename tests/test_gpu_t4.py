@@ -31,10 +31,14 @@ from t4_stats import NAMES, T4_CONFIG, compare, sample_stats  # noqa: E402
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "t4_reference.npz")
 
 
-@pytest.mark.parametrize("precision,engine", [("fp32", "sorted"), ("fp64", "direct")])
-def test_t4_ensemble_statistics_vs_reference(precision, engine):
+@pytest.mark.parametrize("precision,engine,xi_order", [("fp32", "sorted", "id"),
+                                                      ("fp32", "sorted", "slot"),
+                                                      ("fp64", "direct", "id")])
+def test_t4_ensemble_statistics_vs_reference(precision, engine, xi_order):
+    """xi_order='slot' is the sorted engine's performance mode (increments
+    consumed by storage slot): the same distribution, so the same statistics."""
     ref = np.load(GOLDEN)["stats"]
-    cfg = cs.SimConfig(**T4_CONFIG, seed_base=1000, precision=precision)
+    cfg = cs.SimConfig(**T4_CONFIG, seed_base=1000, precision=precision, xi_order=xi_order)
     rows = []
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")

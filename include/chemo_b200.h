@@ -345,6 +345,34 @@ int64_t cs_sim_status_bytes(void);
 int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n);
 
 /* ---------------------------------------------------------------------- */
+/* y-slab decomposition of one system over ranks (slabs.py).     */
+/* The SORTED engine of rank r owns the global cell rows [bounds[r],        */
+/* bounds[r+1]) (bounds: world + 1 ints from 0 to the cell-row count) and   */
+/* keeps copies (ghosts) of the neighbours' boundary rows, so that every    */
+/* owned particle sees its whole reference ring (motion.py:200-245): the    */
+/* forces and the update are the single-domain engine's, bit for bit.  Per  */
+/* step: cs_slab_step_local (forces + update over the owned slots; records  */
+/* whose new row another rank owns, and ghost copies of records landing in  */
+/* a boundary row, go to the outbox), the caller's exchange of the outbox   */
+/* records (dest = rank | kind << 30, kind 0 migrant / 1 ghost; 16-byte     */
+/* records), cs_slab_claim of the records received, cs_slab_finish (sort).  */
+/* Field-free runs (field_active = refresh_active = 0) in this version.     */
+/* ---------------------------------------------------------------------- */
+int cs_slab_config(cs_sim *sim, const int32_t *bounds, int32_t world, int32_t rank);
+/* the owned rows and the ghost rows of the caller's global (id-ordered)
+ * pos / anchor / type arrays -> the engine's records */
+int cs_slab_import(cs_sim *sim, const cs_sim_state *st);
+/* xi: the step's (n_global, 2) increments by particle id */
+int cs_slab_step_local(cs_sim *sim, const cs_sim_state *st, const void *xi);
+/* the outbox after cs_slab_step_local (device pointers; the count is read
+ * back to the host: the exchange sizes its transfers with it) */
+int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t *count);
+int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n);
+int cs_slab_finish(cs_sim *sim);
+/* the owned slot range of the sorted records (tests) */
+int cs_slab_range(cs_sim *sim, int64_t *lo, int64_t *hi);
+
+/* ---------------------------------------------------------------------- */
 /* Ensembles of small realisations (run_ensemble, engine.py:455-484;       */
 /* SURVEY 8f rank 1): one CTA per realisation, state in shared memory,      */
 /* K steps per launch.  The realisations share one cs_sim_params (n =       */

@@ -123,6 +123,14 @@ SIGNATURES = [
     ("cs_sim_stage_times", C_i32, [C_p, C_p, C_i32]),
     ("cs_sim_engine", C_i32, [C_p]),
     ("cs_sim_import", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
+    ("cs_slab_config", C_i32, [C_p, ctypes.POINTER(C_i32), C_i32, C_i32]),
+    ("cs_slab_import", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
+    ("cs_slab_step_local", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p]),
+    ("cs_slab_outbox", C_i32, [C_p, ctypes.POINTER(C_p), ctypes.POINTER(C_p),
+                               ctypes.POINTER(C_i64)]),
+    ("cs_slab_claim", C_i32, [C_p, C_p, C_i64]),
+    ("cs_slab_finish", C_i32, [C_p]),
+    ("cs_slab_range", C_i32, [C_p, ctypes.POINTER(C_i64), ctypes.POINTER(C_i64)]),
     ("cs_sim_export", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
     ("cs_sim_status_device", C_p, [C_p]),
     ("cs_sim_status_bytes", C_i64, []),

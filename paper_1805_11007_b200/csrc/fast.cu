@@ -39,6 +39,7 @@
 #include <stdlib.h>
 
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -102,6 +103,17 @@ struct FastArgs {
     float halff0, halff1, sizef0, sizef1;
     float cutf2[4];     // binary32 prefilter: cut2 * (1 + 1e-5)
     cs_domain dom;
+    // y-slab mode (slabs.py): this rank owns the global cell rows
+    // [b0, b1); its records are those plus copies of the neighbours' boundary
+    // rows (ghosts); forces and the update run over the owned slot range
+    const int *range;    // device [lo, hi) of the owned slots (nullptr: [0, n))
+    int slab, rank, world, b0, b1, per_rows;
+    const int *row_owner;  // device: owner rank of every global cell row
+    const int *bounds;     // device: world + 1 row boundaries
+    Rec *outbox;           // records for other ranks (migrants and ghosts)
+    int *out_dest;         // their destination rank | kind << 30 (0 migrant, 1 ghost)
+    int *out_count;
+    long long out_cap;
 };
 
 // Random gather of the step's increments: keep the 80 MB slice in L2
@@ -405,11 +417,12 @@ k_fast_forces(const DevStatus *st) {
     // persistent grid, warps sweep the slots together (a narrow processing
     // front: ring rows are shared by concurrently running warps)
     const long long wstride = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-         base < a.n; base += wstride) {
+    const long long s_lo = a.range ? a.range[0] : 0, s_hi = a.range ? a.range[1] : a.n;
+    for (long long base = s_lo + (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+         base < s_hi; base += wstride) {
         const long long t = base + lane;
         const int t32 = (int)t;
-        const bool live = t < a.n;
+        const bool live = t < s_hi;
         float4 mer = make_float4(0.f, 0.f, 0.f, 0.f);
         if (live) mer = __ldg(rec + t);
         const float xf = mer.x, yf = mer.y;
@@ -648,6 +661,47 @@ __device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, in
     }
 }
 
+// slab mode: a record for another rank (a migrant to the owner of its new
+// row, or a ghost copy for a neighbour of that owner); a ghost for this rank
+// itself is claimed here directly
+__device__ __noinline__ void slab_emit(const FastArgs &a, DevStatus *st, int step, float4 out,
+                                       int key, int dest, int kind, int lane) {
+    if (dest == a.rank) {
+        const int pb = (key >> BUCKET_SHIFT) * SUBB + (lane & (SUBB - 1));
+        claim_store(a, st, step, pb, atomicAdd(&a.fill[pb], 1), out);
+        return;
+    }
+    const int e = atomicAdd(a.out_count, 1);
+    if (e < a.out_cap) {
+        reinterpret_cast<float4 *>(a.outbox)[e] = out;
+        a.out_dest[e] = dest | (kind << 30);
+    } else {
+        atomicMin(&st->key, err_key(3, 0, CS_SORT_OVERFLOW));
+        st->abort = 1;
+        st->step = step;
+    }
+}
+
+// the slab duties of a record whose new cell row is R: ghost copies for the
+// neighbours of R's owner when R is one of its boundary rows; false when the
+// record leaves (a migrant to R's owner) instead of being claimed here
+__device__ __forceinline__ bool slab_route(const FastArgs &a, DevStatus *st, int step, float4 out,
+                                           int key, int R, int lane) {
+    const int q = a.row_owner[R];
+    int g1 = -1, g2 = -1;
+    if (R == a.bounds[q]) g1 = q > 0 ? q - 1 : (a.per_rows ? a.world - 1 : -1);
+    if (R == a.bounds[q + 1] - 1) g2 = q + 1 < a.world ? q + 1 : (a.per_rows ? 0 : -1);
+    if (g2 == g1) g2 = -1;  // world 2, periodic: one copy for the other rank
+    if (g1 == q) g1 = -1;   // world 1
+    if (g2 == q) g2 = -1;
+    if (g1 >= 0) slab_emit(a, st, step, out, key, g1, 1, lane);
+    if (g2 >= 0) slab_emit(a, st, step, out, key, g2, 1, lane);
+    if (q == a.rank) return true;
+    slab_emit(a, st, step, out, key, q, 0, lane);
+    return false;
+}
+
+template <bool SLAB>
 __global__ void __launch_bounds__(256, CS_UPDATE_MINB)
 k_fast_update(DevStatus *st, int step) {
     const FastArgs &a = cA;
@@ -672,10 +726,11 @@ k_fast_update(DevStatus *st, int step) {
     const int wpart = (threadIdx.x >> 5) & (SUBB - 1);
     bool p_have = false, p_live = false;
     int p_leader = 0, p_rank = 0, p_ret = 0;
-    for (long long tb = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); tb < a.n;
-         tb += stride) {
-        const bool live = tb + lane < a.n;
-        const long long t = live ? tb + lane : a.n - 1;
+    const long long s_lo = SLAB ? a.range[0] : 0, s_hi = SLAB ? a.range[1] : a.n;
+    for (long long tb = s_lo + blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
+         tb < s_hi; tb += stride) {
+        const bool live = tb + lane < s_hi;
+        const long long t = live ? tb + lane : s_hi - 1;
 #else
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.n; t += stride) {
         const bool live = true;
@@ -786,9 +841,11 @@ k_fast_update(DevStatus *st, int step) {
         // ---- bin the stored (binary32) coordinate for the next step (cell
         // histogram: a reduction, no value returned)
         const double nx = (double)out.x, ny = (double)out.y;
-        const int key = cell_axis_fast(ny, a.g.lo1, a.eff1, n1) * n0 +
-                        cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
+        const int cyn = cell_axis_fast(ny, a.g.lo1, a.eff1, n1);
+        const int key = cyn * n0 + cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
 #if CS_CLAIM_AGG
+        bool claim = live;
+        if (SLAB && live && !dead) claim = slab_route(a, st, step, out, key, cyn, lane);
         p_b = (key >> BUCKET_SHIFT) * SUBB + wpart;
         if (a.debug & 12) {  // timing diagnostics only (wrong results)
             if (live && (a.debug & 8)) atomicAdd(&a.fill[p_b], 1);
@@ -796,11 +853,11 @@ k_fast_update(DevStatus *st, int step) {
             p_have = false;
             continue;
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, live ? p_b : -1 - lane);
+        const unsigned peers = __match_any_sync(0xffffffffu, claim ? p_b : -1 - lane);
         p_leader = __ffs(peers) - 1;
         p_rank = __popc(peers & lt);
-        if (live && lane == p_leader) p_ret = atomicAdd(&a.fill[p_b], __popc(peers));
-        p_live = live;
+        if (claim && lane == p_leader) p_ret = atomicAdd(&a.fill[p_b], __popc(peers));
+        p_live = claim;
         p_have = true;
         p_out = out;
 #else
@@ -1173,8 +1230,10 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
 // records (sorted) -> caller arrays (id order); anchor = anchor0 - wraps * L
 __global__ void k_fast_export(const Rec *__restrict__ rec, long long n,
                               const float *__restrict__ anchor0, double size0, double size1,
-                              float *__restrict__ pos, float *__restrict__ anchor) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+                              float *__restrict__ pos, float *__restrict__ anchor,
+                              const int *__restrict__ range) {
+    const long long lo = range ? range[0] : 0, hi = range ? range[1] : n;
+    for (long long t = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; t < hi;
          t += (long long)gridDim.x * blockDim.x) {
         const Rec r = rec[t];
         const unsigned id = r.meta & ID_MASK;
@@ -1184,6 +1243,78 @@ __global__ void k_fast_export(const Rec *__restrict__ rec, long long n,
         const float ay = (float)dsub((double)a0.y, dmul((double)r.wy, size1));
         reinterpret_cast<float2 *>(anchor)[id] = make_float2(ax, ay);
     }
+}
+
+// ---- y-slab mode (cs_slab_*) ----------------------------------------------
+// The cell row of a position, as the update bins it.
+__device__ __forceinline__ int slab_row(float y, const BinGeom &g, const ExactDiv &eff1) {
+    return cell_axis_fast((double)y, g.lo1, eff1, g.n1);
+}
+__device__ __forceinline__ bool slab_keeps(int R, int b0, int b1, int n1, int per) {
+    if (R >= b0 && R < b1) return true;                             // owned
+    if (R == b0 - 1 || (per && b0 == 0 && R == n1 - 1)) return true;  // lower ghost row
+    if (R == b1 || (per && b1 == n1 && R == 0)) return true;          // upper ghost row
+    return false;
+}
+
+// the caller's (id-ordered, global) arrays -> this rank's records: its owned
+// rows and the ghost rows on either side, claimed into their bucket regions
+__global__ void k_slab_import(const float *__restrict__ pos, const float *__restrict__ anchor,
+                              const uint8_t *__restrict__ type, long long n, BinGeom g,
+                              ExactDiv eff0, ExactDiv eff1, int b0, int b1,
+                              Rec *__restrict__ region, int *__restrict__ fill, long long cap,
+                              float *__restrict__ anchor0, DevStatus *st) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float2 p = reinterpret_cast<const float2 *>(pos)[i];
+        reinterpret_cast<float2 *>(anchor0)[i] = reinterpret_cast<const float2 *>(anchor)[i];
+        const int R = slab_row(p.y, g, eff1);
+        if (!slab_keeps(R, b0, b1, g.n1, g.per1)) continue;
+        Rec r;
+        r.x = p.x;
+        r.y = p.y;
+        r.meta = (unsigned)i | ((type && type[i]) ? 0x80000000u : 0u);
+        r.wx = 0;
+        r.wy = 0;
+        const int key = R * g.n0 + cell_axis_fast((double)p.x, g.lo0, eff0, g.n0);
+        const int q = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
+        const int slot = atomicAdd(&fill[q], 1);
+        if (slot < cap) {
+            region[(long long)q * cap + slot] = r;
+        } else {
+            atomicMin(&st->key, err_key(3, q / SUBB, CS_SORT_OVERFLOW));
+            st->abort = 1;
+        }
+    }
+}
+
+// records received from other ranks (migrants and ghosts) claimed into
+// their bucket regions
+__global__ void k_slab_claim(const float4 *__restrict__ in, long long n, BinGeom g, ExactDiv eff0,
+                             ExactDiv eff1, Rec *__restrict__ region, int *__restrict__ fill,
+                             long long cap, DevStatus *st, int step) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 r = in[i];
+        const int key = slab_row(r.y, g, eff1) * g.n0 +
+                        cell_axis_fast((double)r.x, g.lo0, eff0, g.n0);
+        const int q = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
+        const int slot = atomicAdd(&fill[q], 1);
+        if (slot < cap) {
+            reinterpret_cast<float4 *>(region)[(long long)q * cap + slot] = r;
+        } else {
+            atomicMin(&st->key, err_key(3, q / SUBB, CS_SORT_OVERFLOW));
+            st->abort = 1;
+            st->step = step;
+        }
+    }
+}
+
+// the owned slot range [starts(b0 row), starts(b1 row)) of the sorted records
+__global__ void k_slab_range(const int *__restrict__ starts, long long c0, long long c1,
+                             int *__restrict__ range) {
+    range[0] = starts[c0];
+    range[1] = starts[c1];
 }
 
 // fixed-point deposits -> caller rho arrays (float densities)
@@ -1231,6 +1362,11 @@ struct cs_fast {
     double eff0 = 1.0, eff1 = 1.0;  // cell sides
     cs::BinGeom g{};
     bool gather = false;            // deposit by grid rows (k_fast_deposit_rows)
+    // y-slab mode (cs_slab_*): owned rows [b0, b1) of world ranks
+    bool slab = false;
+    int rank = 0, world = 1, b0 = 0, b1 = 0;
+    cs::Buf range, row_owner, bounds, outbox, out_dest, out_count;
+    long long out_cap = 0;
 };
 
 namespace cs {
@@ -1289,7 +1425,9 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
 void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
-                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->gen, &f->depflag})
+                   &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->gen, &f->depflag,
+                   &f->range, &f->row_owner, &f->bounds, &f->outbox, &f->out_dest,
+                   &f->out_count})
         b->release();
     delete f;
 }
@@ -1399,7 +1537,8 @@ int fast_export(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_st
     if (n > 0) {
         k_fast_export<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
             f->rec[f->cur].as<Rec>(), n, f->anchor0.as<float>(), p.domain.hi[0] - p.domain.lo[0],
-            p.domain.hi[1] - p.domain.lo[1], (float *)s->pos, (float *)s->anchor);
+            p.domain.hi[1] - p.domain.lo[1], (float *)s->pos, (float *)s->anchor,
+            f->slab ? f->range.as<int>() : nullptr);
         CS_LAUNCH_CHECK();
     }
     if (p.field_active && s->rho_a && s->rho_b) {
@@ -1497,6 +1636,19 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.sz0 = make_exact_div(p.domain.hi[0] - p.domain.lo[0]);
     a.sz1 = make_exact_div(p.domain.hi[1] - p.domain.lo[1]);
     a.dom = p.domain;
+    a.slab = f->slab ? 1 : 0;
+    a.range = f->slab ? f->range.as<int>() : nullptr;
+    a.rank = f->rank;
+    a.world = f->world;
+    a.b0 = f->b0;
+    a.b1 = f->b1;
+    a.per_rows = c.g.per1;
+    a.row_owner = f->slab ? f->row_owner.as<int>() : nullptr;
+    a.bounds = f->slab ? f->bounds.as<int>() : nullptr;
+    a.outbox = f->slab ? f->outbox.as<Rec>() : nullptr;
+    a.out_dest = f->slab ? f->out_dest.as<int>() : nullptr;
+    a.out_count = f->slab ? f->out_count.as<int>() : nullptr;
+    a.out_cap = f->out_cap;
     if (n > 0) {
         static int resident = 0;  // blocks of k_fast_forces resident per SM
         if (!resident) {
@@ -1527,12 +1679,16 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         // working set (cell histogram + deposit rows near the front) stays in L2
         static int resident_u = 0;
         if (!resident_u) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident_u, k_fast_update, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident_u, k_fast_update<false>, 256,
+                                                          0);
             if (resident_u < 1) resident_u = 1;
         }
         const int grid_u =
             (int)(want < (long long)sms * resident_u ? want : (long long)sms * resident_u);
-        k_fast_update<<<grid_u, 256, 0, ctx->stream>>>(st, step);
+        if (f->slab)
+            k_fast_update<true><<<grid_u, 256, 0, ctx->stream>>>(st, step);
+        else
+            k_fast_update<false><<<grid_u, 256, 0, ctx->stream>>>(st, step);
         CS_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -1554,5 +1710,115 @@ int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, co
 int *fast_rho_q(cs_fast *f) { return f->rho_q.p && !f->gather ? f->rho_q.as<int>() : nullptr; }
 
 bool fast_imported(const cs_fast *f) { return f && f->imported; }
+
+// ---- y-slab mode host side ------------------------------------------------
+int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long long n,
+                     cudaStream_t stream) {
+    if (world < 2 || rank < 0 || rank >= world) {
+        set_error("slab mode: world >= 2 and 0 <= rank < world");
+        return CS_ERR_PARAM;
+    }
+    const int n1 = f->g.n1;
+    std::vector<int> owner((size_t)n1), b((size_t)world + 1);
+    for (int q = 0; q <= world; q++) b[(size_t)q] = bounds[q];
+    if (b[0] != 0 || b[(size_t)world] != n1) {
+        set_error("slab mode: bounds must run from 0 to the %d cell rows", n1);
+        return CS_ERR_PARAM;
+    }
+    for (int q = 0; q < world; q++) {
+        if (b[(size_t)q + 1] <= b[(size_t)q]) {
+            set_error("slab mode: every rank needs at least one cell row");
+            return CS_ERR_PARAM;
+        }
+        for (int r = b[(size_t)q]; r < b[(size_t)q + 1]; r++) owner[(size_t)r] = q;
+    }
+    f->slab = true;
+    f->world = world;
+    f->rank = rank;
+    f->b0 = b[(size_t)rank];
+    f->b1 = b[(size_t)rank + 1];
+    CS_TRY(f->row_owner.ensure(sizeof(int) * (size_t)n1));
+    CS_TRY(f->bounds.ensure(sizeof(int) * ((size_t)world + 1)));
+    CS_TRY(f->range.ensure(sizeof(int) * 4));
+    CS_TRY(f->out_count.ensure(sizeof(int) * 4));
+    f->out_cap = n > 1024 ? n : 1024;  // every record could leave (kicks cross several slabs)
+    CS_TRY(f->outbox.ensure(sizeof(Rec) * (size_t)f->out_cap));
+    CS_TRY(f->out_dest.ensure(sizeof(int) * (size_t)f->out_cap));
+    CS_CUDA(cudaMemcpyAsync(f->row_owner.p, owner.data(), sizeof(int) * owner.size(),
+                            cudaMemcpyHostToDevice, stream));
+    CS_CUDA(cudaMemcpyAsync(f->bounds.p, b.data(), sizeof(int) * b.size(),
+                            cudaMemcpyHostToDevice, stream));
+    CS_CUDA(cudaMemsetAsync(f->range.p, 0, sizeof(int) * 4, stream));
+    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int) * 4, stream));
+    CS_CUDA(cudaStreamSynchronize(stream));  // the host vectors go out of scope
+    return CS_OK;
+}
+
+static int fast_slab_range(cs_ctx *ctx, cs_fast *f) {
+    k_slab_range<<<1, 1, 0, ctx->stream>>>(cell_table(f, f->cur), (long long)f->b0 * f->g.n0,
+                                            (long long)f->b1 * f->g.n0, f->range.as<int>());
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+int fast_slab_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
+                     const GridGeom &gg, const unsigned char bits[3], DevStatus *st, int step) {
+    const long long n = p.n;
+    if (n > 0) {
+        k_slab_import<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+            (const float *)s->pos, (const float *)s->anchor, s->type, n, f->g,
+            make_exact_div(f->g.eff0), make_exact_div(f->g.eff1), f->b0, f->b1,
+            f->region.as<Rec>(), f->fill.as<int>(), f->cap, f->anchor0.as<float>(), st);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
+    CS_TRY(fast_slab_range(ctx, f));
+    f->imported = true;
+    return CS_OK;
+}
+
+int fast_slab_claim(cs_ctx *ctx, cs_fast *f, const void *recs, long long n, DevStatus *st,
+                    int step) {
+    if (n <= 0) return CS_OK;
+    k_slab_claim<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        (const float4 *)recs, n, f->g, make_exact_div(f->g.eff0), make_exact_div(f->g.eff1),
+        f->region.as<Rec>(), f->fill.as<int>(), f->cap, st, step);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
+int fast_slab_outbox(cs_ctx *ctx, cs_fast *f, void **recs, int **dest, long long *count) {
+    int c = 0;
+    CS_CUDA(cudaMemcpyAsync(&c, f->out_count.p, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *recs = f->outbox.p;
+    *dest = f->out_dest.as<int>();
+    *count = c < f->out_cap ? c : f->out_cap;
+    return CS_OK;
+}
+
+int fast_slab_reset_outbox(cs_ctx *ctx, cs_fast *f) {
+    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int), ctx->stream));
+    return CS_OK;
+}
+
+int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
+                   const unsigned char bits[3], DevStatus *st, int step) {
+    CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
+    return fast_slab_range(ctx, f);
+}
+
+int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi) {
+    int r[2] = {0, 0};
+    CS_CUDA(cudaMemcpyAsync(r, f->range.p, sizeof(r), cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *lo = r[0];
+    *hi = r[1];
+    return CS_OK;
+}
 
 }  // namespace cs

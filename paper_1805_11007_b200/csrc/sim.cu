@@ -68,6 +68,17 @@ int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, co
                 const unsigned char bits[3], int part, DevStatus *st, int step);
 bool fast_imported(const cs_fast *f);
 int *fast_rho_q(cs_fast *f);
+int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long long n,
+                     cudaStream_t stream);
+int fast_slab_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_sim_state *s,
+                     const GridGeom &gg, const unsigned char bits[3], DevStatus *st, int step);
+int fast_slab_claim(cs_ctx *ctx, cs_fast *f, const void *recs, long long n, DevStatus *st,
+                    int step);
+int fast_slab_outbox(cs_ctx *ctx, cs_fast *f, void **recs, int **dest, long long *count);
+int fast_slab_reset_outbox(cs_ctx *ctx, cs_fast *f);
+int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
+                   const unsigned char bits[3], DevStatus *st, int step);
+int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi);
 
 struct UpdateArgs {
     const void *xi;
@@ -712,5 +723,93 @@ extern "C" int cs_sim_set_profiling(cs_sim *sim, int32_t on) {
 extern "C" int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n) {
     CS_TRY(cs::sim_collect_stage_times(sim));
     for (int i = 0; i < n && i < CS_N_STAGES; i++) ms[i] = sim->stage_ms[i];
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// y-slab mode of the sorted engine: one rank's share of one
+// system.  The step is split where records cross ranks: cs_slab_step_local
+// (forces + update over the owned slots; leavers and ghost copies go to the
+// outbox), the caller's exchange (slabs.py: NCCL all-to-all, or in-process
+// copies), cs_slab_claim (received records), cs_slab_finish (bucket sort,
+// owned range).
+namespace {
+cs::FastStepCfg slab_cfg(cs_sim *sim) {
+    cs::FastStepCfg c;
+    c.p = &sim->p;
+    c.g = sim->geom;
+    c.pt = sim->pt;
+    c.gg = sim->gg;
+    c.ops = sim->ops;
+    c.bits[0] = sim->bits[0];
+    c.bits[1] = sim->bits[1];
+    c.bits[2] = 0;
+    return c;
+}
+int slab_check(cs_sim *sim) {
+    if (sim->engine != CS_ENGINE_SORTED) {
+        cs::set_error("slab mode runs on the sorted engine (prec CS_F32, engine SORTED)");
+        return CS_ERR_PARAM;
+    }
+    return CS_OK;
+}
+}  // namespace
+
+extern "C" int cs_slab_config(cs_sim *sim, const int32_t *bounds, int32_t world, int32_t rank) {
+    CS_TRY(slab_check(sim));
+    if (sim->p.field_active || sim->p.refresh_active) {
+        cs::set_error("slab mode: the field is not distributed (field_active / refresh_active "
+                      "must be 0)");
+        return CS_ERR_PARAM;
+    }
+    return cs::fast_slab_config(sim->fast, bounds, world, rank, sim->p.n, sim->ctx->stream);
+}
+
+extern "C" int cs_slab_import(cs_sim *sim, const cs_sim_state *st) {
+    CS_TRY(slab_check(sim));
+    return cs::fast_slab_import(sim->ctx, sim->fast, sim->p, st, sim->gg, sim->bits, sim->dstat(),
+                                sim->steps_done);
+}
+
+extern "C" int cs_slab_step_local(cs_sim *sim, const cs_sim_state *st, const void *xi) {
+    CS_TRY(slab_check(sim));
+    const int64_t l0 = sim->ctx->launches;
+    const cs::FastStepCfg c = slab_cfg(sim);
+    CS_TRY(cs::fast_slab_reset_outbox(sim->ctx, sim->fast));
+    CS_TRY(cs::fast_particles(sim->ctx, sim->fast, c, st, xi, sim->dstat(), sim->steps_done, 1));
+    CS_TRY(cs::fast_particles(sim->ctx, sim->fast, c, st, xi, sim->dstat(), sim->steps_done, 2));
+    sim->last_launches = sim->ctx->launches - l0;
+    return CS_OK;
+}
+
+extern "C" int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t *count) {
+    CS_TRY(slab_check(sim));
+    long long c = 0;
+    CS_TRY(cs::fast_slab_outbox(sim->ctx, sim->fast, recs, dest, &c));
+    *count = c;
+    return CS_OK;
+}
+
+extern "C" int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n) {
+    CS_TRY(slab_check(sim));
+    return cs::fast_slab_claim(sim->ctx, sim->fast, recs, n, sim->dstat(), sim->steps_done);
+}
+
+extern "C" int cs_slab_finish(cs_sim *sim) {
+    CS_TRY(slab_check(sim));
+    const int64_t l0 = sim->ctx->launches;
+    CS_TRY(cs::fast_slab_sort(sim->ctx, sim->fast, sim->p, sim->gg, sim->bits, sim->dstat(),
+                              sim->steps_done));
+    sim->steps_done += 1;
+    sim->last_launches += sim->ctx->launches - l0;
+    return CS_OK;
+}
+
+extern "C" int cs_slab_range(cs_sim *sim, int64_t *lo, int64_t *hi) {
+    CS_TRY(slab_check(sim));
+    long long a = 0, b = 0;
+    CS_TRY(cs::fast_slab_range_host(sim->ctx, sim->fast, &a, &b));
+    *lo = a;
+    *hi = b;
     return CS_OK;
 }

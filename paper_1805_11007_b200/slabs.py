@@ -551,3 +551,169 @@ class DeviceSlabBackend:
         pin = torch.tensor(self.chi_pinned, device=pos.device)[types.long()]
         v = torch.where((chi != 1.0)[:, None], v * chi[:, None], v)
         return torch.where(pin[:, None], torch.zeros_like(v), v)
+
+
+# ============================================================================
+# The device slab engine: each rank's share is the SORTED engine in slab mode
+# (csrc/fast.cu, cs_slab_*), records cross ranks as 16-byte device rows
+# ============================================================================
+class LoopbackHub:
+    """All ranks of one process on one device (tests): the exchange hands
+    every rank the records the others addressed to it."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def exchange_all(self, outs):
+        """outs[r] = (recs (M, 4) int32, dest (M,) int32) of rank r ->
+        received[q] = the records addressed to q, from every rank."""
+        got = [[] for _ in range(self.world)]
+        for recs, dest in outs:
+            if recs.shape[0] == 0:
+                continue
+            d = (dest & 0x3FFFFFFF).long()
+            for q in range(self.world):
+                sel = d == q
+                if bool(sel.any()):
+                    got[q].append(recs[sel])
+        return [torch.cat(g) if g else None for g in got]
+
+
+class NcclTransport:
+    """One rank per GPU: the outbox routed by an all-to-all over NCCL
+    (NVLink).  The per-destination counts travel first (one P-int
+    all-to-all, read back to size the payload -- the only host sync of a
+    step), then the 16-byte records."""
+
+    def __init__(self, world: int, group=None):
+        self.world, self.group = world, group
+
+    def exchange(self, recs, dest):
+        W = self.world
+        d = (dest & 0x3FFFFFFF).long()
+        order = torch.argsort(d, stable=True)
+        sc_t = torch.bincount(d, minlength=W).to(torch.int64)
+        rc_t = torch.empty_like(sc_t)
+        dist.all_to_all_single(rc_t, sc_t, group=self.group)
+        both = torch.stack([sc_t, rc_t]).cpu()
+        sc, rc = both[0].tolist(), both[1].tolist()
+        out = torch.empty((sum(rc), 4), dtype=torch.int32, device=recs.device)
+        send = recs[order].contiguous() if recs.shape[0] else recs
+        dist.all_to_all_single(out.view(-1), send.view(-1), [4 * c for c in rc],
+                               [4 * c for c in sc], group=self.group)
+        return out
+
+
+class SlabEngine:
+    """One rank's share of a y-slab decomposed system on its GPU: the sorted
+    engine (binary32 records, reference summation order) over the owned cell
+    rows plus ghost copies of the neighbours' boundary rows.  Bit-identical to
+    the single-domain engine: every owned particle sees its whole reference
+    ring (ghost rows), rows stay in ascending id inside a cell, and the cell
+    geometry is the global one.
+
+    params: cs_sim_params of the WHOLE system (n = N, engine SORTED,
+    field off); state: the caller's global id-ordered arrays (pos, anchor,
+    species), read at import and written back (own particles) by export."""
+
+    def __init__(self, params, state: dict, bounds, rank: int, world: int):
+        from . import _native as N
+        from .engine import DeviceSim
+        self.N = N
+        self.rank, self.world = rank, world
+        self.bounds = np.asarray(bounds, dtype=np.int32)
+        self.sim = DeviceSim(params, state)
+        if self.sim.engine != "sorted":
+            raise ValueError("slab mode needs the sorted engine (binary32, engine='sorted')")
+        lib = self.sim._bind()
+        b = (N.C_i32 * len(self.bounds))(*[int(v) for v in self.bounds])
+        N.check(lib.cs_slab_config(self.sim._h, b, world, rank), "cs_slab_config")
+        N.check(lib.cs_slab_import(self.sim._h, ctypes_byref(self.sim._st)), "cs_slab_import")
+        self._empty = None
+
+    # ---- phases ------------------------------------------------------------
+    def local(self, xi):
+        """Forces + update of the owned particles (xi: the step's global
+        (N, 2) increments by id, on this device)."""
+        N = self.N
+        N.check(self.sim._bind().cs_slab_step_local(self.sim._h, ctypes_byref(self.sim._st),
+                                                   N.ptr(xi)), "cs_slab_step_local")
+
+    def outbox(self):
+        """(records (M, 4) int32, dest (M,) int32) views of the outbox."""
+        import ctypes
+        N = self.N
+        rp, dp, cnt = N.C_p(), N.C_p(), N.C_i64()
+        N.check(self.sim._bind().cs_slab_outbox(self.sim._h, ctypes.byref(rp), ctypes.byref(dp),
+                                                ctypes.byref(cnt)), "cs_slab_outbox")
+        m = int(cnt.value)
+        dev = self.sim.state["pos"].device
+        if m == 0:
+            z = torch.empty((0, 4), dtype=torch.int32, device=dev)
+            return z, torch.empty(0, dtype=torch.int32, device=dev)
+        recs = _device_view(rp.value, (m, 4), torch.int32, dev)
+        dest = _device_view(dp.value, (m,), torch.int32, dev)
+        return recs, dest
+
+    def claim(self, recs):
+        if recs is None or recs.shape[0] == 0:
+            return
+        N = self.N
+        recs = recs.contiguous()
+        N.check(self.sim._bind().cs_slab_claim(self.sim._h, N.ptr(recs), int(recs.shape[0])),
+                "cs_slab_claim")
+        self._keep = recs  # alive until the claim kernel has run (stream order)
+
+    def finish(self):
+        self.N.check(self.sim._bind().cs_slab_finish(self.sim._h), "cs_slab_finish")
+
+    # ---- one step over NCCL (one rank per process) -------------------------
+    def step(self, xi, transport: NcclTransport):
+        self.local(xi)
+        recs, dest = self.outbox()
+        self.claim(transport.exchange(recs, dest))
+        self.finish()
+
+    def status(self):
+        return self.sim.status()
+
+    def export(self):
+        """Own particles' positions / anchors into the global state arrays."""
+        self.sim.export_state()
+
+    def owned_range(self):
+        import ctypes
+        lo, hi = self.N.C_i64(), self.N.C_i64()
+        self.N.check(self.sim._bind().cs_slab_range(self.sim._h, ctypes.byref(lo),
+                                                    ctypes.byref(hi)), "cs_slab_range")
+        return int(lo.value), int(hi.value)
+
+    def close(self):
+        self.sim.close()
+
+
+def step_in_process(engines, hub: LoopbackHub, xi):
+    """One step of every rank of one process (tests): the phases in
+    lockstep, the exchange through the hub."""
+    for e in engines:
+        e.local(xi)
+    got = hub.exchange_all([e.outbox() for e in engines])
+    for e, g in zip(engines, got):
+        e.claim(g)
+    for e in engines:
+        e.finish()
+
+
+def ctypes_byref(x):
+    import ctypes
+    return ctypes.byref(x)
+
+
+def _device_view(ptr: int, shape, dtype, device):
+    """A torch tensor aliasing library-owned device memory."""
+    typestr = {torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+
+    class _Alias:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                    "data": (int(ptr), False), "version": 3}
+    return torch.as_tensor(_Alias(), device=device)

@@ -1,0 +1,96 @@
+"""The y-slab decomposition on the device: W ranks' sorted
+engines in slab mode, stepped in lockstep in one process on one GPU with the
+records exchanged through device copies (slabs.LoopbackHub; over NCCL the
+same records go through slabs.NcclTransport).  With the field off the
+decomposed system must equal the single-domain sorted engine bit for bit:
+the ghost rows give every owned particle its whole reference ring, rows stay
+in ascending id inside a cell, and the cell geometry is the global one."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1805_11007_b200 as cs  # noqa: E402
+from paper_1805_11007_b200 import slabs  # noqa: E402
+
+
+def _params(n, radii, periodic=True):
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        mp = cs.MotionParams(d_alpha=1.0, d_beta=0.5, epsilon=radii[0], cutoff=2 * radii[0],
+                             dt=1e-5, radius_alpha=radii[0], radius_beta=radii[1])
+    dom = cs.Domain.square(1.0, periodic=periodic)
+    grid = cs.Grid.square(8, 1.0, "periodic" if periodic else "neumann")
+    params = cs.sim_params_struct(
+        n=n, prec=1, domain=dom, motion=mp, dt=1e-5, field_active=False, refresh_active=False,
+        grid=grid, fparams=cs.FieldParams(d_c=0.0, k_alpha=0.0, k_beta=0.0, gamma=0.0),
+        kernel=cs.Kernel(kind="cic"), secretes=(False, False), consumes=(False, False),
+        chi=(0.0, 0.0), chi_pinned=(True, True), store_samples=False, store_next=False,
+        engine="sorted")
+    return params, mp, dom
+
+
+def _state(pos, sp):
+    f32 = torch.float32
+    return dict(pos=torch.as_tensor(pos, device="cuda").to(f32).contiguous(),
+                anchor=torch.as_tensor(pos, device="cuda").to(f32).contiguous(),
+                species=torch.as_tensor(sp, device="cuda"), next_pos=None,
+                drift=torch.zeros((pos.shape[0], 2), dtype=torch.float64, device="cuda"),
+                local_c=None, c=None, grad=None, rho_a=None, rho_b=None)
+
+
+def _bounds(pos, mp, dom, world):
+    e, c, cell = mp.pair_table()
+    geom = slabs.CellGeometry.make(dom.lo[1], dom.hi[1], cell)
+    counts = np.bincount(geom.row_of(pos[:, 1].astype(np.float64)), minlength=geom.n)
+    return slabs.SlabLayout.balanced(counts, world).bounds
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_slab_engine_equals_single_domain_bitwise(world, clustered):
+    rng = np.random.default_rng(10 + world)
+    n, steps = 200_000, 6
+    if clustered:  # cfg4's initial condition at 1/400 scale
+        centres = -0.5 + rng.random((64, 2))
+        pos = centres[rng.integers(0, 64, n)] + 0.02 * rng.standard_normal((n, 2))
+        pos = np.mod(pos + 0.5, 1.0) - 0.5
+    else:
+        pos = -0.5 + rng.random((n, 2))
+    pos = pos.astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    radii = (4.9e-4, 9.8e-4)
+    params, mp, dom = _params(n, radii)
+    xi = torch.as_tensor(rng.standard_normal((steps, n, 2)).astype(np.float32), device="cuda")
+    # single domain
+    st1 = _state(pos, sp)
+    one = cs.DeviceSim(params, st1)
+    one.step(xi, steps)
+    one.export_state()
+    assert one.status().code == 0
+    # W slabs sharing the caller's arrays (each exports its own particles)
+    st = _state(pos, sp)
+    bounds = _bounds(pos, mp, dom, world)
+    engines = [slabs.SlabEngine(params, st, bounds, r, world) for r in range(world)]
+    hub = slabs.LoopbackHub(world)
+    owned0 = sum(hi - lo for lo, hi in (e.owned_range() for e in engines))
+    assert owned0 == n
+    for k in range(steps):
+        slabs.step_in_process(engines, hub, xi[k])
+    for e in engines:
+        assert e.status().code == 0
+    owned = sum(hi - lo for lo, hi in (e.owned_range() for e in engines))
+    assert owned == n  # every particle owned by exactly one rank
+    for e in engines:
+        e.export()
+    torch.cuda.synchronize()
+    assert torch.equal(st["pos"], st1["pos"])
+    assert torch.equal(st["anchor"], st1["anchor"])
+    for e in engines:
+        e.close()

@@ -356,7 +356,6 @@ int cs_sim_stage_times(cs_sim *sim, double *ms, int32_t n);
 /* a boundary row, go to the outbox), the caller's exchange of the outbox   */
 /* records (dest = rank | kind << 30, kind 0 migrant / 1 ghost; 16-byte     */
 /* records), cs_slab_claim of the records received, cs_slab_finish (sort).  */
-/* Field-free runs (field_active = refresh_active = 0) in this version.     */
 /* ---------------------------------------------------------------------- */
 int cs_slab_config(cs_sim *sim, const int32_t *bounds, int32_t world, int32_t rank);
 /* the owned rows and the ghost rows of the caller's global (id-ordered)
@@ -371,6 +370,26 @@ int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n);
 int cs_slab_finish(cs_sim *sim);
 /* the owned slot range of the sorted records (tests) */
 int cs_slab_range(cs_sim *sim, int64_t *lo, int64_t *hi);
+/* The field of a slab rank (periodic binary32 grid, n_c = 2^k, CIC): it owns
+ * the grid rows [g0, g1) (an even split, rows a multiple of the spectral
+ * blocking); its particles deposit (int32 fixed point, exact) into the rows
+ * dep_j0 .. dep_j0 + dep_rows - 1 (mod n_c; they include the own rows) --
+ * the caller adds the window rows other ranks own into their owners' rows
+ * (cs_slab_rho: the 2 n_c^2 int32 deposit grids) -- and sample the gradient
+ * of the rows grad_j0 .. grad_j0 + grad_rows - 1 (computed from c rows one
+ * wider, which the caller fetches from their owners).  The implicit solve:
+ * cs_slab_field_rows (forward: own rows -> half spectrum [kx][g1 - g0]),
+ * the caller's all-to-all transpose, cs_slab_field_cols (columns kx0 ..
+ * kx0 + ncols of the blocks [rank][ncols][rp]), the transpose back,
+ * cs_slab_field_rows (inverse: -> c own rows).  Every pass is the
+ * single-domain solve's on the same rows / columns: the decomposed field is
+ * the single-domain field bit for bit. */
+int cs_slab_field_config(cs_sim *sim, int32_t g0, int32_t g1, int32_t dep_j0, int32_t dep_rows,
+                         int32_t grad_j0, int32_t grad_rows);
+void *cs_slab_rho(cs_sim *sim);
+int cs_slab_field_rows(cs_sim *sim, const cs_sim_state *st, void *spec, int32_t inverse);
+int cs_slab_field_cols(cs_sim *sim, void *blocks, int32_t kx0, int32_t ncols, int32_t rp);
+int cs_slab_field_grad(cs_sim *sim, const cs_sim_state *st);
 
 /* ---------------------------------------------------------------------- */
 /* Ensembles of small realisations (run_ensemble, engine.py:455-484;       */

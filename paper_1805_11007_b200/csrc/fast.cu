@@ -1133,7 +1133,10 @@ __global__ void __launch_bounds__(512)
 k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts, BinGeom g,
                     GridGeom gg, ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
                     int *__restrict__ rho_q, const int *__restrict__ exact_flag,
-                    int *__restrict__ other_flag, DevStatus *st, int step) {
+                    int *__restrict__ other_flag, DevStatus *st, int step, int jbase, int jrows,
+                    int cb0, int cb1) {
+    // (slab mode: grid rows jbase .. jbase + jrows - 1, mod n, from the
+    // particles of the own cell rows [cb0, cb1) only; single domain: 0, n, -1)
     extern __shared__ int acc[];  // [DEP_ROWS][2][n]
     // exact overflow checks only when the bucket sort saw a cell populated
     // beyond the conservative bound (returning atomics cost ~20 % here)
@@ -1141,7 +1144,7 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
     __shared__ int ovf_node;
     if (threadIdx.x == 0) ovf_node = -1;
     if (blockIdx.x == 0 && threadIdx.x == 0) *other_flag = 0;  // the next step's flag
-    const int n = gg.n, j0 = blockIdx.x * DEP_ROWS;
+    const int n = gg.n, j0 = jbase + blockIdx.x * DEP_ROWS;
     const long long m = (long long)n * n;
     for (int i = threadIdx.x; i < DEP_ROWS * 2 * n; i += blockDim.x) acc[i] = 0;
     __syncthreads();
@@ -1157,6 +1160,7 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
         int cy = cyw % g.n1;
         if (cy < 0) cy += g.n1;
         if (cyw - cy0 >= g.n1) break;  // fewer cell rows than the window
+        if (cb0 >= 0 && (cy < cb0 || cy >= cb1)) continue;  // ghost rows: other ranks'
         const int kb = starts[(long long)cy * g.n0], ke = starts[(long long)(cy + 1) * g.n0];
         for (int k = kb + threadIdx.x; k < ke; k += blockDim.x) {
             const float4 rv = __ldg(r4 + k);
@@ -1167,7 +1171,7 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
             const double base1 = floor(u1);
             const int b1 = wrap_index(base1, n);
             const int c1 = b1 + 1 == n ? 0 : b1 + 1;
-            int rb = b1 - j0, rc = c1 - j0;  // rows of this block's window, if any
+            int rb = (b1 - j0) % n, rc = (c1 - j0) % n;  // rows of this block's window, if any
             if (rb < 0) rb += n;
             if (rc < 0) rc += n;
             const bool hb = rb < DEP_ROWS, hc = rc < DEP_ROWS;
@@ -1217,8 +1221,9 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
         st->step = step;
     }
     for (int r = 0; r < DEP_ROWS; r++) {
-        const int j = j0 + r;
-        if (j >= n) break;
+        if (blockIdx.x * DEP_ROWS + r >= jrows) break;
+        int j = (j0 + r) % n;
+        if (j < 0) j += n;
         int *ra = rho_q + (long long)j * n, *rbp = rho_q + m + (long long)j * n;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             ra[i] = acc[r * 2 * n + i];
@@ -1365,6 +1370,7 @@ struct cs_fast {
     // y-slab mode (cs_slab_*): owned rows [b0, b1) of world ranks
     bool slab = false;
     int rank = 0, world = 1, b0 = 0, b1 = 0;
+    int dep_j0 = 0, dep_rows = 0;  // slab field: the grid rows this rank deposits into
     cs::Buf range, row_owner, bounds, outbox, out_dest, out_count;
     long long out_cap = 0;
 };
@@ -1502,10 +1508,12 @@ static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         smem_set = smem;
     }
-    k_fast_deposit_rows<<<(gg.n + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
+    const int jbase = f->slab ? f->dep_j0 : 0, jrows = f->slab ? f->dep_rows : gg.n;
+    k_fast_deposit_rows<<<(jrows + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
         f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
         make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>(),
-        f->depflag.as<int>() + (step & 1), f->depflag.as<int>() + ((step + 1) & 1), st, step);
+        f->depflag.as<int>() + (step & 1), f->depflag.as<int>() + ((step + 1) & 1), st, step,
+        jbase, jrows, f->slab ? f->b0 : -1, f->slab ? f->b1 : -1);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;
@@ -1775,6 +1783,7 @@ int fast_slab_import(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const cs_s
     }
     CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
     CS_TRY(fast_slab_range(ctx, f));
+    CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits, st, step));
     f->imported = true;
     return CS_OK;
 }
@@ -1811,6 +1820,14 @@ int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGe
     CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
     return fast_slab_range(ctx, f);
 }
+
+bool fast_slab_gather(const cs_fast *f) { return f->gather; }
+int fast_slab_dep_window(cs_fast *f, int j0, int rows) {
+    f->dep_j0 = j0;
+    f->dep_rows = rows;
+    return CS_OK;
+}
+void *fast_rho_all(cs_fast *f) { return f->rho_q.p; }
 
 int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi) {
     int r[2] = {0, 0};

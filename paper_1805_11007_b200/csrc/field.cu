@@ -150,13 +150,20 @@ __device__ __forceinline__ double d1_per(double cm, double cp, bool wrapped, con
 
 __global__ void __launch_bounds__(256)
 k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double wcell,
-                float *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q) {
+                float *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q,
+                int jbase = 0, int jrows = -1, int own0 = 0, int own1 = 1 << 30) {
+    // (slab mode: the rows jbase .. jbase + jrows - 1 (mod n); the field checks
+    // count the own rows [own0, own1) only)
     if (st->abort) return;
     const long long m = (long long)n * n;
     const int n4 = n >> 2;
     double neg = 0.0;
     int bad = 0, anyneg = 0;
-    for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    if (jrows < 0) jrows = n;
+    for (int jj = blockIdx.x; jj < jrows; jj += gridDim.x) {
+        int j = (jbase + jj) % n;
+        if (j < 0) j += n;
+        const bool check = j >= own0 && j < own1;
         const int jm = j == 0 ? n - 1 : j - 1, jp = j == n - 1 ? 0 : j + 1;
         const float4 *row = reinterpret_cast<const float4 *>(c + (long long)j * n);
         const float4 *rdn = reinterpret_cast<const float4 *>(c + (long long)jm * n);
@@ -175,8 +182,8 @@ k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double
                 gx[q] = d1_per((double)cv[q], (double)cv[q + 2], i == 0 || i == n - 1, kx);
                 gy[q] = d1_per((double)dv[q], (double)uv[q], j == 0 || j == n - 1, ky);
                 const double x = (double)cv[q + 1];
-                if (!isfinite(x)) bad = 1;
-                if (x < 0.0) {
+                if (check && !isfinite(x)) bad = 1;
+                if (check && x < 0.0) {
                     neg += wcell * x;
                     anyneg = 1;
                 }
@@ -233,6 +240,27 @@ __global__ void k_field_finish(DevStatus *st, int step) {
     }
     st->neg_flag = 0;
     st->neg_mass = 0.0;
+}
+
+// slab mode (periodic binary32 grids): the gradient of the grid rows
+// jbase .. jbase + jrows - 1 (mod n) from c rows one wider on either side;
+// the field checks of the own rows [own0, own1)
+int launch_gradient_rows(cs_ctx *ctx, const float *c, const GridGeom &gg, float *grad,
+                         DevStatus *st, int step, int jbase, int jrows, int own0, int own1) {
+    if (!(gg.per && gg.n % 4 == 0 && gg.n >= 8)) {
+        set_error("slab gradient: periodic grid with n_c a multiple of 4");
+        return CS_ERR_PARAM;
+    }
+    const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
+    const int g2 = jrows < 148 * 8 ? jrows : 148 * 8;
+    k_gradient_per4<<<g2 > 0 ? g2 : 1, 256, 0, ctx->stream>>>(c, gg.n, kx, ky, gg.d0 * gg.d1,
+                                                              grad, st, nullptr, jbase, jrows,
+                                                              own0, own1);
+    CS_LAUNCH_CHECK();
+    k_field_finish<<<1, 1, 0, ctx->stream>>>(st, step);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 2;
+    return CS_OK;
 }
 
 int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, void *grad,

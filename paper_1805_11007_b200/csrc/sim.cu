@@ -79,6 +79,16 @@ int fast_slab_reset_outbox(cs_ctx *ctx, cs_fast *f);
 int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
                    const unsigned char bits[3], DevStatus *st, int step);
 int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi);
+bool fast_slab_gather(const cs_fast *f);
+int fast_slab_dep_window(cs_fast *f, int j0, int rows);
+void *fast_rho_all(cs_fast *f);
+int spectral_slab_rows(cs_field_ops *ops, float *c, const int *q, double gamma, double ka,
+                       double kb, double scale, int row0, int rows, void *spec, int inverse,
+                       const DevStatus *st);
+int spectral_slab_cols(cs_field_ops *ops, void *blocks, int kx0, int ncols, int rp,
+                       const DevStatus *st);
+int launch_gradient_rows(cs_ctx *ctx, const float *c, const GridGeom &gg, float *grad,
+                         DevStatus *st, int step, int jbase, int jrows, int own0, int own1);
 
 struct UpdateArgs {
     const void *xi;
@@ -229,6 +239,7 @@ struct cs_sim {
     unsigned char bits[3] = {0, 0, 0};
     int engine = CS_ENGINE_DIRECT;
     cs_fast *fast = nullptr;
+    int slab_g0 = 0, slab_g1 = 0, slab_grad_j0 = 0, slab_grad_rows = 0;  // slab field rows
     cs_ens *ens = nullptr;              // CTA engine: one realisation of the ensemble engine
     cs::Buf cta_drift, cta_lc, cta_type;  // its state rows the caller did not provide
     cs::Buf status;  // this simulation's DevStatus
@@ -757,12 +768,57 @@ int slab_check(cs_sim *sim) {
 
 extern "C" int cs_slab_config(cs_sim *sim, const int32_t *bounds, int32_t world, int32_t rank) {
     CS_TRY(slab_check(sim));
-    if (sim->p.field_active || sim->p.refresh_active) {
-        cs::set_error("slab mode: the field is not distributed (field_active / refresh_active "
-                      "must be 0)");
+    if (sim->p.refresh_active && !sim->p.field_active) {
+        cs::set_error("slab mode: a static field (refresh without field steps) is not supported");
+        return CS_ERR_PARAM;
+    }
+    if (sim->p.field_active &&
+        !(sim->ops && cs::spectral_on(sim->ops) && sim->p.grid.periodic && sim->p.prec == CS_F32 &&
+          sim->p.deposit_kind == CS_CIC && cs::fast_slab_gather(sim->fast))) {
+        cs::set_error("slab mode with the field: periodic binary32 grid of n = 2^k, CIC deposit, "
+                      "periodic domain");
         return CS_ERR_PARAM;
     }
     return cs::fast_slab_config(sim->fast, bounds, world, rank, sim->p.n, sim->ctx->stream);
+}
+
+// The field of a slab rank: own grid rows [g0, g1) (a multiple of the
+// spectral row blocking), the grid rows its particles deposit into (a
+// window that includes the own rows) and the rows whose gradient its
+// particles sample.
+extern "C" int cs_slab_field_config(cs_sim *sim, int32_t g0, int32_t g1, int32_t dep_j0,
+                                    int32_t dep_rows, int32_t grad_j0, int32_t grad_rows) {
+    CS_TRY(slab_check(sim));
+    sim->slab_g0 = g0;
+    sim->slab_g1 = g1;
+    sim->slab_grad_j0 = grad_j0;
+    sim->slab_grad_rows = grad_rows;
+    return cs::fast_slab_dep_window(sim->fast, dep_j0, dep_rows);
+}
+
+extern "C" void *cs_slab_rho(cs_sim *sim) { return cs::fast_rho_all(sim->fast); }
+
+extern "C" int cs_slab_field_rows(cs_sim *sim, const cs_sim_state *st, void *spec,
+                                  int32_t inverse) {
+    CS_TRY(slab_check(sim));
+    const cs_sim_params &p = sim->p;
+    const double scale = (1.0 / 4194304.0) * (1.0 / (sim->gg.d0 * sim->gg.d1));
+    return cs::spectral_slab_rows(sim->ops, (float *)st->c, (const int *)cs::fast_rho_all(sim->fast),
+                                  p.gamma, p.k_alpha, p.k_beta, scale, sim->slab_g0,
+                                  sim->slab_g1 - sim->slab_g0, spec, inverse, sim->dstat());
+}
+
+extern "C" int cs_slab_field_cols(cs_sim *sim, void *blocks, int32_t kx0, int32_t ncols,
+                                  int32_t rp) {
+    CS_TRY(slab_check(sim));
+    return cs::spectral_slab_cols(sim->ops, blocks, kx0, ncols, rp, sim->dstat());
+}
+
+extern "C" int cs_slab_field_grad(cs_sim *sim, const cs_sim_state *st) {
+    CS_TRY(slab_check(sim));
+    return cs::launch_gradient_rows(sim->ctx, (const float *)st->c, sim->gg, (float *)st->grad,
+                                    sim->dstat(), sim->steps_done, sim->slab_grad_j0,
+                                    sim->slab_grad_rows, sim->slab_g0, sim->slab_g1);
 }
 
 extern "C" int cs_slab_import(cs_sim *sim, const cs_sim_state *st) {
@@ -800,6 +856,10 @@ extern "C" int cs_slab_finish(cs_sim *sim) {
     const int64_t l0 = sim->ctx->launches;
     CS_TRY(cs::fast_slab_sort(sim->ctx, sim->fast, sim->p, sim->gg, sim->bits, sim->dstat(),
                               sim->steps_done));
+    // the deposit of the new positions for the next step's field (own
+    // particles, into this rank's deposit window)
+    CS_TRY(cs::fast_resort(sim->ctx, sim->fast, sim->p.n, sim->p, sim->gg, sim->bits, 2,
+                           sim->dstat(), sim->steps_done));
     sim->steps_done += 1;
     sim->last_launches += sim->ctx->launches - l0;
     return CS_OK;

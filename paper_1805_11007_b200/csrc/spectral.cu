@@ -274,6 +274,15 @@ template <class G> struct SrcPlain {
     }
 };
 
+// Which part of the transform a launch does: the single-domain solve is
+// {0, N, 0, NH, 0}.  A y-slab rank (slabs.py) transforms its own grid rows
+// [row0, row0 + rows) into a half spectrum laid out [kx][ld = rows], and the
+// columns kx0 .. kx0 + ncols of the all-to-all transposed spectrum, whose
+// element (kx, ky) sits at [ky / rp][kx - kx0][ky % rp] (rp grid rows per rank).
+struct SpecPart {
+    int row0, ld, kx0, ncols, rp;
+};
+
 // groups (complex row pairs, N/16 threads each) per rows block: up to ~512
 // threads and 150 KB of shared rows, but at least ~2 blocks per SM (small
 // grids are latency-bound: more, smaller blocks)
@@ -302,14 +311,14 @@ template <int N> constexpr int cols_cpb() {
 template <class T, int N, int GPB, class Src>
 __global__ void __launch_bounds__(GPB *(N / 16), (N >= 4096 && sizeof(T) == 4) ? CS_SPEC_ROWS_MINB : 1)
 k_spec_rows_fwd(Src src, typename Cplx<T>::V *__restrict__ specT,
-                const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st) {
+                const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st, SpecPart pt) {
     using V = typename Cplx<T>::V;
     constexpr int NT = N / 16, NH = N / 2 + 1, PAD = pad_len(N);
     extern __shared__ __align__(16) unsigned char s_raw[];
     V *bufs = reinterpret_cast<V *>(s_raw);
     if (st && st->abort) return;
     const int T_ = threadIdx.x, g = T_ / NT, j = T_ % NT;
-    const int y0 = 2 * GPB * blockIdx.x;
+    const int y0 = pt.row0 + 2 * GPB * blockIdx.x;
     V *buf = bufs + g * PAD;
     const long long r0 = (long long)(y0 + 2 * g) * N, r1 = r0 + N;
 #pragma unroll 2
@@ -326,7 +335,7 @@ k_spec_rows_fwd(Src src, typename Cplx<T>::V *__restrict__ specT,
     const T half = (T)0.5;
     for (int kx = T_; kx < NH; kx += GPB * NT) {
         const int kn = (N - kx) & (N - 1);
-        V *o = specT + (long long)kx * N + y0;
+        V *o = specT + (long long)kx * pt.ld + (y0 - pt.row0);
 #pragma unroll
         for (int q = 0; q < GPB; q++) {
             const V z = bufs[q * PAD + sp(kx)], w = bufs[q * PAD + sp(kn)];
@@ -342,26 +351,31 @@ template <class T, int N, int CPB>
 __global__ void __launch_bounds__(CPB *(N / 16), (N >= 4096 && sizeof(T) == 4) ? cols_minb<N>() : 1)
 k_spec_cols(typename Cplx<T>::V *__restrict__ specT, const double *__restrict__ lx,
             const double *__restrict__ ly, double dtdc, double inv_nn,
-            const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st) {
+            const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st, SpecPart pt) {
     using V = typename Cplx<T>::V;
-    constexpr int NT = N / 16, NH = N / 2 + 1, PAD = pad_len(N);
+    constexpr int NT = N / 16, PAD = pad_len(N);
     extern __shared__ __align__(16) unsigned char s_raw[];
     if (st && st->abort) return;
     const int g = threadIdx.x / NT, j = threadIdx.x % NT;
-    const int kx = blockIdx.x * CPB + g;
-    const bool live = kx < NH;  // every thread stays for the barriers
+    const int kl = blockIdx.x * CPB + g;  // column of this launch
+    const bool live = kl < pt.ncols;     // every thread stays for the barriers
     V *col = reinterpret_cast<V *>(s_raw) + g * PAD;
-    V *gcol = specT + (long long)(live ? kx : 0) * N;
+    // element ky of the column: contiguous, or gathered from the rank blocks
+    auto at = [&](int ky) -> V * {
+        if (!pt.rp) return specT + (long long)(live ? kl : 0) * N + ky;
+        return specT + (long long)(ky / pt.rp) * pt.ncols * pt.rp +
+               (long long)(live ? kl : 0) * pt.rp + ky % pt.rp;
+    };
 #pragma unroll 4
-    for (int e = j; e < N / 2; e += NT) {  // two complex values per access
+    for (int e = j; e < N / 2; e += NT) {  // two complex values per access (rp is even)
         V a = mk((T)0, (T)0), b = a;
-        if (live) ld2(gcol + 2 * e, a, b);
+        if (live) ld2(at(2 * e), a, b);
         col[sp(2 * e)] = a;
         col[sp(2 * e + 1)] = b;
     }
     __syncthreads();
     fft<V, N>(col, j, tw);
-    const double lxv = live ? __ldg(lx + kx) : 0.0;
+    const double lxv = live ? __ldg(lx + pt.kx0 + kl) : 0.0;
 #pragma unroll 4
     for (int ky = j; ky < N; ky += NT) {
         const double s = inv_nn / (1.0 - dtdc * (__ldg(ly + ky) + lxv));
@@ -374,7 +388,7 @@ k_spec_cols(typename Cplx<T>::V *__restrict__ specT, const double *__restrict__ 
 #pragma unroll 4
         for (int e = j; e < N / 2; e += NT) {
             const V p = col[sp(2 * e)], q = col[sp(2 * e + 1)];
-            st2(gcol + 2 * e, mk(p.x, -p.y), mk(q.x, -q.y));
+            st2(at(2 * e), mk(p.x, -p.y), mk(q.x, -q.y));
         }
     }
 }
@@ -386,16 +400,16 @@ k_spec_cols(typename Cplx<T>::V *__restrict__ specT, const double *__restrict__ 
 template <class T, int N, int GPB, class G>
 __global__ void __launch_bounds__(GPB *(N / 16), (N >= 4096 && sizeof(T) == 4) ? CS_SPEC_ROWS_MINB : 1)
 k_spec_rows_inv(const typename Cplx<T>::V *__restrict__ specT, G *__restrict__ c,
-                const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st) {
+                const typename Cplx<T>::V *__restrict__ tw, const DevStatus *st, SpecPart pt) {
     using V = typename Cplx<T>::V;
     constexpr int NT = N / 16, NH = N / 2 + 1, PAD = pad_len(N);
     extern __shared__ __align__(16) unsigned char s_raw[];
     V *bufs = reinterpret_cast<V *>(s_raw);
     if (st && st->abort) return;
     const int T_ = threadIdx.x, g = T_ / NT, j = T_ % NT;
-    const int y0 = 2 * GPB * blockIdx.x;
+    const int y0 = pt.row0 + 2 * GPB * blockIdx.x;
     for (int kx = T_; kx < NH; kx += GPB * NT) {
-        const V *in = specT + (long long)kx * N + y0;
+        const V *in = specT + (long long)kx * pt.ld + (y0 - pt.row0);
 #pragma unroll
         for (int q = 0; q < GPB; q++) {
             V a, b;
@@ -427,8 +441,11 @@ int spectral_supported(int n) {
     return n >= 16 && n <= 8192 && (n & (n - 1)) == 0;
 }
 
+// which passes: 1 rows forward, 2 columns, 4 rows inverse (7: the whole solve)
 template <class T, int N, class Src, class G>
-static int spec_run(cs_ctx *ctx, cs_field_ops *ops, const Src &src, G *out, const DevStatus *st) {
+static int spec_run(cs_ctx *ctx, cs_field_ops *ops, const Src &src, G *out, const DevStatus *st,
+                    int passes = 7, SpecPart pt = SpecPart{0, N, 0, N / 2 + 1, 0},
+                    int rows = N, void *spec = nullptr) {
     using V = typename Cplx<T>::V;
     constexpr int GPB = rows_gpb<T, N>(), CPB = cols_cpb<N>(), NH = N / 2 + 1;
     constexpr int rows_smem = GPB * pad_len(N) * (int)sizeof(V);
@@ -443,37 +460,57 @@ static int spec_run(cs_ctx *ctx, cs_field_ops *ops, const Src &src, G *out, cons
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, cols_smem));
         attr = true;
     }
-    V *specT = static_cast<V *>(ops->specT);
+    V *specT = static_cast<V *>(spec ? spec : ops->specT);
     const V *tw = static_cast<const V *>(ops->tw);
-    k_spec_rows_fwd<T, N, GPB, Src><<<N / (2 * GPB), GPB * (N / 16), rows_smem, ctx->stream>>>(
-        src, specT, tw, st);
-    CS_LAUNCH_CHECK();
-    const double inv_nn = 1.0 / ((double)N * (double)N);
-    k_spec_cols<T, N, CPB><<<(NH + CPB - 1) / CPB, CPB * (N / 16), cols_smem, ctx->stream>>>(
-        specT, ops->lx, ops->ly, ops->dt * ops->d_c, inv_nn, tw, st);
-    CS_LAUNCH_CHECK();
-    k_spec_rows_inv<T, N, GPB, G><<<N / (2 * GPB), GPB * (N / 16), rows_smem, ctx->stream>>>(
-        specT, out, tw, st);
-    CS_LAUNCH_CHECK();
-    ctx->launches += 3;
+    if ((passes & 5) && rows % (2 * GPB)) {
+        set_error("spectral solve: %d grid rows per rank is not a multiple of %d", rows, 2 * GPB);
+        return CS_ERR_PARAM;
+    }
+    (void)NH;
+    if (passes & 1) {
+        k_spec_rows_fwd<T, N, GPB, Src><<<rows / (2 * GPB), GPB * (N / 16), rows_smem,
+                                          ctx->stream>>>(src, specT, tw, st, pt);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    if (passes & 2) {
+        const double inv_nn = 1.0 / ((double)N * (double)N);
+        k_spec_cols<T, N, CPB><<<(pt.ncols + CPB - 1) / CPB, CPB * (N / 16), cols_smem,
+                                 ctx->stream>>>(specT, ops->lx, ops->ly, ops->dt * ops->d_c,
+                                                inv_nn, tw, st, pt);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    if (passes & 4) {
+        k_spec_rows_inv<T, N, GPB, G><<<rows / (2 * GPB), GPB * (N / 16), rows_smem,
+                                        ctx->stream>>>(specT, out, tw, st, pt);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
     return CS_OK;
 }
 
 template <class T, class Src, class G>
 static int spec_dispatch(cs_ctx *ctx, cs_field_ops *ops, const Src &src, G *out,
-                         const DevStatus *st) {
+                         const DevStatus *st, int passes = 7, const SpecPart *pt = nullptr,
+                         int rows = 0, void *spec = nullptr) {
+#define CS_SPEC_CASE(NN)                                                                      \
+    case NN:                                                                                  \
+        return pt ? spec_run<T, NN>(ctx, ops, src, out, st, passes, *pt, rows, spec)          \
+                  : spec_run<T, NN>(ctx, ops, src, out, st);
     switch (ops->gg.n) {
-        case 16: return spec_run<T, 16>(ctx, ops, src, out, st);
-        case 32: return spec_run<T, 32>(ctx, ops, src, out, st);
-        case 64: return spec_run<T, 64>(ctx, ops, src, out, st);
-        case 128: return spec_run<T, 128>(ctx, ops, src, out, st);
-        case 256: return spec_run<T, 256>(ctx, ops, src, out, st);
-        case 512: return spec_run<T, 512>(ctx, ops, src, out, st);
-        case 1024: return spec_run<T, 1024>(ctx, ops, src, out, st);
-        case 2048: return spec_run<T, 2048>(ctx, ops, src, out, st);
-        case 4096: return spec_run<T, 4096>(ctx, ops, src, out, st);
-        case 8192: return spec_run<T, 8192>(ctx, ops, src, out, st);
+        CS_SPEC_CASE(16)
+        CS_SPEC_CASE(32)
+        CS_SPEC_CASE(64)
+        CS_SPEC_CASE(128)
+        CS_SPEC_CASE(256)
+        CS_SPEC_CASE(512)
+        CS_SPEC_CASE(1024)
+        CS_SPEC_CASE(2048)
+        CS_SPEC_CASE(4096)
+        CS_SPEC_CASE(8192)
     }
+#undef CS_SPEC_CASE
     set_error("spectral solve: n = %d is not a power of two in [16, 8192]", ops->gg.n);
     return CS_ERR_PARAM;
 }
@@ -532,6 +569,32 @@ int spectral_step_g(cs_field_ops *ops, void *c, const void *ra, const void *rb, 
     }
     SrcG<float> src{(const float *)c, (const float *)ra, (const float *)rb, k};
     return spec_dispatch<float>(ops->ctx, ops, src, (float *)c, st);
+}
+
+// y-slab pieces (binary32, the sorted engine's slab mode): rows forward of
+// the own grid rows [row0, row0 + rows) into spec [NH][rows]; the columns
+// kx0 .. kx0 + ncols of the transposed blocks [rank][ncols][rp]; rows inverse.
+int spectral_slab_rows(cs_field_ops *ops, float *c, const int *q, double gamma, double ka,
+                       double kb, double scale, int row0, int rows, void *spec, int inverse,
+                       const DevStatus *st) {
+    CS_TRY(spec_prepare(ops));
+    const long long m = (long long)ops->gg.n * ops->gg.n;
+    const int NH = ops->gg.n / 2 + 1;
+    SpecPart pt{row0, rows, 0, NH, 0};
+    SrcQ src{c, q, m, spec_rhs(ops->dt, gamma, ka, kb, scale)};
+    return spec_dispatch<float>(ops->ctx, ops, src, c, st, inverse ? 4 : 1, &pt, rows, spec);
+}
+
+int spectral_slab_cols(cs_field_ops *ops, void *blocks, int kx0, int ncols, int rp,
+                       const DevStatus *st) {
+    CS_TRY(spec_prepare(ops));
+    if (rp % 2) {
+        set_error("spectral slab columns: rows per rank must be even");
+        return CS_ERR_PARAM;
+    }
+    SpecPart pt{0, 0, kx0, ncols, rp};
+    SrcPlain<float> none{nullptr};
+    return spec_dispatch<float>(ops->ctx, ops, none, (float *)nullptr, st, 2, &pt, 0, blocks);
 }
 
 // out = solve(rhs), both in the grid dtype

@@ -616,7 +616,8 @@ class SlabEngine:
     field off); state: the caller's global id-ordered arrays (pos, anchor,
     species), read at import and written back (own particles) by export."""
 
-    def __init__(self, params, state: dict, bounds, rank: int, world: int):
+    def __init__(self, params, state: dict, bounds, rank: int, world: int,
+                 field_plan: "FieldPlan | None" = None):
         from . import _native as N
         from .engine import DeviceSim
         self.N = N
@@ -628,8 +629,17 @@ class SlabEngine:
         lib = self.sim._bind()
         b = (N.C_i32 * len(self.bounds))(*[int(v) for v in self.bounds])
         N.check(lib.cs_slab_config(self.sim._h, b, world, rank), "cs_slab_config")
+        self.field = None
+        if field_plan is not None:
+            r = rank
+            j0, k = field_plan.dep[r]
+            gj0, gk = field_plan.grad[r]
+            g0 = int(field_plan.g0[r])
+            N.check(lib.cs_slab_field_config(self.sim._h, g0, g0 + field_plan.rp, j0, k, gj0,
+                                             gk), "cs_slab_field_config")
         N.check(lib.cs_slab_import(self.sim._h, ctypes_byref(self.sim._st)), "cs_slab_import")
-        self._empty = None
+        if field_plan is not None:
+            self.field = SlabField(self, field_plan)
 
     # ---- phases ------------------------------------------------------------
     def local(self, xi):
@@ -669,6 +679,10 @@ class SlabEngine:
 
     # ---- one step over NCCL (one rank per process) -------------------------
     def step(self, xi, transport: NcclTransport):
+        if self.field is not None:
+            if not hasattr(self, "_nf"):
+                self._nf = NcclField(self.field, transport.group)
+            self._nf.step()
         self.local(xi)
         recs, dest = self.outbox()
         self.claim(transport.exchange(recs, dest))
@@ -695,6 +709,8 @@ class SlabEngine:
 def step_in_process(engines, hub: LoopbackHub, xi):
     """One step of every rank of one process (tests): the phases in
     lockstep, the exchange through the hub."""
+    if engines[0].field is not None:
+        field_in_process([e.field for e in engines], move_in_process)
     for e in engines:
         e.local(xi)
     got = hub.exchange_all([e.outbox() for e in engines])
@@ -717,3 +733,197 @@ def _device_view(ptr: int, shape, dtype, device):
         __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
                                     "data": (int(ptr), False), "version": 3}
     return torch.as_tensor(_Alias(), device=device)
+
+
+# ---------------------------------------------------------------------------
+# the field of the device slab engine
+# ---------------------------------------------------------------------------
+@dataclass
+class FieldPlan:
+    """Static row bookkeeping of the distributed field for a layout: every
+    rank owns an even share of the grid rows (the spectral passes' unit of
+    work), deposits into a window covering its own rows and its particles'
+    CIC rows, and samples the gradient of its particles' rows."""
+    n: int                      # grid nodes per axis
+    world: int
+    rp: int                     # grid rows per rank
+    g0: np.ndarray              # (world,) own grid rows [g0, g0 + rp)
+    dep: list                   # per rank: (j0, rows) deposit window (j0 may be < 0: mod n)
+    grad: list                  # per rank: (j0, rows) gradient window
+    kx: np.ndarray              # (world + 1,) kx split of the n/2 + 1 half-spectrum columns
+
+    @classmethod
+    def make(cls, bounds, n1: int, n: int, world: int, blocking: int = 16) -> "FieldPlan":
+        if n % world or (n // world) % 2 or (n // world) % min(blocking, n // world):
+            raise ValueError(f"a {n}^2 grid cannot be split into {world} row slabs")
+        rp = n // world
+        g0 = np.arange(world) * rp
+        eff_over_d = n / n1        # cell side over grid spacing (unit box, periodic grid)
+        dep, grad = [], []
+        for r in range(world):
+            b0, b1 = int(bounds[r]), int(bounds[r + 1])
+            jlo = int(math.floor(b0 * eff_over_d)) - 1
+            jhi = int(math.floor(b1 * eff_over_d)) + 2
+            if jhi - jlo > n:
+                jlo, jhi = 0, n
+            grad.append((jlo, jhi - jlo))
+            d0, d1 = min(jlo, int(g0[r])), max(jhi, int(g0[r]) + rp)
+            if d1 - d0 > n:
+                d0, d1 = 0, n
+            dep.append((d0, d1 - d0))
+        nh = n // 2 + 1
+        kx = np.round(np.linspace(0, nh, world + 1)).astype(np.int64)
+        return cls(n, world, rp, g0, dep, grad, kx)
+
+    def owner(self, j):
+        return (np.asarray(j) % self.n) // self.rp
+
+    def dep_rows(self, s: int, d: int) -> np.ndarray:
+        """Deposit-window rows of rank s that rank d owns (s != d)."""
+        j0, k = self.dep[s]
+        rows = np.arange(j0, j0 + k) % self.n
+        return rows[self.owner(rows) == d]
+
+    def c_rows(self, d: int, s: int) -> np.ndarray:
+        """c rows rank d's gradient window needs (one wider) that rank s owns."""
+        j0, k = self.grad[d]
+        rows = np.unique(np.arange(j0 - 1, j0 + k + 1) % self.n)
+        return rows[self.owner(rows) == s]
+
+
+class SlabField:
+    """The field stage of one slab rank (the sorted engine's arrays) with
+    the exchanges of its grid rows: deposit window rows into their owners,
+    the spectrum transposes of the implicit solve, c rows for the gradient
+    window.  ``move(kind, payload_per_dest) -> payload_per_source`` is the
+    transport (all-to-all over NCCL, or copies between in-process ranks)."""
+
+    def __init__(self, eng: "SlabEngine", plan: FieldPlan):
+        self.eng, self.plan = eng, plan
+        r = eng.rank
+        lib = eng.sim._bind()
+        dev = eng.sim.state["pos"].device
+        n = plan.n
+        self.rho = _device_view(lib.cs_slab_rho(eng.sim._h), (2, n, n), torch.int32, dev)
+        self.c = eng.sim.state["c"].view(n, n)
+        nh = n // 2 + 1
+        kl = int(plan.kx[r + 1] - plan.kx[r])
+        self.spec = torch.empty((nh, plan.rp, 2), dtype=torch.float32, device=dev)
+        self.blocks = torch.empty((plan.world, kl, plan.rp, 2), dtype=torch.float32, device=dev)
+        W = plan.world
+        self.dep_send = [torch.as_tensor(plan.dep_rows(r, d), device=dev) for d in range(W)]
+        self.dep_recv = [torch.as_tensor(plan.dep_rows(s, r), device=dev) for s in range(W)]
+        self.c_send = [torch.as_tensor(plan.c_rows(d, r), device=dev) for d in range(W)]
+        self.c_recv = [torch.as_tensor(plan.c_rows(r, s), device=dev) for s in range(W)]
+        for q in (r,):
+            self.dep_send[q] = self.dep_send[q][:0]
+            self.dep_recv[q] = self.dep_recv[q][:0]
+            self.c_send[q] = self.c_send[q][:0]
+            self.c_recv[q] = self.c_recv[q][:0]
+
+    # payloads for the transport
+    def deposit_out(self):
+        return [self.rho[:, rows, :].reshape(-1) for rows in self.dep_send]
+
+    def deposit_in(self, got):
+        for rows, g in zip(self.dep_recv, got):
+            if rows.numel():
+                self.rho[:, rows, :] += g.view(2, rows.numel(), self.plan.n)
+
+    def spec_rows(self, inverse: bool):
+        e = self.eng
+        e.N.check(e.sim._bind().cs_slab_field_rows(e.sim._h, ctypes_byref(e.sim._st),
+                                                   e.N.ptr(self.spec), int(inverse)),
+                  "cs_slab_field_rows")
+
+    def spec_out(self):
+        p = self.plan
+        return [self.spec[int(p.kx[q]):int(p.kx[q + 1])].reshape(-1) for q in range(p.world)]
+
+    def spec_in_blocks(self, got):
+        for q, g in enumerate(got):
+            self.blocks[q].view(-1).copy_(g)
+
+    def cols(self):
+        e, p, r = self.eng, self.plan, self.eng.rank
+        e.N.check(e.sim._bind().cs_slab_field_cols(
+            e.sim._h, e.N.ptr(self.blocks), int(p.kx[r]), int(p.kx[r + 1] - p.kx[r]), p.rp),
+            "cs_slab_field_cols")
+
+    def blocks_out(self):
+        return [self.blocks[q].reshape(-1) for q in range(self.plan.world)]
+
+    def blocks_in_spec(self, got):
+        p = self.plan
+        for q, g in enumerate(got):
+            self.spec[int(p.kx[q]):int(p.kx[q + 1])].view(-1).copy_(g)
+
+    def c_out(self):
+        return [self.c[rows, :].reshape(-1) for rows in self.c_send]
+
+    def c_in(self, got):
+        for rows, g in zip(self.c_recv, got):
+            if rows.numel():
+                self.c[rows, :] = g.view(rows.numel(), self.plan.n)
+
+    def gradient(self):
+        e = self.eng
+        e.N.check(e.sim._bind().cs_slab_field_grad(e.sim._h, ctypes_byref(e.sim._st)),
+                  "cs_slab_field_grad")
+
+
+def field_in_process(fields, move):
+    """The distributed field step of every in-process rank (lockstep)."""
+    for f, got in zip(fields, move([f.deposit_out() for f in fields])):
+        f.deposit_in(got)
+    for f in fields:
+        f.spec_rows(inverse=False)
+    for f, got in zip(fields, move([f.spec_out() for f in fields])):
+        f.spec_in_blocks(got)
+    for f in fields:
+        f.cols()
+    for f, got in zip(fields, move([f.blocks_out() for f in fields])):
+        f.blocks_in_spec(got)
+    for f in fields:
+        f.spec_rows(inverse=True)
+    for f, got in zip(fields, move([f.c_out() for f in fields])):
+        f.c_in(got)
+    for f in fields:
+        f.gradient()
+
+
+def move_in_process(outs):
+    """outs[s][d] = the payload rank s sends rank d -> got[d][s]."""
+    W = len(outs)
+    return [[outs[s][d] for s in range(W)] for d in range(W)]
+
+
+class NcclField:
+    """The transport of one rank's field exchanges over NCCL: every payload
+    size is a static function of the layout (row lists, kx split), so the
+    all-to-all runs with host-known splits and no synchronisation."""
+
+    def __init__(self, field: SlabField, group=None):
+        self.f, self.group = field, group
+
+    def _a2a(self, out, recv_sizes):
+        dev = out[0].device
+        send = torch.cat([o.reshape(-1) for o in out]) if out else None
+        recv = torch.empty(sum(recv_sizes), dtype=out[0].dtype, device=dev)
+        dist.all_to_all_single(recv, send, recv_sizes, [o.numel() for o in out],
+                               group=self.group)
+        return list(recv.split(recv_sizes))
+
+    def step(self):
+        f, p = self.f, self.f.plan
+        n, W, r = p.n, p.world, self.f.eng.rank
+        kl = int(p.kx[r + 1] - p.kx[r])
+        f.deposit_in(self._a2a(f.deposit_out(), [2 * n * rows.numel() for rows in f.dep_recv]))
+        f.spec_rows(inverse=False)
+        f.spec_in_blocks(self._a2a(f.spec_out(), [kl * p.rp * 2] * W))
+        f.cols()
+        f.blocks_in_spec(self._a2a(f.blocks_out(),
+                                   [int(p.kx[q + 1] - p.kx[q]) * p.rp * 2 for q in range(W)]))
+        f.spec_rows(inverse=True)
+        f.c_in(self._a2a(f.c_out(), [n * rows.numel() for rows in f.c_recv]))
+        f.gradient()

@@ -94,3 +94,81 @@ def test_slab_engine_equals_single_domain_bitwise(world, clustered):
     assert torch.equal(st["anchor"], st1["anchor"])
     for e in engines:
         e.close()
+
+
+def _field_params(n, radii, n_c):
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        mp = cs.MotionParams(d_alpha=1.0, d_beta=0.5, epsilon=radii[0], cutoff=2 * radii[0],
+                             dt=1e-5, radius_alpha=radii[0], radius_beta=radii[1])
+    dom = cs.Domain.square(1.0, periodic=True)
+    grid = cs.Grid.square(n_c, 1.0, "periodic")
+    params = cs.sim_params_struct(
+        n=n, prec=1, domain=dom, motion=mp, dt=1e-5, field_active=True, refresh_active=True,
+        grid=grid, fparams=cs.FieldParams(d_c=1.0, k_alpha=0.1, k_beta=0.03, gamma=0.1),
+        kernel=cs.Kernel(kind="cic"), secretes=(True, False), consumes=(False, True),
+        chi=(1.0, -0.5), chi_pinned=(False, False), store_samples=False, store_next=False,
+        engine="sorted")
+    return params, mp, dom
+
+
+def _field_state(pos, sp, c0, n_c, shared=None):
+    f32 = torch.float32
+    st = _state(pos, sp) if shared is None else dict(shared)
+    st.update(c=torch.as_tensor(c0, device="cuda").to(f32).contiguous(),
+              grad=torch.zeros((n_c * n_c, 2), dtype=f32, device="cuda"),
+              rho_a=torch.zeros(n_c * n_c, dtype=f32, device="cuda"),
+              rho_b=torch.zeros(n_c * n_c, dtype=f32, device="cuda"))
+    return st
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_slab_engine_with_field_equals_single_domain_bitwise(world, clustered):
+    """The distributed field (deposit windows added into their owners' rows
+    in exact int32, the spectral solve split into own-row passes and
+    own-column passes around two all-to-all transposes, gradient windows
+    from fetched c rows) on top of the particle slabs: positions and every
+    rank's own field rows equal the single-domain engine's bit for bit."""
+    rng = np.random.default_rng(20 + world)
+    n, n_c, steps = 100_000, 256, 5
+    if clustered:
+        centres = -0.5 + rng.random((16, 2))
+        pos = centres[rng.integers(0, 16, n)] + 0.03 * rng.standard_normal((n, 2))
+        pos = np.mod(pos + 0.5, 1.0) - 0.5
+    else:
+        pos = -0.5 + rng.random((n, 2))
+    pos = pos.astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    radii = (7e-4, 1.4e-3)
+    c0 = (0.5 + 0.1 * rng.standard_normal(n_c * n_c)).astype(np.float32)
+    params, mp, dom = _field_params(n, radii, n_c)
+    xi = torch.as_tensor(rng.standard_normal((steps, n, 2)).astype(np.float32), device="cuda")
+    st1 = _field_state(pos, sp, c0, n_c)
+    one = cs.DeviceSim(params, st1)
+    one.step(xi, steps)
+    one.export_state()
+    assert one.status().code == 0
+    shared = _state(pos, sp)
+    bounds = _bounds(pos, mp, dom, world)
+    e, c, cell = mp.pair_table()
+    n1 = slabs.CellGeometry.make(dom.lo[1], dom.hi[1], cell).n
+    plan = slabs.FieldPlan.make(bounds, n1, n_c, world)
+    sts = [_field_state(pos, sp, c0, n_c, shared) for _ in range(world)]
+    engines = [slabs.SlabEngine(params, sts[r], bounds, r, world, field_plan=plan)
+               for r in range(world)]
+    hub = slabs.LoopbackHub(world)
+    for k in range(steps):
+        slabs.step_in_process(engines, hub, xi[k])
+    for eng in engines:
+        assert eng.status().code == 0, eng.status().code
+        eng.export()
+    torch.cuda.synchronize()
+    assert torch.equal(shared["pos"], st1["pos"])
+    c1 = st1["c"].view(n_c, n_c)
+    for r in range(world):
+        rows = slice(int(plan.g0[r]), int(plan.g0[r]) + plan.rp)
+        assert torch.equal(sts[r]["c"].view(n_c, n_c)[rows], c1[rows]), r
+    for eng in engines:
+        eng.close()

@@ -179,7 +179,10 @@ def initial_positions(cfg: dict, rng) -> np.ndarray:
     return (-0.5 + rng.random((n, 2))).astype(np.float64)
 
 
-def make_state(cfg: dict, rank: int, xi_by_slot: bool = False):
+def make_state(cfg: dict, rank: int, xi_by_slot: bool = False, engine: str = "auto",
+               build_sim: bool = True):
+    """(DeviceSim, state tensors, initial positions, species) of a config;
+    build_sim=False returns the cs_sim_params in place of the simulation."""
     import torch
     import paper_1805_11007_b200 as cs
     n, n_c = cfg["n"], max(cfg["n_c"], 3)
@@ -227,10 +230,12 @@ def make_state(cfg: dict, rank: int, xi_by_slot: bool = False):
         grid=grid, fparams=fp, kernel=cs.Kernel(kind="cic"),
         secretes=cfg.get("secretes", (False, False)), consumes=cfg.get("consumes", (False, False)),
         chi=cfg["chi"], chi_pinned=cfg["chi_pinned"], store_samples=False, store_next=False,
-        xi_by_slot=xi_by_slot)
+        xi_by_slot=xi_by_slot, engine=engine)
     if cfg["field"] or cfg.get("c0") == "linear_x":
         f = cs.Field(c=st["c"], grad=st["grad"], rho_alpha=st["rho_a"], rho_beta=st["rho_b"])
         cs.gradient(f, cs.build_operators(grid, fp, DT))
+    if not build_sim:
+        return params, st, pos, sp
     sim = cs.DeviceSim(params, st)
     return sim, st, pos, sp
 
@@ -437,6 +442,11 @@ def main():
         if world > 1:
             dist.barrier()
 
+    if world > 1 and cfg["prec"] == "fp32":
+        run_slabs(args, cfg, rank, world, barrier)
+        dist.destroy_process_group()
+        return
+
     sim, st, pos_host, sp_host = make_state(cfg, rank)
     n = cfg["n"]
     K, W = args.steps, max(args.warmup, 0)
@@ -589,6 +599,81 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def slab_setup(cfg: dict, world: int):
+    """(engine params, state tensors, cell-row bounds, field plan) of one
+    system of the config split into world y-slabs: the seeded initial state
+    (rank 0's seed on every rank), count-balanced on the initial cell-row
+    histogram."""
+    from paper_1805_11007_b200 import slabs
+    params, st, pos, sp = make_state(cfg, 0, engine="sorted", build_sim=False)
+    radii = cfg["radii"]
+    cell = 2.0 * (radii[1] if radii else cfg["eps"])
+    geom = slabs.CellGeometry.make(-0.5, 0.5, cell)
+    counts = np.bincount(geom.row_of(pos[:, 1].astype(np.float64)), minlength=geom.n)
+    bounds = slabs.SlabLayout.balanced(counts, world).bounds
+    plan = slabs.FieldPlan.make(bounds, geom.n, cfg["n_c"], world) if cfg["field"] else None
+    return params, st, bounds, plan
+
+
+def run_slabs(args, cfg, rank, world, barrier):
+    """N > 1: ONE system of the config decomposed into y-slabs over the N
+    ranks (slabs.py): strong scaling, value = N_particles * K /
+    (device time of K steps, max over ranks).  Every rank builds the same
+    seeded initial state and increments (rank 0's seed), the layout is
+    count-balanced on the initial cell-row histogram."""
+    import torch
+    import torch.distributed as dist
+    from paper_1805_11007_b200 import slabs
+    n, K, W = cfg["n"], args.steps, max(args.warmup, 0)
+    params, st, bounds, plan = slab_setup(cfg, world)
+    eng = slabs.SlabEngine(params, st, bounds, rank, world, field_plan=plan)
+    tr = slabs.NcclTransport(world)
+    blocks = K + W
+    gen = torch.Generator(device="cuda").manual_seed(SEED)
+    xi = torch.randn((blocks, n, 2), generator=gen, device="cuda", dtype=torch.float32)
+    for w in range(W):
+        eng.step(xi[w], tr)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    with clocks:
+        barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for k in range(K):
+            eng.step(xi[W + k], tr)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = a.elapsed_time(b)
+    code = eng.status().code
+    t = torch.tensor([ms, float(code != 0)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, failed = float(t[0].item()), bool(t[1].item())
+    if failed:
+        raise RuntimeError("slab run failed on some rank")
+    lo, hi = eng.owned_range()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n * K / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 storage)",
+            "data": "synthetic",
+            "config": dict(config_dict(args.config, cfg, world),
+                           parallelism=f"yslab{world}",
+                           decomposition="one system, count-balanced y-slabs of cell rows, "
+                                         "even grid-row split, NCCL all-to-all exchanges"),
+            "engine": "sorted (slab mode)", "clocks": clocks.summary(),
+            "rank0_owned": hi - lo,
+            "e2e": None,
+            "note": "N > 1: one slab-decomposed system (strong scaling); the end-to-end "
+                    "host-increment variant is measured at N = 1",
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
 
 
 def run_e2e(sim, n, dt_, K, W, barrier, world):

@@ -1,36 +1,31 @@
 """y-slab domain decomposition of one system over several GPUs.
 
-One process per GPU (``torch.distributed``, NCCL over NVLink; the same code
-runs on gloo/CPU for the tests).  Rank r owns the whole cell rows
-[b_r, b_{r+1}) of the reference's cell grid (motion.py:171-174: n = int(L /
-cutoff), eff = L / n) and the grid rows whose nodes lie in that y range.
-Boundaries are count-balanced (prefix sum of the per-row particle counts),
-because equal-width slabs cap the efficiency at 53-83 % for clustered
-inputs.
+One process per GPU (``torch.distributed``, NCCL over NVLink).  Rank r owns
+the whole cell rows [b_r, b_{r+1}) of the reference's cell grid
+(motion.py:171-174: n = int(L / cutoff), eff = L / n), count-balanced at the
+start (prefix sum of the per-row particle counts: equal-width slabs cap the
+efficiency at 53-83 % for clustered inputs), and an even share of
+the field's grid rows.  Each rank runs the SORTED engine in slab mode
+(csrc/fast.cu, cs_slab_*) on its particles plus copies of its neighbours'
+boundary cell rows (ghosts).  Per step, in the reference stage order
+(engine.py:369-387):
 
-Per step (Realisation._step_inner order, engine.py:369-387):
+  field      deposit window rows (own particles, int32 fixed point) added
+             into their owners' rows; the implicit spectral solve as own-row
+             passes and own-column passes around two all-to-all transposes
+             of the half spectrum; c rows for the gradient window fetched
+             from their owners; gradient of the window rows
+  particles  pair forces and the update over the owned slots (the update
+             kernel routes records whose new row another rank owns --
+             migrants -- and copies of records landing in a boundary row --
+             ghosts -- into an outbox); one all-to-all of the outbox; the
+             received records claimed; bucket sort; the next deposit
 
-  field (if active)
-    deposit owned particles into local grid rows + one ghost row per side,
-    add the ghost rows into their owners            (grid ghost reduce)
-    rhs on local rows; distributed spectral solve   (two all-to-all transposes)
-    gradient with one ghost row of c per side       (grid ghost fetch)
-    one ghost row of grad per side for the bilinear drift
-  particles
-    halo: every rank sends its first and last owned cell row to its
-    neighbours (the cell side is >= the cutoff, so one row covers the ring)
-    forces on owned + ghost particles (global cell geometry, rows in id
-    order -> the reference summation order), EM, boundaries on owned
-    migration: all-to-all by the owner of the new cell row (kicks can cross
-    several slabs: 0.46 vs a 0.125-high slab at 8 GPUs)
-  status: all-reduce (min error key)
-
-Every collective is ``all_to_all_single`` or ``all_reduce``.  The local
-compute comes from a backend object (``DeviceSlabBackend`` below runs the
-library's C-ABI ops on the rank's GPU; the tests plug in the oracle).  With
-the field off the decomposition is bit-identical to the single-domain run:
-ghosts provide every ring neighbour, local rows stay in ascending id, and
-the cell geometry is the global one.
+Every pass is the single-domain engine's on the same records, rows and
+columns, so the decomposed run is the single-domain run bit for bit
+(tests/test_gpu_slab_engine.py, ranks emulated in one process).  The grid
+exchanges have sizes fixed by the layout; the particle all-to-all sends its
+per-peer counts first (the step's one host synchronisation).
 """
 
 from __future__ import annotations
@@ -106,451 +101,6 @@ class CellGeometry:
             return f.clamp(0, self.n - 1).long()
         f = np.floor((np.asarray(y, dtype=float) - self.lo) / self.eff)
         return np.clip(f, 0, self.n - 1).astype(np.int64)
-
-
-def grid_row_bounds(layout: SlabLayout, geom: CellGeometry, n_c: int, lo: float,
-                    spacing: float) -> np.ndarray:
-    """Grid-row boundaries: node row j belongs to the owner of the cell row
-    of its y coordinate (nodes are co-partitioned with the particles)."""
-    ys = lo + spacing * np.arange(n_c)
-    owners = layout.owner_of_row(geom.row_of(ys))
-    gb = [0]
-    for r in range(1, layout.world):
-        gb.append(int(np.searchsorted(owners, r, side="left")))
-    gb.append(n_c)
-    return np.asarray(gb, dtype=np.int64)
-
-
-# ----------------------------------------------------------------------------
-# collectives
-# ----------------------------------------------------------------------------
-def exchange(tensors, dest, world: int, group=None):
-    """Route rows of every tensor in ``tensors`` (same leading length) to the
-    rank in ``dest``; returns the received tensors, rows ordered by source
-    rank then by original order.  Two all_to_all_single calls per tensor
-    (counts, payload)."""
-    dev = dest.device
-    order = torch.argsort(dest, stable=True)
-    send_counts = torch.bincount(dest, minlength=world).to(torch.int64)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    sc = send_counts.cpu().tolist()
-    rc = recv_counts.cpu().tolist()
-    out = []
-    for t in tensors:
-        src = t[order]
-        tail = tuple(src.shape[1:])
-        width = int(np.prod(tail)) if tail else 1
-        flat = src.reshape(-1, width) if width > 1 else src.reshape(-1, 1)
-        if flat.dtype in (torch.uint8, torch.bool, torch.int16):
-            flat = flat.to(torch.int32)
-            back = t.dtype
-        else:
-            back = None
-        recv = torch.empty((sum(rc), width), dtype=flat.dtype, device=dev)
-        dist.all_to_all_single(recv.view(-1), flat.contiguous().view(-1),
-                               [c * width for c in rc], [c * width for c in sc], group=group)
-        if back is not None:
-            recv = recv.to(back)
-        out.append(recv.reshape((sum(rc),) + tail))
-    return out
-
-
-def exchange_flat(blocks, world: int, group=None):
-    """All-to-all of arbitrary per-destination blocks (same dtype):
-    ``blocks[q]`` goes to rank q; returns the flat 1-D chunks received from
-    every rank (the caller knows their shapes)."""
-    dev = blocks[0].device
-    sc = [int(b.numel()) for b in blocks]
-    counts = torch.tensor(sc, dtype=torch.int64, device=dev)
-    rcounts = torch.empty_like(counts)
-    dist.all_to_all_single(rcounts, counts, group=group)
-    rc = rcounts.cpu().tolist()
-    send = torch.cat([b.reshape(-1) for b in blocks]).contiguous()
-    recv = torch.empty(sum(rc), dtype=send.dtype, device=dev)
-    dist.all_to_all_single(recv, send, rc, sc, group=group)
-    return list(recv.split(rc))
-
-
-def exchange_rows(blocks, world: int, group=None):
-    """All-to-all of per-destination row blocks with a common width m:
-    ``blocks[q]`` (rows, m) goes to rank q; returns the blocks received."""
-    m = blocks[0].shape[1]
-    return [f.reshape(-1, m) for f in exchange_flat(blocks, world, group)]
-
-
-# ----------------------------------------------------------------------------
-# distributed spectral solve of (I - dt d_c L) c = rhs on a periodic grid
-# ----------------------------------------------------------------------------
-class DistributedSpectralSolver:
-    """Row-slab 2-D real FFT diagonalisation (field.py:162-201's system, the
-    periodic closure): rfft along x on local rows, transpose (all-to-all) to
-    kx column blocks, FFT along y, multiply by the inverse eigenvalues, and
-    back.  Same linear system as the single-GPU cuFFT path."""
-
-    def __init__(self, n: int, spacing, dt: float, d_c: float, grid_bounds, rank: int,
-                 world: int, device, group=None):
-        self.n, self.rank, self.world, self.group = n, rank, world, group
-        self.gb = np.asarray(grid_bounds)
-        nh = n // 2 + 1
-        self.cb = np.round(np.linspace(0, nh, world + 1)).astype(np.int64)
-        hx, hy = float(spacing[0]), float(spacing[1])
-        k = np.arange(n)
-        lam_x = (2.0 * np.cos(2.0 * np.pi * k / n) - 2.0) / hx ** 2
-        lam_y = (2.0 * np.cos(2.0 * np.pi * k / n) - 2.0) / hy ** 2
-        c0, c1 = self.cb[rank], self.cb[rank + 1]
-        eig = 1.0 / (1.0 - dt * d_c * (lam_y[:, None] + lam_x[None, c0:c1]))
-        self.eig = torch.as_tensor(eig, device=device)
-
-    def solve(self, rhs_rows: torch.Tensor) -> torch.Tensor:
-        """rhs_rows: (g1 - g0, n) local rows -> solution rows (same shape)."""
-        n, W = self.n, self.world
-        spec = torch.fft.rfft(rhs_rows.double(), dim=1)            # (rows, nh)
-        blocks = [torch.view_as_real(spec[:, self.cb[q]:self.cb[q + 1]]).contiguous()
-                  for q in range(W)]
-        got = exchange_flat(blocks, W, self.group)                  # rows from every rank
-        ncols = int(self.cb[self.rank + 1] - self.cb[self.rank])
-        col = torch.view_as_complex(torch.cat([g.reshape(-1, ncols, 2) for g in got], 0)
-                                    .contiguous())
-        col = torch.fft.ifft(torch.fft.fft(col, dim=0) * self.eig, dim=0)
-        # back: my kx columns, split by the destination's rows
-        rows_of = [int(self.gb[q + 1] - self.gb[q]) for q in range(W)]
-        back = [torch.view_as_real(b).contiguous() for b in col.split(rows_of, 0)]
-        got = exchange_flat(back, W, self.group)
-        nh = n // 2 + 1
-        mine = rhs_rows.shape[0]
-        parts = [torch.view_as_complex(g.reshape(mine, -1, 2).contiguous()) for g in got]
-        full = torch.cat(parts, 1)
-        assert full.shape[1] == nh
-        return torch.fft.irfft(full, n=n, dim=1)
-
-
-def ghost_rows(local: torch.Tensor, rank: int, world: int, periodic: bool, group=None):
-    """(row above the slab's first row, row below its last row) fetched from
-    the neighbours (None at a non-periodic wall)."""
-    up = (rank - 1) % world
-    dn = (rank + 1) % world
-    m = local.shape[1]
-    empty = local.new_zeros((0, m))
-    blocks = [empty] * world
-    # my first row goes to the rank above me (it is their "below" ghost),
-    # my last row to the rank below
-    if world == 1:
-        first, last = local[-1:], local[:1]
-        return (first if periodic else None), (last if periodic else None)
-    blocks = [empty for _ in range(world)]
-    if periodic or rank > 0:
-        blocks[up] = torch.cat([blocks[up], local[:1]], 0)
-    if periodic or rank < world - 1:
-        blocks[dn] = torch.cat([blocks[dn], local[-1:]], 0)
-    got = exchange_rows(blocks, world, group)
-    above = got[up] if (periodic or rank > 0) else None     # last row of the rank above
-    below = got[dn] if (periodic or rank < world - 1) else None
-    if above is not None and above.shape[0] == 2:           # world == 2, periodic: both
-        above = above[1:]
-    if below is not None and below.shape[0] == 2:
-        below = below[:1]
-    return above, below
-
-
-def reduce_ghost_rows(top: torch.Tensor, bottom: torch.Tensor, rank: int, world: int,
-                      periodic: bool, group=None):
-    """Send the deposit rows that belong to the neighbours (``top`` = the row
-    just above my first row, ``bottom`` = just below my last row) and return
-    (what the rank above sent for my first row, what the rank below sent for
-    my last row) to be added."""
-    m = top.shape[1]
-    empty = top.new_zeros((0, m))
-    if world == 1:
-        return (bottom if periodic else torch.zeros_like(top)), \
-               (top if periodic else torch.zeros_like(bottom))
-    up = (rank - 1) % world
-    dn = (rank + 1) % world
-    blocks = [empty for _ in range(world)]
-    if periodic or rank > 0:
-        blocks[up] = torch.cat([blocks[up], top], 0)
-    if periodic or rank < world - 1:
-        blocks[dn] = torch.cat([blocks[dn], bottom], 0)
-    got = exchange_rows(blocks, world, group)
-    z = torch.zeros_like(top)
-    # the rank above sent its "bottom" (my first row); the rank below its "top"
-    from_up = got[up] if (periodic or rank > 0) else z
-    from_dn = got[dn] if (periodic or rank < world - 1) else z
-    if world == 2 and periodic:
-        # up == dn: that rank sent [top, bottom] in this order
-        pair = got[up]
-        from_dn, from_up = pair[:1], pair[1:]
-    return from_up, from_dn
-
-
-# ----------------------------------------------------------------------------
-# particle state of one rank
-# ----------------------------------------------------------------------------
-@dataclass
-class SlabState:
-    ids: torch.Tensor        # (n_r,) int64, ascending
-    pos: torch.Tensor        # (n_r, 2)
-    anchor: torch.Tensor     # (n_r, 2)
-    types: torch.Tensor      # (n_r,) uint8
-
-    def sort_by_id(self) -> "SlabState":
-        o = torch.argsort(self.ids)
-        return SlabState(self.ids[o], self.pos[o], self.anchor[o], self.types[o])
-
-
-def scatter_initial(ids, pos, types, layout: SlabLayout, geom: CellGeometry, rank: int,
-                    device, dtype) -> SlabState:
-    """Every rank keeps the particles of its slab (inputs replicated)."""
-    rows = geom.row_of(pos[:, 1])
-    mine = layout.owner_of_row(rows) == rank
-    p = torch.as_tensor(pos[mine], device=device).to(dtype)
-    return SlabState(torch.as_tensor(ids[mine], device=device, dtype=torch.int64), p,
-                     p.clone(), torch.as_tensor(types[mine], device=device))
-
-
-class SlabRunner:
-    """Steps one rank's slab.  ``backend`` provides the local compute:
-
-      forces(pos, types, ids) -> (n, 2) float64 forces of every given row
-      em(pos, types, force, xi, drift) -> proposals (n, 2)
-      boundaries(next, anchor) -> (status, bad_i, bad_ax), in place
-      deposit(pos, types) -> (rho_a, rho_b) full-grid arrays (n_c^2,)
-      rhs(c_rows, ra_rows, rb_rows) -> rhs rows
-      gradient(c_ext) -> (rows, n_c, 2) from c rows with one ghost row per side
-      bilinear_grad(grad_ext, row0, pos, types) -> drift (n, 2)
-    """
-
-    def __init__(self, backend, layout: SlabLayout, geom: CellGeometry, rank: int, world: int,
-                 periodic_y: bool, field=None, group=None):
-        self.be, self.layout, self.geom = backend, layout, geom
-        self.rank, self.world, self.per = rank, world, periodic_y
-        self.group = group
-        self.field = field          # dict(n_c, gb, solver) or None
-
-    # ---- halo ------------------------------------------------------------
-    def halo(self, st: SlabState) -> SlabState:
-        b0, b1 = int(self.layout.bounds[self.rank]), int(self.layout.bounds[self.rank + 1])
-        rows = self.geom.row_of(st.pos[:, 1])
-        W = self.world
-        up, dn = (self.rank - 1) % W, (self.rank + 1) % W
-        sel_up = rows == b0            # my first row -> rank above (their lower ghost)
-        sel_dn = rows == b1 - 1        # my last row -> rank below
-        if not self.per:
-            sel_up &= self.rank > 0
-            sel_dn &= self.rank < W - 1
-        dest = torch.full_like(st.ids, -1)
-        parts_ids, parts_pos, parts_t, parts_dest = [], [], [], []
-        for sel, d in ((sel_up, up), (sel_dn, dn)):
-            if W == 1:
-                break
-            parts_ids.append(st.ids[sel])
-            parts_pos.append(st.pos[sel])
-            parts_t.append(st.types[sel])
-            parts_dest.append(torch.full((int(sel.sum()),), d, dtype=torch.int64,
-                                         device=st.ids.device))
-        if W == 1:
-            return SlabState(st.ids[:0], st.pos[:0], st.anchor[:0], st.types[:0])
-        ids = torch.cat(parts_ids)
-        pos = torch.cat(parts_pos)
-        ty = torch.cat(parts_t)
-        dest = torch.cat(parts_dest)
-        r_ids, r_pos, r_t = exchange([ids, pos, ty], dest, W, self.group)
-        # the same particle may arrive twice when world == 2 (periodic): keep one
-        if r_ids.numel():
-            u, inv = torch.unique(r_ids, return_inverse=True)
-            first = torch.full_like(u, r_ids.numel())
-            first.scatter_reduce_(0, inv, torch.arange(r_ids.numel(), device=u.device),
-                                  reduce="amin")
-            r_ids, r_pos, r_t = r_ids[first], r_pos[first], r_t[first]
-        return SlabState(r_ids, r_pos, r_pos.clone(), r_t)
-
-    # ---- migration -----------------------------------------------------
-    def migrate(self, st: SlabState) -> SlabState:
-        rows = self.geom.row_of(st.pos[:, 1])
-        dest = self.layout.owner_of_row(rows).to(torch.int64)
-        ids, pos, anc, ty = exchange([st.ids, st.pos, st.anchor, st.types], dest, self.world,
-                                     self.group)
-        return SlabState(ids, pos, anc, ty).sort_by_id()
-
-    # ---- one step ------------------------------------------------------
-    def step(self, st: SlabState, xi_own: torch.Tensor, c_rows=None):
-        """Advance the owned particles (xi_own rows match st rows) and the
-        local field rows; returns (state, c_rows, status key)."""
-        be = self.be
-        drift = torch.zeros_like(st.pos, dtype=torch.float64)
-        if self.field is not None:
-            f = self.field
-            gb = f["gb"]
-            g0, g1 = int(gb[self.rank]), int(gb[self.rank + 1])
-            n_c = f["n_c"]
-            ra, rb = be.deposit(st.pos, st.types)                   # full grid, owned particles
-            ra = ra.view(n_c, n_c)
-            rb = rb.view(n_c, n_c)
-            # local rows + the ghost rows just outside the slab (periodic wrap)
-            def rows_ext(a):
-                above = a[(g0 - 1) % n_c:(g0 - 1) % n_c + 1]
-                below = a[g1 % n_c:g1 % n_c + 1]
-                return a[g0:g1].clone(), above, below
-            ra_l, ra_up, ra_dn = rows_ext(ra)
-            rb_l, rb_up, rb_dn = rows_ext(rb)
-            top = torch.cat([ra_up, rb_up], 1)
-            bot = torch.cat([ra_dn, rb_dn], 1)
-            from_up, from_dn = reduce_ghost_rows(top, bot, self.rank, self.world, self.per,
-                                                 self.group)
-            ra_l[0] += from_up[0, :n_c]
-            rb_l[0] += from_up[0, n_c:]
-            ra_l[-1] += from_dn[0, :n_c]
-            rb_l[-1] += from_dn[0, n_c:]
-            rhs = be.rhs(c_rows, ra_l, rb_l)
-            c_rows = f["solver"].solve(rhs).to(c_rows.dtype)
-            up, dn = ghost_rows(c_rows, self.rank, self.world, self.per, self.group)
-            c_ext = torch.cat([up, c_rows, dn], 0)
-            grad = be.gradient(c_ext)                                # (rows, n_c, 2)
-            gup, gdn = ghost_rows(grad.reshape(grad.shape[0], -1), self.rank, self.world,
-                                  self.per, self.group)
-            g_ext = torch.cat([gup, grad.reshape(grad.shape[0], -1), gdn], 0)
-            drift = be.bilinear_grad(g_ext.reshape(-1, n_c, 2), g0 - 1, st.pos, st.types)
-        ghosts = self.halo(st)
-        all_ids = torch.cat([st.ids, ghosts.ids])
-        all_pos = torch.cat([st.pos, ghosts.pos])
-        all_t = torch.cat([st.types, ghosts.types])
-        o = torch.argsort(all_ids)
-        forces_sorted = be.forces(all_pos[o], all_t[o], all_ids[o])
-        forces = torch.empty_like(forces_sorted)
-        forces[o] = forces_sorted
-        f_own = forces[: st.ids.numel()]
-        nxt = be.em(st.pos, st.types, f_own, xi_own, drift)
-        anc = st.anchor.clone()
-        status, bad_i, bad_ax = be.boundaries(nxt, anc)
-        key = torch.tensor([status * (1 << 40) + (int(st.ids[bad_i]) if status else 0)
-                            if status else (1 << 62)], dtype=torch.int64, device=st.ids.device)
-        dist.all_reduce(key, op=dist.ReduceOp.MIN, group=self.group)
-        new = SlabState(st.ids, nxt, anc, st.types)
-        return self.migrate(new), c_rows, int(key.item())
-
-
-# ----------------------------------------------------------------------------
-# device backend: the library's C-ABI ops on this rank's GPU
-# ----------------------------------------------------------------------------
-class DeviceSlabBackend:
-    """Local compute of one rank on its GPU.  Pair forces, the EM proposal,
-    boundaries and deposits run in libchemo_b200 (cs_soft_forces, cs_em_step,
-    cs_apply_boundaries, cs_deposit) on the global geometry; the slab-local
-    grid stencils (rhs, gradient rows, bilinear drift) are exact elementwise
-    restatements of the reference arithmetic on the rank's rows."""
-
-    def __init__(self, domain, motion, grid=None, fparams=None, chi=(0.0, 1.0),
-                 chi_pinned=(True, False), secretes=(True, False), consumes=(False, True),
-                 dt=1e-5):
-        from . import _native as N
-        self.N = N
-        self.domain, self.motion, self.grid, self.fp = domain, motion, grid, fparams
-        self.chi, self.chi_pinned = chi, chi_pinned
-        self.secretes, self.consumes = secretes, consumes
-        self.dt = float(dt)
-        eps, cut, cell = motion.pair_table()
-        self.pp = N.pair_struct(eps, cut, cell)
-        self.dom = N.domain_struct(domain.lo, domain.hi, domain.periodic)
-        self.D = torch.tensor([motion.d_alpha, motion.d_beta], dtype=torch.float64)
-
-    def forces(self, pos, types, ids):
-        import ctypes
-        N = self.N
-        n = pos.shape[0]
-        out = torch.empty((n, 2), dtype=torch.float64, device=pos.device)
-        if n:
-            N.check(N.load_library().cs_soft_forces(
-                N.context(), N.prec_code(pos.dtype), N.ptr(pos.contiguous()),
-                N.ptr(types.contiguous()), n, ctypes.byref(self.dom), ctypes.byref(self.pp),
-                N.ptr(out)), "cs_soft_forces")
-        return out
-
-    def em(self, pos, types, force, xi, drift):
-        from .motion import em_step
-        D = self.D.to(pos.device)[types.long()]
-        return em_step(pos, D, drift, force, self.dt, xi=xi.to(pos.dtype))
-
-    def boundaries(self, nxt, anchor):
-        import ctypes
-        N = self.N
-        bi, ba = ctypes.c_int64(-1), ctypes.c_int32(-1)
-        n = nxt.shape[0]
-        if n == 0:
-            return 0, -1, -1
-        st = N.load_library().cs_apply_boundaries(
-            N.context(), N.prec_code(nxt.dtype), N.ptr(nxt), N.ptr(anchor), N.C_p(0), n,
-            ctypes.byref(self.dom), ctypes.byref(bi), ctypes.byref(ba))
-        N.check(st, "cs_apply_boundaries")
-        return st, bi.value, ba.value
-
-    def deposit(self, pos, types):
-        from .coupling import Kernel, deposit as dep
-        from .particles import Population
-        kern = Kernel(kind="cic")
-        sec = torch.tensor(self.secretes, device=pos.device)[types.long()]
-        con = torch.tensor(self.consumes, device=pos.device)[types.long()]
-        n = pos.shape[0]
-        z = torch.zeros((n, 2), dtype=torch.float64, device=pos.device)
-        out = []
-        for mask in (sec, con):
-            sp = torch.where(mask, 0, 1).to(torch.uint8)
-            pop = Population(ids=torch.arange(n, device=pos.device), positions=pos,
-                             next_positions=pos, species=sp, drift=z,
-                             local_concentration=z[:, 0], start_anchor=pos)
-            out.append(dep(pop, self.grid, kern, 0).to(torch.float64))
-        return out[0], out[1]
-
-    def rhs(self, c, ra, rb):
-        fp, dt = self.fp, self.dt
-        r = c.double() * (1.0 - dt * fp.gamma) if fp.gamma else c.double().clone()
-        if fp.k_alpha:
-            r = r + (dt * fp.k_alpha) * ra
-        if fp.k_beta:
-            r = r - (rb * c.double()) * (dt * fp.k_beta)
-        return r
-
-    def gradient(self, c_ext):
-        """(rows, n, 2) central differences (periodic grid, field.py:128-137)
-        for the interior rows of c_ext (one ghost row above and below)."""
-        hx, hy = (float(v) for v in self.grid.spacing)
-        c = c_ext.double()
-        m1x, p1x = -1.0 / (2.0 * hx), 1.0 / (2.0 * hx)
-        m1y, p1y = -1.0 / (2.0 * hy), 1.0 / (2.0 * hy)
-        mid = c[1:-1]
-        gx = m1x * torch.roll(mid, 1, 1) + p1x * torch.roll(mid, -1, 1)
-        gy = m1y * c[:-2] + p1y * c[2:]
-        return torch.stack([gx, gy], -1)
-
-    def bilinear_grad(self, g_ext, row0, pos, types):
-        """Bilinear drift (coupling.py:216-262, periodic) from grad rows
-        row0 .. row0 + len(g_ext) - 1 (global row indices, may be -1)."""
-        n_c = self.grid.n_c
-        lo = torch.as_tensor(self.grid.lo, device=pos.device)
-        h = torch.as_tensor(self.grid.spacing, device=pos.device)
-        u = (pos.double() - lo) / h
-        f = torch.floor(u)
-        fr = u - f
-        b = f.long()
-        bx = torch.remainder(b[:, 0], n_c)
-        cx = torch.remainder(bx + 1, n_c)
-        by = b[:, 1] - row0
-        # global row b1 maps to local row b1 - row0; a wrap at the seam keeps
-        # the local offset (ghost rows carry the wrapped neighbours)
-        by = torch.where(by < 0, by + n_c, by)
-        by = torch.where(by >= g_ext.shape[0], by - n_c, by)
-        cy = by + 1
-        f0, f1 = fr[:, 0], fr[:, 1]
-        w00 = (1.0 - f0) * (1.0 - f1)
-        w10 = f0 * (1.0 - f1)
-        w01 = (1.0 - f0) * f1
-        w11 = f0 * f1
-        g = g_ext.double()
-        v = (w00[:, None] * g[by, bx] + w10[:, None] * g[by, cx]) + w01[:, None] * g[cy, bx]
-        v = v + w11[:, None] * g[cy, cx]
-        chi = torch.tensor(self.chi, dtype=torch.float64, device=pos.device)[types.long()]
-        pin = torch.tensor(self.chi_pinned, device=pos.device)[types.long()]
-        v = torch.where((chi != 1.0)[:, None], v * chi[:, None], v)
-        return torch.where(pin[:, None], torch.zeros_like(v), v)
 
 
 # ============================================================================

@@ -172,3 +172,46 @@ def test_slab_engine_with_field_equals_single_domain_bitwise(world, clustered):
         assert torch.equal(sts[r]["c"].view(n_c, n_c)[rows], c1[rows]), r
     for eng in engines:
         eng.close()
+
+
+def test_bench_slab_setup_in_process():
+    """bench.py's N > 1 path (one system over W slabs): its setup (seeded
+    state, count-balanced bounds, field plan) at cfg3's parameters and 1/50
+    of its size, the W ranks emulated in one process: the single-domain
+    engine's result bit for bit."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    cfg = dict(bench.CONFIGS["cfg3"], n=200_000, n_c=512)
+    world, steps = 4, 3
+    one, st1, _, _ = bench.make_state(cfg, 0)
+    assert one.engine == "sorted"
+    xi = torch.randn((steps, cfg["n"], 2), generator=torch.Generator(device="cuda")
+                     .manual_seed(5), device="cuda")
+    one.step(xi, steps)
+    one.export_state()
+    params, _, bounds, plan = bench.slab_setup(cfg, world)
+    engines, states = [], []
+    shared = None
+    for r in range(world):
+        _, st, _, _ = bench.make_state(cfg, 0, engine="sorted", build_sim=False)
+        if shared is None:
+            shared = st
+        else:
+            for key in ("pos", "anchor", "species"):
+                st[key] = shared[key]
+        states.append(st)
+        engines.append(slabs.SlabEngine(params, st, bounds, r, world, field_plan=plan))
+    hub = slabs.LoopbackHub(world)
+    for k in range(steps):
+        slabs.step_in_process(engines, hub, xi[k])
+    for eng in engines:
+        assert eng.status().code == 0
+        eng.export()
+    torch.cuda.synchronize()
+    assert torch.equal(shared["pos"], st1["pos"])
+    n_c = cfg["n_c"]
+    for r in range(world):
+        rows = slice(int(plan.g0[r]), int(plan.g0[r]) + plan.rp)
+        assert torch.equal(states[r]["c"].view(n_c, n_c)[rows], st1["c"].view(n_c, n_c)[rows])

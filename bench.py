@@ -421,6 +421,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-perf-mode", action="store_true")
+    ap.add_argument("--rebalance-every", type=int, default=25,
+                    help="N > 1: re-balance the y-slabs every M steps (0: never)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -645,6 +647,8 @@ def run_slabs(args, cfg, rank, world, barrier):
         a.record(stream)
         for k in range(K):
             eng.step(xi[W + k], tr)
+            if args.rebalance_every and (k + 1) % args.rebalance_every == 0 and k + 1 < K:
+                eng.rebalance(tr, eng.n1, cfg["n_c"] if cfg["field"] else None)
         b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -664,7 +668,8 @@ def run_slabs(args, cfg, rank, world, barrier):
             "data": "synthetic",
             "config": dict(config_dict(args.config, cfg, world),
                            parallelism=f"yslab{world}",
-                           decomposition="one system, count-balanced y-slabs of cell rows, "
+                           decomposition="one system, count-balanced y-slabs of cell rows "
+                                         f"(re-balanced every {args.rebalance_every} steps), "
                                          "even grid-row split, NCCL all-to-all exchanges"),
             "engine": "sorted (slab mode)", "clocks": clocks.summary(),
             "rank0_owned": hi - lo,

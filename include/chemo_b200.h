@@ -390,6 +390,15 @@ void *cs_slab_rho(cs_sim *sim);
 int cs_slab_field_rows(cs_sim *sim, const cs_sim_state *st, void *spec, int32_t inverse);
 int cs_slab_field_cols(cs_sim *sim, void *blocks, int32_t kx0, int32_t ncols, int32_t rp);
 int cs_slab_field_grad(cs_sim *sim, const cs_sim_state *st);
+/* Re-balancing every M steps: the per-row counts of the owned records
+ * (hist: device int32[cell rows], summed over ranks by the caller), then
+ * cs_slab_rebalance with the new bounds (every owned record routed under
+ * them: claimed, or into the outbox with the ghost copies of the new
+ * boundary rows), the caller's exchange and cs_slab_claim, the new deposit /
+ * gradient windows (cs_slab_field_config), cs_slab_finish_rebalance. */
+int cs_slab_row_counts(cs_sim *sim, int32_t *hist);
+int cs_slab_rebalance(cs_sim *sim, const int32_t *bounds);
+int cs_slab_finish_rebalance(cs_sim *sim);
 
 /* ---------------------------------------------------------------------- */
 /* Ensembles of small realisations (run_ensemble, engine.py:455-484;       */

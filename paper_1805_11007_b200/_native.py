@@ -136,6 +136,9 @@ SIGNATURES = [
     ("cs_slab_field_rows", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p, C_i32]),
     ("cs_slab_field_cols", C_i32, [C_p, C_p, C_i32, C_i32, C_i32]),
     ("cs_slab_field_grad", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
+    ("cs_slab_row_counts", C_i32, [C_p, C_p]),
+    ("cs_slab_rebalance", C_i32, [C_p, ctypes.POINTER(C_i32)]),
+    ("cs_slab_finish_rebalance", C_i32, [C_p]),
     ("cs_sim_export", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
     ("cs_sim_status_device", C_p, [C_p]),
     ("cs_sim_status_bytes", C_i64, []),

@@ -882,6 +882,35 @@ k_fast_update(DevStatus *st, int step) {
 #endif
 }
 
+// Slab re-balancing: every owned record (old range) routed under the new
+// row bounds without moving -- claimed here, or sent to its new owner, plus
+// ghost copies for the neighbours of its row's owner (slab_route).
+__global__ void __launch_bounds__(256) k_slab_reroute(DevStatus *st, int step) {
+    const FastArgs &a = cA;
+    const long long lo = a.range[0], hi = a.range[1];
+    const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
+    const int lane = threadIdx.x & 31;
+    for (long long t = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; t < hi;
+         t += (long long)gridDim.x * blockDim.x) {
+        const float4 out = rec[t];
+        const int cy = cell_axis_fast((double)out.y, a.g.lo1, a.eff1, a.g.n1);
+        const int key = cy * a.g.n0 + cell_axis_fast((double)out.x, a.g.lo0, a.eff0, a.g.n0);
+        if (slab_route(a, st, step, out, key, cy, lane)) {
+            const int pb = (key >> BUCKET_SHIFT) * SUBB + (lane & (SUBB - 1));
+            claim_store(a, st, step, pb, atomicAdd(&a.fill[pb], 1), out);
+        }
+    }
+}
+
+// per-row counts of the owned records (the re-balancing histogram)
+__global__ void k_slab_hist(const Rec *__restrict__ rec, const int *__restrict__ range, BinGeom g,
+                            ExactDiv eff1, int *__restrict__ hist) {
+    const long long lo = range[0], hi = range[1];
+    for (long long t = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; t < hi;
+         t += (long long)gridDim.x * blockDim.x)
+        atomicAdd(&hist[cell_axis_fast((double)rec[t].y, g.lo1, eff1, g.n1)], 1);
+}
+
 // caller arrays (id order) -> records claimed into their bucket regions
 // (the same claim as k_fast_update's), anchors kept as the wrap origin
 __global__ void k_fast_import(const float *__restrict__ pos, const float *__restrict__ anchor,
@@ -1614,7 +1643,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     }
     a.xi = (const float *)xi;
     a.xi_slot = p.xi_by_slot ? 1 : 0;
-    a.grad = (const float *)s->grad;
+    a.grad = s ? (const float *)s->grad : nullptr;
     a.rho_q = f->rho_q.as<int>();
     a.n = n;
     a.g = c.g;
@@ -1682,6 +1711,14 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
             CS_LAUNCH_CHECK();
             ctx->launches += 2;
         }
+        if (part & 4) {  // slab re-balancing (the constant block is this call's)
+            CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0, cudaMemcpyHostToDevice,
+                                            ctx->stream));
+            k_slab_reroute<<<sms * 8, 256, 0, ctx->stream>>>(st, step);
+            CS_LAUNCH_CHECK();
+            ctx->launches += 1;
+            return CS_OK;
+        }
         if (!(part & 2)) return CS_OK;
         // persistent grid: one contiguous processing front, so the atomics'
         // working set (cell histogram + deposit rows near the front) stays in L2
@@ -1747,6 +1784,7 @@ int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long lo
     f->b1 = b[(size_t)rank + 1];
     CS_TRY(f->row_owner.ensure(sizeof(int) * (size_t)n1));
     CS_TRY(f->bounds.ensure(sizeof(int) * ((size_t)world + 1)));
+    const bool first = f->range.p == nullptr;  // a re-balance keeps the owned range (re-routed)
     CS_TRY(f->range.ensure(sizeof(int) * 4));
     CS_TRY(f->out_count.ensure(sizeof(int) * 4));
     f->out_cap = n > 1024 ? n : 1024;  // every record could leave (kicks cross several slabs)
@@ -1756,7 +1794,7 @@ int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long lo
                             cudaMemcpyHostToDevice, stream));
     CS_CUDA(cudaMemcpyAsync(f->bounds.p, b.data(), sizeof(int) * b.size(),
                             cudaMemcpyHostToDevice, stream));
-    CS_CUDA(cudaMemsetAsync(f->range.p, 0, sizeof(int) * 4, stream));
+    if (first) CS_CUDA(cudaMemsetAsync(f->range.p, 0, sizeof(int) * 4, stream));
     CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int) * 4, stream));
     CS_CUDA(cudaStreamSynchronize(stream));  // the host vectors go out of scope
     return CS_OK;
@@ -1821,7 +1859,18 @@ int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGe
     return fast_slab_range(ctx, f);
 }
 
+int fast_slab_hist(cs_ctx *ctx, cs_fast *f, int *hist) {
+    CS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (size_t)f->g.n1, ctx->stream));
+    k_slab_hist<<<148 * 8, 256, 0, ctx->stream>>>(f->rec[f->cur].as<Rec>(), f->range.as<int>(),
+                                                  f->g, make_exact_div(f->g.eff1), hist);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
 bool fast_slab_gather(const cs_fast *f) { return f->gather; }
+int fast_slab_world(const cs_fast *f) { return f->world; }
+int fast_slab_rank(const cs_fast *f) { return f->rank; }
 int fast_slab_dep_window(cs_fast *f, int j0, int rows) {
     f->dep_j0 = j0;
     f->dep_rows = rows;

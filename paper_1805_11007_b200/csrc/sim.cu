@@ -80,6 +80,9 @@ int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGe
                    const unsigned char bits[3], DevStatus *st, int step);
 int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi);
 bool fast_slab_gather(const cs_fast *f);
+int fast_slab_hist(cs_ctx *ctx, cs_fast *f, int *hist);
+int fast_slab_world(const cs_fast *f);
+int fast_slab_rank(const cs_fast *f);
 int fast_slab_dep_window(cs_fast *f, int j0, int rows);
 void *fast_rho_all(cs_fast *f);
 int spectral_slab_rows(cs_field_ops *ops, float *c, const int *q, double gamma, double ka,
@@ -851,7 +854,26 @@ extern "C" int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n) {
     return cs::fast_slab_claim(sim->ctx, sim->fast, recs, n, sim->dstat(), sim->steps_done);
 }
 
-extern "C" int cs_slab_finish(cs_sim *sim) {
+// Re-balancing: the per-row counts of the owned records (device int[n1]),
+// then cs_slab_rebalance with the new bounds (every owned record routed
+// under them into the outbox or claimed; the caller exchanges, claims and
+// calls cs_slab_finish with advance = 0).
+extern "C" int cs_slab_row_counts(cs_sim *sim, int32_t *hist) {
+    CS_TRY(slab_check(sim));
+    return cs::fast_slab_hist(sim->ctx, sim->fast, hist);
+}
+
+extern "C" int cs_slab_rebalance(cs_sim *sim, const int32_t *bounds) {
+    CS_TRY(slab_check(sim));
+    cs_fast *f = sim->fast;
+    CS_TRY(cs::fast_slab_config(f, bounds, cs::fast_slab_world(f), cs::fast_slab_rank(f), sim->p.n,
+                                sim->ctx->stream));
+    CS_TRY(cs::fast_slab_reset_outbox(sim->ctx, f));
+    const cs::FastStepCfg c = slab_cfg(sim);
+    return cs::fast_particles(sim->ctx, f, c, nullptr, nullptr, sim->dstat(), sim->steps_done, 4);
+}
+
+static int slab_finish(cs_sim *sim, bool advance) {
     CS_TRY(slab_check(sim));
     const int64_t l0 = sim->ctx->launches;
     CS_TRY(cs::fast_slab_sort(sim->ctx, sim->fast, sim->p, sim->gg, sim->bits, sim->dstat(),
@@ -860,10 +882,14 @@ extern "C" int cs_slab_finish(cs_sim *sim) {
     // particles, into this rank's deposit window)
     CS_TRY(cs::fast_resort(sim->ctx, sim->fast, sim->p.n, sim->p, sim->gg, sim->bits, 2,
                            sim->dstat(), sim->steps_done));
-    sim->steps_done += 1;
+    if (advance) sim->steps_done += 1;
     sim->last_launches += sim->ctx->launches - l0;
     return CS_OK;
 }
+
+extern "C" int cs_slab_finish(cs_sim *sim) { return slab_finish(sim, true); }
+
+extern "C" int cs_slab_finish_rebalance(cs_sim *sim) { return slab_finish(sim, false); }
 
 extern "C" int cs_slab_range(cs_sim *sim, int64_t *lo, int64_t *hi) {
     CS_TRY(slab_check(sim));

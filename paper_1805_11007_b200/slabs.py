@@ -179,6 +179,8 @@ class SlabEngine:
         lib = self.sim._bind()
         b = (N.C_i32 * len(self.bounds))(*[int(v) for v in self.bounds])
         N.check(lib.cs_slab_config(self.sim._h, b, world, rank), "cs_slab_config")
+        e_, c_, cell = _pair_cell(params)
+        self.n1 = max(1, int((params.domain.hi[1] - params.domain.lo[1]) / cell))
         self.field = None
         if field_plan is not None:
             r = rank
@@ -241,6 +243,51 @@ class SlabEngine:
     def status(self):
         return self.sim.status()
 
+    # ---- re-balancing (every M steps) --------------------------------------
+    def row_counts(self):
+        """Per-cell-row counts of the owned particles (device int32)."""
+        h = torch.empty(int(self.n1), dtype=torch.int32, device=self.sim.state["pos"].device)
+        self.N.check(self.sim._bind().cs_slab_row_counts(self.sim._h, self.N.ptr(h)),
+                     "cs_slab_row_counts")
+        return h
+
+    def rebalance_begin(self, bounds, field_plan: "FieldPlan | None" = None):
+        """Adopt new row bounds: the owned records are routed under them
+        into the outbox (or claimed); the caller exchanges and claims, then
+        calls rebalance_end()."""
+        N = self.N
+        self.bounds = np.asarray(bounds, dtype=np.int32)
+        b = (N.C_i32 * len(self.bounds))(*[int(v) for v in self.bounds])
+        lib = self.sim._bind()
+        N.check(lib.cs_slab_rebalance(self.sim._h, b), "cs_slab_rebalance")
+        if field_plan is not None:
+            r = self.rank
+            j0, k = field_plan.dep[r]
+            gj0, gk = field_plan.grad[r]
+            g0 = int(field_plan.g0[r])
+            N.check(lib.cs_slab_field_config(self.sim._h, g0, g0 + field_plan.rp, j0, k, gj0,
+                                             gk), "cs_slab_field_config")
+            self.field = SlabField(self, field_plan)
+            if hasattr(self, "_nf"):
+                del self._nf
+
+    def rebalance_end(self):
+        self.N.check(self.sim._bind().cs_slab_finish_rebalance(self.sim._h),
+                     "cs_slab_finish_rebalance")
+
+    def rebalance(self, transport: NcclTransport, n1: int, n_c: int | None = None):
+        """One rank's re-balancing over NCCL: the global row histogram
+        (all-reduce), count-balanced bounds, the records re-routed."""
+        h = self.row_counts().to(torch.int64)
+        dist.all_reduce(h, group=transport.group)
+        counts = h.cpu().numpy()
+        bounds = SlabLayout.balanced(counts, self.world).bounds
+        plan = FieldPlan.make(bounds, n1, n_c, self.world) if self.field is not None else None
+        self.rebalance_begin(bounds, plan)
+        recs, dest = self.outbox()
+        self.claim(transport.exchange(recs, dest))
+        self.rebalance_end()
+
     def export(self):
         """Own particles' positions / anchors into the global state arrays."""
         self.sim.export_state()
@@ -254,6 +301,29 @@ class SlabEngine:
 
     def close(self):
         self.sim.close()
+
+
+def _pair_cell(params):
+    return None, None, float(params.pairs.cell_cutoff)
+
+
+def rebalance_in_process(engines, hub: LoopbackHub, n_c: int | None = None):
+    """Re-balance every in-process rank (tests): the summed row histogram,
+    count-balanced bounds, the records re-routed through the hub."""
+    counts = sum(e.row_counts().to(torch.int64) for e in engines).cpu().numpy()
+    world = len(engines)
+    bounds = SlabLayout.balanced(counts, world).bounds
+    plan = None
+    if engines[0].field is not None:
+        plan = FieldPlan.make(bounds, len(counts), n_c, world)
+    for e in engines:
+        e.rebalance_begin(bounds, plan)
+    got = hub.exchange_all([e.outbox() for e in engines])
+    for e, g in zip(engines, got):
+        e.claim(g)
+    for e in engines:
+        e.rebalance_end()
+    return bounds
 
 
 def step_in_process(engines, hub: LoopbackHub, xi):

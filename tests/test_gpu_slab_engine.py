@@ -215,3 +215,55 @@ def test_bench_slab_setup_in_process():
     for r in range(world):
         rows = slice(int(plan.g0[r]), int(plan.g0[r]) + plan.rp)
         assert torch.equal(states[r]["c"].view(n_c, n_c)[rows], st1["c"].view(n_c, n_c)[rows])
+
+
+@pytest.mark.parametrize("field", [False, True])
+def test_slab_rebalancing_keeps_the_single_domain_result(field):
+    """Re-balancing every M steps: clustered particles on EVEN
+    slabs (badly balanced), re-balanced to the count-balanced bounds after 2
+    steps: the run still equals the single-domain engine bit for bit, and
+    the re-balanced slabs hold within 5 % of N / W particles."""
+    world, n, n_c, steps = 4, 100_000, 256, 5
+    rng = np.random.default_rng(31)
+    centres = -0.5 + rng.random((8, 2))
+    pos = centres[rng.integers(0, 8, n)] + 0.03 * rng.standard_normal((n, 2))
+    pos = (np.mod(pos + 0.5, 1.0) - 0.5).astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    radii = (7e-4, 1.4e-3)
+    c0 = (0.5 + 0.1 * rng.standard_normal(n_c * n_c)).astype(np.float32)
+    if field:
+        params, mp, dom = _field_params(n, radii, n_c)
+    else:
+        params, mp, dom = _params(n, radii)
+    xi = torch.as_tensor(rng.standard_normal((steps, n, 2)).astype(np.float32), device="cuda")
+    st1 = _field_state(pos, sp, c0, n_c) if field else _state(pos, sp)
+    one = cs.DeviceSim(params, st1)
+    one.step(xi, steps)
+    one.export_state()
+    e, c, cell = mp.pair_table()
+    n1 = slabs.CellGeometry.make(dom.lo[1], dom.hi[1], cell).n
+    bounds = slabs.SlabLayout.even(n1, world).bounds
+    plan = slabs.FieldPlan.make(bounds, n1, n_c, world) if field else None
+    shared = _state(pos, sp)
+    sts = [_field_state(pos, sp, c0, n_c, shared) if field else shared for _ in range(world)]
+    engines = [slabs.SlabEngine(params, sts[r], bounds, r, world, field_plan=plan)
+               for r in range(world)]
+    hub = slabs.LoopbackHub(world)
+    for k in range(2):
+        slabs.step_in_process(engines, hub, xi[k])
+    new = slabs.rebalance_in_process(engines, hub, n_c)
+    assert not np.array_equal(new, bounds)
+    owned = [hi - lo for lo, hi in (eng.owned_range() for eng in engines)]
+    assert sum(owned) == n and max(owned) <= 1.05 * n / world, owned
+    for k in range(2, steps):
+        slabs.step_in_process(engines, hub, xi[k])
+    for eng in engines:
+        assert eng.status().code == 0
+        eng.export()
+    torch.cuda.synchronize()
+    assert torch.equal(shared["pos"], st1["pos"])
+    if field:
+        new_plan = slabs.FieldPlan.make(new, n1, n_c, world)
+        for r in range(world):
+            rows = slice(int(new_plan.g0[r]), int(new_plan.g0[r]) + new_plan.rp)
+            assert torch.equal(sts[r]["c"].view(n_c, n_c)[rows], st1["c"].view(n_c, n_c)[rows])

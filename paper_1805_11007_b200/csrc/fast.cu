@@ -1200,9 +1200,12 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
             const double base1 = floor(u1);
             const int b1 = wrap_index(base1, n);
             const int c1 = b1 + 1 == n ? 0 : b1 + 1;
-            int rb = (b1 - j0) % n, rc = (c1 - j0) % n;  // rows of this block's window, if any
-            if (rb < 0) rb += n;
-            if (rc < 0) rc += n;
+            // rows of this block's window, if any (j0 in [-n, 2n): two wraps at most)
+            int rb = b1 - j0, rc = c1 - j0;
+            rb += rb < 0 ? n : (rb >= n ? -n : 0);
+            rc += rc < 0 ? n : (rc >= n ? -n : 0);
+            rb += rb < 0 ? n : 0;
+            rc += rc < 0 ? n : 0;
             const bool hb = rb < DEP_ROWS, hc = rc < DEP_ROWS;
             if (!hb && !hc) continue;
             const double f1 = dsub(u1, base1);

@@ -548,7 +548,8 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         sim->last_launches = ctx->launches - l0;
         return CS_OK;
     }
-    for (int kk = 0; kk < k; kk++) {
+    // one step of the direct engine
+    auto one = [&](int kk) -> int {
         const int step = sim->steps_done + kk;
         const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
         // the cell list and the deposit bins come from the same start-of-step
@@ -665,7 +666,9 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                                 u + (size_t)kk * (size_t)u_stride, n, p.react_p_ab,
                                 p.react_r_beta, p.dt, st));
         }
-    }
+            return CS_OK;
+    };
+    for (int kk = 0; kk < k; kk++) CS_TRY(one(kk));
     sim->steps_done += k;
     sim->last_launches = ctx->launches - l0;
     return CS_OK;

@@ -287,10 +287,10 @@ int sim_create(cs_ctx *ctx, const cs_sim_params *p, cs_sim **out) {
     auto *sim = new cs_sim();
     sim->ctx = ctx;
     sim->p = *p;
-    // field solve concurrent with the pair forces on a side stream: opt-in
-    // (measured at cfg3: 1.705 ms/step with it, 1.691 without -- the forces
-    // kernel is issue-bound and the solve gets too few SM slots beside it)
-    sim->overlap = getenv("CS_OVERLAP") ? 1 : 0;
+    // field solve (spectral passes + gradient) concurrent with the pair forces
+    // on a high-priority side stream (measured at cfg3, round 2: 1.317 ->
+    // 1.278 ms/step; CS_NO_OVERLAP=1 serialises them)
+    sim->overlap = getenv("CS_NO_OVERLAP") ? 0 : 1;
     *out = sim;
     if (p->interaction == 1) {
         sim->geom = make_geom(p->domain, p->pairs.cell_cutoff);

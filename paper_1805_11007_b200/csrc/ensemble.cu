@@ -963,6 +963,8 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
                                  (int)e->smem));
     CS_CUDA(cudaFuncSetAttribute(k_ensemble<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)e->smem));
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble<768>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)e->smem));
     CS_TRY(e->status.ensure(sizeof(DevStatus) * (size_t)n_real));
     std::vector<DevStatus> init((size_t)n_real);
     for (auto &d : init) {
@@ -1009,6 +1011,8 @@ int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u
     a.step0 = e->steps_done;
     if (e->threads == 1024)
         k_ensemble<1024><<<e->n_real, 1024, e->smem, e->ctx->stream>>>(a);
+    else if (e->threads == 768)
+        k_ensemble<768><<<e->n_real, 768, e->smem, e->ctx->stream>>>(a);
     else if (e->threads == 512)
         k_ensemble<512><<<e->n_real, 512, e->smem, e->ctx->stream>>>(a);
     else

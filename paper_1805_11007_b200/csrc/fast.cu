@@ -10,28 +10,36 @@
 // rebuilds the order every step with one counting-sort pass, so all
 // per-particle traffic is coalesced and neighbour cells are contiguous.
 //
-// Per step (after the field step of sim.cu):
-//   k_fast_forces  pair forces over the 3x3 reference ring per sorted slot
-//                  (binary32 prefilter in the candidate loop, exact test and
-//                  pair terms evaluated warp-cooperatively, canonical order)
-//   k_fast_update  bilinear drift, EM proposal with xi[id], boundaries with
-//                  wrap counting, new cell key + histogram atomic (its
-//                  return value is the record's rank in the new cell)
-//   k_scan         exclusive scan of the histogram -> next cell table (and
-//                  histogram reset)
-//   k_fast_scatter counting-sort scatter of the new records
-//   k_fast_deposit CIC deposit of the new positions for the next step's
-//                  field, over the freshly sorted records (L2-local integer
-//                  reductions, deterministic)
+// Per step (the field solve of fast_field runs on a side stream, overlapped
+// with the forces):
+//   k_fast_forces          pair forces over the 3x3 reference ring per sorted
+//                          slot (binary32 prefilter in the candidate loop
+//                          except across a periodic seam, exact test and pair
+//                          terms in binary64, canonical id order); owners with
+//                          too many hits, or at seams / walls, are deferred
+//   k_fast_forces_generic  the deferred owners, one warp each
+//   k_fast_update          bilinear drift, EM proposal with xi (by id, or by
+//                          storage slot in the performance mode), boundaries
+//                          with wrap counting, new cell key; the record is
+//                          claimed into one of SUBB parts of its bucket
+//                          (1024 consecutive cells) with a warp-aggregated
+//                          atomic -- in slab mode migrants and ghost copies
+//                          go to the outbox instead (slab_route)
+//   k_scan                 exclusive scan of the bucket-part fills
+//   k_bucket_sort          one CTA per bucket: counting sort of the claimed
+//                          records into cells in shared memory, records of a
+//                          cell ordered by id, next cell table
+//   k_fast_deposit_rows    CIC deposit of the new positions for the next
+//                          step's field: one CTA per grid row gathers the
+//                          records of the cell rows under it (int32 fixed
+//                          point, deterministic)
 //
-// Force summation order.  Inside a cell the records are in arbitrary
-// (atomic-arrival) order, so the kernel does not rely on storage order:
-// per ring cell it sums the accepted pairs in ascending particle id --
-// exactly the reference's order (motion.py:206-243) -- by a single pass
-// when a cell contributes at most one pair (the common case) and an
-// id-ordered selection pass otherwise.  The force on every particle is
-// therefore bit-identical to the reference arithmetic on the stored
-// binary32 coordinates.
+// Force summation order.  Records of a cell are stored in id order and the
+// ring cells are visited in the reference's order, so the accepted pairs of
+// an owner are summed in ascending particle id -- the reference's order
+// (motion.py:206-243).  The force on every particle is therefore
+// bit-identical to the reference arithmetic on the stored binary32
+// coordinates.
 //
 // Deposits accumulate w * 2^22 (w = CIC corner weight) in int32 per node:
 // integer addition is associative, so the field is run-to-run

@@ -89,7 +89,8 @@ struct FastArgs {
     long long cap;      // slots per sub-bucket region
     double2 *force;     // pair force per sorted slot (binary64)
     int *gen;           // slots the force kernel defers to k_fast_forces_generic
-    int *gen_count;     // gen[0, *gen_count); reset by k_fast_update
+    int *gen_count;     // gen[0, *gen_count); reset by k_fast_update (fused: a memset)
+    int *gen_dead;      // fused: the run state the force kernel saw at its start
     int debug;          // diagnostics bitmask (CS_FAST_DEBUG): 1 plain xi loads,
                         // 2 skip deposits, 64 no pair terms, 128 no candidate walk, 4 store records at the slot index
                         // without claims, 8 the same plus a fire-and-forget
@@ -383,6 +384,138 @@ __device__ __noinline__ double2 ring_forces_generic(const float4 *__restrict__ r
     return make_double2(fx, fy);
 }
 
+// store a record at its claimed bucket slot (or flag the overflow)
+__device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, int step, int b,
+                                            int slot, float4 out) {
+    if (slot < a.cap) {
+        reinterpret_cast<float4 *>(a.region)[(long long)b * a.cap + slot] = out;
+    } else {
+        atomicMin(&st->key, err_key(3, b / SUBB, CS_SORT_OVERFLOW));
+        st->abort = 1;
+        st->step = step;
+    }
+}
+
+// The update's inputs of one slot that do not depend on its pair force: the
+// increment and the four gradient nodes of its bilinear stencil (the fused
+// kernel issues these loads before its candidate walk)
+struct UpdIn {
+    float2 z, v00, v10, v01, v11;
+    double bf0, bf1;
+};
+
+__device__ __forceinline__ UpdIn upd_load(const FastArgs &a, float4 mer, long long t, bool dead) {
+    UpdIn u;
+    const unsigned meta = __float_as_uint(mer.z);
+    const int ti = (int)(meta >> 31);
+    const unsigned id = meta & ID_MASK;
+    // the particle's increment: xi[id] (the reference's layout: a random
+    // gather, kept in L2 by evict_last), or xi[slot] in performance mode
+    // (xi_by_slot: a coalesced stream)
+    if (a.xi_slot)
+        u.z = __ldcs(reinterpret_cast<const float2 *>(a.xi) + t);
+    else if (a.debug & 1)
+        u.z = __ldg(reinterpret_cast<const float2 *>(a.xi) + id);
+    else
+        u.z = ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
+    const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
+    u.v00 = make_float2(0.f, 0.f);
+    u.v10 = u.v01 = u.v11 = u.v00;
+    u.bf0 = u.bf1 = 0.0;
+    if (a.refresh && !dead && !pinned) {
+        const Cic bst = cic_stencil((double)mer.x, (double)mer.y, a.gg, a.gd0, a.gd1);
+        u.bf0 = bst.f0;
+        u.bf1 = bst.f1;
+        const float2 *g2 = reinterpret_cast<const float2 *>(a.grad);
+        u.v00 = __ldg(g2 + bst.i00);
+        u.v10 = __ldg(g2 + bst.i10);
+        u.v01 = __ldg(g2 + bst.i01);
+        u.v11 = __ldg(g2 + bst.i11);
+    }
+    return u;
+}
+
+// Drift refresh, EM proposal and boundaries of one slot given its pair force
+// (zero without interactions): the new record and its cell (key, row).  A
+// dead run (an earlier error) keeps the record unchanged.
+__device__ __forceinline__ float4 upd_finish(const FastArgs &a, DevStatus *st, int step,
+                                             float4 mer, const UpdIn &u, double fx, double fy,
+                                             bool dead, bool live, int &key, int &cyn) {
+    const unsigned meta = __float_as_uint(mer.z);
+    const unsigned wbits = __float_as_uint(mer.w);
+    const double x = (double)mer.x, y = (double)mer.y;
+    const int ti = (int)(meta >> 31);
+    const unsigned id = meta & ID_MASK;
+    const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
+    const bool do_drift = a.refresh && !dead && !pinned;
+    // ---- drift refresh at the start-of-step position (coupling.py:302-325)
+    const double chi = ti ? a.chi[1] : a.chi[0];
+    double dr0 = 0.0, dr1 = 0.0;
+    if (do_drift) {
+        Cic b;  // bilinear weights (coupling.py:251-254) from the kept offsets
+        const double g0 = dsub(1.0, u.bf0), g1 = dsub(1.0, u.bf1);
+        b.w00 = dmul(g0, g1);
+        b.w10 = dmul(u.bf0, g1);
+        b.w01 = dmul(g0, u.bf1);
+        b.w11 = dmul(u.bf0, u.bf1);
+        dr0 = dadd(dadd(dadd(dmul(b.w00, (double)u.v00.x), dmul(b.w10, (double)u.v10.x)),
+                        dmul(b.w01, (double)u.v01.x)),
+                   dmul(b.w11, (double)u.v11.x));
+        dr1 = dadd(dadd(dadd(dmul(b.w00, (double)u.v00.y), dmul(b.w10, (double)u.v10.y)),
+                        dmul(b.w01, (double)u.v01.y)),
+                   dmul(b.w11, (double)u.v11.y));
+        if (chi != 1.0) {
+            dr0 = dmul(dr0, chi);
+            dr1 = dmul(dr1, chi);
+        }
+    }
+    // ---- EM proposal (motion.py:281-282)
+    const double amp = ti ? a.amp[1] : a.amp[0];
+    double v0 = dadd(dadd(dadd(x, dmul(amp, (double)u.z.x)), dmul(dr0, a.dt)), dmul(fx, a.dt));
+    double v1 = dadd(dadd(dadd(y, dmul(amp, (double)u.z.y)), dmul(dr1, a.dt)), dmul(fy, a.dt));
+    int w0 = (short)(wbits & 0xffffu), w1 = (short)(wbits >> 16);
+    bool ok = !dead && live;
+    if (ok && !(isfinite(v0) && isfinite(v1))) {
+        atomicMin(&st->key, err_key(0, id, CS_NONFINITE));
+        st->abort = 1;
+        st->step = step;
+        ok = false;
+    }
+    if (ok) {
+        const double r0 = v0, r1 = v1;
+        int code = boundary_axis_wraps(v0, w0, a.dom.lo[0], a.dom.hi[0], a.sz0,
+                                       a.dom.periodic[0]);
+        int ax = 0;
+        if (!code) {
+            code = boundary_axis_wraps(v1, w1, a.dom.lo[1], a.dom.hi[1], a.sz1,
+                                       a.dom.periodic[1]);
+            ax = 1;
+        }
+        if (code) {
+            atomicMin(&st->key, err_key(1 + ax, id, code));
+            st->abort = 1;
+            st->step = step;
+            if (ax == 0) v0 = r0;  // the raw proposal stays visible for the message
+            else v1 = r1;
+            ok = false;
+        }
+    }
+    float4 out;
+    if (dead) {
+        out = mer;
+    } else {
+        out.x = (float)v0;
+        out.y = (float)v1;
+        out.z = mer.z;
+        out.w = __uint_as_float(((unsigned)(w1 & 0xffff) << 16) | (unsigned)(w0 & 0xffff));
+    }
+    // ---- the cell of the stored (binary32) coordinate for the next step
+    const double nx = (double)out.x, ny = (double)out.y;
+    cyn = cell_axis_fast(ny, a.g.lo1, a.eff1, a.g.n1);
+    key = cyn * a.g.n0 + cell_axis_fast(nx, a.g.lo0, a.eff0, a.g.n0);
+    return out;
+}
+
 constexpr int ACC_MAX = 8;          // accepted pairs buffered per particle
 constexpr int WARPS_PER_BLOCK = 4;  // k_fast_forces block = 128 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
@@ -412,8 +545,14 @@ struct WarpQueue {
 //  3. each owner adds its terms in j order = canonical order.
 // Ring cells on a periodic seam or a wall, axes with < 5 cells, and lanes
 // with > ACC_MAX hits are deferred to k_fast_forces_generic (generic walk).
+//
+// FUSED: the update of every non-deferred slot runs in the same iteration
+// (its increment and gradient loads issued before the walk, so they arrive
+// during it); the pair force never goes to memory.  The deferred owners are
+// updated by k_fast_forces_generic<true>.
+template <bool FUSED>
 __global__ void __launch_bounds__(128, 5)  // 96 regs: measured best (4: 560, 6: 513 us)
-k_fast_forces(const DevStatus *st) {
+k_fast_forces(DevStatus *st, int step) {
     const FastArgs &a = cA;
     __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
     WarpQueue &wq = wq_all[threadIdx.x >> 5];
@@ -426,6 +565,13 @@ k_fast_forces(const DevStatus *st) {
     // front: ring rows are shared by concurrently running warps)
     const long long wstride = (long long)gridDim.x * blockDim.x;
     const long long s_lo = a.range ? a.range[0] : 0, s_hi = a.range ? a.range[1] : a.n;
+    // FUSED: the previous iteration's bucket claim (stored once this
+    // iteration's loads are in flight)
+    const int wpart = (threadIdx.x >> 5) & (SUBB - 1);
+    bool p_have = false, p_live = false;
+    int p_leader = 0, p_rank = 0, p_ret = 0, p_b = 0;
+    float4 p_out = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (FUSED && blockIdx.x == 0 && threadIdx.x == 0) *a.gen_dead = dead ? 1 : 0;
     for (long long base = s_lo + (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
          base < s_hi; base += wstride) {
         const long long t = base + lane;
@@ -433,6 +579,14 @@ k_fast_forces(const DevStatus *st) {
         const bool live = t < s_hi;
         float4 mer = make_float4(0.f, 0.f, 0.f, 0.f);
         if (live) mer = __ldg(rec + t);
+        UpdIn u;
+        if (FUSED) {
+            u = upd_load(a, mer, live ? t : s_lo, dead);
+            if (p_have) {
+                const int basev = __shfl_sync(0xffffffffu, p_ret, p_leader);
+                if (p_live) claim_store(a, st, step, p_b, basev + p_rank, p_out);
+            }
+        }
         const float xf = mer.x, yf = mer.y;
         const double x = (double)xf, y = (double)yf;
         const int ti = (int)(__float_as_uint(mer.z) >> 31);
@@ -553,7 +707,25 @@ k_fast_forces(const DevStatus *st) {
             }
             __syncwarp();
         }
-        if (live && !generic) a.force[t] = make_double2(fx, fy);
+        if (FUSED) {
+            const bool own = live && !generic;
+            int key, cyn;
+            const float4 out = upd_finish(a, st, step, mer, u, fx, fy, dead, own, key, cyn);
+            p_b = (key >> BUCKET_SHIFT) * SUBB + wpart;
+            const unsigned peers = __match_any_sync(0xffffffffu, own ? p_b : -1 - lane);
+            p_leader = __ffs(peers) - 1;
+            p_rank = __popc(peers & lt);
+            if (own && lane == p_leader) p_ret = atomicAdd(&a.fill[p_b], __popc(peers));
+            p_live = own;
+            p_have = true;
+            p_out = out;
+        } else if (live && !generic) {
+            a.force[t] = make_double2(fx, fy);
+        }
+    }
+    if (FUSED && p_have) {
+        const int basev = __shfl_sync(0xffffffffu, p_ret, p_leader);
+        if (p_live) claim_store(a, st, step, p_b, basev + p_rank, p_out);
     }
 }
 
@@ -565,10 +737,25 @@ k_fast_forces(const DevStatus *st) {
 // (pair_test: minimum image with rint) and the pair term are the reference's.
 // Lane 0 then adds the terms cell by cell.  A cell with more than GEN_K
 // accepted pairs sends the owner through ring_forces_generic instead.
+// the fused update of one deferred owner (one thread) and its bucket claim
+__device__ __noinline__ void generic_claim(const FastArgs &a, DevStatus *st, int step, float4 me,
+                                           double fx, double fy, bool dead, int q) {
+    const int t = a.gen[q];
+    const UpdIn u = upd_load(a, me, t, dead);
+    int key, cyn;
+    const float4 out = upd_finish(a, st, step, me, u, fx, fy, dead, true, key, cyn);
+    const int pb = (key >> BUCKET_SHIFT) * SUBB + (q & (SUBB - 1));
+    claim_store(a, st, step, pb, atomicAdd(&a.fill[pb], 1), out);
+}
 constexpr int GEN_K = 8;
-__global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st) {
+//
+// FUSED: lane 0 then updates the owner (the fused kernel's update, with the
+// run state that kernel saw at its start) and claims its record.
+template <bool FUSED>
+__global__ void __launch_bounds__(128) k_fast_forces_generic(DevStatus *st, int step) {
     const FastArgs &a = cA;
-    if (st->abort != 0) return;
+    const bool dead = FUSED ? *a.gen_dead != 0 : st->abort != 0;
+    if (!FUSED && dead) return;
     const int cnt = *a.gen_count;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
     const int lane = threadIdx.x & 31;
@@ -577,6 +764,10 @@ __global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st
          q += (gridDim.x * blockDim.x) >> 5) {
         const int t = a.gen[q];
         const float4 me = __ldg(rec + t);
+        if (FUSED && dead) {  // an earlier step failed: the record stays as it is
+            if (lane == 0) generic_claim(a, st, step, me, 0.0, 0.0, true, q);
+            continue;
+        }
         const double x = (double)me.x, y = (double)me.y;
         const int cx = cell_axis_fast(x, a.g.lo0, a.eff0, n0);
         const int cy = cell_axis_fast(y, a.g.lo1, a.eff1, n1);
@@ -628,9 +819,12 @@ __global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st
             }
         }
         if (__any_sync(0xffffffffu, over)) {
-            if (lane == 0)
-                a.force[t] = ring_forces_generic(rec, a.starts, t, me.x, me.y, x, y, cx, cy, n0,
-                                                 n1, pr);
+            if (lane == 0) {
+                const double2 fr = ring_forces_generic(rec, a.starts, t, me.x, me.y, x, y, cx, cy,
+                                                       n0, n1, pr);
+                if (FUSED) generic_claim(a, st, step, me, fr.x, fr.y, false, q);
+                else a.force[t] = fr;
+            }
             continue;
         }
         double fx = 0.0, fy = 0.0;
@@ -648,7 +842,10 @@ __global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st
                 }
             }
         }
-        if (lane == 0) a.force[t] = make_double2(fx, fy);
+        if (lane == 0) {
+            if (FUSED) generic_claim(a, st, step, me, fx, fy, false, q);
+            else a.force[t] = make_double2(fx, fy);
+        }
     }
 }
 
@@ -657,18 +854,6 @@ __global__ void __launch_bounds__(128) k_fast_forces_generic(const DevStatus *st
 #ifndef CS_UPDATE_MINB
 #define CS_UPDATE_MINB 4  // measured with the bucket claims: 4: 320 us, 5: 327 (spills), 6: 380
 #endif
-// store a record at its claimed bucket slot (or flag the overflow)
-__device__ __forceinline__ void claim_store(const FastArgs &a, DevStatus *st, int step, int b,
-                                            int slot, float4 out) {
-    if (slot < a.cap) {
-        reinterpret_cast<float4 *>(a.region)[(long long)b * a.cap + slot] = out;
-    } else {
-        atomicMin(&st->key, err_key(3, b / SUBB, CS_SORT_OVERFLOW));
-        st->abort = 1;
-        st->step = step;
-    }
-}
-
 // slab mode: a record for another rank (a migrant to the owner of its new
 // row, or a ghost copy for a neighbour of that owner); a ghost for this rank
 // itself is claimed here directly
@@ -715,8 +900,6 @@ k_fast_update(DevStatus *st, int step) {
     const FastArgs &a = cA;
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.gen_count = 0;  // k_fast_forces_generic has run
     const bool dead = st->abort != 0;
-    const int m = a.gg.n * a.gg.n;
-    const int n0 = a.g.n0, n1 = a.g.n1;
     const float4 *__restrict__ rec = reinterpret_cast<const float4 *>(a.rec);
     // the bucket claim of one iteration is consumed (record stored at its
     // slot) in the next, after that iteration's loads are in flight: the
@@ -746,23 +929,7 @@ k_fast_update(DevStatus *st, int step) {
         const float4 mer = __ldcs(rec + t);
         double2 f = make_double2(0.0, 0.0);
         if (a.interact) f = __ldcs(a.force + t);
-        const float xf = mer.x, yf = mer.y;
-        const unsigned meta = __float_as_uint(mer.z);
-        const unsigned wbits = __float_as_uint(mer.w);
-        const double x = (double)xf, y = (double)yf;
-        const int ti = (int)(meta >> 31);
-        const unsigned id = meta & ID_MASK;
-        // the particle's increment: xi[id] (the reference's layout: a random
-        // gather, kept in L2 by evict_last), or xi[slot] in performance mode
-        // (xi_by_slot: a coalesced stream)
-        float2 z;
-        if (a.xi_slot)
-            z = __ldcs(reinterpret_cast<const float2 *>(a.xi) + t);
-        else if (a.debug & 1)
-            z = __ldg(reinterpret_cast<const float2 *>(a.xi) + id);
-        else
-            z = ld_evict_last(reinterpret_cast<const float2 *>(a.xi) + id);
-        const double fx = f.x, fy = f.y;  // zero without interactions
+        const UpdIn u = upd_load(a, mer, t, dead);
 #if CS_CLAIM_AGG
         if (p_have) {
             const int basev = __shfl_sync(0xffffffffu, p_ret, p_leader);
@@ -771,86 +938,8 @@ k_fast_update(DevStatus *st, int step) {
 #else
         if (p_b >= 0) claim_store(a, st, step, p_b, p_slot, p_out);
 #endif
-        const int pinned = ti ? a.chi_pinned[1] : a.chi_pinned[0];
-        const bool do_drift = a.refresh && !dead && !pinned;
-        float2 v00 = make_float2(0.f, 0.f), v10 = v00, v01 = v00, v11 = v00;
-        double bf0 = 0.0, bf1 = 0.0;
-        if (do_drift) {
-            const Cic bst = cic_stencil(x, y, a.gg, a.gd0, a.gd1);
-            bf0 = bst.f0;
-            bf1 = bst.f1;
-            const float2 *g2 = reinterpret_cast<const float2 *>(a.grad);
-            v00 = __ldg(g2 + bst.i00);
-            v10 = __ldg(g2 + bst.i10);
-            v01 = __ldg(g2 + bst.i01);
-            v11 = __ldg(g2 + bst.i11);
-        }
-        // ---- drift refresh at the start-of-step position (coupling.py:302-325)
-        const double chi = ti ? a.chi[1] : a.chi[0];
-        double dr0 = 0.0, dr1 = 0.0;
-        if (do_drift) {
-            Cic b;  // bilinear weights (coupling.py:251-254) from the kept offsets
-            const double g0 = dsub(1.0, bf0), g1 = dsub(1.0, bf1);
-            b.w00 = dmul(g0, g1);
-            b.w10 = dmul(bf0, g1);
-            b.w01 = dmul(g0, bf1);
-            b.w11 = dmul(bf0, bf1);
-            dr0 = dadd(dadd(dadd(dmul(b.w00, (double)v00.x), dmul(b.w10, (double)v10.x)),
-                            dmul(b.w01, (double)v01.x)),
-                       dmul(b.w11, (double)v11.x));
-            dr1 = dadd(dadd(dadd(dmul(b.w00, (double)v00.y), dmul(b.w10, (double)v10.y)),
-                            dmul(b.w01, (double)v01.y)),
-                       dmul(b.w11, (double)v11.y));
-            if (chi != 1.0) {
-                dr0 = dmul(dr0, chi);
-                dr1 = dmul(dr1, chi);
-            }
-        }
-        // ---- EM proposal (motion.py:281-282)
-        const double amp = ti ? a.amp[1] : a.amp[0];
-        double v0 = dadd(dadd(dadd(x, dmul(amp, (double)z.x)), dmul(dr0, a.dt)), dmul(fx, a.dt));
-        double v1 = dadd(dadd(dadd(y, dmul(amp, (double)z.y)), dmul(dr1, a.dt)), dmul(fy, a.dt));
-        int w0 = (short)(wbits & 0xffffu), w1 = (short)(wbits >> 16);
-        bool ok = !dead && live;
-        if (ok && !(isfinite(v0) && isfinite(v1))) {
-            atomicMin(&st->key, err_key(0, id, CS_NONFINITE));
-            st->abort = 1;
-            st->step = step;
-            ok = false;
-        }
-        if (ok) {
-            const double r0 = v0, r1 = v1;
-            int code = boundary_axis_wraps(v0, w0, a.dom.lo[0], a.dom.hi[0], a.sz0,
-                                           a.dom.periodic[0]);
-            int ax = 0;
-            if (!code) {
-                code = boundary_axis_wraps(v1, w1, a.dom.lo[1], a.dom.hi[1], a.sz1,
-                                           a.dom.periodic[1]);
-                ax = 1;
-            }
-            if (code) {
-                atomicMin(&st->key, err_key(1 + ax, id, code));
-                st->abort = 1;
-                st->step = step;
-                if (ax == 0) v0 = r0;  // the raw proposal stays visible for the message
-                else v1 = r1;
-                ok = false;
-            }
-        }
-        float4 out;
-        if (dead) {
-            out = mer;
-        } else {
-            out.x = (float)v0;
-            out.y = (float)v1;
-            out.z = mer.z;
-            out.w = __uint_as_float(((unsigned)(w1 & 0xffff) << 16) | (unsigned)(w0 & 0xffff));
-        }
-        // ---- bin the stored (binary32) coordinate for the next step (cell
-        // histogram: a reduction, no value returned)
-        const double nx = (double)out.x, ny = (double)out.y;
-        const int cyn = cell_axis_fast(ny, a.g.lo1, a.eff1, n1);
-        const int key = cyn * n0 + cell_axis_fast(nx, a.g.lo0, a.eff0, n0);
+        int key, cyn;
+        const float4 out = upd_finish(a, st, step, mer, u, f.x, f.y, dead, live, key, cyn);
 #if CS_CLAIM_AGG
         bool claim = live;
         if (SLAB && live && !dead) claim = slab_route(a, st, step, out, key, cyn, lane);
@@ -1448,7 +1537,7 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     CS_TRY(f->rec[1].ensure(nr));
     CS_TRY(f->region.ensure(sizeof(Rec) * (size_t)f->nbucket * SUBB * (size_t)f->cap));
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
-    CS_TRY(f->gen.ensure(sizeof(int) * (size_t)(n + 1 > 1 ? n + 1 : 2)));  // list + counter
+    CS_TRY(f->gen.ensure(sizeof(int) * (size_t)(n + 2)));  // counter, run state, list
     CS_CUDA(cudaMemset(f->gen.p, 0, f->gen.bytes));
     CS_TRY(f->depflag.ensure(sizeof(int) * 2));  // exact-deposit flags by step parity
     CS_CUDA(cudaMemset(f->depflag.p, 0, f->depflag.bytes));
@@ -1634,6 +1723,15 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
     return CS_OK;
 }
 
+// The fused force + update kernel (k_fast_forces<true>): interacting
+// particles, one domain (slab mode keeps the split kernels).  CS_FUSED=0/1
+// overrides the default.
+bool fast_fused(const cs_fast *f, const cs_sim_params &p) {
+    if (p.interaction != 1 || f->slab) return false;
+    const char *e = getenv("CS_FUSED");
+    return e ? atoi(e) != 0 : false;
+}
+
 // part: 1 = pair forces, 2 = update (drift, EM, boundaries, binning)
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
                    const void *xi, DevStatus *st, int step, int part) {
@@ -1647,7 +1745,8 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.cap = f->cap;
     a.force = f->force.as<double2>();
     a.gen_count = f->gen.as<int>();
-    a.gen = f->gen.as<int>() + 1;
+    a.gen_dead = f->gen.as<int>() + 1;
+    a.gen = f->gen.as<int>() + 2;
     {
         const char *dbg = getenv("CS_FAST_DEBUG");
         a.debug = dbg ? atoi(dbg) : 0;
@@ -1697,10 +1796,14 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.out_dest = f->slab ? f->out_dest.as<int>() : nullptr;
     a.out_count = f->slab ? f->out_count.as<int>() : nullptr;
     a.out_cap = f->out_cap;
+    const bool fused = fast_fused(f, p);
     if (n > 0) {
-        static int resident = 0;  // blocks of k_fast_forces resident per SM
+        static int resident_s[2] = {0, 0};  // blocks of k_fast_forces resident per SM
+        int &resident = resident_s[fused ? 1 : 0];
         if (!resident) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_fast_forces, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &resident, fused ? (const void *)k_fast_forces<true> : (const void *)k_fast_forces<false>, 128,
+                0);
             if (resident < 1) resident = 1;
         }
         int sms = 148;
@@ -1715,10 +1818,20 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         if (part & 1)  // the update reuses the forces' constant block
             CS_CUDA(cudaMemcpyToSymbolAsync(cA, &a, sizeof(FastArgs), 0,
                                             cudaMemcpyHostToDevice, ctx->stream));
-        if (a.interact && (part & 1)) {
-            k_fast_forces<<<grid, 128, 0, ctx->stream>>>(st);
+        if (fused && (part & 1)) {  // forces + update; part 2 has nothing left to do
+            k_fast_forces<true><<<grid, 128, 0, ctx->stream>>>(st, step);
             CS_LAUNCH_CHECK();
-            k_fast_forces_generic<<<sms * 16, 128, 0, ctx->stream>>>(st);
+            k_fast_forces_generic<true><<<sms * 16, 128, 0, ctx->stream>>>(st, step);
+            CS_LAUNCH_CHECK();
+            CS_CUDA(cudaMemsetAsync(a.gen_count, 0, sizeof(int), ctx->stream));
+            ctx->launches += 2;
+            return CS_OK;
+        }
+        if (fused && (part & 2)) return CS_OK;
+        if (a.interact && (part & 1)) {
+            k_fast_forces<false><<<grid, 128, 0, ctx->stream>>>(st, step);
+            CS_LAUNCH_CHECK();
+            k_fast_forces_generic<false><<<sms * 16, 128, 0, ctx->stream>>>(st, step);
             CS_LAUNCH_CHECK();
             ctx->launches += 2;
         }

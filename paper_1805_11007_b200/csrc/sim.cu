@@ -64,6 +64,7 @@ int fast_field(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state
                DevStatus *st, int step);
 int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_state *s,
                    const void *xi, DevStatus *st, int step, int part);
+bool fast_fused(const cs_fast *f, const cs_sim_params &p);
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
                 const unsigned char bits[3], int part, DevStatus *st, int step);
 bool fast_imported(const cs_fast *f);
@@ -498,7 +499,8 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         }
         // fork/join of the field solve (skipped while profiling, so that the
         // stage times stay additive)
-        const bool ov = p.field_active && sim->overlap && !sim->profiling;
+        const bool ov = p.field_active && sim->overlap && !sim->profiling &&
+                        !fast_fused(sim->fast, p);  // the fused update needs the gradient
         if (ov) CS_TRY(sim->ensure_side());
         c.overlap = ov ? 1 : 0;
         for (int kk = 0; kk < k; kk++) {

@@ -462,6 +462,7 @@ struct cs_field_ops {
     int kind = 0;  // 0 identity, 1 dct, 2 fft
     double dt = 0, d_c = 0;
     double *F = nullptr, *Inv = nullptr, *E = nullptr, *T1 = nullptr, *T2 = nullptr;
+    double *FT = nullptr, *InvT = nullptr;  // transposes (grids <= 128^2: k_gemm_rows2)
     double *lx = nullptr, *ly = nullptr;
     void *rhs = nullptr;   // G (fft / identity) or double (dct)
     void *spec = nullptr;  // complex n x (n/2+1) (cuFFT path)

@@ -441,6 +441,120 @@ k_gemm16(const double *__restrict__ A, const double *__restrict__ B, const doubl
     }
 }
 
+// Grids up to 128^2: two GEMMs of the modal solve per launch.  A block owns
+// ROWS2 rows r: P_r = L_r M (M staged whole in shared memory), then
+// out_r = (P_r N^T) * E_r with N^T = NT staged in the same buffer.  Each
+// output is the k-ordered fma chain from +0.0 of k_gemm / k_gemm16 (without
+// their zero padding), so the solve is unchanged; half the launches, and
+// no round trip of the intermediate through memory.
+constexpr int ROWS2 = 2;
+constexpr int ROWS2_MAX_N = 128;
+
+// one bulk copy (TMA engine) of `bytes` into shared memory, completing on
+// the mbarrier at `bar` (phase `ph`)
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
+                                          unsigned long long *bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(d), "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long *bar, unsigned ph) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W;\n}" ::"r"(b), "r"(ph)
+        : "memory");
+}
+
+template <class O>
+__global__ void __launch_bounds__(128)
+k_gemm_rows2(const double *__restrict__ L, const double *__restrict__ M,
+             const double *__restrict__ NT, const double *__restrict__ E, O *__restrict__ out,
+             int n) {
+    extern __shared__ __align__(16) double sm2[];
+    __shared__ unsigned long long bar;
+    double *Ms = sm2;                       // n * n
+    double *lrow = Ms + (size_t)n * n;      // [k][ROWS2]
+    double *prow = lrow + ROWS2 * n;        // [k][ROWS2]
+    const int r0 = blockIdx.x * ROWS2, c = threadIdx.x;
+    const unsigned bytes = (unsigned)(sizeof(double) * n * n);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&bar))
+                     : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        bulk_load(Ms, M, bytes, &bar);
+    }
+    for (int i = threadIdx.x; i < ROWS2 * n; i += blockDim.x) {
+        const int u = i / n, k = i - u * n, r = r0 + u;
+        lrow[k * ROWS2 + u] = r < n ? __ldg(L + (size_t)r * n + k) : 0.0;
+    }
+    __syncthreads();
+    bar_wait(&bar, 0);
+    double acc[ROWS2];
+#pragma unroll
+    for (int u = 0; u < ROWS2; u++) acc[u] = 0.0;
+    if (c < n) {
+#pragma unroll 4
+        for (int k = 0; k < n; k++) {
+            const double m = Ms[k * n + c];
+#pragma unroll
+            for (int u = 0; u < ROWS2; u++) acc[u] = fma(lrow[k * ROWS2 + u], m, acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < ROWS2; u++) prow[c * ROWS2 + u] = acc[u];
+    }
+    __syncthreads();  // every read of Ms done: reuse it for N^T
+    if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_load(Ms, NT, bytes, &bar);
+    }
+    bar_wait(&bar, 1);
+    if (c < n) {
+#pragma unroll
+        for (int u = 0; u < ROWS2; u++) acc[u] = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < n; k++) {
+            const double m = Ms[k * n + c];
+#pragma unroll
+            for (int u = 0; u < ROWS2; u++) acc[u] = fma(prow[k * ROWS2 + u], m, acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < ROWS2; u++) {
+            const int r = r0 + u;
+            if (r < n) {
+                double val = acc[u];
+                if (E) val *= E[(size_t)r * n + c];
+                out[(size_t)r * n + c] = (O)val;
+            }
+        }
+    }
+}
+
+template <class O>
+static int gemm_rows2(cs_ctx *ctx, const double *L, const double *M, const double *NT,
+                      const double *E, O *out, int n) {
+    const size_t smem = sizeof(double) * ((size_t)n * n + 2 * ROWS2 * (size_t)n);
+    static size_t set = 0;
+    if (smem > set) {
+        CS_CUDA(cudaFuncSetAttribute(k_gemm_rows2<double>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CS_CUDA(cudaFuncSetAttribute(k_gemm_rows2<float>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set = smem;
+    }
+    const int threads = (n + 31) / 32 * 32;
+    k_gemm_rows2<O><<<(n + ROWS2 - 1) / ROWS2, threads, smem, ctx->stream>>>(L, M, NT, E, out, n);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
+    return CS_OK;
+}
+
 template <class O>
 int gemm(cs_ctx *ctx, const double *A, const double *B, bool tb, const double *E, O *C, int n) {
     if (n <= 256) {
@@ -560,6 +674,18 @@ int field_ops_create(cs_ctx *ctx, int prec, const cs_grid *g, double d_c, double
         CS_CUDA(cudaMemcpy(ops->F, F.data(), m * 8, cudaMemcpyHostToDevice));
         CS_CUDA(cudaMemcpy(ops->Inv, Inv.data(), m * 8, cudaMemcpyHostToDevice));
         CS_CUDA(cudaMemcpy(ops->E, E.data(), m * 8, cudaMemcpyHostToDevice));
+        if (n <= ROWS2_MAX_N) {  // transposed copies for k_gemm_rows2
+            std::vector<double> FT(m), InvT(m);
+            for (int k = 0; k < n; k++)
+                for (int j = 0; j < n; j++) {
+                    FT[(size_t)j * n + k] = F[(size_t)k * n + j];
+                    InvT[(size_t)j * n + k] = Inv[(size_t)k * n + j];
+                }
+            CS_CUDA(cudaMalloc(&ops->FT, m * 8));
+            CS_CUDA(cudaMalloc(&ops->InvT, m * 8));
+            CS_CUDA(cudaMemcpy(ops->FT, FT.data(), m * 8, cudaMemcpyHostToDevice));
+            CS_CUDA(cudaMemcpy(ops->InvT, InvT.data(), m * 8, cudaMemcpyHostToDevice));
+        }
         return CS_OK;
     }
     // periodic: eigenvalues (2 cos(2 pi k / n) - 2) / h^2 of the circulant
@@ -592,7 +718,8 @@ void field_ops_destroy(cs_field_ops *ops) {
         cufftDestroy(ops->pf);
         cufftDestroy(ops->pi);
     }
-    for (void *p : {(void *)ops->F, (void *)ops->Inv, (void *)ops->E, (void *)ops->T1,
+    for (void *p : {(void *)ops->F, (void *)ops->Inv, (void *)ops->FT, (void *)ops->InvT,
+                    (void *)ops->E, (void *)ops->T1,
                     (void *)ops->T2, (void *)ops->lx, (void *)ops->ly, ops->rhs, ops->spec,
                     ops->specT, ops->tw})
         if (p) cudaFree(p);
@@ -613,6 +740,13 @@ int field_solve_rhs(cs_field_ops *ops, void *out) {
     if (ops->kind == 1) {
         // modal = E * (F X F^T); out = Inv modal Inv^T (field.py:166-167)
         const double *X = (const double *)ops->rhs;
+        if (ops->FT && n % 2 == 0 && !getenv("CS_GEMM16")) {
+            CS_TRY(gemm_rows2<double>(ctx, ops->F, X, ops->FT, ops->E, ops->T2, n));
+            if (ops->prec == CS_F64)
+                return gemm_rows2<double>(ctx, ops->Inv, ops->T2, ops->InvT, nullptr,
+                                          (double *)out, n);
+            return gemm_rows2<float>(ctx, ops->Inv, ops->T2, ops->InvT, nullptr, (float *)out, n);
+        }
         CS_TRY(gemm<double>(ctx, ops->F, X, false, nullptr, ops->T1, n));
         CS_TRY(gemm<double>(ctx, ops->T1, ops->F, true, ops->E, ops->T2, n));
         CS_TRY(gemm<double>(ctx, ops->Inv, ops->T2, false, nullptr, ops->T1, n));

@@ -181,6 +181,159 @@ k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,
     }
 }
 
+// the reference pair loop of one particle, summed (the rare fallback)
+template <class P>
+__device__ __noinline__ double2 pair_loop_sum(const P *__restrict__ pos,
+                                              const uint8_t *__restrict__ type,
+                                              const int *__restrict__ order,
+                                              const int *__restrict__ starts, BinGeom g,
+                                              PairTab pt, int i) {
+    double fx = 0.0, fy = 0.0;
+    pair_loop(pos, type, order, starts, g, pt, i, [&](int, double s, double dx0, double dx1) {
+        fx = dadd(fx, dmul(s, dx0));
+        fy = dadd(fy, dmul(s, dx1));
+    });
+    return make_double2(fx, fy);
+}
+
+// Small systems (cfg1: 10^4 particles) are latency-bound in k_soft_forces:
+// ~80 blocks, one lane per owner walking ~17 candidates in series.  Here
+// nine lanes share an owner, lane c9 walking ring cell c9 (three owners per
+// warp) and buffering its accepted pairs; the warp then evaluates all
+// buffered pair terms together, one per lane, and the owner's first lane
+// adds them cell by cell: candidate order, bitwise equal to k_soft_forces.
+// A cell with more than RING_K accepted pairs sends the owner through
+// pair_loop.
+constexpr int RING_K = 6;
+constexpr int RING_WARPS = 4;
+constexpr long long RING_MAX_N = 1 << 16;
+
+struct RingBuf {
+    double dx[27 * RING_K], dy[27 * RING_K], r2[27 * RING_K];  // lane-major: lane * RING_K + u
+    unsigned char tt[27 * RING_K];
+    unsigned char nt[32];
+    short base[33];  // exclusive prefix of nt over the lanes
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * RING_WARPS)
+k_soft_forces_ring(const int *__restrict__ order, const int *__restrict__ starts, long long n,
+                   BinGeom g, PairTab pt, double *__restrict__ out, const DevStatus *st,
+                   const P *__restrict__ spos, const uint8_t *__restrict__ stype,
+                   const P *__restrict__ pos, const uint8_t *__restrict__ type) {
+    if (st && st->abort) return;
+    __shared__ RingBuf bufs[RING_WARPS];
+    RingBuf &B = bufs[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / 9, c9 = lane - 9 * grp;  // grp 3: lanes 27-31, idle
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; 3 * w < n;
+         w += warps) {
+        const long long t = 3 * w + grp;
+        const bool live = grp < 3 && t < n;
+        int nt = 0;
+        bool over = false;
+        if (live) {
+            double xi, yi;
+            load2(spos, t, xi, yi);
+            const int ti = stype ? (int)stype[t] : 0;
+            const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
+            const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
+            const int o1 = c9 / 3 - 1, o0 = c9 % 3 - 1;
+            int g1 = cy + o1, g0 = cx + o0;
+            bool ok = true;
+            if (g.per1) {
+                if ((g.n1 == 1 && o1 != 0) || (g.n1 == 2 && o1 == 1)) ok = false;
+                g1 = g1 < 0 ? g1 + g.n1 : (g1 >= g.n1 ? g1 - g.n1 : g1);
+            } else if (g1 < 0 || g1 >= g.n1) {
+                ok = false;
+            }
+            if (g.per0) {
+                if ((g.n0 == 1 && o0 != 0) || (g.n0 == 2 && o0 == 1)) ok = false;
+                g0 = g0 < 0 ? g0 + g.n0 : (g0 >= g.n0 ? g0 - g.n0 : g0);
+            } else if (g0 < 0 || g0 >= g.n0) {
+                ok = false;
+            }
+            if (ok) {
+                const int f = g1 * g.n0 + g0;
+                const int kb = starts[f], ke = starts[f + 1];
+                for (int k = kb; k < ke; k++) {
+                    if (k == (int)t) continue;
+                    double xj, yj;
+                    load2(spos, k, xj, yj);
+                    double dx0 = dsub(xj, xi);
+                    double dx1 = dsub(yj, yi);
+                    if (g.per0) dx0 = df_min_image(dx0, g.size0);
+                    if (g.per1) dx1 = df_min_image(dx1, g.size1);
+                    const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                    const int tt = ti * 2 + (stype ? (int)stype[k] : 0);
+                    if (r2 > pt.cut2[tt] || r2 == 0.0) continue;
+                    if (nt == RING_K) {
+                        over = true;
+                        break;
+                    }
+                    const int q = lane * RING_K + nt;
+                    B.dx[q] = dx0;
+                    B.dy[q] = dx1;
+                    B.r2[q] = r2;
+                    B.tt[q] = (unsigned char)tt;
+                    nt++;
+                }
+            }
+        }
+        // exclusive prefix of the lanes' counts; the pairs are then evaluated
+        // one per lane (term written back over the lane's dx / dy slot)
+        int inc = nt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        B.nt[lane] = (unsigned char)nt;
+        B.base[lane] = (short)(inc - nt);
+        if (lane == 31) B.base[32] = (short)inc;
+        __syncwarp();
+        const int total = B.base[32];
+        for (int e = lane; e < total; e += 32) {
+            int lo = 0, hi = 26;  // the last lane with base <= e
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (B.base[mid] <= e) lo = mid;
+                else hi = mid - 1;
+            }
+            const int q = lo * RING_K + (e - B.base[lo]);
+            const double r2 = B.r2[q];
+            const double eps = pt.eps[B.tt[q]];
+            const double r = dsqrt(r2);
+            const double sc = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
+            B.dx[q] = dmul(sc, B.dx[q]);
+            B.dy[q] = dmul(sc, B.dy[q]);
+        }
+        const unsigned gmask = grp < 3 ? 0x1ffu << (9 * grp) : 0u;
+        const bool gover = (__ballot_sync(0xffffffffu, over) & gmask) != 0;
+        __syncwarp();
+        if (live && c9 == 0) {
+            const int i = order[t];
+            double fx = 0.0, fy = 0.0;
+            if (gover) {
+                const double2 f = pair_loop_sum(pos, type, order, starts, g, pt, i);
+                fx = f.x;
+                fy = f.y;
+            } else {
+                for (int c = 0; c < 9; c++) {
+                    const int m = B.nt[lane + c];
+                    for (int u = 0; u < m; u++) {
+                        fx = dadd(fx, B.dx[(lane + c) * RING_K + u]);
+                        fy = dadd(fy, B.dy[(lane + c) * RING_K + u]);
+                    }
+                }
+            }
+            reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
+        }
+        __syncwarp();
+    }
+}
+
 template <class P>
 __global__ void k_count_pairs(const P *__restrict__ pos, const uint8_t *__restrict__ type,
                               const int *__restrict__ order, const int *__restrict__ starts,
@@ -322,6 +475,23 @@ int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *ty
     const int *order = ctx->order.as<int>(), *starts = ctx->starts.as<int>();
     // bin_particles left the positions (and types) in cell order in ctx->spos / stype
     uint8_t *stype = type ? ctx->stype.as<uint8_t>() : nullptr;
+    static const int ring_env = getenv("CS_RING_FORCES") ? atoi(getenv("CS_RING_FORCES")) : -1;
+    const bool ring = ring_env >= 0 ? ring_env != 0 : n <= RING_MAX_N;
+    if (ring) {
+        const long long warps = (n + 2) / 3;
+        const int blocks = (int)((warps + RING_WARPS - 1) / RING_WARPS);
+        if (prec == CS_F64)
+            k_soft_forces_ring<double><<<blocks, 32 * RING_WARPS, 0, ctx->stream>>>(
+                order, starts, n, g, pt, out, st, ctx->spos.as<double>(), stype,
+                static_cast<const double *>(pos), type);
+        else
+            k_soft_forces_ring<float><<<blocks, 32 * RING_WARPS, 0, ctx->stream>>>(
+                order, starts, n, g, pt, out, st, ctx->spos.as<float>(), stype,
+                static_cast<const float *>(pos), type);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+        return CS_OK;
+    }
     if (prec == CS_F64)
         k_soft_forces<double><<<grid_for(n, B), B, 0, ctx->stream>>>(
             static_cast<const double *>(pos), type, order, starts, n, g, pt, out, st,

@@ -477,31 +477,53 @@ k_gemm_rows2(const double *__restrict__ L, const double *__restrict__ M,
              const double *__restrict__ NT, const double *__restrict__ E, O *__restrict__ out,
              int n) {
     extern __shared__ __align__(16) double sm2[];
-    __shared__ unsigned long long bar;
+    // one single-use barrier per half of M and of N^T: the first half of
+    // each phase runs while the second half lands, and N^T's first half
+    // streams into M's rows once every thread is past them
+    __shared__ unsigned long long bar[4];
     double *Ms = sm2;                       // n * n
     double *lrow = Ms + (size_t)n * n;      // [k][ROWS2]
     double *prow = lrow + ROWS2 * n;        // [k][ROWS2]
     const int r0 = blockIdx.x * ROWS2, c = threadIdx.x;
-    const unsigned bytes = (unsigned)(sizeof(double) * n * n);
+    const int h = n / 2;
+    const unsigned hb = (unsigned)(sizeof(double) * h * n);
+    const unsigned tb = (unsigned)(sizeof(double) * (n - h) * n);
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(&bar))
-                     : "memory");
+        for (int b = 0; b < 4; b++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&bar[b]))
+                         : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        bulk_load(Ms, M, bytes, &bar);
+        bulk_load(Ms, M, hb, &bar[0]);
+        bulk_load(Ms + (size_t)h * n, M + (size_t)h * n, tb, &bar[1]);
     }
     for (int i = threadIdx.x; i < ROWS2 * n; i += blockDim.x) {
         const int u = i / n, k = i - u * n, r = r0 + u;
         lrow[k * ROWS2 + u] = r < n ? __ldg(L + (size_t)r * n + k) : 0.0;
     }
     __syncthreads();
-    bar_wait(&bar, 0);
     double acc[ROWS2];
 #pragma unroll
     for (int u = 0; u < ROWS2; u++) acc[u] = 0.0;
-    if (c < n) {
+    const bool on = c < n;
+    bar_wait(&bar[0], 0);
+    if (on) {
 #pragma unroll 4
-        for (int k = 0; k < n; k++) {
+        for (int k = 0; k < h; k++) {
+            const double m = Ms[k * n + c];
+#pragma unroll
+            for (int u = 0; u < ROWS2; u++) acc[u] = fma(lrow[k * ROWS2 + u], m, acc[u]);
+        }
+    }
+    __syncthreads();  // M's first half consumed: N^T's first half goes there
+    if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_load(Ms, NT, hb, &bar[2]);
+    }
+    bar_wait(&bar[1], 0);
+    if (on) {
+#pragma unroll 4
+        for (int k = h; k < n; k++) {
             const double m = Ms[k * n + c];
 #pragma unroll
             for (int u = 0; u < ROWS2; u++) acc[u] = fma(lrow[k * ROWS2 + u], m, acc[u]);
@@ -509,17 +531,26 @@ k_gemm_rows2(const double *__restrict__ L, const double *__restrict__ M,
 #pragma unroll
         for (int u = 0; u < ROWS2; u++) prow[c * ROWS2 + u] = acc[u];
     }
-    __syncthreads();  // every read of Ms done: reuse it for N^T
+    __syncthreads();
     if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_load(Ms, NT, bytes, &bar);
+        bulk_load(Ms + (size_t)h * n, NT + (size_t)h * n, tb, &bar[3]);
     }
-    bar_wait(&bar, 1);
-    if (c < n) {
 #pragma unroll
-        for (int u = 0; u < ROWS2; u++) acc[u] = 0.0;
+    for (int u = 0; u < ROWS2; u++) acc[u] = 0.0;
+    bar_wait(&bar[2], 0);
+    if (on) {
 #pragma unroll 4
-        for (int k = 0; k < n; k++) {
+        for (int k = 0; k < h; k++) {
+            const double m = Ms[k * n + c];
+#pragma unroll
+            for (int u = 0; u < ROWS2; u++) acc[u] = fma(prow[k * ROWS2 + u], m, acc[u]);
+        }
+    }
+    bar_wait(&bar[3], 0);
+    if (on) {
+#pragma unroll 4
+        for (int k = h; k < n; k++) {
             const double m = Ms[k * n + c];
 #pragma unroll
             for (int u = 0; u < ROWS2; u++) acc[u] = fma(prow[k * ROWS2 + u], m, acc[u]);

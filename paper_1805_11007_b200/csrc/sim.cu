@@ -551,6 +551,8 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         return CS_OK;
     }
     // one step of the direct engine
+    if (p.field_active && p.interaction == 1 && sim->overlap && !sim->profiling)
+        CS_TRY(sim->ensure_side());
     auto one = [&](int kk) -> int {
         const int step = sim->steps_done + kk;
         const void *xik = (const char *)xi + (size_t)kk * (size_t)stride * es;
@@ -567,7 +569,22 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
             CS_TRY(bin_particles(ctx, p.prec, s->pos, n, sim->geom, s->type, &db, &dep_binned));
             binned = true;
         }
+        // the field chain (deposit, solve, gradient) only meets the pair
+        // forces at the update: it runs on the side stream concurrently
+        // (small systems leave most SMs idle in either)
+        const bool ovd = binned && sim->overlap && !sim->profiling && sim->side;
         if (p.field_active) {
+            cudaStream_t main = ctx->stream;
+            if (ovd) {
+                CS_CUDA(cudaEventRecord(sim->ev_fork, main));
+                CS_CUDA(cudaStreamWaitEvent(sim->side, sim->ev_fork, 0));
+                ctx->stream = sim->side;
+            }
+            struct Restore {
+                cs_ctx *c;
+                cudaStream_t s;
+                ~Restore() { c->stream = s; }
+            } restore{ctx, main};
             {
                 StageMark m(sim, CS_STAGE_DEPOSIT);
                 if (dep_binned)
@@ -595,6 +612,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 StageMark m(sim, CS_STAGE_GRADIENT);
                 CS_TRY(launch_gradient(ctx, p.prec, s->c, sim->gg, s->grad, st, step));
             }
+            if (ovd) CS_CUDA(cudaEventRecord(sim->ev_join, sim->side));
         }
         const double *force = nullptr;
         if (p.interaction == 1) {
@@ -635,6 +653,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         a.propose_only = p.interaction == 2;
         a.dom = p.domain;
         a.gg = sim->gg;
+        if (ovd && p.field_active) CS_CUDA(cudaStreamWaitEvent(ctx->stream, sim->ev_join, 0));
         if (n > 0) {
             StageMark m(sim, CS_STAGE_UPDATE);
             const int B = 256;

@@ -59,7 +59,7 @@ struct DevStatus {
     int abort;
     int step;
     int field_bad;
-    int pad;
+    unsigned blocks_done;     // gradient launches: blocks past their field checks
     long long clamped;
     long long neg_steps;
     double first_neg;
@@ -318,9 +318,23 @@ struct DepBin;
 int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const BinGeom &g,
                   const uint8_t *type = nullptr, const DepBin *dep = nullptr,
                   bool *dep_done = nullptr);
+// the implicit solve's right-hand side c (1 - dt gamma) + dt ka rho_a -
+// dt kb rho_b c (field.py:226-232), fused into the deposit gather of a
+// DCT-solved grid (rhs in binary64)
+struct RhsCoef {
+    double one_m_dtg, dka, dkb;
+    int has_g, has_a, has_b;
+};
+RhsCoef make_rhs_coef(double dt, double ka, double kb, double gamma);
+struct RhsFuse {
+    const void *c;  // grid dtype
+    RhsCoef k;
+    double *rhs;
+};
 int launch_deposit_binned(cs_ctx *ctx, int prec, const GridGeom &gg, int kind, double h,
                           double cutoff, const int *starts, int off, void *ra, void *rb,
-                          const DevStatus *st);
+                          const DevStatus *st,
+                          const RhsFuse *rf = nullptr);
 int exclusive_scan_i32(cs_ctx *ctx, const int *in, int *out, long long n,
                        int *zero_in = nullptr);
 // forces.cu

@@ -132,11 +132,14 @@ k_dep_gather_cic(const int *__restrict__ starts, int off, const P *__restrict__ 
 // The same sums with four lanes per node, lane q summing corner pass q of
 // its node; the node's first lane then adds the passes in order 0..3 (as
 // k_dep_gather_cic): 4x the threads, a quarter of the serial chain each.
-template <class P, class G>
+// RHS: the node's rhs of the implicit solve as well (k_rhs's arithmetic on
+// the stored densities).
+template <class P, class G, bool RHS>
 __global__ void __launch_bounds__(128)
 k_dep_gather_cic4(const int *__restrict__ starts, int off, const P *__restrict__ spos,
                   const unsigned *__restrict__ meta, GridGeom gg, G *__restrict__ ra,
-                  G *__restrict__ rb, const DevStatus *st) {
+                  G *__restrict__ rb, const DevStatus *st, const G *__restrict__ c,
+                  RhsCoef rk, double *__restrict__ rhs) {
     if (st && st->abort) return;
     const int n = gg.n;
     const long long m4 = 4LL * n * n;
@@ -185,8 +188,16 @@ k_dep_gather_cic4(const int *__restrict__ starts, int off, const P *__restrict__
             }
         }
         if (q == 0 && g < m4) {
-            ra[l] = (G)sa;
-            rb[l] = (G)sb;
+            const G ga = (G)sa, gb = (G)sb;
+            ra[l] = ga;
+            rb[l] = gb;
+            if (RHS) {
+                const double cv = (double)c[l];
+                double r = rk.has_g ? dmul(cv, rk.one_m_dtg) : cv;
+                if (rk.has_a) r = dadd(r, dmul(rk.dka, (double)ga));
+                if (rk.has_b) r = dsub(r, dmul(dmul((double)gb, cv), rk.dkb));
+                rhs[l] = r;
+            }
         }
     }
 }
@@ -307,15 +318,19 @@ bool gauss_too_wide(const GridGeom &gg, double cutoff) {
 template <class P, class G>
 static int dep_gather_t(cs_ctx *ctx, const int *starts, int off, const P *spos,
                         const unsigned *meta, const GridGeom &gg, int kind, double h,
-                        double cutoff, G *ra, G *rb, const DevStatus *st) {
+                        double cutoff, G *ra, G *rb, const DevStatus *st,
+                        const RhsFuse *rf = nullptr) {
     const long long nb = (long long)gg.n * gg.n;
     if (kind == CS_CIC) {
-        if (getenv("CS_DEP_GATHER1"))
+        if (rf)
+            k_dep_gather_cic4<P, G, true><<<grid_for(4 * nb, 128), 128, 0, ctx->stream>>>(
+                starts, off, spos, meta, gg, ra, rb, st, (const G *)rf->c, rf->k, rf->rhs);
+        else if (getenv("CS_DEP_GATHER1"))
             k_dep_gather_cic<P, G><<<grid_for(nb, 256), 256, 0, ctx->stream>>>(
                 starts, off, spos, meta, gg, ra, rb, st);
         else
-            k_dep_gather_cic4<P, G><<<grid_for(4 * nb, 128), 128, 0, ctx->stream>>>(
-                starts, off, spos, meta, gg, ra, rb, st);
+            k_dep_gather_cic4<P, G, false><<<grid_for(4 * nb, 128), 128, 0, ctx->stream>>>(
+                starts, off, spos, meta, gg, ra, rb, st, nullptr, RhsCoef{}, nullptr);
     } else {
         const GaussParams gp = make_gauss(gg, h, cutoff);
         k_dep_gather_gauss<P, G><<<grid_for(nb, 128), 128, 0, ctx->stream>>>(
@@ -331,14 +346,14 @@ static int dep_gather_t(cs_ctx *ctx, const int *starts, int off, const P *spos,
 // their slots are numbered from n (off = n).
 int launch_deposit_binned(cs_ctx *ctx, int prec, const GridGeom &gg, int kind, double h,
                           double cutoff, const int *starts, int off, void *ra, void *rb,
-                          const DevStatus *st) {
+                          const DevStatus *st, const RhsFuse *rf) {
     if (prec == CS_F64)
         return dep_gather_t<double, double>(ctx, starts, off, ctx->dep_pos.as<double>(),
                                             ctx->dep_meta.as<unsigned>(), gg, kind, h, cutoff,
-                                            (double *)ra, (double *)rb, st);
+                                            (double *)ra, (double *)rb, st, rf);
     return dep_gather_t<float, float>(ctx, starts, off, ctx->dep_pos.as<float>(),
                                       ctx->dep_meta.as<unsigned>(), gg, kind, h, cutoff,
-                                      (float *)ra, (float *)rb, st);
+                                      (float *)ra, (float *)rb, st, rf);
 }
 
 template <class P, class G>

@@ -73,15 +73,48 @@ D1Coef make_d1(double h) {
 
 // grad = (d1x c, d1y c); when st != NULL also the step_field post-checks on
 // c: any non-finite node and the weighted mass of the negative nodes.
+// Serial epilogue of the field checks of one step (after every block's
+// atomics): a non-finite node stops the run, a negative weighted mass is
+// counted.
+__device__ __forceinline__ void field_finish_body(DevStatus *st, int step) {
+    volatile DevStatus *v = st;
+    if (v->abort) return;
+    if (v->field_bad) {
+        st->key = err_key(0, 0, CS_FIELD_NONFINITE);
+        st->abort = 1;
+        st->step = step;
+    }
+    if (v->neg_flag && v->neg_mass < -1e-12) {
+        if (v->neg_steps == 0) st->first_neg = v->neg_mass;
+        st->neg_steps = v->neg_steps + 1;
+    }
+    st->neg_flag = 0;
+    st->neg_mass = 0.0;
+}
+
+// thread 0 of every block of a gradient launch, after its block's atomics:
+// the last block to arrive runs the epilogue (step >= 0) and re-arms the
+// counter
+__device__ __forceinline__ void field_checks_arrive(DevStatus *st, int step) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->blocks_done, 1u);
+    if (prev + 1 == gridDim.x) {
+        __threadfence();
+        if (step >= 0) field_finish_body(st, step);
+        st->blocks_done = 0;
+    }
+}
+
 template <class G>
 __global__ void __launch_bounds__(256)
 k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double wcell,
-           G *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q) {
-    if (st && st->abort) return;
+           G *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q, int step) {
+    const bool dead = st && st->abort;
     const long long m = (long long)n * n;
     double neg = 0.0;
     int bad = 0, anyneg = 0;
     // rows j = blockIdx.x + k gridDim.x; threads stride along the row
+    if (!dead)
     for (int j = blockIdx.x; j < n; j += gridDim.x)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const long long l = (long long)j * n + i;
@@ -134,6 +167,7 @@ k_gradient(const G *__restrict__ c, int n, int per, D1Coef kx, D1Coef ky, double
             atomicAdd(&st->neg_mass, t);
             atomicExch(&st->neg_flag, 1);
         }
+        field_checks_arrive(st, step);
     }
 }
 
@@ -150,16 +184,17 @@ __device__ __forceinline__ double d1_per(double cm, double cp, bool wrapped, con
 
 __global__ void __launch_bounds__(256)
 k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double wcell,
-                float *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q,
+                float *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q, int step,
                 int jbase = 0, int jrows = -1, int own0 = 0, int own1 = 1 << 30) {
     // (slab mode: the rows jbase .. jbase + jrows - 1 (mod n); the field checks
     // count the own rows [own0, own1) only)
-    if (st->abort) return;
+    const bool dead = st->abort != 0;
     const long long m = (long long)n * n;
     const int n4 = n >> 2;
     double neg = 0.0;
     int bad = 0, anyneg = 0;
     if (jrows < 0) jrows = n;
+    if (dead) jrows = 0;
     for (int jj = blockIdx.x; jj < jrows; jj += gridDim.x) {
         int j = (jbase + jj) % n;
         if (j < 0) j += n;
@@ -223,24 +258,10 @@ k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double
             atomicAdd(&st->neg_mass, tsum);
             atomicExch(&st->neg_flag, 1);
         }
+        field_checks_arrive(st, step);
     }
 }
 
-// Serial epilogue of the field checks of one step.
-__global__ void k_field_finish(DevStatus *st, int step) {
-    if (st->abort) return;
-    if (st->field_bad) {
-        st->key = err_key(0, 0, CS_FIELD_NONFINITE);
-        st->abort = 1;
-        st->step = step;
-    }
-    if (st->neg_flag && st->neg_mass < -1e-12) {
-        if (st->neg_steps == 0) st->first_neg = st->neg_mass;
-        st->neg_steps += 1;
-    }
-    st->neg_flag = 0;
-    st->neg_mass = 0.0;
-}
 
 // slab mode (periodic binary32 grids): the gradient of the grid rows
 // jbase .. jbase + jrows - 1 (mod n) from c rows one wider on either side;
@@ -254,12 +275,10 @@ int launch_gradient_rows(cs_ctx *ctx, const float *c, const GridGeom &gg, float 
     const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
     const int g2 = jrows < 148 * 8 ? jrows : 148 * 8;
     k_gradient_per4<<<g2 > 0 ? g2 : 1, 256, 0, ctx->stream>>>(c, gg.n, kx, ky, gg.d0 * gg.d1,
-                                                              grad, st, nullptr, jbase, jrows,
-                                                              own0, own1);
+                                                              grad, st, nullptr, step, jbase,
+                                                              jrows, own0, own1);
     CS_LAUNCH_CHECK();
-    k_field_finish<<<1, 1, 0, ctx->stream>>>(st, step);
-    CS_LAUNCH_CHECK();
-    ctx->launches += 2;
+    ctx->launches += 1;
     return CS_OK;
 }
 
@@ -270,30 +289,32 @@ int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, vo
     const double wcell = gg.d0 * gg.d1;
     const int B = 256;
     const int g2 = gg.n < 148 * 8 ? gg.n : 148 * 8;
+    // (the field-check epilogue runs in the launch's last block, step >= 0)
     if (prec == CS_F64)
         k_gradient<double><<<g2, B, 0, ctx->stream>>>(
-            (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st, zero_q);
+            (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st, zero_q, step);
     else if (gg.per && st && gg.n % 4 == 0 && gg.n >= 8 && !getenv("CS_GRAD_GENERIC"))
         k_gradient_per4<<<g2, B, 0, ctx->stream>>>((const float *)c, gg.n, kx, ky, wcell,
-                                                  (float *)grad, st, zero_q);
+                                                  (float *)grad, st, zero_q, step);
     else
         k_gradient<float><<<g2, B, 0, ctx->stream>>>(
-            (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st, zero_q);
+            (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st, zero_q, step);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
-    if (st && step >= 0) {
-        k_field_finish<<<1, 1, 0, ctx->stream>>>(st, step);
-        CS_LAUNCH_CHECK();
-        ctx->launches += 1;
-    }
     return CS_OK;
 }
 
 // ------------------------------------------------------------------ rhs
-struct RhsCoef {
-    double one_m_dtg, dka, dkb;
-    int has_g, has_a, has_b;
-};
+RhsCoef make_rhs_coef(double dt, double ka, double kb, double gamma) {
+    RhsCoef k;
+    k.has_g = gamma != 0.0;
+    k.has_a = ka != 0.0;
+    k.has_b = kb != 0.0;
+    k.one_m_dtg = 1.0 - dt * gamma;
+    k.dka = dt * ka;
+    k.dkb = dt * kb;
+    return k;
+}
 
 template <class G, class R>
 __global__ void k_rhs(const G *__restrict__ c, const G *__restrict__ ra, const G *__restrict__ rb,
@@ -825,13 +846,7 @@ int field_rhs(cs_field_ops *ops, const void *c, const void *ra, const void *rb, 
               double kb, double gamma, const DevStatus *st) {
     cs_ctx *ctx = ops->ctx;
     const double dt = ops->dt;
-    RhsCoef k;
-    k.has_g = gamma != 0.0;
-    k.has_a = ka != 0.0;
-    k.has_b = kb != 0.0;
-    k.one_m_dtg = 1.0 - dt * gamma;
-    k.dka = dt * ka;
-    k.dkb = dt * kb;
+    const RhsCoef k = make_rhs_coef(dt, ka, kb, gamma);
     const long long m = (long long)ops->gg.n * ops->gg.n;
     const int B = 256;
     const int G = grid_for(m, B, 148 * 16);

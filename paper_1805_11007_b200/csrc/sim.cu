@@ -585,13 +585,22 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                 cudaStream_t s;
                 ~Restore() { c->stream = s; }
             } restore{ctx, main};
+            // a DCT-solved grid takes the solve's rhs from the CIC gather itself
+            const bool rhs_fused = dep_binned && p.deposit_kind == CS_CIC &&
+                                   sim->ops->kind == 1;
             {
                 StageMark m(sim, CS_STAGE_DEPOSIT);
+                RhsFuse rf;
+                if (rhs_fused) {
+                    rf.c = s->c;
+                    rf.k = make_rhs_coef(sim->ops->dt, p.k_alpha, p.k_beta, p.gamma);
+                    rf.rhs = (double *)sim->ops->rhs;
+                }
                 if (dep_binned)
                     CS_TRY(launch_deposit_binned(
                         ctx, p.prec, sim->gg, p.deposit_kind, p.kernel_h, p.kernel_cutoff,
                         ctx->starts.as<int>() + (size_t)sim->geom.n0 * sim->geom.n1, (int)n,
-                        s->rho_a, s->rho_b, st));
+                        s->rho_a, s->rho_b, st, rhs_fused ? &rf : nullptr));
                 else
                     CS_TRY(launch_deposit(ctx, p.prec, s->pos, s->type, n, sim->gg,
                                           p.deposit_kind, p.kernel_h, p.kernel_cutoff, sim->bits,
@@ -603,8 +612,9 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
                     CS_TRY(spectral_step_g(sim->ops, s->c, s->rho_a, s->rho_b, p.gamma,
                                            p.k_alpha, p.k_beta, st));
                 } else {
-                                    CS_TRY(field_rhs(sim->ops, s->c, s->rho_a, s->rho_b, p.k_alpha, p.k_beta,
-                                     p.gamma, st));
+                    if (!rhs_fused)
+                        CS_TRY(field_rhs(sim->ops, s->c, s->rho_a, s->rho_b, p.k_alpha,
+                                         p.k_beta, p.gamma, st));
                     CS_TRY(field_solve_rhs(sim->ops, s->c));
                 }
             }

@@ -106,6 +106,35 @@ def test_sorted_equals_direct_bitwise_clustered(periodic):
     assert torch.equal(sa["pos"], sb["pos"])
 
 
+@pytest.mark.parametrize("clustered", [False, True])
+def test_block_call_equals_single_step_calls_bitwise(clustered):
+    """One k-step call (the bench's timed region: the field solve forked to
+    the side stream every step) against k one-step calls: the same records,
+    anchors and field, bit for bit -- uniform and with cfg4-like clusters."""
+    rng = np.random.default_rng(21)
+    n, k = 150_000, 5
+    if clustered:
+        centres = -0.5 + rng.random((64, 2))
+        pos = centres[rng.integers(0, 64, n)] + 0.02 * rng.standard_normal((n, 2))
+        pos = (np.mod(pos + 0.5, 1.0) - 0.5).astype(np.float32)
+    else:
+        pos = (-0.5 + rng.random((n, 2))).astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    xi = torch.as_tensor(rng.standard_normal((k, n, 2)).astype(np.float32), device="cuda")
+    radii = (5e-4, 1e-3)
+    a, sa = _sim(pos, sp, engine="sorted", field=True, radii=radii)
+    b, sb = _sim(pos, sp, engine="sorted", field=True, radii=radii)
+    a.step(xi, k)
+    for j in range(k):
+        b.step(xi[j], 1)
+    a.export_state()
+    b.export_state()
+    assert a.status().code == 0 and b.status().code == 0
+    assert torch.equal(sa["pos"], sb["pos"])
+    assert torch.equal(sa["anchor"], sb["anchor"])
+    assert torch.equal(sa["c"], sb["c"])
+
+
 def test_sorted_engine_field_one_step_vs_oracle_and_deterministic():
     n, n_c = 40000, 256
     pos, sp, xi = _inputs(n, 2)

@@ -626,9 +626,10 @@ k_fast_forces(DevStatus *st, int step) {
                 }
             }
         }
-        // ---- 1. candidate walk (warp-uniform trip count)
+        // ---- 1. candidate walk (warp-uniform trip count): a prefilter hit
+        // goes into the lane's own column of the queue's slot array,
+        // ck[j * 32 + lane] = partner slot of the lane's j-th hit
         const int totmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
-        int qn = 0;  // queue length (warp-uniform)
         for (int j = 0; j < totmax; j += 2) {
             const int ka = k;
             if (++k == kend) {
@@ -652,22 +653,30 @@ k_fast_forces(DevStatus *st, int step) {
             const float cb = (__float_as_uint(qb.z) >> 31) ? cf1 : cf0;
             const bool ha = j < tot && ka != t32 && fmaf(dax, dax, day * day) <= ca;
             const bool hb = j + 1 < tot && kb != t32 && fmaf(dbx, dbx, dby * dby) <= cb;
-            const unsigned ma = __ballot_sync(0xffffffffu, ha && nacc < ACC_MAX);
-            if (ha && nacc < ACC_MAX) {
-                const int e = qn + __popc(ma & lt);
-                wq.ck[e] = ka;
-                wq.oj[e] = (unsigned short)(lane * ACC_MAX + nacc);
-            }
+            if (ha && nacc < ACC_MAX) wq.ck[nacc * 32 + lane] = ka;
             nacc += ha;
-            qn += __popc(ma);
-            const unsigned mb = __ballot_sync(0xffffffffu, hb && nacc < ACC_MAX);
-            if (hb && nacc < ACC_MAX) {
-                const int e = qn + __popc(mb & lt);
-                wq.ck[e] = kb;
-                wq.oj[e] = (unsigned short)(lane * ACC_MAX + nacc);
-            }
+            if (hb && nacc < ACC_MAX) wq.ck[nacc * 32 + lane] = kb;
             nacc += hb;
-            qn += __popc(mb);
+        }
+        // the hits compacted level by level into queue entries (in place:
+        // entry e <= j * 32 + lane, and a level is read before it is written),
+        // each tagged with the owner's term index lane * ACC_MAX + j
+        int qn = 0;  // queue length (warp-uniform)
+        {
+            const int nq = nacc < ACC_MAX ? nacc : ACC_MAX;
+            const int lev = (int)__reduce_max_sync(0xffffffffu, (unsigned)nq);
+            for (int j = 0; j < lev; j++) {
+                const bool has = j < nq;
+                const unsigned m = __ballot_sync(0xffffffffu, has);
+                const int kk = has ? wq.ck[j * 32 + lane] : 0;
+                __syncwarp();
+                if (has) {
+                    const int e = qn + __popc(m & lt);
+                    wq.ck[e] = kk;
+                    wq.oj[e] = (unsigned short)(lane * ACC_MAX + j);
+                }
+                qn += __popc(m);
+            }
         }
         if (nacc > ACC_MAX) generic = true;  // its queued terms are computed, not used
         if (generic) {

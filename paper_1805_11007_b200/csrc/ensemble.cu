@@ -388,13 +388,29 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
     if (a.field || a.refresh)
         for (int l = tid; l < m; l += NT) c[l] = a.c[(long long)m * s + l];
     if (tid == 0) s_abort = st->abort;
+    if (a.interact)
+        for (int f = tid; f <= a.ncell; f += NT) starts[f] = 0;
     long long clamped = 0;
     unsigned long long high_n = 0;
     double high = 0.0;
     __syncthreads();
+#ifdef CS_CTA_TIMING
+    __shared__ long long s_t[12];
+    long long t_last = clock64();
+    if (tid == 0) for (int q = 0; q < 12; q++) s_t[q] = 0;
+#define CS_TICK(i) do { if (tid == 0) { const long long now_ = clock64(); s_t[i] += now_ - t_last; t_last = now_; } } while (0)
+#else
+#define CS_TICK(i) do { } while (0)
+#endif
     for (int kk = 0; kk < a.k_steps; kk++) {
         if (s_abort) break;
         const int step = a.step0 + kk;
+        CS_TICK(0);
+        // this thread's first increment of the step, requested before the
+        // step's other phases (one global-memory latency off the EM phase)
+        const double *xk = a.xi + (long long)kk * a.xs + 2LL * n * s;
+        double2 xpre = make_double2(0.0, 0.0);
+        if (tid < n) xpre = *reinterpret_cast<const double2 *>(xk + 2 * tid);
         const GridGeom &gg = a.gg;
         const int nc = gg.n;
         if (a.field) {
@@ -488,8 +504,9 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         }
         // ---- cell list + pair forces (motion.py:170-245)
         if (a.interact) {
-            for (int f = tid; f <= a.ncell; f += NT) starts[f] = 0;
-            __syncthreads();
+            // (the cell counts were cleared before the first step and by the
+            // previous step's EM phase, which does not read the cell table)
+            CS_TICK(1);
             for (int p = tid; p < n; p += NT) {
                 const int k = cell_axis(pos[2 * p + 1], a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
                               cell_axis(pos[2 * p], a.g.lo0, a.g.eff0, a.g.n0);
@@ -497,6 +514,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 atomicAdd(&starts[k + 1], 1);
             }
             __syncthreads();
+            CS_TICK(2);
             {  // inclusive scan of starts[1..ncell] (the counts): a run of cells
                // per thread, then the block's run totals
                 const int per = (a.ncell + NT - 1) / NT;
@@ -522,13 +540,14 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 }
                 __syncthreads();
                 int acc = inc - run + (warp > 0 ? s_flag[warp - 1] : 0);
-                for (int f = f0; f < f1; f++) {
+                for (int f = f0; f < f1; f++) {  // starts[f] = first slot of cell f
                     acc += starts[f];
                     starts[f] = acc;
+                    if (f < a.ncell) cur[f] = acc;  // and its claim cursor
                 }
+                if (tid == 0) cur[0] = 0;
                 __syncthreads();
-                for (int f = tid; f < a.ncell; f += NT) cur[f] = starts[f];
-                __syncthreads();
+                CS_TICK(3);
             }
             {
                 // stable placement (ascending index inside a cell,
@@ -539,6 +558,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 int *slots = reinterpret_cast<int *>(frc);
                 for (int p = tid; p < n; p += NT) slots[atomicAdd(&cur[key[p]], 1)] = p;
                 __syncthreads();
+                CS_TICK(4);
                 for (int t = tid; t < n; t += NT) {
                     const int v = slots[t];
                     const int k = key[v];
@@ -549,19 +569,146 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 }
             }
             __syncthreads();
+            CS_TICK(5);
             if (a.thread_forces) {
                 // sparse systems (<= 2 particles per cell; the single-
-                // realisation CTA engine): one thread per particle walks its
-                // ring in the reference order (common.cuh pair_loop)
-                for (int i = tid; i < n; i += NT) {
+                // realisation CTA engine): a lane per particle walks its ring in
+                // the reference order (as common.cuh pair_loop) with the exact
+                // test only, keeping up to four accepted partners; the warp's
+                // accepted pairs are then evaluated one per lane (the binary64
+                // sqrt / exp / divisions on dense lanes instead of once per
+                // lane that happens to hold a pair) and every owner adds its
+                // terms in walk order.  All exchange is by shuffles.
+                const BinGeom &g = a.g;
+                const unsigned ltm = (1u << lane) - 1u;
+                for (int ib = warp * 32; ib < n; ib += NT) {
+                    const int i = ib + lane;
+                    const bool live = i < n;
+                    double xi = 0.0, yi = 0.0;
+                    int ti = 0, nacc = 0, pj0 = 0, pj1 = 0, pj2 = 0, pj3 = 0;
+                    if (live) {
+                        xi = pos[2 * i];
+                        yi = pos[2 * i + 1];
+                        ti = type[i] ? 1 : 0;
+                        const int cy = key[i] / g.n0, cx = key[i] - cy * g.n0;  // binned above
+                        auto candidate = [&](int k) {
+                            const int j = order[k];
+                            if (j == i) return;
+                            double dx0 = dsub(pos[2 * j], xi);
+                            double dx1 = dsub(pos[2 * j + 1], yi);
+                            if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
+                            if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
+                            const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                            const int t = ti * 2 + (type[j] ? 1 : 0);
+                            if (r2 > a.pt.cut2[t] || r2 == 0.0) return;
+                            if (nacc == 0) pj0 = j;
+                            else if (nacc == 1) pj1 = j;
+                            else if (nacc == 2) pj2 = j;
+                            else if (nacc == 3) pj3 = j;
+                            nacc++;
+                        };
+                        // the ring's cells of one row are consecutive in the
+                        // cell table unless the row wraps around a periodic
+                        // axis: one slot range per row, in the reference's
+                        // order (o0 ascending, ascending index inside a cell)
+                        const bool rows = !g.per0 || (g.n0 >= 3 && cx >= 1 && cx + 1 < g.n0);
+                        const int c0 = cx >= 1 ? cx - 1 : 0, c1 = cx + 1 < g.n0 ? cx + 1 : g.n0 - 1;
+                        for (int o1 = -1; o1 <= 1; o1++) {
+                            int g1 = cy + o1;
+                            if (g.per1) {
+                                if (g.n1 == 1 && o1 != 0) continue;
+                                if (g.n1 == 2 && o1 == 1) continue;
+                                g1 = (int)pymod(g1, g.n1);
+                            } else if (g1 < 0 || g1 >= g.n1) {
+                                continue;
+                            }
+                            if (rows) {
+                                const int kend = starts[g1 * g.n0 + c1 + 1];
+                                for (int k = starts[g1 * g.n0 + c0]; k < kend; k++) candidate(k);
+                                continue;
+                            }
+                            for (int o0 = -1; o0 <= 1; o0++) {
+                                int g0 = cx + o0;
+                                if (g.per0) {
+                                    if (g.n0 == 1 && o0 != 0) continue;
+                                    if (g.n0 == 2 && o0 == 1) continue;
+                                    g0 = (int)pymod(g0, g.n0);
+                                } else if (g0 < 0 || g0 >= g.n0) {
+                                    continue;
+                                }
+                                const int f = g1 * g.n0 + g0;
+                                const int kend = starts[f + 1];
+                                for (int k = starts[f]; k < kend; k++) candidate(k);
+                            }
+                        }
+                    }
+                    CS_TICK(8);
+                    const int nq = nacc < 4 ? nacc : 4;
+                    // entries level by level: (lane, s) -> b_s + its rank in level s
+                    const unsigned m0 = __ballot_sync(0xffffffffu, nq > 0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, nq > 1);
+                    const unsigned m2 = __ballot_sync(0xffffffffu, nq > 2);
+                    const unsigned m3 = __ballot_sync(0xffffffffu, nq > 3);
+                    const int b1 = __popc(m0), b2 = b1 + __popc(m1), b3 = b2 + __popc(m2);
+                    const int total = b3 + __popc(m3);
                     double fx = 0.0, fy = 0.0;
-                    pair_loop(pos, type, order, starts, a.g, a.pt, i,
-                              [&](int, double sc, double dx0, double dx1) {
-                                  fx = dadd(fx, dmul(sc, dx0));
-                                  fy = dadd(fy, dmul(sc, dx1));
-                              });
-                    frc[2 * i] = fx;
-                    frc[2 * i + 1] = fy;
+                    for (int r0 = 0; r0 < total; r0 += 32) {
+                        const int e = r0 + lane;
+                        const int lv = e >= b3 ? 3 : (e >= b2 ? 2 : (e >= b1 ? 1 : 0));
+                        const unsigned ml = lv == 3 ? m3 : (lv == 2 ? m2 : (lv == 1 ? m1 : m0));
+                        const int bl = lv == 3 ? b3 : (lv == 2 ? b2 : (lv == 1 ? b1 : 0));
+                        const int ow = e < total ? (int)__fns(ml, 0, e - bl + 1) : lane;
+                        const int q0 = __shfl_sync(0xffffffffu, pj0, ow);
+                        const int q1 = __shfl_sync(0xffffffffu, pj1, ow);
+                        const int q2 = __shfl_sync(0xffffffffu, pj2, ow);
+                        const int q3 = __shfl_sync(0xffffffffu, pj3, ow);
+                        const double xo = __shfl_sync(0xffffffffu, xi, ow);
+                        const double yo = __shfl_sync(0xffffffffu, yi, ow);
+                        const int to = __shfl_sync(0xffffffffu, ti, ow);
+                        double tx = 0.0, ty = 0.0;
+                        if (e < total) {
+                            const int j = lv == 3 ? q3 : (lv == 2 ? q2 : (lv == 1 ? q1 : q0));
+                            double dx0 = dsub(pos[2 * j], xo);
+                            double dx1 = dsub(pos[2 * j + 1], yo);
+                            if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
+                            if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
+                            const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                            const double eps = a.pt.eps[to * 2 + (type[j] ? 1 : 0)];
+                            const double rr = dsqrt(r2);
+                            const double sc = -ddiv(cs_exp(-ddiv(rr, eps)), dmul(eps, rr));
+                            tx = dmul(sc, dx0);
+                            ty = dmul(sc, dx1);
+                        }
+                        // owners take their terms in level (= walk) order
+#pragma unroll
+                        for (int s2 = 0; s2 < 4; s2++) {
+                            if ((s2 == 1 && !m1) || (s2 == 2 && !m2) || (s2 == 3 && !m3)) break;
+                            const unsigned mm = s2 == 3 ? m3 : (s2 == 2 ? m2 : (s2 == 1 ? m1 : m0));
+                            const int bb = s2 == 3 ? b3 : (s2 == 2 ? b2 : (s2 == 1 ? b1 : 0));
+                            const int src = bb + __popc(mm & ltm) - r0;
+                            const bool mine = s2 < nq && src >= 0 && src < 32;
+                            const double vx = __shfl_sync(0xffffffffu, tx, mine ? src : 0);
+                            const double vy = __shfl_sync(0xffffffffu, ty, mine ? src : 0);
+                            if (mine) {
+                                fx = dadd(fx, vx);
+                                fy = dadd(fy, vy);
+                            }
+                        }
+                    }
+                    CS_TICK(9);
+                    if (live) {
+                        if (nacc > 4) {  // more partners than kept: the plain loop
+                            fx = 0.0;
+                            fy = 0.0;
+                            pair_loop(pos, type, order, starts, a.g, a.pt, i,
+                                      [&](int, double sc, double dx0, double dx1) {
+                                          fx = dadd(fx, dmul(sc, dx0));
+                                          fy = dadd(fy, dmul(sc, dx1));
+                                      });
+                        }
+                        frc[2 * i] = fx;
+                        frc[2 * i + 1] = fy;
+                    }
                 }
             } else {
             // one warp per particle: the lanes test its ring candidates 32 at
@@ -678,19 +825,20 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             }
         }
         __syncthreads();
+        CS_TICK(6);
         // ---- Euler-Maruyama + boundaries (motion.py:268-282, 355-430)
-        const double *xk = a.xi + (long long)kk * a.xs + 2LL * n * s;
+        if (a.interact)  // the next step's cell counts
+            for (int f = tid; f <= a.ncell; f += NT) starts[f] = 0;
         for (int p = tid; p < n; p += NT) {
             const int t = type[p] ? 1 : 0;
             const double amp = a.amp[t];
+            const double z0 = p == tid ? xpre.x : xk[2 * p], z1 = p == tid ? xpre.y : xk[2 * p + 1];
             const double f0 = a.interact ? frc[2 * p] : 0.0, f1 = a.interact ? frc[2 * p + 1] : 0.0;
             double i0, i1;
             force_increment(f0, f1, a.dt, a.tamed, i0, i1);
             double v[2];
-            v[0] = dadd(dadd(dadd(pos[2 * p], dmul(amp, xk[2 * p])), dmul(drift[2 * p], a.dt)),
-                        i0);
-            v[1] = dadd(dadd(dadd(pos[2 * p + 1], dmul(amp, xk[2 * p + 1])),
-                             dmul(drift[2 * p + 1], a.dt)),
+            v[0] = dadd(dadd(dadd(pos[2 * p], dmul(amp, z0)), dmul(drift[2 * p], a.dt)), i0);
+            v[1] = dadd(dadd(dadd(pos[2 * p + 1], dmul(amp, z1)), dmul(drift[2 * p + 1], a.dt)),
                         i1);
             const double raw0 = v[0], raw1 = v[1];
             bool ok = isfinite(v[0]) && isfinite(v[1]);
@@ -715,6 +863,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             anc[2 * p + 1] = an[1];
         }
         __syncthreads();
+        CS_TICK(7);
         if (s_abort) break;
         // ---- fixed-step reactions (reactions.py:43-81)
         if (a.react) {
@@ -746,6 +895,13 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         }
     }
     __syncthreads();
+#ifdef CS_CTA_TIMING
+    if (tid == 0 && blockIdx.x == 0)
+        printf("cta timing (cycles/step): top %lld zero %lld count %lld scan %lld claim %lld rank %lld force %lld (walk %lld eval %lld) em %lld\n",
+               s_t[0] / a.k_steps, s_t[1] / a.k_steps, s_t[2] / a.k_steps, s_t[3] / a.k_steps,
+               s_t[4] / a.k_steps, s_t[5] / a.k_steps, s_t[6] / a.k_steps, s_t[8] / a.k_steps,
+               s_t[9] / a.k_steps, s_t[7] / a.k_steps);
+#endif
     for (int i = tid; i < 2 * n; i += NT) {
         a.pos[2 * n * s + i] = pos[i];
         a.anchor[2 * n * s + i] = anc[i];

@@ -15,6 +15,8 @@
 //                  cell's particles with a smaller index (ascending index
 //                  inside each cell, as the reference's stable sort)
 // The result is bit-identical to the reference's `order`/`starts`.
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -103,6 +105,141 @@ __global__ void k_seg_rank(const int *__restrict__ slots, const int *__restrict_
         spos[2 * (s + rank)] = pos[2 * (long long)v];
         spos[2 * (s + rank) + 1] = pos[2 * (long long)v + 1];
         if (type) stype[s + rank] = type[v];
+    }
+}
+
+// Mid-size systems (cfg1: 10^4 particles, 10^4 cells + 128^2 deposit bins;
+// cfg2: 10^5 particles) are bound by the four dependent launches above, each
+// a few microseconds of work: k_bin_coop runs the same four phases in ONE
+// cooperative launch with grid-wide barriers between them.  The scan is two
+// level: every block sums its contiguous segment of the counts, all blocks
+// scan the block sums (at most a few hundred) and then their own segment.
+// Same keys, starts, order and deposit lists as the multi-kernel path.
+constexpr int BIN_COOP_THREADS = 256;
+
+template <class P, bool DEP>
+__global__ void __launch_bounds__(BIN_COOP_THREADS)
+k_bin_coop(const P *__restrict__ pos, long long n, BinGeom g, int *__restrict__ keys,
+           int *__restrict__ counts, int *__restrict__ starts, int *__restrict__ slots,
+           int *__restrict__ order, const uint8_t *__restrict__ type, P *__restrict__ spos,
+           uint8_t *__restrict__ stype, DepBin dep, int nall, P *__restrict__ dpos,
+           unsigned *__restrict__ dmeta, int *__restrict__ block_sums) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int nflat = g.n0 * g.n1;
+    const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long gstride = (long long)gridDim.x * blockDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int s_w[BIN_COOP_THREADS / 32];
+    // segment of the count array each block scans
+    const int seg = (nall + gridDim.x - 1) / gridDim.x;
+    // ---- keys and counts (k_bin_count)
+    for (long long i = gtid; i < n; i += gstride) {
+        double x, y;
+        load2(pos, i, x, y);
+        const int key = cell_axis(y, g.lo1, g.eff1, g.n1) * g.n0 + cell_axis(x, g.lo0, g.eff0, g.n0);
+        keys[i] = key;
+        atomicAdd(&counts[key], 1);
+        if (DEP) {
+            int dk = -1;
+            if (route_bits(type, i, dep.route)) {
+                const GridGeom &gg = dep.gg;
+                const double u0 = ddiv(dsub(x, gg.lo0), gg.d0);
+                const double u1 = ddiv(dsub(y, gg.lo1), gg.d1);
+                if (fabs(u0) < 0x1p52 && fabs(u1) < 0x1p52) {
+                    dk = nflat + dep_bin_axis(u1, dep.kind, gg.n, gg.per) * gg.n +
+                         dep_bin_axis(u0, dep.kind, gg.n, gg.per);
+                    atomicAdd(&counts[dk], 1);
+                }
+            }
+            keys[n + i] = dk;
+        }
+    }
+    grid.sync();
+    // ---- exclusive scan of counts[0, nall) -> starts (starts[nall] = total)
+    const int s0 = min((int)blockIdx.x * seg, nall), s1 = min(s0 + seg, nall);
+    auto block_sum = [&](int v) {  // sum of v over the block, in every thread
+        __syncthreads();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_w[warp] = v;
+        __syncthreads();
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < BIN_COOP_THREADS / 32; w++) t += s_w[w];
+        return t;
+    };
+    {
+        int part = 0;
+        for (int c = s0 + tid; c < s1; c += BIN_COOP_THREADS) part += counts[c];
+        const int tot = block_sum(part);
+        if (tid == 0) block_sums[blockIdx.x] = tot;
+    }
+    grid.sync();
+    {
+        int part = 0;  // counts of the segments before this block's
+        for (int b = tid; b < (int)blockIdx.x; b += BIN_COOP_THREADS) part += block_sums[b];
+        int carry = block_sum(part);
+        if (blockIdx.x == gridDim.x - 1) {
+            int all = 0;
+            for (int b = tid; b < (int)gridDim.x; b += BIN_COOP_THREADS) all += block_sums[b];
+            all = block_sum(all);
+            if (tid == 0) starts[nall] = all;
+        }
+        for (int c0 = s0; c0 < s1; c0 += BIN_COOP_THREADS) {  // tiles of the segment, in order
+            const int c = c0 + tid;
+            const int v = c < s1 ? counts[c] : 0;
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += u;
+            }
+            __syncthreads();
+            if (lane == 31) s_w[warp] = inc;
+            __syncthreads();
+            int wb = 0, tile = 0;
+#pragma unroll
+            for (int w = 0; w < BIN_COOP_THREADS / 32; w++) {
+                wb += w < warp ? s_w[w] : 0;
+                tile += s_w[w];
+            }
+            if (c < s1) starts[c] = carry + wb + inc - v;
+            carry += tile;
+        }
+    }
+    grid.sync();
+    // ---- unordered placement into the cell / bin ranges (k_bin_scatter); the
+    // countdown leaves counts all-zero for the next call
+    for (long long i = gtid; i < n; i += gstride) {
+        const int key = keys[i];
+        slots[starts[key] + atomicSub(&counts[key], 1) - 1] = (int)i;
+        if (DEP) {
+            const int dk = keys[n + i];
+            if (dk >= 0) slots[starts[dk] + atomicSub(&counts[dk], 1) - 1] = (int)i;
+        }
+    }
+    grid.sync();
+    // ---- stable order inside a cell / bin and the sorted copies (k_seg_rank)
+    const long long total = DEP ? (long long)starts[nall] : n;
+    for (long long t = gtid; t < total; t += gstride) {
+        const int v = slots[t];
+        const bool isdep = DEP && t >= n;
+        const int key = isdep ? keys[n + v] : keys[v];
+        const int sb = starts[key], se = starts[key + 1];
+        int rank = 0;
+        for (int u = sb; u < se; u++) rank += slots[u] < v;
+        if (isdep) {
+            const long long d = sb + rank - n;
+            reinterpret_cast<typename Vec2<P>::T *>(dpos)[d] =
+                reinterpret_cast<const typename Vec2<P>::T *>(pos)[v];
+            dmeta[d] = (unsigned)v | (route_bits(type, v, dep.route) << 30);
+            continue;
+        }
+        order[sb + rank] = v;
+        spos[2 * (sb + rank)] = pos[2 * (long long)v];
+        spos[2 * (sb + rank) + 1] = pos[2 * (long long)v + 1];
+        if (type) stype[sb + rank] = type[v];
     }
 }
 
@@ -285,6 +422,44 @@ int bin_particles(cs_ctx *ctx, int prec, const void *pos, long long n, const Bin
     }
     const DepBin none{};
     const DepBin &d = dep ? *dep : none;
+    if (n > 0 && n <= (1LL << 16) && !getenv("CS_BIN_MULTI")) {  // (10^5: no faster, measured)
+        // one cooperative launch; every block resident (grid-wide barriers)
+        static int coop_blocks = 0;
+        if (!coop_blocks) {
+            int dev = 0, sms = 0, coop = 0, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bin_coop<double, true>,
+                                                          BIN_COOP_THREADS, 0);
+            coop_blocks = coop && per > 0 ? sms * (per > 2 ? 2 : per) : -1;
+        }
+        if (coop_blocks > 0) {
+            CS_TRY(ctx->coop_sums.ensure(sizeof(int) * (size_t)coop_blocks));  // segment totals
+            int grid = grid_for(dep ? 2 * n : n, BIN_COOP_THREADS, coop_blocks);
+            int *keys = ctx->keys.as<int>(), *counts = ctx->counts.as<int>();
+            int *starts = ctx->starts.as<int>(), *slots = ctx->skeys.as<int>();
+            int *order = ctx->order.as<int>(), *bsums = ctx->coop_sums.as<int>();
+            int nall_i = (int)nall;
+            long long nn = n;
+            BinGeom gv = g;
+            DepBin dv = d;
+            const void *fn;
+            void *spos = ctx->spos.p, *dpos = ctx->dep_pos.p;
+            unsigned *dmeta = ctx->dep_meta.as<unsigned>();
+            if (prec == CS_F64)
+                fn = dep ? (const void *)k_bin_coop<double, true> : (const void *)k_bin_coop<double, false>;
+            else
+                fn = dep ? (const void *)k_bin_coop<float, true> : (const void *)k_bin_coop<float, false>;
+            void *args[] = {(void *)&pos, &nn, &gv, &keys, &counts, &starts, &slots, &order,
+                            (void *)&type, &spos, &stype, &dv, &nall_i, &dpos, &dmeta, &bsums};
+            CS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BIN_COOP_THREADS), args, 0,
+                                                ctx->stream));
+            ctx->launches += 1;
+            if (dep_done) *dep_done = dep != nullptr;
+            return CS_OK;
+        }
+    }
     for (int phase = 0; phase < 3; phase++) {
         if (phase == 1) CS_TRY(exclusive_scan_i32(ctx, ctx->counts.as<int>(),
                                                   ctx->starts.as<int>(), nall));

@@ -189,7 +189,7 @@ int cs_ctx_destroy(cs_ctx *ctx) {
     if (!ctx) return CS_OK;
     cudaStreamSynchronize(ctx->stream);
     for (Buf *b : {&ctx->keys, &ctx->skeys, &ctx->counts, &ctx->starts, &ctx->order,
-                   &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->status, &ctx->pair_counts,
+                   &ctx->force, &ctx->tile_flags, &ctx->tmp, &ctx->coop_sums, &ctx->status, &ctx->pair_counts,
                    &ctx->pair_offsets, &ctx->host_scratch, &ctx->zpar, &ctx->obs, &ctx->spos,
                    &ctx->stype, &ctx->dep_keys, &ctx->dep_counts, &ctx->dep_starts,
                    &ctx->dep_slots, &ctx->dep_pos, &ctx->dep_meta})

@@ -86,6 +86,7 @@ struct cs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cs::Buf keys, skeys, counts, starts, order, force, tile_flags, tmp, status, zpar, obs, spos,
+        coop_sums,
         stype,
         pair_counts, pair_offsets, host_scratch,
         // ordered deposit (deposit.cu): bin keys / counts / starts, slots, sorted copies

@@ -7,7 +7,7 @@ import sys
 
 TIME = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
         "s": 1.0, "second": 1.0}
-KERNELS = {"k_fast_forces(": "forces", "k_fast_forces_generic": "forces_generic",
+KERNELS = {"k_fast_forces<": "forces", "k_fast_forces_generic": "forces_generic",
            "k_fast_update": "update", "k_scan": "scan",
            "k_bucket_sort": "bucket_sort", "k_fast_deposit_rows": "deposit_rows",
            "k_spec_cols": "spec_cols"}
@@ -26,7 +26,7 @@ def main(rep, out, config):
         d = dict(zip(hdr, r))
         name = d.get("Kernel Name", "")
         for k, tag in KERNELS.items():
-            if name.startswith(k) or ("(" not in k and k in name):
+            if k in name:
                 unit_r = rows[1][hdr.index("dram__bytes_read.sum")]
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
                 rd = float(d["dram__bytes_read.sum"]) * scale[rows[1][hdr.index("dram__bytes_read.sum")]]

@@ -357,7 +357,25 @@ __device__ __noinline__ void ens_deposit(const EnsArgs &a, const double *pos, co
     }
 }
 
-template <int NT>
+// the reference pair loop of one particle (rare: a particle with more accepted
+// partners than the lane-dense path keeps)
+__device__ __forceinline__ double2 ens_forces_plain(const double *pos, const uint8_t *type,
+                                                 const int *order, const int *starts,
+                                                 const BinGeom &g, const PairTab &pt, int i) {
+    double fx = 0.0, fy = 0.0;
+    pair_loop(pos, type, order, starts, g, pt, i, [&](int, double sc, double dx0, double dx1) {
+        fx = dadd(fx, dmul(sc, dx0));
+        fy = dadd(fy, dmul(sc, dx1));
+    });
+    return make_double2(fx, fy);
+}
+
+// LEAN: the instantiation for a field-free, reaction-free realisation with
+// thread-per-particle forces (cfg0 on the CTA engine).  The general kernel is
+// ~290 KB of code; a step of such a system jumps over most of it, and the
+// instruction fetches of every jump target cost more than the work between
+// them -- this instantiation compiles the unused stages out.
+template <int NT, bool LEAN = false>
 __global__ void __launch_bounds__(NT)
 k_ensemble(const __grid_constant__ EnsArgs a) {
     extern __shared__ double sm[];
@@ -385,7 +403,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         lc[i] = a.local_c[n * s + i];
         type[i] = a.type[n * s + i];
     }
-    if (a.field || a.refresh)
+    if (!LEAN && (a.field || a.refresh))
         for (int l = tid; l < m; l += NT) c[l] = a.c[(long long)m * s + l];
     if (tid == 0) s_abort = st->abort;
     if (a.interact)
@@ -413,7 +431,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         if (tid < n) xpre = *reinterpret_cast<const double2 *>(xk + 2 * tid);
         const GridGeom &gg = a.gg;
         const int nc = gg.n;
-        if (a.field) {
+        if (!LEAN && a.field) {
             // ---- deposit_both (coupling.py:77-110, 113-138), every node summed
             // in the reference's particle order (see deposit.cu): depositing
             // particles binned by deposit row (CIC: base row, gaussian: nearest
@@ -483,7 +501,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             if (s_abort) break;
         }
         // ---- refresh (coupling.py:302-325)
-        if (a.refresh) {
+        if (!LEAN && a.refresh) {
             for (int p = tid; p < n; p += NT) {
                 Bilin b;
                 clamped += 2 * bilinear_stencil(pos[2 * p], pos[2 * p + 1], gg, b);
@@ -507,6 +525,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             // (the cell counts were cleared before the first step and by the
             // previous step's EM phase, which does not read the cell table)
             CS_TICK(1);
+#pragma unroll 1
             for (int p = tid; p < n; p += NT) {
                 const int k = cell_axis(pos[2 * p + 1], a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
                               cell_axis(pos[2 * p], a.g.lo0, a.g.eff0, a.g.n0);
@@ -556,9 +575,11 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 // its cell start + the number of the cell's particles with a
                 // smaller index
                 int *slots = reinterpret_cast<int *>(frc);
+#pragma unroll 1
                 for (int p = tid; p < n; p += NT) slots[atomicAdd(&cur[key[p]], 1)] = p;
                 __syncthreads();
                 CS_TICK(4);
+#pragma unroll 1
                 for (int t = tid; t < n; t += NT) {
                     const int v = slots[t];
                     const int k = key[v];
@@ -570,7 +591,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             }
             __syncthreads();
             CS_TICK(5);
-            if (a.thread_forces) {
+            if (LEAN || a.thread_forces) {
                 // sparse systems (<= 2 particles per cell; the single-
                 // realisation CTA engine): a lane per particle walks its ring in
                 // the reference order (as common.cuh pair_loop) with the exact
@@ -698,13 +719,10 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                     CS_TICK(9);
                     if (live) {
                         if (nacc > 4) {  // more partners than kept: the plain loop
-                            fx = 0.0;
-                            fy = 0.0;
-                            pair_loop(pos, type, order, starts, a.g, a.pt, i,
-                                      [&](int, double sc, double dx0, double dx1) {
-                                          fx = dadd(fx, dmul(sc, dx0));
-                                          fy = dadd(fy, dmul(sc, dx1));
-                                      });
+                            const double2 ff = ens_forces_plain(pos, type, order, starts, a.g,
+                                                                a.pt, i);
+                            fx = ff.x;
+                            fy = ff.y;
                         }
                         frc[2 * i] = fx;
                         frc[2 * i + 1] = fy;
@@ -829,6 +847,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         // ---- Euler-Maruyama + boundaries (motion.py:268-282, 355-430)
         if (a.interact)  // the next step's cell counts
             for (int f = tid; f <= a.ncell; f += NT) starts[f] = 0;
+#pragma unroll 1
         for (int p = tid; p < n; p += NT) {
             const int t = type[p] ? 1 : 0;
             const double amp = a.amp[t];
@@ -866,7 +885,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         CS_TICK(7);
         if (s_abort) break;
         // ---- fixed-step reactions (reactions.py:43-81)
-        if (a.react) {
+        if (!LEAN && a.react) {
             const double *uk = a.u + (long long)kk * a.us + (long long)n * s;
             for (int p = tid; p < n; p += NT) {
                 const double ui = uk[p];
@@ -911,7 +930,7 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
         a.local_c[n * s + i] = lc[i];
         a.type[n * s + i] = type[i];
     }
-    if (a.field)
+    if (!LEAN && a.field)
         for (int l = tid; l < m; l += NT) a.c[(long long)m * s + l] = c[l];
     if (clamped) atomicAdd((unsigned long long *)&st->clamped, (unsigned long long)clamped);
     if (high_n) {
@@ -1115,6 +1134,8 @@ int ens_create(cs_ctx *ctx, const cs_sim_params *p, int n_real, cs_ens **out) {
     }
     CS_CUDA(cudaFuncSetAttribute(k_ensemble<ENS_THREADS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem));
+    CS_CUDA(cudaFuncSetAttribute(k_ensemble<1024, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem));
     CS_CUDA(cudaFuncSetAttribute(k_ensemble<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)e->smem));
     CS_CUDA(cudaFuncSetAttribute(k_ensemble<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1165,7 +1186,9 @@ int ens_step(cs_ens *e, const cs_ens_state *s, const double *xi, const double *u
     a.st = e->status.as<DevStatus>();
     a.k_steps = k;
     a.step0 = e->steps_done;
-    if (e->threads == 1024)
+    if (e->threads == 1024 && a.thread_forces && !a.field && !a.refresh && !a.react)
+        k_ensemble<1024, true><<<e->n_real, 1024, e->smem, e->ctx->stream>>>(a);
+    else if (e->threads == 1024)
         k_ensemble<1024><<<e->n_real, 1024, e->smem, e->ctx->stream>>>(a);
     else if (e->threads == 768)
         k_ensemble<768><<<e->n_real, 768, e->smem, e->ctx->stream>>>(a);

@@ -378,7 +378,7 @@ __device__ __forceinline__ double2 ens_forces_plain(const double *pos, const uin
 template <int NT, bool LEAN = false>
 __global__ void __launch_bounds__(NT)
 k_ensemble(const __grid_constant__ EnsArgs a) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     __shared__ int s_abort;
     __shared__ double s_red[NT / 32];
     __shared__ int s_flag[NT / 32];
@@ -527,8 +527,9 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             CS_TICK(1);
 #pragma unroll 1
             for (int p = tid; p < n; p += NT) {
-                const int k = cell_axis(pos[2 * p + 1], a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
-                              cell_axis(pos[2 * p], a.g.lo0, a.g.eff0, a.g.n0);
+                const double2 xp = reinterpret_cast<const double2 *>(pos)[p];
+                const int k = cell_axis(xp.y, a.g.lo1, a.g.eff1, a.g.n1) * a.g.n0 +
+                              cell_axis(xp.x, a.g.lo0, a.g.eff0, a.g.n0);
                 key[p] = k;
                 atomicAdd(&starts[k + 1], 1);
             }
@@ -536,8 +537,9 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             CS_TICK(2);
             {  // inclusive scan of starts[1..ncell] (the counts): a run of cells
                // per thread, then the block's run totals
-                const int per = (a.ncell + NT - 1) / NT;
-                const int f0 = 1 + tid * per, f1 = min(f0 + per, a.ncell + 1);
+                // (an odd run length: the threads' runs start on distinct banks)
+                const int per = ((a.ncell + NT - 1) / NT) | 1;
+                const int f0 = min(1 + tid * per, a.ncell + 1), f1 = min(f0 + per, a.ncell + 1);
                 int run = 0;
                 for (int f = f0; f < f1; f++) run += starts[f];
                 int inc = run;
@@ -608,15 +610,17 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                     double xi = 0.0, yi = 0.0;
                     int ti = 0, nacc = 0, pj0 = 0, pj1 = 0, pj2 = 0, pj3 = 0;
                     if (live) {
-                        xi = pos[2 * i];
-                        yi = pos[2 * i + 1];
+                        const double2 pi = reinterpret_cast<const double2 *>(pos)[i];
+                        xi = pi.x;
+                        yi = pi.y;
                         ti = type[i] ? 1 : 0;
                         const int cy = key[i] / g.n0, cx = key[i] - cy * g.n0;  // binned above
                         auto candidate = [&](int k) {
                             const int j = order[k];
                             if (j == i) return;
-                            double dx0 = dsub(pos[2 * j], xi);
-                            double dx1 = dsub(pos[2 * j + 1], yi);
+                            const double2 pj = reinterpret_cast<const double2 *>(pos)[j];
+                            double dx0 = dsub(pj.x, xi);
+                            double dx1 = dsub(pj.y, yi);
                             if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
                             if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
                             const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
@@ -689,8 +693,9 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                         double tx = 0.0, ty = 0.0;
                         if (e < total) {
                             const int j = lv == 3 ? q3 : (lv == 2 ? q2 : (lv == 1 ? q1 : q0));
-                            double dx0 = dsub(pos[2 * j], xo);
-                            double dx1 = dsub(pos[2 * j + 1], yo);
+                            const double2 pj = reinterpret_cast<const double2 *>(pos)[j];
+                            double dx0 = dsub(pj.x, xo);
+                            double dx1 = dsub(pj.y, yo);
                             if (g.per0) dx0 = dsub(dx0, dmul(g.size0, rint(ddiv(dx0, g.size0))));
                             if (g.per1) dx1 = dsub(dx1, dmul(g.size1, rint(ddiv(dx1, g.size1))));
                             const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
@@ -852,17 +857,20 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
             const int t = type[p] ? 1 : 0;
             const double amp = a.amp[t];
             const double z0 = p == tid ? xpre.x : xk[2 * p], z1 = p == tid ? xpre.y : xk[2 * p + 1];
-            const double f0 = a.interact ? frc[2 * p] : 0.0, f1 = a.interact ? frc[2 * p + 1] : 0.0;
+            double2 *pos2 = reinterpret_cast<double2 *>(pos), *anc2 = reinterpret_cast<double2 *>(anc);
+            const double2 fp = a.interact ? reinterpret_cast<const double2 *>(frc)[p]
+                                          : make_double2(0.0, 0.0);
+            const double2 xp = pos2[p], dp = reinterpret_cast<const double2 *>(drift)[p];
             double i0, i1;
-            force_increment(f0, f1, a.dt, a.tamed, i0, i1);
+            force_increment(fp.x, fp.y, a.dt, a.tamed, i0, i1);
             double v[2];
-            v[0] = dadd(dadd(dadd(pos[2 * p], dmul(amp, z0)), dmul(drift[2 * p], a.dt)), i0);
-            v[1] = dadd(dadd(dadd(pos[2 * p + 1], dmul(amp, z1)), dmul(drift[2 * p + 1], a.dt)),
-                        i1);
+            v[0] = dadd(dadd(dadd(xp.x, dmul(amp, z0)), dmul(dp.x, a.dt)), i0);
+            v[1] = dadd(dadd(dadd(xp.y, dmul(amp, z1)), dmul(dp.y, a.dt)), i1);
             const double raw0 = v[0], raw1 = v[1];
             bool ok = isfinite(v[0]) && isfinite(v[1]);
             if (!ok) set_status(st, &s_abort, err_key(0, p, CS_NONFINITE), step);
-            double an[2] = {anc[2 * p], anc[2 * p + 1]};
+            const double2 ap = anc2[p];
+            double an[2] = {ap.x, ap.y};
             for (int ax = 0; ok && ax < 2; ax++) {
                 const int code = boundary_axis(v[ax], an[ax], a.dom.lo[ax], a.dom.hi[ax],
                                                a.dom.periodic[ax]);
@@ -872,14 +880,11 @@ k_ensemble(const __grid_constant__ EnsArgs a) {
                 }
             }
             if (!ok) {  // the raw proposal stays visible for the host's message
-                pos[2 * p] = raw0;
-                pos[2 * p + 1] = raw1;
+                pos2[p] = make_double2(raw0, raw1);
                 continue;
             }
-            pos[2 * p] = v[0];
-            pos[2 * p + 1] = v[1];
-            anc[2 * p] = an[0];
-            anc[2 * p + 1] = an[1];
+            pos2[p] = make_double2(v[0], v[1]);
+            anc2[p] = make_double2(an[0], an[1]);
         }
         __syncthreads();
         CS_TICK(7);

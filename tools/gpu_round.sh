@@ -14,6 +14,10 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 0 > $O/bench_ref
 for c in cfg0 cfg1 cfg2 cfg2f32 cfg4; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; echo $c rc=$?
 done
+# the small configs over their whole 1000-step workload (one call: launch overhead amortised)
+for c in cfg0 cfg1; do
+  timeout 900 python bench.py --config $c --steps 1000 --warmup 5 --no-cpu-baseline > $O/bench_${c}_1000steps.json 2> $O/bench_${c}_1000.err; echo $c-1000 rc=$?
+done
 timeout 900 python bench_ensemble.py > $O/bench_ensemble_fig1.json 2> $O/ens.err; echo ens rc=$?
 timeout 600 python tools/spec_bench.py > $O/spec_bench.txt 2>&1; echo spec rc=$?
 A="bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-perf-mode"

@@ -501,8 +501,11 @@ def main():
     # ---- stage times (separate profiled pass, same stream, CUDA events)
     sim.set_profiling(True)
     KP = min(K, 10)
-    for k in range(KP):
-        sim.step(xi[(W + k) % blocks], 1)
+    if W + KP <= blocks:  # one call, as the timed run (the engine sees the coming step's block)
+        sim.step(xi[W:W + KP], KP)
+    else:
+        for k in range(KP):
+            sim.step(xi[(W + k) % blocks], 1)
     stages = {k: v / KP for k, v in sim.stage_times().items()}
     sim.set_profiling(False)
     t_fu = stages["bin"] + stages["force"] + stages["update"]
@@ -551,8 +554,11 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             pms = float(t.item())
         sim2.set_profiling(True)
-        for k in range(KP):
-            sim2.step(xi[(W + k) % blocks], 1)
+        if W + KP <= blocks:
+            sim2.step(xi[W:W + KP], KP)
+        else:
+            for k in range(KP):
+                sim2.step(xi[(W + k) % blocks], 1)
         pst = {k: v / KP for k, v in sim2.stage_times().items()}
         sim2.set_profiling(False)
         p_fu = pst["bin"] + pst["force"] + pst["update"]

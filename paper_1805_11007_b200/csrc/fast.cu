@@ -1072,12 +1072,21 @@ __device__ __noinline__ bool deposit_record(float4 rv, GridGeom gg, ExactDiv d0,
 // A deposit add that overflows the int32 fixed-point sum stops the run with
 // CS_DEPOSIT_OVERFLOW (checked on every add here; the row deposit checks its
 // adds once a cell exceeds the conservative population bound cell_max).
+// XI: the coming step's increments (an (N, 2) array by particle id) are
+// gathered here, by the ids of the records being placed, and stored by
+// destination slot; that step's update reads them as a coalesced stream.
+// The gather costs the same wherever it runs while the array fits the L2
+// (cfg3: update 313 -> 256 us, this kernel 154 -> 277 us); beyond it (cfg4:
+// 640 MB) the update's one load in flight per thread is the limit and the
+// four independent loads per thread here are not (13.0 -> 12.3 ms/step).
+template <bool XI>
 __global__ void __launch_bounds__(BSORT_THREADS)
 k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long long cap,
               long long nbucket, BinGeom g, ExactDiv eff0, ExactDiv eff1, long long nflat,
               Rec *__restrict__ out, int *__restrict__ starts, GridGeom gg, ExactDiv d0,
               ExactDiv d1, unsigned bits0, unsigned bits1, int *__restrict__ rho_q, int deposit,
-              int cell_max, int *__restrict__ dep_exact, DevStatus *st, int step) {
+              int cell_max, int *__restrict__ dep_exact, DevStatus *st, int step,
+              const float2 *__restrict__ xi_next, float2 *__restrict__ xi_slot) {
     // [SUBB cap] ids by slot, then codes (cell | arrival << 10 | part << 25) of
     // the records beyond the register-resident ones
     extern __shared__ int s_dyn[];
@@ -1223,7 +1232,13 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
     }
     __syncthreads();
     const unsigned bits_dep = deposit ? (bits0 | bits1) : 0u;
-    auto place = [&](float4 r, int code) {
+    float2 xv[RPT];  // XI: the register-resident records' increments, loads issued together
+    if (XI) {
+#pragma unroll
+        for (int k = 0; k < RPT; k++)
+            if (cc[k] >= 0) xv[k] = ld_evict_last(xi_next + (__float_as_uint(rr[k].z) & ID_MASK));
+    }
+    auto place = [&](float4 r, int code, float2 z, bool have_z) {
         const int lc = code & LC_MASK;
         const int kb = s_beg[lc], len = s_beg[lc + 1] - kb;
         int rank = 0;
@@ -1232,6 +1247,10 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
             for (int k = 0; k < len; k++) rank += s_id[kb + k] < id ? 1 : 0;
         }
         reinterpret_cast<float4 *>(out)[off + kb + rank] = r;
+        if (XI) {
+            if (!have_z) z = ld_evict_last(xi_next + (__float_as_uint(r.z) & ID_MASK));
+            __stcs(xi_slot + off + kb + rank, z);
+        }
         if (bits_dep) {
             const unsigned bits = (__float_as_uint(r.z) >> 31) ? bits1 : bits0;
             if (bits && deposit_record(r, gg, d0, d1, bits, rho_q, gg.n * gg.n)) {
@@ -1244,11 +1263,11 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
     };
 #pragma unroll
     for (int k = 0; k < RPT; k++)
-        if (cc[k] >= 0) place(rr[k], cc[k]);
+        if (cc[k] >= 0) place(rr[k], cc[k], XI ? xv[k] : make_float2(0.f, 0.f), true);
     for (int i = tid + RPT * BSORT_THREADS; i < cnt; i += BSORT_THREADS) {
         const int code = s_code[i - RPT * BSORT_THREADS];
         const int q = code >> 25;
-        place(__ldg(r4 + (long long)q * cap + (i - s_pre[q])), code);
+        place(__ldg(r4 + (long long)q * cap + (i - s_pre[q])), code, make_float2(0.f, 0.f), false);
     }
 }
 
@@ -1497,6 +1516,11 @@ constexpr int STARTS_OFF = 0;
 
 struct cs_fast {
     cs::Buf rec[2], region, fill, boff, starts[2], anchor0, rho_q, force, gen, depflag;
+    // the coming step's increments in storage-slot order (gathered by id in
+    // the bucket sort when the caller's block holds that step and the array
+    // is beyond the L2: xi_ready)
+    cs::Buf xi_slot;
+    bool xi_ready = false;
     int cur = 0;
     bool imported = false;
     long long nflat = 0;
@@ -1570,6 +1594,7 @@ void fast_destroy(cs_fast *f) {
     if (!f) return;
     for (Buf *b : {&f->rec[0], &f->rec[1], &f->region, &f->fill, &f->boff, &f->starts[0],
                    &f->starts[1], &f->anchor0, &f->rho_q, &f->force, &f->gen, &f->depflag,
+                   &f->xi_slot,
                    &f->range, &f->row_owner, &f->bounds, &f->outbox, &f->out_dest,
                    &f->out_count})
         b->release();
@@ -1602,8 +1627,10 @@ static int deposit_cell_max(const GridGeom &gg, const cs_fast *f) {
 // bucket sort into the next record array and cell table (in-cell id order;
 // the atomic-mode deposit of the next step's field rides along).
 static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
-                     const unsigned char bits[3], DevStatus *st, int step) {
+                     const unsigned char bits[3], DevStatus *st, int step,
+                     const void *xi_next = nullptr) {
     const int nxt = 1 - f->cur;
+    if (xi_next) CS_TRY(f->xi_slot.ensure(sizeof(float2) * (size_t)(p.n > 0 ? p.n : 1)));
     CS_TRY(exclusive_scan_i32(ctx, f->fill.as<int>(), f->boff.as<int>(), f->nbucket * SUBB,
                               f->fill.as<int>()));
     const char *dbg = getenv("CS_FAST_DEBUG");
@@ -1614,20 +1641,25 @@ static int fast_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const Grid
     const size_t smem = sizeof(int) * (size_t)(SUBB * f->cap + (extra > 0 ? extra : 0));
     static size_t smem_set = 0;
     if (smem > smem_set) {  // static + dynamic may pass 48 KB before the dynamic part does
-        CS_CUDA(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+        CS_CUDA(cudaFuncSetAttribute(k_bucket_sort<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CS_CUDA(cudaFuncSetAttribute(k_bucket_sort<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = smem;
     }
-    k_bucket_sort<<<(unsigned)f->nbucket, BSORT_THREADS, smem, ctx->stream>>>(
+    auto kern = xi_next ? k_bucket_sort<true> : k_bucket_sort<false>;
+    kern<<<(unsigned)f->nbucket, BSORT_THREADS, smem, ctx->stream>>>(
         f->region.as<Rec>(), f->boff.as<int>(), f->cap, f->nbucket, f->g,
         make_exact_div(f->g.eff0), make_exact_div(f->g.eff1), f->nflat, f->rec[nxt].as<Rec>(),
         cell_table(f, nxt), gg, make_exact_div(d0), make_exact_div(d1), dep ? bits[0] : 0u,
         dep ? bits[1] : 0u, f->rho_q.as<int>(), dep && !f->gather,
         dep && f->gather && (bits[0] | bits[1]) ? deposit_cell_max(gg, f) : 0,
-        f->depflag.as<int>() + (step & 1), st, step);
+        f->depflag.as<int>() + (step & 1), st, step, (const float2 *)xi_next,
+        xi_next ? f->xi_slot.as<float2>() : nullptr);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     f->cur = nxt;
+    f->xi_ready = xi_next != nullptr;
     return CS_OK;
 }
 
@@ -1762,6 +1794,10 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     }
     a.xi = (const float *)xi;
     a.xi_slot = p.xi_by_slot ? 1 : 0;
+    if (f->xi_ready && !(part & 4)) {  // gathered into slot order by the last bucket sort
+        a.xi = f->xi_slot.as<float>();
+        a.xi_slot = 1;
+    }
     a.grad = s ? (const float *)s->grad : nullptr;
     a.rho_q = f->rho_q.as<int>();
     a.n = n;
@@ -1876,9 +1912,18 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
 // part 1: bucket sort into the next record array / cell table (+ the
 // atomic-mode deposit); part 2: the row-gathered deposit (periodic grids)
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3], int part, DevStatus *st, int step) {
+                const unsigned char bits[3], int part, DevStatus *st, int step,
+                const void *xi_next) {
     (void)n;
-    if (part & 1) CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step));
+    // xi_next: the coming step's (N, 2) increments by id, or nullptr when the
+    // caller's block ends here.  Gathered ahead only when the array is well
+    // beyond the L2 (k_bucket_sort<true>; CS_XI_PREGATHER=0/1 overrides)
+    if (xi_next) {
+        const char *e = getenv("CS_XI_PREGATHER");
+        const bool big = sizeof(float2) * (double)p.n > 256e6;
+        if (p.xi_by_slot || f->slab || !(e ? atoi(e) != 0 : big)) xi_next = nullptr;
+    }
+    if (part & 1) CS_TRY(fast_sort(ctx, f, p, gg, bits, st, step, xi_next));
     if (part & 2) CS_TRY(fast_deposit_rows(ctx, f, p, gg, bits, st, step));
     return CS_OK;
 }
@@ -1888,6 +1933,11 @@ int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, co
 int *fast_rho_q(cs_fast *f) { return f->rho_q.p && !f->gather ? f->rho_q.as<int>() : nullptr; }
 
 bool fast_imported(const cs_fast *f) { return f && f->imported; }
+
+// a new step call: increments gathered ahead belong to the previous call's block
+void fast_begin_call(cs_fast *f) {
+    if (f) f->xi_ready = false;
+}
 
 // ---- y-slab mode host side ------------------------------------------------
 int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long long n,

@@ -66,7 +66,9 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
                    const void *xi, DevStatus *st, int step, int part);
 bool fast_fused(const cs_fast *f, const cs_sim_params &p);
 int fast_resort(cs_ctx *ctx, cs_fast *f, long long n, const cs_sim_params &p, const GridGeom &gg,
-                const unsigned char bits[3], int part, DevStatus *st, int step);
+                const unsigned char bits[3], int part, DevStatus *st, int step,
+                const void *xi_next = nullptr);
+void fast_begin_call(cs_fast *f);
 bool fast_imported(const cs_fast *f);
 int *fast_rho_q(cs_fast *f);
 int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long long n,
@@ -499,6 +501,7 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
         }
         // fork/join of the field solve (skipped while profiling, so that the
         // stage times stay additive)
+        fast_begin_call(sim->fast);  // no increments gathered ahead by an earlier call
         const bool ov = p.field_active && sim->overlap && !sim->profiling &&
                         !fast_fused(sim->fast, p);  // the fused update needs the gradient
         if (ov) CS_TRY(sim->ensure_side());
@@ -540,7 +543,12 @@ int sim_step(cs_sim *sim, const cs_sim_state *s, const void *xi, int64_t stride,
             }
             {
                 StageMark m(sim, CS_STAGE_BIN);
-                CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 1, st, step));
+                // (large systems: the bucket sort also gathers the coming
+                // step's increments into slot order when this call holds them)
+                const void *xi_next =
+                    kk + 1 < k ? (const char *)xik + (size_t)stride * es : nullptr;
+                CS_TRY(fast_resort(ctx, sim->fast, n, p, sim->gg, sim->bits, 1, st, step,
+                                   xi_next));
             }
             // in-cell id order + deposit for the next step's field
             StageMark m(sim, CS_STAGE_DEPOSIT);

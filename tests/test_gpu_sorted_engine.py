@@ -106,11 +106,17 @@ def test_sorted_equals_direct_bitwise_clustered(periodic):
     assert torch.equal(sa["pos"], sb["pos"])
 
 
+@pytest.mark.parametrize("pregather", [False, True])
 @pytest.mark.parametrize("clustered", [False, True])
-def test_block_call_equals_single_step_calls_bitwise(clustered):
+def test_block_call_equals_single_step_calls_bitwise(clustered, pregather, monkeypatch):
     """One k-step call (the bench's timed region: the field solve forked to
     the side stream every step) against k one-step calls: the same records,
-    anchors and field, bit for bit -- uniform and with cfg4-like clusters."""
+    anchors and field, bit for bit -- uniform and with cfg4-like clusters.
+    pregather: the block call's bucket sort also gathers the coming step's
+    increments into storage-slot order (what large systems do, forced here
+    by CS_XI_PREGATHER=1), so its updates read them as a stream while the
+    one-step calls gather them by id."""
+    monkeypatch.setenv("CS_XI_PREGATHER", "1" if pregather else "0")
     rng = np.random.default_rng(21)
     n, k = 150_000, 5
     if clustered:

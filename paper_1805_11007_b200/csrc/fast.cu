@@ -1283,7 +1283,8 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
 #endif
 constexpr int DEP_ROWS = CS_DEP_ROWS;  // grid rows per block of k_fast_deposit_rows
 
-__global__ void __launch_bounds__(512)
+template <int NT>  // threads per block (launch bound: registers)
+__global__ void __launch_bounds__(NT)
 k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts, BinGeom g,
                     GridGeom gg, ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
                     int *__restrict__ rho_q, const int *__restrict__ exact_flag,
@@ -1674,12 +1675,18 @@ static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
     const int smem = (int)(DEP_ROWS * 2 * sizeof(int) * (size_t)gg.n);
     static int smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
-        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows,
+        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows<512>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows<1024>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         smem_set = smem;
     }
     const int jbase = f->slab ? f->dep_j0 : 0, jrows = f->slab ? f->dep_rows : gg.n;
-    k_fast_deposit_rows<<<(jrows + DEP_ROWS - 1) / DEP_ROWS, 512, smem, ctx->stream>>>(
+    // a block's row accumulators take 64 KB at 4096 nodes per row (3 blocks of
+    // 512 threads per SM) and 128 KB at 8192 (one block per SM: 1024 threads)
+    const int threads = smem > 100 * 1024 ? 1024 : 512;
+    auto kern = threads == 1024 ? k_fast_deposit_rows<1024> : k_fast_deposit_rows<512>;
+    kern<<<(jrows + DEP_ROWS - 1) / DEP_ROWS, threads, smem, ctx->stream>>>(
         f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
         make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>(),
         f->depflag.as<int>() + (step & 1), f->depflag.as<int>() + ((step + 1) & 1), st, step,

@@ -522,7 +522,7 @@ constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
 
 struct WarpQueue {
     int ck[QCAP];                  // queue entry -> partner slot
-    unsigned short oj[QCAP];       // queue entry -> owner term index lane * ACC_MAX + j
+    unsigned short oj[QCAP];       // queue entry -> owner term index j * 32 + lane
     double tx[QCAP], ty[QCAP];     // owner term index -> pair term (lane regions)
     float ox[32], oy[32];          // owner coordinates
     int oti[32];
@@ -537,7 +537,9 @@ struct WarpQueue {
 //     (k_fast_cellfix), so slot order along the rows is exactly the
 //     reference's ring order (o1, o0, id)); binary32 prefilter hits are
 //     enqueued into the warp's queue at ballot/popc positions, tagged with
-//     the owner's term index lane * ACC_MAX + j (j = the owner's j-th hit);
+//     the owner's term index j * 32 + lane (j = the owner's j-th hit; lanes
+//     of one j side by side: the owners read their terms without bank
+//     conflicts, 8-way with lane * ACC_MAX + j);
 //  2. the queue is evaluated ~1/32 per lane: exact reference test (binary64)
 //     and pair term, written to the owner's term index (+0.0 for prefilter
 //     false positives: the owners' sums start at +0.0 and so are never -0.0,
@@ -660,7 +662,7 @@ k_fast_forces(DevStatus *st, int step) {
         }
         // the hits compacted level by level into queue entries (in place:
         // entry e <= j * 32 + lane, and a level is read before it is written),
-        // each tagged with the owner's term index lane * ACC_MAX + j
+        // each tagged with the owner's term index j * 32 + lane
         int qn = 0;  // queue length (warp-uniform)
         {
             const int nq = nacc < ACC_MAX ? nacc : ACC_MAX;
@@ -673,7 +675,7 @@ k_fast_forces(DevStatus *st, int step) {
                 if (has) {
                     const int e = qn + __popc(m & lt);
                     wq.ck[e] = kk;
-                    wq.oj[e] = (unsigned short)(lane * ACC_MAX + j);
+                    wq.oj[e] = (unsigned short)(j * 32 + lane);
                 }
                 qn += __popc(m);
             }
@@ -694,7 +696,7 @@ k_fast_forces(DevStatus *st, int step) {
             __syncwarp();
             for (int e = lane; e < qn; e += 32) {
                 const int o = wq.oj[e];
-                const int ow = o / ACC_MAX;
+                const int ow = o & 31;
                 const float4 q = __ldg(rec + wq.ck[e]);
                 const int tt = wq.oti[ow] * 2 + (int)(__float_as_uint(q.z) >> 31);
                 // interior ring (fast path): |dx| <= 2 cells < L/2, so the
@@ -711,8 +713,8 @@ k_fast_forces(DevStatus *st, int step) {
             __syncwarp();
             // ---- 3. owners add their terms in canonical order
             for (int j = 0; j < nacc; j++) {
-                fx = dadd(fx, wq.tx[lane * ACC_MAX + j]);
-                fy = dadd(fy, wq.ty[lane * ACC_MAX + j]);
+                fx = dadd(fx, wq.tx[j * 32 + lane]);
+                fy = dadd(fy, wq.ty[j * 32 + lane]);
             }
             __syncwarp();
         }

@@ -181,6 +181,133 @@ k_soft_forces(const P *__restrict__ pos, const uint8_t *__restrict__ type,
     }
 }
 
+// Dense rings (cfg2: ~360 candidates and ~75 accepted pairs per owner).  A
+// lane per owner leaves a 10^5-particle system with 3125 warps, ~5 per
+// scheduler, and every trip is one dependent load -> distance -> test chain
+// (ncu: no eligible warp 53 % of the cycles, 8 % of the FP64 roof).  Here a
+// WARP owns a particle: the lanes test 32 consecutive candidates of the
+// flattened ring at a time (coalesced reads of the cell-ordered copies),
+// accepted pairs are appended to the warp's queue in candidate order
+// (ballot / popc), the queue is evaluated one pair per lane, and lanes 0 / 1
+// add the x / y terms in queue order = candidate order = the reference's.
+// Same arithmetic as k_soft_forces, term for term: bitwise equal results.
+constexpr int WF_WARPS = 8;
+constexpr int WF_Q = 192;
+
+struct WfBuf {
+    double dx[WF_Q], dy[WF_Q], r2[WF_Q];
+    unsigned char tt[WF_Q];
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * WF_WARPS)
+k_soft_forces_warp(const int *__restrict__ order, const int *__restrict__ starts, long long n,
+                   BinGeom g, PairTab pt, double *__restrict__ out, const DevStatus *st,
+                   const P *__restrict__ spos, const uint8_t *__restrict__ stype) {
+    if (st && st->abort) return;
+    __shared__ WfBuf bufs[WF_WARPS];
+    WfBuf &B = bufs[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const long long wstride = (long long)gridDim.x * WF_WARPS;
+    for (long long t = blockIdx.x * (long long)WF_WARPS + (threadIdx.x >> 5); t < n; t += wstride) {
+        double xi, yi;
+        load2(spos, t, xi, yi);
+        const int ti = stype ? (int)stype[t] : 0;
+        const int cx = cell_axis(xi, g.lo0, g.eff0, g.n0);
+        const int cy = cell_axis(yi, g.lo1, g.eff1, g.n1);
+        double fsum = 0.0;  // lane 0: the x sum, lane 1: the y sum
+        int nq = 0;
+        auto flush = [&]() {
+            __syncwarp();
+            for (int e = lane; e < nq; e += 32) {
+                const double eps = pt.eps[B.tt[e]];
+                const double r = dsqrt(B.r2[e]);
+                const double sc = -ddiv(cs_exp(-ddiv(r, eps)), dmul(eps, r));
+                B.dx[e] = dmul(sc, B.dx[e]);
+                B.dy[e] = dmul(sc, B.dy[e]);
+            }
+            __syncwarp();
+            if (lane < 2) {
+                const double *src = lane ? B.dy : B.dx;
+                for (int e = 0; e < nq; e++) fsum = dadd(fsum, src[e]);
+            }
+            __syncwarp();
+            nq = 0;
+        };
+        // the slots [s, e) of consecutive ring cells, 64 candidates per trip:
+        // both groups' position loads are in flight before either distance
+        // test (a trip is otherwise one dependent load -> subtract -> test chain)
+        auto segment = [&](int s, int e) {
+            for (int k0 = s; k0 < e; k0 += 64) {
+                if (nq + 64 > WF_Q) flush();
+                int slot[2];
+                bool live2[2];
+                double xj[2], yj[2];
+                int tj[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int k = k0 + 32 * h + lane;
+                    live2[h] = k < e;
+                    slot[h] = live2[h] ? k : (int)t;  // idle lanes re-read the owner
+                    load2(spos, slot[h], xj[h], yj[h]);
+                    tj[h] = stype ? (int)stype[slot[h]] : 0;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    double dx0 = dsub(xj[h], xi);
+                    double dx1 = dsub(yj[h], yi);
+                    if (g.per0) dx0 = df_min_image(dx0, g.size0);
+                    if (g.per1) dx1 = df_min_image(dx1, g.size1);
+                    const double r2 = dadd(dmul(dx0, dx0), dmul(dx1, dx1));
+                    const int tt = ti * 2 + tj[h];
+                    const bool acc =
+                        live2[h] && slot[h] != (int)t && !(r2 > pt.cut2[tt] || r2 == 0.0);
+                    const unsigned msk = __ballot_sync(0xffffffffu, acc);
+                    if (acc) {
+                        const int q = nq + __popc(msk & lt);
+                        B.dx[q] = dx0;
+                        B.dy[q] = dx1;
+                        B.r2[q] = r2;
+                        B.tt[q] = (unsigned char)tt;
+                    }
+                    nq += __popc(msk);
+                }
+            }
+        };
+        // ring rows in reference order (o1 outer; the periodic de-duplication
+        // and wall skips of motion.py:206-222).  The cells of a ring row are
+        // consecutive in the cell table unless the row wraps around a periodic
+        // x axis: then one slot range per row, else cell by cell (o0 inner).
+        const bool xrow = !g.per0 || (g.n0 >= 3 && cx >= 1 && cx + 1 < g.n0);
+        const int c0 = cx >= 1 ? cx - 1 : 0, c1 = cx + 1 < g.n0 ? cx + 1 : g.n0 - 1;
+        for (int o1 = -1; o1 <= 1; o1++) {
+            int g1 = cy + o1;
+            if (g.per1) {
+                if ((g.n1 == 1 && o1 != 0) || (g.n1 == 2 && o1 == 1)) continue;
+                g1 = g1 < 0 ? g1 + g.n1 : (g1 >= g.n1 ? g1 - g.n1 : g1);
+            } else if (g1 < 0 || g1 >= g.n1) {
+                continue;
+            }
+            if (xrow) {
+                segment(starts[g1 * g.n0 + c0], starts[g1 * g.n0 + c1 + 1]);
+                continue;
+            }
+            for (int o0 = -1; o0 <= 1; o0++) {
+                int g0 = cx + o0;
+                if ((g.n0 == 1 && o0 != 0) || (g.n0 == 2 && o0 == 1)) continue;
+                g0 = g0 < 0 ? g0 + g.n0 : (g0 >= g.n0 ? g0 - g.n0 : g0);
+                const int f = g1 * g.n0 + g0;
+                segment(starts[f], starts[f + 1]);
+            }
+        }
+        flush();
+        const double fx = __shfl_sync(0xffffffffu, fsum, 0);
+        const double fy = __shfl_sync(0xffffffffu, fsum, 1);
+        if (lane == 0) reinterpret_cast<double2 *>(out)[order[t]] = make_double2(fx, fy);
+    }
+}
+
 // the reference pair loop of one particle, summed (the rare fallback)
 template <class P>
 __device__ __noinline__ double2 pair_loop_sum(const P *__restrict__ pos,
@@ -475,6 +602,22 @@ int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *ty
     const int *order = ctx->order.as<int>(), *starts = ctx->starts.as<int>();
     // bin_particles left the positions (and types) in cell order in ctx->spos / stype
     uint8_t *stype = type ? ctx->stype.as<uint8_t>() : nullptr;
+    // dense rings (>= 48 candidates per owner on average): a warp per owner
+    // (CS_WARP_FORCES=0/1 overrides, read per call: tests run every kernel on the same inputs)
+    const char *we = getenv("CS_WARP_FORCES");
+    const double cand = 9.0 * (double)n / ((double)g.n0 * (double)g.n1);
+    if (we ? atoi(we) != 0 : (n > RING_MAX_N && cand >= 48.0)) {
+        const int blocks = grid_for(n, WF_WARPS, 148 * 64);
+        if (prec == CS_F64)
+            k_soft_forces_warp<double><<<blocks, 32 * WF_WARPS, 0, ctx->stream>>>(
+                order, starts, n, g, pt, out, st, ctx->spos.as<double>(), stype);
+        else
+            k_soft_forces_warp<float><<<blocks, 32 * WF_WARPS, 0, ctx->stream>>>(
+                order, starts, n, g, pt, out, st, ctx->spos.as<float>(), stype);
+        CS_LAUNCH_CHECK();
+        ctx->launches += 1;
+        return CS_OK;
+    }
     static const int ring_env = getenv("CS_RING_FORCES") ? atoi(getenv("CS_RING_FORCES")) : -1;
     const bool ring = ring_env >= 0 ? ring_env != 0 : n <= RING_MAX_N;
     if (ring) {

@@ -92,12 +92,17 @@ def test_pair_sets_bit_exact_hetero(periodic):
     assert np.array_equal(f, f_or)
 
 
+@pytest.mark.parametrize("kernel", ["auto", "warp", "lane"])
 @pytest.mark.parametrize("case", ["cfg2_periodic", "cfg2_walls", "dense_ring", "two_cells"])
-def test_dense_cell_forces_bitwise(case):
+def test_dense_cell_forces_bitwise(case, kernel, monkeypatch):
     """Dense cell lists: BASELINE cfg2's density (~40 particles per cell,
     ~360 ring candidates, ~75 accepted pairs per particle, periodic and
     walled), ~1500-candidate rings, and 2-cell periodic axes (ring
-    de-duplication), bitwise against the oracle."""
+    de-duplication), bitwise against the oracle -- with the kernel the
+    library picks (cfg2: a warp per owner), with the warp-per-owner kernel
+    forced and with the lane-per-owner kernels."""
+    if kernel != "auto":
+        monkeypatch.setenv("CS_WARP_FORCES", "1" if kernel == "warp" else "0")
     rng = np.random.default_rng({"cfg2_periodic": 21, "cfg2_walls": 22, "dense_ring": 23,
                                  "two_cells": 24}[case])
     periodic = case != "cfg2_walls"

@@ -606,7 +606,7 @@ int launch_soft_forces(cs_ctx *ctx, int prec, const void *pos, const uint8_t *ty
     // (CS_WARP_FORCES=0/1 overrides, read per call: tests run every kernel on the same inputs)
     const char *we = getenv("CS_WARP_FORCES");
     const double cand = 9.0 * (double)n / ((double)g.n0 * (double)g.n1);
-    if (we ? atoi(we) != 0 : (n > RING_MAX_N && cand >= 48.0)) {
+    if (we ? atoi(we) != 0 : cand >= 48.0) {
         const int blocks = grid_for(n, WF_WARPS, 148 * 64);
         if (prec == CS_F64)
             k_soft_forces_warp<double><<<blocks, 32 * WF_WARPS, 0, ctx->stream>>>(

@@ -44,6 +44,7 @@
 // Deposits accumulate w * 2^22 (w = CIC corner weight) in int32 per node:
 // integer addition is associative, so the field is run-to-run
 // deterministic; resolution 2.4e-7 of a particle mass per contribution.
+#include <stddef.h>
 #include <stdlib.h>
 
 #include <utility>
@@ -516,17 +517,33 @@ __device__ __forceinline__ float4 upd_finish(const FastArgs &a, DevStatus *st, i
     return out;
 }
 
-constexpr int ACC_MAX = 8;          // accepted pairs buffered per particle
+#ifndef CS_ACC_MAX
+#define CS_ACC_MAX 8
+#endif
+constexpr int ACC_MAX = CS_ACC_MAX;  // accepted pairs buffered per particle
 constexpr int WARPS_PER_BLOCK = 4;  // k_fast_forces block = 128 threads
 constexpr int QCAP = 32 * ACC_MAX;  // pair-term queue per warp
+// candidates of a ring the force kernel walks itself; beyond it the owner is
+// deferred.  The walk stores the j-th prefilter hit of a lane at int index
+// j * 32 + lane from the start of the warp's queue: (TOT_MAX - 1) hits stay
+// inside ck + oj + tx + ty = 5.5 ACC_MAX rows of 32 ints
+constexpr int TOT_MAX = ACC_MAX * 11 / 2;
 
-struct WarpQueue {
+// store to a shared-memory byte address (the walk's hit column: one 32-bit
+// address register, no generic pointer to carry along)
+__device__ __forceinline__ void sts_i32(unsigned addr, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+struct WarpQueue {  // (member order matters to the walk's stores: TOT_MAX)
     int ck[QCAP];                  // queue entry -> partner slot
     unsigned short oj[QCAP];       // queue entry -> owner term index j * 32 + lane
     double tx[QCAP], ty[QCAP];     // owner term index -> pair term (lane regions)
     float ox[32], oy[32];          // owner coordinates
     int oti[32];
 };
+static_assert(offsetof(WarpQueue, ox) >= sizeof(int) * 32 * (TOT_MAX - 1) && offsetof(WarpQueue, ck) == 0,
+              "the walk's hit columns must end before the owner arrays");
 
 // Pair forces of every sorted slot -> force[t] (binary64).
 //
@@ -558,6 +575,7 @@ k_fast_forces(DevStatus *st, int step) {
     const FastArgs &a = cA;
     __shared__ WarpQueue wq_all[WARPS_PER_BLOCK];
     WarpQueue &wq = wq_all[threadIdx.x >> 5];
+    int *wq_ck = reinterpret_cast<int *>(&wq);  // ck, running on into oj / tx / ty (TOT_MAX)
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;  // lanes below this one
     const bool dead = st->abort != 0;
@@ -615,6 +633,10 @@ k_fast_forces(DevStatus *st, int step) {
                 }
                 tot = (se[0] - sa[0]) + (se[1] - sa[1]) + (se[2] - sa[2]);
                 if (a.debug & 128) tot = 0;  // timing diagnostic: no walk
+                if (tot > TOT_MAX) {  // dense ring: the warp-per-owner pass (see the walk)
+                    generic = true;
+                    tot = 0;
+                }
 #pragma unroll
                 for (int r = 2; r >= 0; r--) {  // push front, skipping empty rows
                     if (se[r] > sa[r]) {
@@ -630,8 +652,23 @@ k_fast_forces(DevStatus *st, int step) {
         }
         // ---- 1. candidate walk (warp-uniform trip count): a prefilter hit
         // goes into the lane's own column of the queue's slot array,
-        // ck[j * 32 + lane] = partner slot of the lane's j-th hit
+        // ck[j * 32 + lane] = partner slot of the lane's j-th hit.  A hit is
+        // 0 < d2 <= c, tested as one unsigned compare of the bit patterns
+        // (d2 >= +0 and c > 0: binary32 order is integer order, and
+        // bits(+0) - 1 wraps to the top): d2 == 0 is the owner itself -- also
+        // the record a lane past its own tot re-reads -- or a partner at the
+        // same stored coordinates, whose exact r2 == 0 the reference skips
+        // (motion.py:238).  The store is not bounded by ACC_MAX: a ring has at
+        // most TOT_MAX candidates, and rows 8 .. TOT_MAX - 1 of the lane's
+        // column fall into oj / tx / ty of the warp's own queue, which are
+        // written and read only after the walk (owners with more than
+        // ACC_MAX hits are deferred below).
+        const int c0m = cf0 > 0.f ? __float_as_int(cf0) - 1 : 0;
+        const int c1m = cf1 > 0.f ? __float_as_int(cf1) - 1 : 0;
+        const unsigned qp0 = (unsigned)__cvta_generic_to_shared(wq_ck + lane);
+        unsigned qp = qp0;  // shared-memory byte address of the lane's next hit
         const int totmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
+#pragma unroll 2
         for (int j = 0; j < totmax; j += 2) {
             const int ka = k;
             if (++k == kend) {
@@ -651,15 +688,21 @@ k_fast_forces(DevStatus *st, int step) {
             const float4 qb = __ldg(rec + (j + 1 < tot ? kb : t32));
             const float dax = qa.x - xf, day = qa.y - yf;
             const float dbx = qb.x - xf, dby = qb.y - yf;
-            const float ca = (__float_as_uint(qa.z) >> 31) ? cf1 : cf0;
-            const float cb = (__float_as_uint(qb.z) >> 31) ? cf1 : cf0;
-            const bool ha = j < tot && ka != t32 && fmaf(dax, dax, day * day) <= ca;
-            const bool hb = j + 1 < tot && kb != t32 && fmaf(dbx, dbx, dby * dby) <= cb;
-            if (ha && nacc < ACC_MAX) wq.ck[nacc * 32 + lane] = ka;
-            nacc += ha;
-            if (hb && nacc < ACC_MAX) wq.ck[nacc * 32 + lane] = kb;
-            nacc += hb;
+            const unsigned ca = (unsigned)((__float_as_int(qa.z) < 0) ? c1m : c0m);
+            const unsigned cb = (unsigned)((__float_as_int(qb.z) < 0) ? c1m : c0m);
+            const bool ha = (unsigned)(__float_as_int(fmaf(dax, dax, day * day)) - 1) <= ca;
+            const bool hb = (unsigned)(__float_as_int(fmaf(dbx, dbx, dby * dby)) - 1) <= cb;
+            if (ha) {
+                sts_i32(qp, ka);
+                qp += 128;
+            }
+            if (hb) {
+                sts_i32(qp, kb);
+                qp += 128;
+            }
         }
+        asm volatile("" ::: "memory");  // the hit stores above precede the queue reads below
+        nacc = (int)(qp - qp0) >> 7;
         // the hits compacted level by level into queue entries (in place:
         // entry e <= j * 32 + lane, and a level is read before it is written),
         // each tagged with the owner's term index j * 32 + lane

@@ -1328,7 +1328,9 @@ k_bucket_sort(const Rec *__restrict__ region, const int *__restrict__ boff, long
 #endif
 constexpr int DEP_ROWS = CS_DEP_ROWS;  // grid rows per block of k_fast_deposit_rows
 
-template <int NT>  // threads per block (launch bound: registers)
+// P2: the grid size is a power of two (every BASELINE grid): node and window
+// indices wrap with a mask instead of the compare / add sequences.
+template <int NT, bool P2>  // threads per block (launch bound: registers)
 __global__ void __launch_bounds__(NT)
 k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts, BinGeom g,
                     GridGeom gg, ExactDiv d0, ExactDiv d1, unsigned bits0, unsigned bits1,
@@ -1369,22 +1371,30 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
             // the periodic branch of cic_stencil, y first (the row filter)
             const double u1 = ediv(dsub((double)rv.y, gg.lo1), d1);
             const double base1 = floor(u1);
-            const int b1 = wrap_index(base1, n);
-            const int c1 = b1 + 1 == n ? 0 : b1 + 1;
+            // (P2: base1 lies in [-1, n] for in-domain records; the mask is
+            // pymod for every int, and a non-finite coordinate -- the run is
+            // already stopped -- saturates)
+            const int b1 = P2 ? ((int)base1 & (n - 1)) : wrap_index(base1, n);
+            const int c1 = P2 ? ((b1 + 1) & (n - 1)) : (b1 + 1 == n ? 0 : b1 + 1);
             // rows of this block's window, if any (j0 in [-n, 2n): two wraps at most)
             int rb = b1 - j0, rc = c1 - j0;
-            rb += rb < 0 ? n : (rb >= n ? -n : 0);
-            rc += rc < 0 ? n : (rc >= n ? -n : 0);
-            rb += rb < 0 ? n : 0;
-            rc += rc < 0 ? n : 0;
+            if (P2) {
+                rb &= n - 1;
+                rc &= n - 1;
+            } else {
+                rb += rb < 0 ? n : (rb >= n ? -n : 0);
+                rc += rc < 0 ? n : (rc >= n ? -n : 0);
+                rb += rb < 0 ? n : 0;
+                rc += rc < 0 ? n : 0;
+            }
             const bool hb = rb < DEP_ROWS, hc = rc < DEP_ROWS;
             if (!hb && !hc) continue;
             const double f1 = dsub(u1, base1);
             const double u0 = ediv(dsub((double)rv.x, gg.lo0), d0);
             const double base0 = floor(u0);
             const double f0 = dsub(u0, base0);
-            const int b0 = wrap_index(base0, n);
-            const int c0 = b0 + 1 == n ? 0 : b0 + 1;
+            const int b0 = P2 ? ((int)base0 & (n - 1)) : wrap_index(base0, n);
+            const int c0 = P2 ? ((b0 + 1) & (n - 1)) : (b0 + 1 == n ? 0 : b0 + 1);
             const double g0 = dsub(1.0, f0);
 #pragma unroll
             for (int h = 0; h < 2; h++) {
@@ -1720,17 +1730,19 @@ static int fast_deposit_rows(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p,
     const int smem = (int)(DEP_ROWS * 2 * sizeof(int) * (size_t)gg.n);
     static int smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
-        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows<512>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CS_CUDA(cudaFuncSetAttribute(k_fast_deposit_rows<1024>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (auto k : {k_fast_deposit_rows<512, false>, k_fast_deposit_rows<512, true>,
+                       k_fast_deposit_rows<1024, false>, k_fast_deposit_rows<1024, true>})
+            CS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         smem_set = smem;
     }
     const int jbase = f->slab ? f->dep_j0 : 0, jrows = f->slab ? f->dep_rows : gg.n;
     // a block's row accumulators take 64 KB at 4096 nodes per row (3 blocks of
     // 512 threads per SM) and 128 KB at 8192 (one block per SM: 1024 threads)
     const int threads = smem > 100 * 1024 ? 1024 : 512;
-    auto kern = threads == 1024 ? k_fast_deposit_rows<1024> : k_fast_deposit_rows<512>;
+    const bool p2 = (gg.n & (gg.n - 1)) == 0 && !getenv("CS_DEP_NO_P2");
+    auto kern = threads == 1024
+                    ? (p2 ? k_fast_deposit_rows<1024, true> : k_fast_deposit_rows<1024, false>)
+                    : (p2 ? k_fast_deposit_rows<512, true> : k_fast_deposit_rows<512, false>);
     kern<<<(jrows + DEP_ROWS - 1) / DEP_ROWS, threads, smem, ctx->stream>>>(
         f->rec[f->cur].as<Rec>(), cell_table(f, f->cur), f->g, gg, make_exact_div(d0),
         make_exact_div(d1), bits[0], bits[1], f->rho_q.as<int>(),

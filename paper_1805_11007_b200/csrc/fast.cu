@@ -1339,7 +1339,7 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
                     int cb0, int cb1) {
     // (slab mode: grid rows jbase .. jbase + jrows - 1, mod n, from the
     // particles of the own cell rows [cb0, cb1) only; single domain: 0, n, -1)
-    extern __shared__ int acc[];  // [DEP_ROWS][2][n]
+    extern __shared__ __align__(16) int acc[];  // [DEP_ROWS][2][n]
     // exact overflow checks only when the bucket sort saw a cell populated
     // beyond the conservative bound (returning atomics cost ~20 % here)
     const bool exact = *exact_flag != 0;
@@ -1348,7 +1348,13 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
     if (blockIdx.x == 0 && threadIdx.x == 0) *other_flag = 0;  // the next step's flag
     const int n = gg.n, j0 = jbase + blockIdx.x * DEP_ROWS;
     const long long m = (long long)n * n;
-    for (int i = threadIdx.x; i < DEP_ROWS * 2 * n; i += blockDim.x) acc[i] = 0;
+    const bool vec4 = (n & 3) == 0;  // rows of whole int4s (accumulators and both grids)
+    if (vec4) {
+        for (int i = threadIdx.x; i < DEP_ROWS * 2 * n / 4; i += blockDim.x)
+            reinterpret_cast<int4 *>(acc)[i] = make_int4(0, 0, 0, 0);
+    } else {
+        for (int i = threadIdx.x; i < DEP_ROWS * 2 * n; i += blockDim.x) acc[i] = 0;
+    }
     __syncthreads();
     // cell rows that can hold a particle with y in [lo + (j0-1) d, lo + (j0+R) d):
     // the cell index is monotone in y, so the rows of the (slightly widened)
@@ -1359,9 +1365,10 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
     const int cy1 = (int)floor(ddiv(dsub(yhi, g.lo1), g.eff1));
     const float4 *r4 = reinterpret_cast<const float4 *>(rec);
     for (int cyw = cy0; cyw <= cy1; cyw++) {
-        int cy = cyw % g.n1;
-        if (cy < 0) cy += g.n1;
         if (cyw - cy0 >= g.n1) break;  // fewer cell rows than the window
+        int cy = cyw;  // (the window starts within one period of the domain)
+        while (cy < 0) cy += g.n1;
+        while (cy >= g.n1) cy -= g.n1;
         if (cb0 >= 0 && (cy < cb0 || cy >= cb1)) continue;  // ghost rows: other ranks'
         const int kb = starts[(long long)cy * g.n0], ke = starts[(long long)(cy + 1) * g.n0];
         for (int k = kb + threadIdx.x; k < ke; k += blockDim.x) {
@@ -1438,9 +1445,17 @@ k_fast_deposit_rows(const Rec *__restrict__ rec, const int *__restrict__ starts,
         int j = (j0 + r) % n;
         if (j < 0) j += n;
         int *ra = rho_q + (long long)j * n, *rbp = rho_q + m + (long long)j * n;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            ra[i] = acc[r * 2 * n + i];
-            rbp[i] = acc[r * 2 * n + n + i];
+        if (vec4) {
+            const int4 *sa = reinterpret_cast<const int4 *>(acc + r * 2 * n);
+            for (int i = threadIdx.x; i < n / 4; i += blockDim.x) {
+                reinterpret_cast<int4 *>(ra)[i] = sa[i];
+                reinterpret_cast<int4 *>(rbp)[i] = sa[n / 4 + i];
+            }
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                ra[i] = acc[r * 2 * n + i];
+                rbp[i] = acc[r * 2 * n + n + i];
+            }
         }
     }
 }

@@ -106,6 +106,31 @@ def test_sorted_equals_direct_bitwise_clustered(periodic):
     assert torch.equal(sa["pos"], sb["pos"])
 
 
+@pytest.mark.parametrize("r_b", [0.0035, 0.005, 0.0075])
+def test_sorted_equals_direct_bitwise_dense_rings(r_b):
+    """Uniform systems of 2, 4 and 9 particles per cell (rings of ~18, ~36 and
+    ~83 candidates): the force walk's hit columns run past the 8 buffered hits
+    into the rest of the warp's queue, owners with more than 8 hits and rings
+    beyond the walk's candidate bound (44) go to the deferred warp-per-owner
+    pass -- the direct engine's positions bit for bit (a small dt keeps the
+    overlapping particles' displacements inside the box)."""
+    rng = np.random.default_rng(21)
+    n = 40_000
+    pos = (-0.5 + rng.random((n, 2))).astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    xi = rng.standard_normal((3, n, 2)).astype(np.float32)
+    radii = (r_b / 2, r_b)
+    a, sa = _sim(pos, sp, engine="sorted", field=False, radii=radii, dt=1e-10)
+    b, sb = _sim(pos, sp, engine="direct", field=False, radii=radii, dt=1e-10)
+    x = torch.as_tensor(xi, device="cuda")
+    a.step(x, 3)
+    b.step(x, 3)
+    a.export_state()
+    assert a.status().code == 0 and b.status().code == 0
+    assert torch.equal(sa["pos"], sb["pos"])
+    assert not torch.equal(sa["pos"], torch.as_tensor(pos, device="cuda"))
+
+
 @pytest.mark.parametrize("pregather", [False, True])
 @pytest.mark.parametrize("clustered", [False, True])
 def test_block_call_equals_single_step_calls_bitwise(clustered, pregather, monkeypatch):
@@ -310,14 +335,21 @@ def test_sorted_engine_dense_cells_below_the_node_limit_run():
     assert a.status().code == 0
 
 
-def test_row_gather_deposit_bitwise_equals_atomic_deposit(monkeypatch):
+@pytest.mark.parametrize("n_c,generic_wrap", [(512, False), (512, True), (384, False),
+                                              (250, False)])
+def test_row_gather_deposit_bitwise_equals_atomic_deposit(n_c, generic_wrap, monkeypatch):
     """k_fast_deposit_rows (periodic grids: deposit gathered per grid row, no
     atomics to HBM) against the atomic deposit: identical fixed-point grids,
-    hence identical fields and positions, over several steps."""
-    n, n_c = 60_000, 512
+    hence identical fields and positions, over several steps -- on a
+    power-of-two grid with the mask wraps and with the generic ones
+    (CS_DEP_NO_P2), and on grids that are not powers of two (384: int4 row
+    copies; 250: scalar ones; their solve is cuFFT's)."""
+    n = 60_000
     pos, sp, xi = _inputs(n, 13)
     x = torch.as_tensor(xi, device="cuda")
     out = {}
+    if generic_wrap:
+        monkeypatch.setenv("CS_DEP_NO_P2", "1")
     for mode in ("rows", "atomic"):
         if mode == "atomic":
             monkeypatch.setenv("CS_ATOMIC_DEPOSIT", "1")
@@ -329,6 +361,7 @@ def test_row_gather_deposit_bitwise_equals_atomic_deposit(monkeypatch):
         assert a.status().code == 0
         out[mode] = {k: sa[k].clone() for k in ("pos", "c", "grad", "rho_a", "rho_b")}
     monkeypatch.delenv("CS_ATOMIC_DEPOSIT", raising=False)
+    monkeypatch.delenv("CS_DEP_NO_P2", raising=False)
     for k in out["rows"]:
         assert torch.equal(out["rows"][k], out["atomic"][k]), k
 

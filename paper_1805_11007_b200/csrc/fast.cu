@@ -1934,7 +1934,13 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         // with the field solve running concurrently (side stream), leave one
         // block's worth of registers per SM to its kernels
-        const int per_sm = (c.overlap && resident > 1) ? resident - 1 : resident;
+        static int leave = -1;  // CS_FORCE_LEAVE: resident blocks per SM left to the side stream
+        if (leave < 0) {
+            const char *e = getenv("CS_FORCE_LEAVE");
+            leave = e ? atoi(e) : 1;
+        }
+        const int per_sm =
+            c.overlap ? (resident - leave > 1 ? resident - leave : 1) : resident;
         const long long want_f = (n + 127) / 128;
         const int grid =
             (int)(want_f < (long long)sms * per_sm ? want_f : (long long)sms * per_sm);

@@ -182,10 +182,13 @@ __device__ __forceinline__ double d1_per(double cm, double cp, bool wrapped, con
     return wrapped ? dadd(dadd(0.0, ap), am) : dadd(dadd(0.0, am), ap);
 }
 
+// A block owns strips of R consecutive rows x 1024 columns and slides down
+// them with rows j-1, j, j+1 of its four columns in registers: one new
+// 16-byte load per row instead of three (R = 1: a row per strip).
 __global__ void __launch_bounds__(256)
 k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double wcell,
                 float *__restrict__ grad, DevStatus *st, int *__restrict__ zero_q, int step,
-                int jbase = 0, int jrows = -1, int own0 = 0, int own1 = 1 << 30) {
+                int R, int jbase = 0, int jrows = -1, int own0 = 0, int own1 = 1 << 30) {
     // (slab mode: the rows jbase .. jbase + jrows - 1 (mod n); the field checks
     // count the own rows [own0, own1) only)
     const bool dead = st->abort != 0;
@@ -195,19 +198,24 @@ k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double
     int bad = 0, anyneg = 0;
     if (jrows < 0) jrows = n;
     if (dead) jrows = 0;
-    for (int jj = blockIdx.x; jj < jrows; jj += gridDim.x) {
-        int j = (jbase + jj) % n;
+    const int nchunk = (n4 + 255) >> 8, ngroups = (jrows + R - 1) / R;
+    for (int sidx = blockIdx.x; sidx < ngroups * nchunk; sidx += gridDim.x) {
+        const int rg = sidx / nchunk, t = (sidx - rg * nchunk) * 256 + threadIdx.x;
+        if (t >= n4) continue;
+        const int jj0 = rg * R, jj1 = jj0 + R < jrows ? jj0 + R : jrows;
+        int j = (jbase + jj0) % n;
         if (j < 0) j += n;
-        const bool check = j >= own0 && j < own1;
-        const int jm = j == 0 ? n - 1 : j - 1, jp = j == n - 1 ? 0 : j + 1;
-        const float4 *row = reinterpret_cast<const float4 *>(c + (long long)j * n);
-        const float4 *rdn = reinterpret_cast<const float4 *>(c + (long long)jm * n);
-        const float4 *rup = reinterpret_cast<const float4 *>(c + (long long)jp * n);
-        for (int t = threadIdx.x; t < n4; t += blockDim.x) {
-            const int i0 = 4 * t;
-            const float4 v = row[t], dn = rdn[t], up = rup[t];
-            const float left = c[(long long)j * n + (i0 == 0 ? n - 1 : i0 - 1)];
-            const float right = c[(long long)j * n + (i0 + 4 == n ? 0 : i0 + 4)];
+        const int i0 = 4 * t;
+        const int il = i0 == 0 ? n - 1 : i0 - 1, ir = i0 + 4 == n ? 0 : i0 + 4;
+        const float4 *c4 = reinterpret_cast<const float4 *>(c);
+        float4 dn = c4[(long long)(j == 0 ? n - 1 : j - 1) * n4 + t];
+        float4 v = c4[(long long)j * n4 + t];
+        for (int jj = jj0; jj < jj1; jj++) {
+            const int jp = j == n - 1 ? 0 : j + 1;
+            const float4 up = c4[(long long)jp * n4 + t];
+            const float left = c[(long long)j * n + il];
+            const float right = c[(long long)j * n + ir];
+            const bool check = j >= own0 && j < own1;
             const float cv[6] = {left, v.x, v.y, v.z, v.w, right};
             const float dv[4] = {dn.x, dn.y, dn.z, dn.w}, uv[4] = {up.x, up.y, up.z, up.w};
             double gx[4], gy[4];
@@ -231,6 +239,9 @@ k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double
                 *reinterpret_cast<int4 *>(zero_q + l) = make_int4(0, 0, 0, 0);
                 *reinterpret_cast<int4 *>(zero_q + l + m) = make_int4(0, 0, 0, 0);
             }
+            dn = v;
+            v = up;
+            j = jp;
         }
     }
     __shared__ double s_neg[8];
@@ -263,6 +274,20 @@ k_gradient_per4(const float *__restrict__ c, int n, D1Coef kx, D1Coef ky, double
 }
 
 
+// rows per strip and grid of k_gradient_per4: strips of up to 8 rows, but at
+// least about two blocks per resident slot (8 blocks of 256 threads per SM);
+// measured at 4096^2 (CS_GRAD_ROWS): 1 row 61.7, 4: 53.6, 8: 53.8, 13: 60.3,
+// 16: 56.1 us
+static void gradient_per4_shape(int n, int jrows, int *R, int *grid) {
+    const int nchunk = ((n >> 2) + 255) >> 8, slots = 148 * 8;
+    int r = (int)((long long)jrows * nchunk / (2 * slots));
+    if (const char *e = getenv("CS_GRAD_ROWS")) r = atoi(e);
+    r = r < 1 ? 1 : (r > 8 && !getenv("CS_GRAD_ROWS") ? 8 : (r > 16 ? 16 : r));
+    const long long strips = (long long)((jrows + r - 1) / r) * nchunk;
+    *R = r;
+    *grid = (int)(strips < 1 ? 1 : (strips < slots ? strips : slots));
+}
+
 // slab mode (periodic binary32 grids): the gradient of the grid rows
 // jbase .. jbase + jrows - 1 (mod n) from c rows one wider on either side;
 // the field checks of the own rows [own0, own1)
@@ -273,10 +298,10 @@ int launch_gradient_rows(cs_ctx *ctx, const float *c, const GridGeom &gg, float 
         return CS_ERR_PARAM;
     }
     const D1Coef kx = make_d1(gg.d0), ky = make_d1(gg.d1);
-    const int g2 = jrows < 148 * 8 ? jrows : 148 * 8;
-    k_gradient_per4<<<g2 > 0 ? g2 : 1, 256, 0, ctx->stream>>>(c, gg.n, kx, ky, gg.d0 * gg.d1,
-                                                              grad, st, nullptr, step, jbase,
-                                                              jrows, own0, own1);
+    int R, g2;
+    gradient_per4_shape(gg.n, jrows, &R, &g2);
+    k_gradient_per4<<<g2, 256, 0, ctx->stream>>>(c, gg.n, kx, ky, gg.d0 * gg.d1, grad, st,
+                                                 nullptr, step, R, jbase, jrows, own0, own1);
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;
@@ -293,12 +318,15 @@ int launch_gradient(cs_ctx *ctx, int prec, const void *c, const GridGeom &gg, vo
     if (prec == CS_F64)
         k_gradient<double><<<g2, B, 0, ctx->stream>>>(
             (const double *)c, gg.n, gg.per, kx, ky, wcell, (double *)grad, st, zero_q, step);
-    else if (gg.per && st && gg.n % 4 == 0 && gg.n >= 8 && !getenv("CS_GRAD_GENERIC"))
-        k_gradient_per4<<<g2, B, 0, ctx->stream>>>((const float *)c, gg.n, kx, ky, wcell,
-                                                  (float *)grad, st, zero_q, step);
-    else
+    else if (gg.per && st && gg.n % 4 == 0 && gg.n >= 8 && !getenv("CS_GRAD_GENERIC")) {
+        int R, g4;
+        gradient_per4_shape(gg.n, gg.n, &R, &g4);
+        k_gradient_per4<<<g4, B, 0, ctx->stream>>>((const float *)c, gg.n, kx, ky, wcell,
+                                                  (float *)grad, st, zero_q, step, R);
+    } else {
         k_gradient<float><<<g2, B, 0, ctx->stream>>>(
             (const float *)c, gg.n, gg.per, kx, ky, wcell, (float *)grad, st, zero_q, step);
+    }
     CS_LAUNCH_CHECK();
     ctx->launches += 1;
     return CS_OK;

@@ -421,6 +421,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-perf-mode", action="store_true")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the N > 1 slab path (NCCL transports) even with one rank")
     ap.add_argument("--rebalance-every", type=int, default=25,
                     help="N > 1: re-balance the y-slabs every M steps (0: never)")
     args = ap.parse_args()
@@ -436,15 +438,19 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    slabs_on = (world > 1 or args.force_slabs) and cfg["prec"] == "fp32"
+    if world > 1 or slabs_on:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    if world > 1 and cfg["prec"] == "fp32":
+    if slabs_on:
         run_slabs(args, cfg, rank, world, barrier)
         dist.destroy_process_group()
         return
@@ -647,12 +653,14 @@ def run_slabs(args, cfg, rank, world, barrier):
     stream = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    launches = 0
     with clocks:
         barrier()
         torch.cuda.synchronize()
         a.record(stream)
         for k in range(K):
             eng.step(xi[W + k], tr)
+            launches += eng.sim.launches()  # forces / update / sort / deposit of the step
             if args.rebalance_every and (k + 1) % args.rebalance_every == 0 and k + 1 < K:
                 eng.rebalance(tr, eng.n1, cfg["n_c"] if cfg["field"] else None)
         b.record(stream)
@@ -678,6 +686,7 @@ def run_slabs(args, cfg, rank, world, barrier):
                                          f"(re-balanced every {args.rebalance_every} steps), "
                                          "even grid-row split, NCCL all-to-all exchanges"),
             "engine": "sorted (slab mode)", "clocks": clocks.summary(),
+            "gpu_launches": launches,  # rank 0's particle kernels (the field passes not counted)
             "rank0_owned": hi - lo,
             "e2e": None,
             "note": "N > 1: one slab-decomposed system (strong scaling); the end-to-end "

@@ -2027,8 +2027,9 @@ void fast_begin_call(cs_fast *f) {
 // ---- y-slab mode host side ------------------------------------------------
 int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long long n,
                      cudaStream_t stream) {
-    if (world < 2 || rank < 0 || rank >= world) {
-        set_error("slab mode: world >= 2 and 0 <= rank < world");
+    if (world < 1 || rank < 0 || rank >= world) {  // (world 1: one slab, no ghosts -- the
+                                                   // transports' code path on one rank)
+        set_error("slab mode: world >= 1 and 0 <= rank < world");
         return CS_ERR_PARAM;
     }
     const int n1 = f->g.n1;

@@ -52,7 +52,7 @@ def _bounds(pos, mp, dom, world):
     return slabs.SlabLayout.balanced(counts, world).bounds
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("clustered", [False, True])
 def test_slab_engine_equals_single_domain_bitwise(world, clustered):
     rng = np.random.default_rng(10 + world)
@@ -123,7 +123,7 @@ def _field_state(pos, sp, c0, n_c, shared=None):
     return st
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("clustered", [False, True])
 def test_slab_engine_with_field_equals_single_domain_bitwise(world, clustered):
     """The distributed field (deposit windows added into their owners' rows

@@ -540,10 +540,16 @@ class NcclField:
         kl = int(p.kx[r + 1] - p.kx[r])
         f.deposit_in(self._a2a(f.deposit_out(), [2 * n * rows.numel() for rows in f.dep_recv]))
         f.spec_rows(inverse=False)
-        f.spec_in_blocks(self._a2a(f.spec_out(), [kl * p.rp * 2] * W))
+        # the two spectrum transposes move straight between the engine's
+        # buffers: the kx slices of spec (nh, rp, 2) are consecutive and so are
+        # the per-rank blocks (W, kl, rp, 2), i.e. the all-to-all's own layout
+        by_kx = [int(p.kx[q + 1] - p.kx[q]) * p.rp * 2 for q in range(W)]
+        by_rank = [kl * p.rp * 2] * W
+        dist.all_to_all_single(f.blocks.view(-1), f.spec.view(-1), by_rank, by_kx,
+                               group=self.group)
         f.cols()
-        f.blocks_in_spec(self._a2a(f.blocks_out(),
-                                   [int(p.kx[q + 1] - p.kx[q]) * p.rp * 2 for q in range(W)]))
+        dist.all_to_all_single(f.spec.view(-1), f.blocks.view(-1), by_kx, by_rank,
+                               group=self.group)
         f.spec_rows(inverse=True)
         f.c_in(self._a2a(f.c_out(), [n * rows.numel() for rows in f.c_recv]))
         f.gradient()

@@ -1,3 +1,8 @@
+# Force-kernel queue depth sweep (DESIGN 6a): bench line, kernel time, L1 / L2 hit rates,
+# resident warps and instruction count of k_fast_forces / k_fast_forces_generic for the default
+# build and the CS_ACC_MAX = 6 / 4 variants.  Build the variants first (here, no GPU needed):
+#   python -c "from paper_1805_11007_b200 import build as b; \
+#     [b.build(out=f'paper_1805_11007_b200/_build/var/acc{k}.so', extra=[f'-DCS_ACC_MAX={k}']) for k in (6, 4)]"
 export PYTHONPATH=.
 mkdir -p gpurun_out/s5
 M=gpu__time_duration.sum,l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum

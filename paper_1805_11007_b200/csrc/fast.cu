@@ -1636,9 +1636,14 @@ int fast_create(cs_fast **out, long long n, const BinGeom &g, const GridGeom *gg
     if (cap > 24576 / SUBB) cap = 24576 / SUBB;
     if (const char *e = getenv("CS_BUCKET_CAP")) cap = atoll(e);  // tests: force overflows
     f->cap = (cap + 7) / 8 * 8;
-    const size_t nr = sizeof(Rec) * (size_t)(n > 0 ? n : 1);
+    // (+ 32 records: a lane past the end of the last warp's slots re-reads "its own" slot
+    // in the force walk)
+    const size_t nr = sizeof(Rec) * (size_t)((n > 0 ? n : 1) + 32);
     CS_TRY(f->rec[0].ensure(nr));
     CS_TRY(f->rec[1].ensure(nr));
+    for (int b = 0; b < 2; b++)  // the tail reads as zeros (no prefilter hit: d2 == 0)
+        CS_CUDA(cudaMemset(static_cast<char *>(f->rec[b].p) + nr - 32 * sizeof(Rec), 0,
+                           32 * sizeof(Rec)));
     CS_TRY(f->region.ensure(sizeof(Rec) * (size_t)f->nbucket * SUBB * (size_t)f->cap));
     CS_TRY(f->force.ensure(sizeof(double2) * (size_t)(n > 0 ? n : 1)));
     CS_TRY(f->gen.ensure(sizeof(int) * (size_t)(n + 2)));  // counter, run state, list

@@ -607,7 +607,8 @@ k_fast_forces(DevStatus *st, int step) {
                 if (p_live) claim_store(a, st, step, p_b, basev + p_rank, p_out);
             }
         }
-        const float xf = mer.x, yf = mer.y;
+        // (a lane past the range never hits: its d2 is NaN, above every cutoff's bit pattern)
+        const float xf = live ? mer.x : __int_as_float(0x7fc00000), yf = mer.y;
         const double x = (double)xf, y = (double)yf;
         const int ti = (int)(__float_as_uint(mer.z) >> 31);
         const float cf0 = ti ? a.cutf2[2] : a.cutf2[0];

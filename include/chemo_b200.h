@@ -368,6 +368,15 @@ int cs_slab_step_local(cs_sim *sim, const cs_sim_state *st, const void *xi);
 int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t *count);
 int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n);
 int cs_slab_finish(cs_sim *sim);
+/* packed exchange, no host round trip in the step: `seg` outbox slots and a
+ * device counter per destination rank (0: back to the tagged outbox);
+ * records [world][seg] and counts [world] as device pointers -- what an
+ * equal-split all-to-all sends as it is -- and the claim of what was received
+ * in the same layout.  More than seg records for one rank in a step stop the
+ * run with CS_SORT_OVERFLOW. */
+int cs_slab_exchange_cap(cs_sim *sim, int64_t seg);
+int cs_slab_outbox_packed(cs_sim *sim, void **recs, int32_t **counts, int64_t *seg);
+int cs_slab_claim_packed(cs_sim *sim, const void *inbox, const int32_t *counts, int64_t seg);
 /* the owned slot range of the sorted records (tests) */
 int cs_slab_range(cs_sim *sim, int64_t *lo, int64_t *hi);
 /* The field of a slab rank (periodic binary32 grid, n_c = 2^k, CIC): it owns

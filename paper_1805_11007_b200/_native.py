@@ -130,6 +130,10 @@ SIGNATURES = [
                                ctypes.POINTER(C_i64)]),
     ("cs_slab_claim", C_i32, [C_p, C_p, C_i64]),
     ("cs_slab_finish", C_i32, [C_p]),
+    ("cs_slab_exchange_cap", C_i32, [C_p, C_i64]),
+    ("cs_slab_outbox_packed", C_i32, [C_p, ctypes.POINTER(C_p), ctypes.POINTER(C_p),
+                                      ctypes.POINTER(C_i64)]),
+    ("cs_slab_claim_packed", C_i32, [C_p, C_p, C_p, C_i64]),
     ("cs_slab_range", C_i32, [C_p, ctypes.POINTER(C_i64), ctypes.POINTER(C_i64)]),
     ("cs_slab_field_config", C_i32, [C_p, C_i32, C_i32, C_i32, C_i32, C_i32, C_i32]),
     ("cs_slab_rho", C_p, [C_p]),

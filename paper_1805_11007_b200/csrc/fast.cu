@@ -122,8 +122,9 @@ struct FastArgs {
     const int *bounds;     // device: world + 1 row boundaries
     Rec *outbox;           // records for other ranks (migrants and ghosts)
     int *out_dest;         // their destination rank | kind << 30 (0 migrant, 1 ghost)
-    int *out_count;
+    int *out_count;        // [0]: records in the outbox; [1 + q]: records for rank q (packed)
     long long out_cap;
+    long long out_seg;     // packed exchange: rank q's records at outbox[q * out_seg ...) (0: off)
 };
 
 // Random gather of the step's increments: keep the 80 MB slice in L2
@@ -919,6 +920,20 @@ __device__ __noinline__ void slab_emit(const FastArgs &a, DevStatus *st, int ste
         claim_store(a, st, step, pb, atomicAdd(&a.fill[pb], 1), out);
         return;
     }
+    if (a.out_seg > 0) {
+        // packed exchange: a segment of out_seg slots per destination and its
+        // own counter -- the layout an equal-split all-to-all sends as it is,
+        // so the step needs no host round trip for the counts
+        const int e = atomicAdd(a.out_count + 1 + dest, 1);
+        if (e < a.out_seg) {
+            reinterpret_cast<float4 *>(a.outbox)[(long long)dest * a.out_seg + e] = out;
+            return;
+        }
+        atomicMin(&st->key, err_key(3, 0, CS_SORT_OVERFLOW));
+        st->abort = 1;
+        st->step = step;
+        return;
+    }
     const int e = atomicAdd(a.out_count, 1);
     if (e < a.out_cap) {
         reinterpret_cast<float4 *>(a.outbox)[e] = out;
@@ -1607,6 +1622,7 @@ struct cs_fast {
     int dep_j0 = 0, dep_rows = 0;  // slab field: the grid rows this rank deposits into
     cs::Buf range, row_owner, bounds, outbox, out_dest, out_count;
     long long out_cap = 0;
+    long long out_seg = 0;  // packed exchange: slots per destination (0: one outbox + dest tags)
 };
 
 namespace cs {
@@ -1926,6 +1942,7 @@ int fast_particles(cs_ctx *ctx, cs_fast *f, const FastStepCfg &c, const cs_sim_s
     a.out_dest = f->slab ? f->out_dest.as<int>() : nullptr;
     a.out_count = f->slab ? f->out_count.as<int>() : nullptr;
     a.out_cap = f->out_cap;
+    a.out_seg = (part & 4) ? 0 : f->out_seg;  // a re-balance can move every record: tagged outbox
     const bool fused = fast_fused(f, p);
     if (n > 0) {
         static int resident_s[2] = {0, 0};  // blocks of k_fast_forces resident per SM
@@ -2061,7 +2078,7 @@ int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long lo
     CS_TRY(f->bounds.ensure(sizeof(int) * ((size_t)world + 1)));
     const bool first = f->range.p == nullptr;  // a re-balance keeps the owned range (re-routed)
     CS_TRY(f->range.ensure(sizeof(int) * 4));
-    CS_TRY(f->out_count.ensure(sizeof(int) * 4));
+    CS_TRY(f->out_count.ensure(sizeof(int) * (size_t)(4 + world)));
     f->out_cap = n > 1024 ? n : 1024;  // every record could leave (kicks cross several slabs)
     CS_TRY(f->outbox.ensure(sizeof(Rec) * (size_t)f->out_cap));
     CS_TRY(f->out_dest.ensure(sizeof(int) * (size_t)f->out_cap));
@@ -2070,7 +2087,7 @@ int fast_slab_config(cs_fast *f, const int *bounds, int world, int rank, long lo
     CS_CUDA(cudaMemcpyAsync(f->bounds.p, b.data(), sizeof(int) * b.size(),
                             cudaMemcpyHostToDevice, stream));
     if (first) CS_CUDA(cudaMemsetAsync(f->range.p, 0, sizeof(int) * 4, stream));
-    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int) * 4, stream));
+    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int) * (size_t)(4 + world), stream));
     CS_CUDA(cudaStreamSynchronize(stream));  // the host vectors go out of scope
     return CS_OK;
 }
@@ -2124,7 +2141,66 @@ int fast_slab_outbox(cs_ctx *ctx, cs_fast *f, void **recs, int **dest, long long
 }
 
 int fast_slab_reset_outbox(cs_ctx *ctx, cs_fast *f) {
-    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int), ctx->stream));
+    CS_CUDA(cudaMemsetAsync(f->out_count.p, 0, sizeof(int) * (size_t)(1 + f->world), ctx->stream));
+    return CS_OK;
+}
+
+// Packed exchange: seg slots of the outbox per destination rank (0: back to
+// the tagged outbox).  The outbox holds out_cap >= N records.
+int fast_slab_exchange_cap(cs_fast *f, long long seg) {
+    if (seg < 0 || seg * f->world > f->out_cap) {
+        set_error("slab exchange: %lld slots per rank exceed the outbox (%lld records, %d ranks)",
+                  seg, f->out_cap, f->world);
+        return CS_ERR_PARAM;
+    }
+    f->out_seg = seg;
+    return CS_OK;
+}
+
+// device pointers of the packed outbox: records [world][seg], counts [world]
+int fast_slab_outbox_packed(cs_fast *f, void **recs, int **counts, long long *seg) {
+    *recs = f->outbox.p;
+    *counts = f->out_count.as<int>() + 1;
+    *seg = f->out_seg;
+    return CS_OK;
+}
+
+// the records received in packed form (segment s = from rank s, counts[s]
+// of its seg slots filled; counts on the device) claimed into their buckets
+__global__ void k_slab_claim_packed(const float4 *__restrict__ in, const int *__restrict__ counts,
+                                    long long seg, BinGeom g, ExactDiv eff0, ExactDiv eff1,
+                                    Rec *__restrict__ region, int *__restrict__ fill,
+                                    long long cap, DevStatus *st, int step) {
+    const int sgm = blockIdx.y;
+    int cnt = counts[sgm];
+    if (cnt > seg) cnt = (int)seg;  // (the sender stopped the run)
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < cnt;
+         j += (long long)gridDim.x * blockDim.x) {
+        const float4 r = in[(long long)sgm * seg + j];
+        const int key = slab_row(r.y, g, eff1) * g.n0 +
+                        cell_axis_fast((double)r.x, g.lo0, eff0, g.n0);
+        const int q = (key >> BUCKET_SHIFT) * SUBB + (threadIdx.x & (SUBB - 1));
+        const int slot = atomicAdd(&fill[q], 1);
+        if (slot < cap) {
+            reinterpret_cast<float4 *>(region)[(long long)q * cap + slot] = r;
+        } else {
+            atomicMin(&st->key, err_key(3, q / SUBB, CS_SORT_OVERFLOW));
+            st->abort = 1;
+            st->step = step;
+        }
+    }
+}
+
+int fast_slab_claim_packed(cs_ctx *ctx, cs_fast *f, const void *inbox, const int *counts,
+                           long long seg, DevStatus *st, int step) {
+    if (seg <= 0) return CS_OK;
+    int gx = grid_for(seg, 256);
+    if (gx > 148 * 4) gx = 148 * 4;
+    k_slab_claim_packed<<<dim3((unsigned)gx, (unsigned)f->world), 256, 0, ctx->stream>>>(
+        (const float4 *)inbox, counts, seg, f->g, make_exact_div(f->g.eff0),
+        make_exact_div(f->g.eff1), f->region.as<Rec>(), f->fill.as<int>(), f->cap, st, step);
+    CS_LAUNCH_CHECK();
+    ctx->launches += 1;
     return CS_OK;
 }
 

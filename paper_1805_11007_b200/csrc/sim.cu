@@ -79,6 +79,10 @@ int fast_slab_claim(cs_ctx *ctx, cs_fast *f, const void *recs, long long n, DevS
                     int step);
 int fast_slab_outbox(cs_ctx *ctx, cs_fast *f, void **recs, int **dest, long long *count);
 int fast_slab_reset_outbox(cs_ctx *ctx, cs_fast *f);
+int fast_slab_exchange_cap(cs_fast *f, long long seg);
+int fast_slab_outbox_packed(cs_fast *f, void **recs, int **counts, long long *seg);
+int fast_slab_claim_packed(cs_ctx *ctx, cs_fast *f, const void *inbox, const int *counts,
+                           long long seg, DevStatus *st, int step);
 int fast_slab_sort(cs_ctx *ctx, cs_fast *f, const cs_sim_params &p, const GridGeom &gg,
                    const unsigned char bits[3], DevStatus *st, int step);
 int fast_slab_range_host(cs_ctx *ctx, cs_fast *f, long long *lo, long long *hi);
@@ -894,6 +898,33 @@ extern "C" int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t 
 extern "C" int cs_slab_claim(cs_sim *sim, const void *recs, int64_t n) {
     CS_TRY(slab_check(sim));
     return cs::fast_slab_claim(sim->ctx, sim->fast, recs, n, sim->dstat(), sim->steps_done);
+}
+
+// Packed exchange (no host round trip in the step): cs_slab_exchange_cap
+// gives every destination rank `seg` slots of the outbox and its own device
+// counter; cs_slab_outbox_packed returns the device pointers (records
+// [world][seg], counts [world]) -- the layout an equal-split all-to-all
+// sends as it is; cs_slab_claim_packed claims what was received in the same
+// layout.  A destination that gets more than seg records in a step stops the
+// run with CS_SORT_OVERFLOW.  seg = 0 returns to the tagged outbox.
+extern "C" int cs_slab_exchange_cap(cs_sim *sim, int64_t seg) {
+    CS_TRY(slab_check(sim));
+    return cs::fast_slab_exchange_cap(sim->fast, seg);
+}
+
+extern "C" int cs_slab_outbox_packed(cs_sim *sim, void **recs, int32_t **counts, int64_t *seg) {
+    CS_TRY(slab_check(sim));
+    long long s = 0;
+    CS_TRY(cs::fast_slab_outbox_packed(sim->fast, recs, counts, &s));
+    *seg = s;
+    return CS_OK;
+}
+
+extern "C" int cs_slab_claim_packed(cs_sim *sim, const void *inbox, const int32_t *counts,
+                                    int64_t seg) {
+    CS_TRY(slab_check(sim));
+    return cs::fast_slab_claim_packed(sim->ctx, sim->fast, inbox, counts, seg, sim->dstat(),
+                                      sim->steps_done);
 }
 
 // Re-balancing: the per-row counts of the owned records (device int[n1]),

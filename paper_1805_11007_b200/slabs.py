@@ -24,8 +24,11 @@ boundary cell rows (ghosts).  Per step, in the reference stage order
 Every pass is the single-domain engine's on the same records, rows and
 columns, so the decomposed run is the single-domain run bit for bit
 (tests/test_gpu_slab_engine.py, ranks emulated in one process).  The grid
-exchanges have sizes fixed by the layout; the particle all-to-all sends its
-per-peer counts first (the step's one host synchronisation).
+exchanges have sizes fixed by the layout.  The particle all-to-all either
+sends its per-peer counts first and reads them back (NcclTransport: one host
+synchronisation per step) or, once a few such steps have sized it, moves
+fixed per-destination segments and their device-side counts
+(PackedNcclTransport: no host synchronisation in the step).
 """
 
 from __future__ import annotations
@@ -154,6 +157,65 @@ class NcclTransport:
         return out
 
 
+class PackedNcclTransport(NcclTransport):
+    """The records' exchange without a host round trip: every rank keeps
+    `seg` outbox slots and a device counter per destination
+    (SlabEngine.set_exchange_cap), so the counts and the records travel as two
+    equal-split all-to-alls straight from / into device buffers.  `seg` comes
+    from calibrate(): a few steps through the counted exchange of
+    NcclTransport, whose per-destination maxima -- reduced over the ranks,
+    times a safety factor -- bound a step's traffic; a step that exceeds it
+    stops the run (CS_SORT_OVERFLOW), it is never silently dropped."""
+
+    def __init__(self, world: int, group=None, factor: float = 4.0, floor: int = 4096):
+        super().__init__(world, group)
+        self.factor, self.floor = factor, floor
+        self.peak = 0      # largest per-destination count seen by the counted exchange
+        self.seg = 0       # slots per destination of the packed exchange (0: not calibrated)
+        self._inbox = self._in_counts = None
+
+    def exchange(self, recs, dest):
+        if recs.shape[0]:
+            d = (dest & 0x3FFFFFFF).long()
+            self.peak = max(self.peak, int(torch.bincount(d, minlength=self.world).max()))
+        return super().exchange(recs, dest)
+
+    def calibrate(self) -> int:
+        """Agree on `seg` over the ranks (after some counted exchanges)."""
+        t = torch.tensor([self.peak], dtype=torch.int64,
+                         device=torch.device("cuda", torch.cuda.current_device()))
+        if self.world > 1 or dist.is_initialized():
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        seg = max(self.floor, int(self.factor * int(t.item())))
+        self.seg = max(self.seg, (seg + 255) // 256 * 256)
+        return self.seg
+
+    def exchange_packed(self, out_recs, out_counts):
+        """out_recs (W, seg, 4) int32, out_counts (W,) int32 (device views of
+        the engine's outbox) -> (inbox (W, seg, 4), in_counts (W,))."""
+        if self._inbox is None or self._inbox.shape != out_recs.shape:
+            self._inbox = torch.empty_like(out_recs)
+            self._in_counts = torch.empty_like(out_counts)
+        dist.all_to_all_single(self._in_counts, out_counts, group=self.group)
+        dist.all_to_all_single(self._inbox.view(-1), out_recs.view(-1), group=self.group)
+        return self._inbox, self._in_counts
+
+
+class PackedLoopbackHub(LoopbackHub):
+    """The packed exchange between the ranks of one process (tests)."""
+
+    def exchange_all_packed(self, outs):
+        """outs[r] = (recs (W, seg, 4), counts (W,)) of rank r ->
+        received[q] = (inbox (W, seg, 4), in_counts (W,)): segment s from rank s."""
+        W = self.world
+        got = []
+        for q in range(W):
+            inbox = torch.stack([outs[s][0][q] for s in range(W)])
+            counts = torch.stack([outs[s][1][q] for s in range(W)])
+            got.append((inbox, counts))
+        return got
+
+
 class SlabEngine:
     """One rank's share of a y-slab decomposed system on its GPU: the sorted
     engine (binary32 records, reference summation order) over the owned cell
@@ -217,6 +279,33 @@ class SlabEngine:
         dest = _device_view(dp.value, (m,), torch.int32, dev)
         return recs, dest
 
+    def set_exchange_cap(self, seg: int):
+        """Packed exchange with `seg` outbox slots per destination rank
+        (0: the tagged outbox of outbox() / claim())."""
+        self.N.check(self.sim._bind().cs_slab_exchange_cap(self.sim._h, int(seg)),
+                     "cs_slab_exchange_cap")
+        self._seg = int(seg)
+
+    def outbox_packed(self):
+        """(records (W, seg, 4) int32, counts (W,) int32): device views, no
+        host round trip."""
+        import ctypes
+        N = self.N
+        rp, cp, seg = N.C_p(), N.C_p(), N.C_i64()
+        N.check(self.sim._bind().cs_slab_outbox_packed(self.sim._h, ctypes.byref(rp),
+                                                      ctypes.byref(cp), ctypes.byref(seg)),
+                "cs_slab_outbox_packed")
+        dev = self.sim.state["pos"].device
+        W, sg = self.world, int(seg.value)
+        return (_device_view(rp.value, (W, sg, 4), torch.int32, dev),
+                _device_view(cp.value, (W,), torch.int32, dev))
+
+    def claim_packed(self, inbox, in_counts):
+        N = self.N
+        N.check(self.sim._bind().cs_slab_claim_packed(self.sim._h, N.ptr(inbox),
+                                                     N.ptr(in_counts), int(inbox.shape[1])),
+                "cs_slab_claim_packed")
+
     def claim(self, recs):
         if recs is None or recs.shape[0] == 0:
             return
@@ -235,9 +324,15 @@ class SlabEngine:
             if not hasattr(self, "_nf"):
                 self._nf = NcclField(self.field, transport.group)
             self._nf.step()
+        seg = getattr(transport, "seg", 0)
+        if seg != getattr(self, "_seg", 0):
+            self.set_exchange_cap(seg)
         self.local(xi)
-        recs, dest = self.outbox()
-        self.claim(transport.exchange(recs, dest))
+        if seg:  # packed: counts and records stay on the device
+            self.claim_packed(*transport.exchange_packed(*self.outbox_packed()))
+        else:
+            recs, dest = self.outbox()
+            self.claim(transport.exchange(recs, dest))
         self.finish()
 
     def status(self):
@@ -284,8 +379,8 @@ class SlabEngine:
         bounds = SlabLayout.balanced(counts, self.world).bounds
         plan = FieldPlan.make(bounds, n1, n_c, self.world) if self.field is not None else None
         self.rebalance_begin(bounds, plan)
-        recs, dest = self.outbox()
-        self.claim(transport.exchange(recs, dest))
+        recs, dest = self.outbox()  # (a re-balance always goes through the tagged outbox)
+        self.claim(NcclTransport.exchange(transport, recs, dest))
         self.rebalance_end()
 
     def export(self):
@@ -333,9 +428,14 @@ def step_in_process(engines, hub: LoopbackHub, xi):
         field_in_process([e.field for e in engines], move_in_process)
     for e in engines:
         e.local(xi)
-    got = hub.exchange_all([e.outbox() for e in engines])
-    for e, g in zip(engines, got):
-        e.claim(g)
+    if getattr(engines[0], "_seg", 0):
+        got = hub.exchange_all_packed([e.outbox_packed() for e in engines])
+        for e, g in zip(engines, got):
+            e.claim_packed(*g)
+    else:
+        got = hub.exchange_all([e.outbox() for e in engines])
+        for e, g in zip(engines, got):
+            e.claim(g)
     for e in engines:
         e.finish()
 

@@ -96,6 +96,82 @@ def test_slab_engine_equals_single_domain_bitwise(world, clustered):
         e.close()
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_packed_exchange_equals_single_domain_bitwise(world, clustered):
+    """The exchange without a host round trip (a segment of outbox slots and a
+    device counter per destination rank, claimed from the same layout): two
+    counted steps size the segments, the rest run packed -- the single
+    domain's positions and anchors bit for bit."""
+    rng = np.random.default_rng(40 + world)
+    n, steps = 200_000, 6
+    if clustered:
+        centres = -0.5 + rng.random((64, 2))
+        pos = centres[rng.integers(0, 64, n)] + 0.02 * rng.standard_normal((n, 2))
+        pos = np.mod(pos + 0.5, 1.0) - 0.5
+    else:
+        pos = -0.5 + rng.random((n, 2))
+    pos = pos.astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    params, mp, dom = _params(n, (4.9e-4, 9.8e-4))
+    xi = torch.as_tensor(rng.standard_normal((steps, n, 2)).astype(np.float32), device="cuda")
+    st1 = _state(pos, sp)
+    one = cs.DeviceSim(params, st1)
+    one.step(xi, steps)
+    one.export_state()
+    st = _state(pos, sp)
+    bounds = _bounds(pos, mp, dom, world)
+    engines = [slabs.SlabEngine(params, st, bounds, r, world) for r in range(world)]
+    hub = slabs.PackedLoopbackHub(world)
+    peak = 0
+    for k in range(2):  # counted steps: the largest per-destination traffic
+        for e in engines:
+            e.local(xi[k])
+        outs = [e.outbox() for e in engines]
+        for recs, dest in outs:
+            if recs.shape[0]:
+                peak = max(peak, int(torch.bincount((dest & 0x3FFFFFFF).long()).max()))
+        for e, g in zip(engines, hub.exchange_all(outs)):
+            e.claim(g)
+        for e in engines:
+            e.finish()
+    assert peak > 0
+    seg = (2 * peak + 255) // 256 * 256
+    for e in engines:
+        e.set_exchange_cap(seg)
+    for k in range(2, steps):
+        slabs.step_in_process(engines, hub, xi[k])
+    for e in engines:
+        assert e.status().code == 0
+        e.export()
+    torch.cuda.synchronize()
+    assert torch.equal(st["pos"], st1["pos"])
+    assert torch.equal(st["anchor"], st1["anchor"])
+    for e in engines:
+        e.close()
+
+
+def test_packed_exchange_overflow_stops_the_run():
+    """A destination that gets more records in a step than its segment holds
+    stops the run (CS_SORT_OVERFLOW) instead of dropping records."""
+    rng = np.random.default_rng(5)
+    n, world = 100_000, 2
+    pos = (-0.5 + rng.random((n, 2))).astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    params, mp, dom = _params(n, (4.9e-4, 9.8e-4))
+    xi = torch.as_tensor(rng.standard_normal((1, n, 2)).astype(np.float32), device="cuda")
+    st = _state(pos, sp)
+    bounds = _bounds(pos, mp, dom, world)
+    engines = [slabs.SlabEngine(params, st, bounds, r, world) for r in range(world)]
+    hub = slabs.PackedLoopbackHub(world)
+    for e in engines:
+        e.set_exchange_cap(8)
+    slabs.step_in_process(engines, hub, xi[0])
+    assert any(e.status().code == cs._native.CS_SORT_OVERFLOW for e in engines)
+    for e in engines:
+        e.close()
+
+
 def _field_params(n, radii, n_c):
     import warnings
     with warnings.catch_warnings():

@@ -4,6 +4,8 @@ tests/test_gpu_slab_engine.py):
 
 * NcclTransport.exchange routes every outbox record (16 bytes, destination
   rank | kind << 30) to its destination, exactly once;
+* PackedNcclTransport.exchange_packed moves the per-destination segments and
+  their counts with equal-split all-to-alls (no host round trip);
 * NcclField's static all-to-all moves the deposit-window rows, the spectrum
   blocks and the c rows with the sizes the FieldPlan row lists give both
   sides, without a count exchange;
@@ -66,6 +68,45 @@ def test_transport_routes_every_record_once(world, tmp_path):
     seen = np.sort(np.concatenate(seen))
     expect = np.sort(np.concatenate([np.arange(50 + 17 * r) + 1000 * r for r in range(world)]))
     assert np.array_equal(seen, expect)  # exactly once
+
+
+def _packed_worker(rank, world, port, outdir):
+    dist = _init(rank, world, port)
+    try:
+        seg = 16
+        out = torch.zeros((world, seg, 4), dtype=torch.int32)
+        counts = torch.zeros(world, dtype=torch.int32)
+        for d in range(world):
+            c = 3 + rank + 2 * d  # records rank -> d
+            counts[d] = c
+            out[d, :c, 0] = torch.arange(c, dtype=torch.int32)
+            out[d, :c, 1] = rank
+            out[d, :c, 2] = d
+        t = slabs.PackedNcclTransport(world)
+        t.seg = seg
+        inbox, in_counts = t.exchange_packed(out, counts)
+        np.savez(os.path.join(outdir, f"p{rank}.npz"), inbox=inbox.numpy(),
+                 counts=in_counts.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_packed_transport_moves_segments_and_counts(world, tmp_path):
+    """PackedNcclTransport.exchange_packed: segment s of a rank's inbox is
+    what rank s put into its segment for that rank, with its count -- two
+    equal-split all-to-alls, no sizes read on the host."""
+    import torch.multiprocessing as mp
+    mp.spawn(_packed_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world)
+    for r in range(world):
+        got = np.load(os.path.join(tmp_path, f"p{r}.npz"))
+        for s_ in range(world):
+            c = 3 + s_ + 2 * r
+            assert got["counts"][s_] == c
+            seg = got["inbox"][s_]
+            assert np.array_equal(seg[:c, 0], np.arange(c))
+            assert np.all(seg[:c, 1] == s_) and np.all(seg[:c, 2] == r)
+            assert np.all(seg[c:] == 0)
 
 
 class _FakeEngine:

@@ -250,6 +250,59 @@ def test_slab_engine_with_field_equals_single_domain_bitwise(world, clustered):
         eng.close()
 
 
+def test_slab_step_over_nccl_on_one_rank_equals_single_domain_bitwise():
+    """The N > 1 step as bench.py drives it -- SlabEngine.step over real NCCL
+    (NcclField's static exchanges and transposes, the counted record exchange
+    for two steps, then the packed one, a re-balance in between) -- on a
+    one-rank process group (one B200 per session): positions, anchors and the
+    field equal the single-domain engine's bit for bit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    rng = np.random.default_rng(77)
+    n, n_c, steps = 100_000, 256, 6
+    pos = (-0.5 + rng.random((n, 2))).astype(np.float32)
+    sp = (np.arange(n) >= n // 2).astype(np.uint8)
+    c0 = (0.5 + 0.1 * rng.standard_normal(n_c * n_c)).astype(np.float32)
+    params, mp, dom = _field_params(n, (7e-4, 1.4e-3), n_c)
+    xi = torch.as_tensor(rng.standard_normal((steps, n, 2)).astype(np.float32), device="cuda")
+    st1 = _field_state(pos, sp, c0, n_c)
+    one = cs.DeviceSim(params, st1)
+    one.step(xi, steps)
+    one.export_state()
+    assert one.status().code == 0
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        st = _field_state(pos, sp, c0, n_c)
+        bounds = _bounds(pos, mp, dom, 1)
+        e, c, cell = mp.pair_table()
+        n1 = slabs.CellGeometry.make(dom.lo[1], dom.hi[1], cell).n
+        plan = slabs.FieldPlan.make(bounds, n1, n_c, 1)
+        eng = slabs.SlabEngine(params, st, bounds, 0, 1, field_plan=plan)
+        tr = slabs.PackedNcclTransport(1)
+        for k in range(steps):
+            eng.step(xi[k], tr)
+            if k == 1:
+                assert tr.calibrate() >= 4096
+            if k == 3:
+                eng.rebalance(tr, n1, n_c)
+        assert eng.status().code == 0
+        eng.export()
+        torch.cuda.synchronize()
+        assert torch.equal(st["pos"], st1["pos"])
+        assert torch.equal(st["anchor"], st1["anchor"])
+        assert torch.equal(st["c"], st1["c"])
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_bench_slab_setup_in_process():
     """bench.py's N > 1 path (one system over W slabs): its setup (seeded
     state, count-balanced bounds, field plan) at cfg3's parameters and 1/50

@@ -649,8 +649,9 @@ def run_slabs(args, cfg, rank, world, barrier):
     blocks = K + W
     gen = torch.Generator(device="cuda").manual_seed(SEED)
     xi = torch.randn((blocks, n, 2), generator=gen, device="cuda", dtype=torch.float32)
+    overlap = not os.environ.get("CS_SLAB_NO_OVERLAP")  # field step beside the pair forces
     for w in range(W):
-        eng.step(xi[w], tr)
+        eng.step(xi[w], tr, overlap)
     if W > 0 and not os.environ.get("CS_SLAB_COUNTED"):
         tr.calibrate()
     torch.cuda.synchronize()
@@ -663,7 +664,7 @@ def run_slabs(args, cfg, rank, world, barrier):
         torch.cuda.synchronize()
         a.record(stream)
         for k in range(K):
-            eng.step(xi[W + k], tr)
+            eng.step(xi[W + k], tr, overlap)
             launches += eng.sim.launches()  # forces / update / sort / deposit of the step
             if args.rebalance_every and (k + 1) % args.rebalance_every == 0 and k + 1 < K:
                 eng.rebalance(tr, eng.n1, cfg["n_c"] if cfg["field"] else None)

@@ -363,6 +363,10 @@ int cs_slab_config(cs_sim *sim, const int32_t *bounds, int32_t world, int32_t ra
 int cs_slab_import(cs_sim *sim, const cs_sim_state *st);
 /* xi: the step's (n_global, 2) increments by particle id */
 int cs_slab_step_local(cs_sim *sim, const cs_sim_state *st, const void *xi);
+/* its two halves as separate calls: part 1 = outbox reset + pair forces, part
+ * 2 = update (the caller may run the field step on another stream beside
+ * part 1 and join before part 2) */
+int cs_slab_step_part(cs_sim *sim, const cs_sim_state *st, const void *xi, int32_t part);
 /* the outbox after cs_slab_step_local (device pointers; the count is read
  * back to the host: the exchange sizes its transfers with it) */
 int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t *count);

@@ -126,6 +126,7 @@ SIGNATURES = [
     ("cs_slab_config", C_i32, [C_p, ctypes.POINTER(C_i32), C_i32, C_i32]),
     ("cs_slab_import", C_i32, [C_p, ctypes.POINTER(SimState_t)]),
     ("cs_slab_step_local", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p]),
+    ("cs_slab_step_part", C_i32, [C_p, ctypes.POINTER(SimState_t), C_p, C_i32]),
     ("cs_slab_outbox", C_i32, [C_p, ctypes.POINTER(C_p), ctypes.POINTER(C_p),
                                ctypes.POINTER(C_i64)]),
     ("cs_slab_claim", C_i32, [C_p, C_p, C_i64]),

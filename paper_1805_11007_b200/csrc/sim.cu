@@ -887,6 +887,26 @@ extern "C" int cs_slab_step_local(cs_sim *sim, const cs_sim_state *st, const voi
     return CS_OK;
 }
 
+// the two halves of cs_slab_step_local as separate calls (part 1: outbox
+// reset + pair forces, part 2: update), so that the caller can run the
+// distributed field step -- which the forces do not read -- on another
+// stream beside part 1 and join before part 2
+extern "C" int cs_slab_step_part(cs_sim *sim, const cs_sim_state *st, const void *xi,
+                                 int32_t part) {
+    CS_TRY(slab_check(sim));
+    if (part != 1 && part != 2) {
+        cs::set_error("cs_slab_step_part: part is 1 (forces) or 2 (update)");
+        return CS_ERR_PARAM;
+    }
+    const int64_t l0 = sim->ctx->launches;
+    const cs::FastStepCfg c = slab_cfg(sim);
+    if (part == 1) CS_TRY(cs::fast_slab_reset_outbox(sim->ctx, sim->fast));
+    CS_TRY(cs::fast_particles(sim->ctx, sim->fast, c, st, xi, sim->dstat(), sim->steps_done,
+                              part));
+    sim->last_launches = (part == 1 ? 0 : sim->last_launches) + sim->ctx->launches - l0;
+    return CS_OK;
+}
+
 extern "C" int cs_slab_outbox(cs_sim *sim, void **recs, int32_t **dest, int64_t *count) {
     CS_TRY(slab_check(sim));
     long long c = 0;

@@ -263,6 +263,18 @@ class SlabEngine:
         N.check(self.sim._bind().cs_slab_step_local(self.sim._h, ctypes_byref(self.sim._st),
                                                    N.ptr(xi)), "cs_slab_step_local")
 
+    def forces(self, xi):
+        """First half of local(): the outbox reset and the pair forces."""
+        N = self.N
+        N.check(self.sim._bind().cs_slab_step_part(self.sim._h, ctypes_byref(self.sim._st),
+                                                  N.ptr(xi), 1), "cs_slab_step_part")
+
+    def update(self, xi):
+        """Second half of local(): the update (needs the field step's gradient)."""
+        N = self.N
+        N.check(self.sim._bind().cs_slab_step_part(self.sim._h, ctypes_byref(self.sim._st),
+                                                  N.ptr(xi), 2), "cs_slab_step_part")
+
     def outbox(self):
         """(records (M, 4) int32, dest (M,) int32) views of the outbox."""
         import ctypes
@@ -319,15 +331,31 @@ class SlabEngine:
         self.N.check(self.sim._bind().cs_slab_finish(self.sim._h), "cs_slab_finish")
 
     # ---- one step over NCCL (one rank per process) -------------------------
-    def step(self, xi, transport: NcclTransport):
-        if self.field is not None:
-            if not hasattr(self, "_nf"):
-                self._nf = NcclField(self.field, transport.group)
-            self._nf.step()
+    def step(self, xi, transport: NcclTransport, overlap: bool = True):
+        """One step over NCCL.  overlap: the distributed field step (its
+        exchanges and transposes included) runs on a side stream beside the
+        pair forces, which do not read the field; the update joins them."""
         seg = getattr(transport, "seg", 0)
         if seg != getattr(self, "_seg", 0):
             self.set_exchange_cap(seg)
-        self.local(xi)
+        if self.field is not None:
+            if not hasattr(self, "_nf"):
+                self._nf = NcclField(self.field, transport.group)
+            if overlap:
+                main = torch.cuda.current_stream()
+                if not hasattr(self, "_side"):
+                    self._side = torch.cuda.Stream(device=main.device)
+                self._side.wait_stream(main)  # the deposit of the last finish()
+                with torch.cuda.stream(self._side):
+                    self._nf.step()
+                self.forces(xi)
+                main.wait_stream(self._side)
+                self.update(xi)
+            else:
+                self._nf.step()
+                self.local(xi)
+        else:
+            self.local(xi)
         if seg:  # packed: counts and records stay on the device
             self.claim_packed(*transport.exchange_packed(*self.outbox_packed()))
         else:
@@ -550,9 +578,17 @@ class SlabField:
             if rows.numel():
                 self.rho[:, rows, :] += g.view(2, rows.numel(), self.plan.n)
 
+    def _lib(self):
+        """The library bound to the CURRENT torch stream (SlabEngine.step runs
+        the field step on a side stream beside the pair forces)."""
+        e = self.eng
+        lib = e.N.load_library()
+        lib.cs_ctx_set_stream(e.sim._ctx, e.N.C_p(torch.cuda.current_stream().cuda_stream))
+        return lib
+
     def spec_rows(self, inverse: bool):
         e = self.eng
-        e.N.check(e.sim._bind().cs_slab_field_rows(e.sim._h, ctypes_byref(e.sim._st),
+        e.N.check(self._lib().cs_slab_field_rows(e.sim._h, ctypes_byref(e.sim._st),
                                                    e.N.ptr(self.spec), int(inverse)),
                   "cs_slab_field_rows")
 
@@ -566,7 +602,7 @@ class SlabField:
 
     def cols(self):
         e, p, r = self.eng, self.plan, self.eng.rank
-        e.N.check(e.sim._bind().cs_slab_field_cols(
+        e.N.check(self._lib().cs_slab_field_cols(
             e.sim._h, e.N.ptr(self.blocks), int(p.kx[r]), int(p.kx[r + 1] - p.kx[r]), p.rp),
             "cs_slab_field_cols")
 
@@ -588,7 +624,7 @@ class SlabField:
 
     def gradient(self):
         e = self.eng
-        e.N.check(e.sim._bind().cs_slab_field_grad(e.sim._h, ctypes_byref(e.sim._st)),
+        e.N.check(self._lib().cs_slab_field_grad(e.sim._h, ctypes_byref(e.sim._st)),
                   "cs_slab_field_grad")
 
 

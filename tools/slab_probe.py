@@ -25,6 +25,7 @@ xi = torch.randn((4, cfg["n"], 2), device="cuda", dtype=torch.float32)
 for w in range(3):
     eng.step(xi[w], tr)
 nf = eng._nf
+torch.cuda.synchronize()
 acc = {}
 
 

@@ -172,6 +172,7 @@ class PackedNcclTransport(NcclTransport):
         self.factor, self.floor = factor, floor
         self.peak = 0      # largest per-destination count seen by the counted exchange
         self.seg = 0       # slots per destination of the packed exchange (0: not calibrated)
+        self.pending = False  # after a re-balance: one counted step, then calibrate() again
         self._inbox = self._in_counts = None
 
     def exchange(self, recs, dest):
@@ -335,7 +336,11 @@ class SlabEngine:
         """One step over NCCL.  overlap: the distributed field step (its
         exchanges and transposes included) runs on a side stream beside the
         pair forces, which do not read the field; the update joins them."""
-        seg = getattr(transport, "seg", 0)
+        # (the step after a re-balance goes through the counted exchange and
+        # re-sizes the packed one: the boundary rows, hence the ghost traffic,
+        # have moved)
+        recal = getattr(transport, "pending", False) and getattr(transport, "seg", 0) > 0
+        seg = 0 if recal else getattr(transport, "seg", 0)
         if seg != getattr(self, "_seg", 0):
             self.set_exchange_cap(seg)
         if self.field is not None:
@@ -362,6 +367,9 @@ class SlabEngine:
             recs, dest = self.outbox()
             self.claim(transport.exchange(recs, dest))
         self.finish()
+        if recal:
+            transport.pending = False
+            transport.calibrate()
 
     def status(self):
         return self.sim.status()
@@ -410,6 +418,8 @@ class SlabEngine:
         recs, dest = self.outbox()  # (a re-balance always goes through the tagged outbox)
         self.claim(NcclTransport.exchange(transport, recs, dest))
         self.rebalance_end()
+        if hasattr(transport, "pending"):
+            transport.pending = True
 
     def export(self):
         """Own particles' positions / anchors into the global state arrays."""
